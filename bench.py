@@ -1,0 +1,480 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SparseRT hot path (effective GFLOP/s = 2*nnz*N / t).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload rn50_b8] [--dtype f32]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...     # the CPU oracle arm (rank 0 only)
+
+A "step" is one pass of the executor over one batch of synthetic input for every layer of
+the workload (the plans are built once, offline, like the paper's inspector; their
+build time is reported in config.plan_build_ms).  Default workload (BASELINE.json
+configs[1]): the eight ResNet-50 1x1 layers of PAPER.md Table 1, 90% sparsity,
+batch 8 per GPU, fp32 (the paper's precision).  L2 is flushed (256 MiB write)
+before every timed step, outside the timed events, so every layer reads cold HBM.
+
+Multi-GPU: one process per GPU, each with a replicated plan and its own batch (weak
+scaling for the layer workloads: no collective on the data path); the conv workload
+(configs[4]) shards the fixed batch of 256 images over ranks (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import gen  # noqa: E402
+
+METRIC = "effective GFLOP/s (2·nnz·N) and speedup vs dense GEMM at 90/95% sparsity"
+
+
+# ----------------------------------------------------------------------------- workloads
+
+def workload_layers(name: str, sparsity: int, world: int):
+    """Returns (layers, scaling, description).  layer = dict(kind, M, K, N | conv geometry)."""
+    if name in ("rn50_b8", "rn50_b1"):
+        b = 8 if name == "rn50_b8" else 1
+        layers = [dict(kind="spmm", name=f"rn50_p{p}", M=gen.TABLE1[p][0], K=gen.TABLE1[p][1],
+                       N=gen.TABLE1[p][2] * b) for p in gen.RN50_1X1]
+        return layers, "weak", f"ResNet-50 1x1 layers (Table 1 p1-p8), batch {b} per GPU"
+    if name == "mbv1_b32":
+        layers = [dict(kind="spmm", name=f"mbv1_p{p}", M=gen.TABLE1[p][0], K=gen.TABLE1[p][1],
+                       N=gen.TABLE1[p][2] * 32) for p in gen.MBV1_PW]
+        return layers, "weak", "MobileNetV1 pointwise layers (Table 1 p12-p20), batch 32 per GPU"
+    if name == "bert":
+        layers = [dict(kind="spmm", name=f"bert_{M}x{K}", M=M, K=K, N=32 * 512) for M, K in gen.BERT_FC]
+        return layers, "weak", "BERT-base FFN layers, N = 32 x 512 per GPU"
+    if name == "conv":
+        B = 256
+        if B % world:
+            raise SystemExit("conv workload: world size must divide 256")
+        return ([dict(kind="conv", name="rn50_conv3x3_256ch_14", M=256, K=9 * 256, c_in=256,
+                      H=14, W=14, B=B // world)], "strong",
+                "ResNet-50 3x3 conv 256ch 14x14, batch 256 sharded over GPUs")
+    if name == "tiny":
+        return [dict(kind="spmm", name="tiny", M=64, K=64, N=128)], "weak", "tiny 64x64x128"
+    raise SystemExit(f"unknown workload {name}")
+
+
+def layer_N(L):
+    return L["N"] if L["kind"] == "spmm" else L["B"] * L["H"] * L["W"]
+
+
+def make_inputs(L, sparsity, rank):
+    seed = gen.case_seed(L["name"], sparsity)
+    w = gen.pruned_weights(L["M"], L["K"], sparsity, seed=seed)
+    if L["kind"] == "spmm":
+        x = gen.uniform_x(L["K"], L["N"], seed=seed + 1 + 1000 * rank)
+    else:
+        x = gen.relu_normal_x((L["c_in"], L["B"], L["H"], L["W"]), seed=seed + 1 + 1000 * rank)
+    return w, x
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- peaks
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm_gbs=float(d["hbm_gbs"]), sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)),
+                    source="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback")
+
+
+def alu_peak_gflops(sm_mhz: float) -> float:
+    # 148 SMs x 128 FP32 lanes x 2 flop/FMA x clock
+    return 148 * 128 * 2 * sm_mhz * 1e-3
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def _samples_for(layers, ins, cols):
+    samples = []
+    for (w, x), Lx in zip(ins, layers):
+        if Lx["kind"] == "spmm":
+            n = min(cols, Lx["N"])
+            samples.append(("spmm", w, np.ascontiguousarray(x[:, :n]).astype(np.float64), n))
+        else:
+            hw = Lx["H"] * Lx["W"]
+            nb = max(1, min(Lx["B"], cols // hw))
+            samples.append(("conv", w, np.ascontiguousarray(x[:, :nb]).astype(np.float64), nb * hw))
+    return samples
+
+
+def oracle_step_sample(layers, sparsity, per_step_s: float, rank: int):
+    """Bounded sample: the first n columns (whole images for conv) of every layer, n sized by
+    a calibration run so that one oracle step takes about per_step_s seconds."""
+    ins = [make_inputs(L, sparsity, rank) for L in layers]
+    cols = 32 if layers[0]["kind"] == "spmm" else layers[0]["H"] * layers[0]["W"]
+    for _ in range(4):
+        samples = _samples_for(layers, ins, cols)
+        t0 = time.perf_counter()
+        run_oracle_step(samples)
+        dt = time.perf_counter() - t0
+        if dt > 0.5 * per_step_s or all(s[3] >= layer_N(L) for s, L in zip(samples, layers)):
+            break
+        cols = int(cols * min(64.0, max(2.0, per_step_s / max(dt, 1e-4))))
+    cols = max(1, int(cols * min(1.0, per_step_s / max(dt, 1e-4))))
+    return _samples_for(layers, ins, cols)
+
+
+def run_oracle_step(samples):
+    import oracle
+    flops = 0
+    for kind, w, x, n in samples:
+        if kind == "spmm":
+            oracle.spmm(w.M, w.K, w.row_ptr, w.col_idx, w.values.astype(np.float64), x)
+        else:
+            oracle.conv3x3(w.M, w.row_ptr, w.col_idx, w.values.astype(np.float64), x)
+        flops += 2 * w.nnz * n
+    return flops
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    layers, scaling, desc = workload_layers(args.workload, args.sparsity, 1)
+    budget = float(os.environ.get("SPARSERT_REF_BUDGET_S", "120"))
+    per_step = max(0.05, min(2.0, budget / max(1, args.steps + args.warmup)))
+    samples = oracle_step_sample(layers, args.sparsity, per_step, rank)
+    for _ in range(args.warmup):
+        run_oracle_step(samples)
+    t0 = time.perf_counter()
+    flops = 0
+    for _ in range(args.steps):
+        flops += run_oracle_step(samples)
+    dt = time.perf_counter() - t0
+    value = flops / dt / 1e9
+    cores = oracle.default_threads()
+    sample_desc = "; ".join(f"{L['name']}: first {n} of {layer_N(L)} columns"
+                            for L, (_, _, _, n) in zip(layers, samples))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / max(1, args.steps) * 1e3, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "description": desc, "sparsity_pct": args.sparsity,
+                   "oracle": "oracle/oracle.c (dense-expanded m-k-n triple loop, double, OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": sample_desc},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="rn50_b8",
+                    choices=["rn50_b8", "rn50_b1", "mbv1_b32", "bert", "conv", "tiny"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f16"])
+    ap.add_argument("--sparsity", type=int, default=90)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip e2e/dense/cpu legs (for ncu runs)")
+    args = ap.parse_args()
+    if args.warmup < 3 and not args.quick:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2008_11849_b200 as srt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    tdt = torch.float16 if args.dtype == "f16" else torch.float32
+    S = 2 if args.dtype == "f16" else 4
+
+    layers, scaling, desc = workload_layers(args.workload, args.sparsity, world)
+    plans, xs, ys, host = [], [], [], []
+    build_ms = []
+    for L in layers:
+        w, x = make_inputs(L, args.sparsity, rank)
+        if L["kind"] == "spmm":
+            p = srt.Plan.from_csr(w, dtype=tdt, n_hint=L["N"], device=local)
+        else:
+            p = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=L["c_in"],
+                                  h=L["H"], w=L["W"], n_hint=L["B"], device=local)
+        build_ms.append(p.info["build_ms"])
+        X = torch.from_numpy(x).to(dev).to(tdt).contiguous()
+        if L["kind"] == "spmm":
+            Y = torch.empty((L["M"], L["N"]), dtype=tdt, device=dev)
+        else:
+            Y = torch.empty((L["M"], L["B"], L["H"], L["W"]), dtype=tdt, device=dev)
+        plans.append((p, w))
+        xs.append(X)
+        ys.append(Y)
+        host.append(x)
+    stream = torch.cuda.current_stream(dev)
+
+    def call(i, X=None, Y=None):
+        p, _ = plans[i]
+        if layers[i]["kind"] == "spmm":
+            p.spmm(xs[i] if X is None else X, ys[i] if Y is None else Y, stream=stream)
+        else:
+            p.conv3x3(xs[i] if X is None else X, ys[i] if Y is None else Y, stream=stream)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    nl = len(layers)
+    flops_step = sum(2 * plans[i][1].nnz * layer_N(layers[i]) for i in range(nl))
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        flush.zero_()
+        for i in range(nl):
+            call(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
+    for s in range(args.steps):
+        flush.zero_()
+        ev[s][0].record(stream)
+        for i in range(nl):
+            call(i)
+            ev[s][i + 1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    step_ms = [ev[s][0].elapsed_time(ev[s][nl]) for s in range(args.steps)]
+    layer_ms = [statistics.fmean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(args.steps))
+                for i in range(nl)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_max = float(t.item())
+    value = flops_step * world * args.steps / (total_ms_max * 1e-3) / 1e9 if scaling == "weak" \
+        else flops_step * world * args.steps / (total_ms_max * 1e-3) / 1e9
+    launches = args.steps * nl
+
+    # ---------------- roofline of the dominant kernel (longest layer)
+    peaks = load_peaks()
+    alu = alu_peak_gflops(peaks["sm_max_mhz"])
+    per_layer = []
+    for i, L in enumerate(layers):
+        p, w = plans[i]
+        N = layer_N(L)
+        x_bytes = S * (L["K"] if L["kind"] == "spmm" else L["c_in"]) * N
+        y_bytes = S * L["M"] * N
+        alg_bytes = x_bytes + y_bytes + p.info["plan_bytes"]
+        flops = 2 * w.nnz * N
+        t_fma = flops / (alu * 1e9)
+        t_hbm = alg_bytes / (peaks["hbm_gbs"] * 1e9)
+        bound = "alu" if t_fma >= t_hbm else "hbm"
+        sec = layer_ms[i] * 1e-3
+        per_layer.append(dict(name=L["name"], M=L["M"], K=L["K"], N=N, nnz=w.nnz, ms=layer_ms[i],
+                              gflops=flops / sec / 1e9, bound=bound,
+                              roof_frac=max(t_fma, t_hbm) / sec, alg_bytes=alg_bytes))
+    dom = max(range(nl), key=lambda i: layer_ms[i])
+    d = per_layer[dom]
+    sec = d["ms"] * 1e-3
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_{args.dtype}_s{args.sparsity}.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(d["name"])
+    if d["bound"] == "hbm":
+        roof = {"bound": "hbm", "achieved": d["alg_bytes"] / sec / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s"}
+    else:
+        roof = {"bound": "alu", "achieved": 2 * d["nnz"] * d["N"] / sec / 1e12,
+                "peak": alu / 1e3, "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = traffic
+    roof["kernel"] = d["name"]
+    roof["peak_source"] = peaks["source"] if roof["bound"] == "hbm" else \
+        "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"
+    roof["alg_bytes_per_launch"] = d["alg_bytes"]
+    roof["flops_per_launch"] = 2 * d["nnz"] * d["N"]
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if not (args.no_e2e or args.quick):
+        hx = [torch.from_numpy(h).to(tdt).pin_memory() for h in host]
+        hy = [torch.empty(tuple(y.shape), dtype=tdt).pin_memory() for y in ys]
+        h2d = sum(h.numel() * S for h in hx)
+        d2h = sum(y.numel() * S for y in hy)
+        n_e2e = max(3, min(args.steps, 50))
+        for s in range(2):
+            for i in range(nl):
+                xs[i].copy_(hx[i], non_blocking=True)
+                call(i)
+                hy[i].copy_(ys[i], non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(n_e2e):
+            for i in range(nl):
+                xs[i].copy_(hx[i], non_blocking=True)
+                call(i)
+                hy[i].copy_(ys[i], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops_step * world * n_e2e / (float(te.item()) * 1e-3) / 1e9,
+               "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "steps": n_e2e}
+
+    # ---------------- dense GEMM context (same shapes, W densified, cold L2)
+    dense = None
+    if not (args.no_dense or args.quick) and rank == 0:
+        dense = {}
+        prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cudnn.benchmark = True
+        for label, ddt, tf32 in [("fp32_sgemm", torch.float32, False), ("fp16_tc", torch.float16, False)]:
+            torch.backends.cuda.matmul.allow_tf32 = tf32
+            tot = 0.0
+            for i, L in enumerate(layers):
+                w = plans[i][1]
+                Wd = torch.from_numpy(gen.to_dense(w, np.float32)).to(dev, ddt)
+                if L["kind"] == "spmm":
+                    Xd = xs[i].to(ddt)
+                    fn = lambda: torch.matmul(Wd, Xd)
+                else:
+                    import torch.nn.functional as F
+                    Xn = xs[i].to(ddt).permute(1, 0, 2, 3).contiguous()
+                    Wc = Wd.reshape(L["M"], L["c_in"], 3, 3)
+                    fn = lambda: F.conv2d(Xn, Wc, padding=1)
+                for _ in range(3):
+                    fn()
+                reps = 10
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ms = []
+                for _ in range(reps):
+                    flush.zero_()
+                    e0.record(stream)
+                    fn()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(e0.elapsed_time(e1))
+                tot += statistics.median(ms)
+            sparse_step = statistics.median(step_ms)
+            dense[label] = {"ms_per_step": tot, "speedup_of_sparse": tot / sparse_step}
+        torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if not (args.no_cpu_baseline or args.quick) and rank == 0 and world == 1:
+        import oracle
+        samples = oracle_step_sample(layers, args.sparsity, 10.0, rank)
+        t0 = time.perf_counter()
+        fl = run_oracle_step(samples)
+        dt = time.perf_counter() - t0
+        cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": oracle.default_threads(),
+               "kind": "oracle",
+               "sample": "; ".join(f"{L['name']}: first {n} of {layer_N(L)} columns"
+                                   for L, (_, _, _, n) in zip(layers, samples)),
+               "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"{args.workload}_s{args.sparsity}_{args.dtype}",
+                       "description": desc, "sparsity_pct": args.sparsity,
+                       "layers": [f"{L['M']}x{L['K']}xN{layer_N(L)}" for L in layers],
+                       "l2": "flushed (256 MiB write) before every timed step, outside the events",
+                       "plan_build_ms": build_ms,
+                       "parallelism": f"N-sharded x{world}, replicated plan, no collective"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, "layers": per_layer, "dense_baseline": dense,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,158 @@
+/*
+ * sparsert.h — C ABI of the B200-native SparseRT hot path (arXiv 2008.11849).
+ *
+ * The operation (Sec. 3.2 "Terminology"):  A x B = C with the
+ * sparse matrix A = W (M x K, pruned, pattern fixed before inference) and the
+ * dense matrix B = X (K x N), C = Y (M x N), "C-style row-major default layout".
+ * Batch is folded into N (N = batch*H*W for 1x1 convs, batch*seq for FC layers).
+ * Sparse 3x3 convolutions are the same SpMM on a "virtual" im2col B
+ * (Sec. 3.6).
+ *
+ * Inspector / executor split (Sec. 2.3): sparse_plan_create is the
+ * offline inspector (validation, row grouping, nnz-balanced row panels, K
+ * chunking and packing, tile selection; Sec. 3.4, Sec. 3.7
+ * P:259-263); sparse_spmm / sparse_conv3x3 are the executors (Alg. 3,
+ * P:187-206), launched asynchronously on the caller's CUDA stream.
+ *
+ * All entry points are extern "C", never throw, and return a sparse_status.
+ * A failing call leaves a thread-local human-readable detail retrievable with
+ * sparse_last_error().  No entry point ever falls back to a CPU computation.
+ */
+#ifndef SPARSERT_H_
+#define SPARSERT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t is passed as an opaque pointer so this header does not need the
+ * CUDA headers; 0 / NULL means the legacy default stream of the current thread. */
+typedef void* sparse_stream_t;
+
+typedef struct sparse_plan_s* sparse_plan_t; /* opaque, immutable after create */
+
+enum sparse_status {
+  SPARSE_OK = 0,
+  SPARSE_EINVAL = 1,       /* bad argument: null pointer, negative/zero dim, bad dtype/kind,
+                              misuse (conv call on an SpMM plan, compute on a host-only plan) */
+  SPARSE_EMATRIX = 2,      /* invalid CSR: row_ptr[0] != 0, row_ptr not monotone, row_ptr[M] != nnz,
+                              col_idx out of [0,K), columns not strictly increasing within a row
+                              (unsorted or duplicate), non-finite value, explicit zero (unless
+                              opts->drop_zeros), |value| > 65504 for an fp16 plan.  The detail
+                              names the row. */
+  SPARSE_EUNSUPPORTED = 3, /* e.g. K > 65535, conv with K != 9*c_in, tile override out of range */
+  SPARSE_ENOMEM = 4,       /* host or device allocation failed */
+  SPARSE_ECUDA = 5,        /* CUDA error (no device, launch failure); detail in sparse_last_error() */
+  SPARSE_EINTERNAL = 6
+};
+
+/* X, Y and the plan's values share the dtype; accumulation is always fp32.
+ * SPARSE_F16: W is rounded to fp16 (RN-even) at plan time; each product
+ * f16 x f16 is exact in fp32; Y is rounded RN-even to fp16 once. */
+enum sparse_dtype { SPARSE_F32 = 0, SPARSE_F16 = 1 };
+enum sparse_kind { SPARSE_SPMM = 0, SPARSE_CONV3X3 = 1 };
+
+/* Device value for a host-only plan: the inspector runs and the plan can be
+ * inspected (sparse_plan_info / sparse_plan_dump) but nothing is uploaded and
+ * the compute calls return SPARSE_EINVAL.  Used by CPU-only tests. */
+#define SPARSE_DEVICE_HOST_ONLY (-2)
+
+typedef struct {
+  int32_t kind;       /* SPARSE_SPMM (default) | SPARSE_CONV3X3 */
+  int32_t c_in, h, w; /* conv only: K must equal 9*c_in; H, W fixed at plan time (the paper
+                         specialises each kernel to its problem shape) */
+  int64_t n_hint;     /* expected N (SpMM) or batch (conv); 0 = unknown.  Drives the tile heuristic. */
+  int32_t tune;       /* 0 = heuristic; 1 = timed search over <= 100 candidates —
+                         requires a device and n_hint > 0 */
+  int32_t device;     /* CUDA ordinal; -1 = current device; SPARSE_DEVICE_HOST_ONLY = no upload */
+  int32_t drop_zeros; /* 0 = reject explicit zeros; 1 = drop them */
+  /* Tile overrides (0 = automatic).  None of these changes a result except split_k and
+     k_chunk, which fix the per-row summation order. */
+  int32_t warps;         /* warps per CTA (thread groups of the paper's block): 1..8 */
+  int32_t rows_per_warp; /* R: 1, 2, 4 or 8 */
+  int32_t k_chunk;       /* Kc: K rows staged per pipeline stage (SpMM: multiple of 8, 8..256);
+                            conv: input channels per stage (1..64) */
+  int32_t split_k;       /* G_k thread groups splitting each row's nonzeros: 1,2,4,8 */
+} sparse_plan_opts;
+
+/* Fill *opts with defaults (kind SPMM, device -1, everything else 0). */
+void sparse_plan_opts_init(sparse_plan_opts* opts);
+
+/* Inspector (offline).  W is M x K in CSR: row_ptr int32[M+1], col_idx int32[nnz],
+ * values float32[nnz] — host arrays, borrowed for the duration of the call only.
+ * On success *out owns the plan and its device memory on opts->device.
+ * Errors: EINVAL (null out / arrays, M or K < 1, nnz < 0, bad dtype/kind),
+ * EMATRIX (invalid CSR, see above), EUNSUPPORTED, ENOMEM, ECUDA. */
+int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
+                       const int32_t* row_ptr, const int32_t* col_idx,
+                       const float* values, int32_t dtype,
+                       const sparse_plan_opts* opts);
+
+/* Executor, Y[M x N] = W[M x K] * X[K x N] (overwrite, beta = 0).
+ * X, Y: DEVICE pointers on the plan's device, dtype of the plan, row-major with
+ * N contiguous; ldx, ldy in elements (>= N).  Caller-owned; must not alias.
+ * Every element of Y[:, :N] is written exactly once (rows without nonzeros get +0).
+ * Asynchronous on `stream`.  N == 0 is a no-op.  16-byte aligned X/Y and ldx*s,
+ * ldy*s take the vectorised path; anything else takes the element-wise GPU path.
+ * Errors: EINVAL (null plan/pointers with N > 0, ld < N, conv plan, host-only
+ * plan), ECUDA (launch failure). */
+int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y,
+                int64_t ldy, sparse_stream_t stream);
+
+/* Executor for a SPARSE_CONV3X3 plan (Sec. 3.6):
+ *   y[co][b][oy][ox] = sum_{ci,dy,dx} W[co][(ci*3+dy)*3+dx] * x[ci][b][oy+dy-1][ox+dx-1]
+ * stride 1, zero padding 1, cross-correlation (== PyTorch conv2d with OIHW weight
+ * W.reshape(C_out, C_in, 3, 3)).  x: DEVICE [C_in][batch][H][W], y: DEVICE
+ * [C_out][batch][H][W], contiguous ("CNHW", so N = batch*H*W).  batch == 0 is a
+ * no-op.  Errors: EINVAL (SpMM plan, null pointers, host-only plan), ECUDA. */
+int sparse_conv3x3(sparse_plan_t plan, int64_t batch, const void* x, void* y,
+                   sparse_stream_t stream);
+
+/* Free the plan and its device memory (north-star name).  Must not race with
+ * work still enqueued that uses the plan.  NULL is a no-op. */
+int plan_destroy(sparse_plan_t plan);
+int sparse_plan_destroy(sparse_plan_t plan); /* alias */
+
+typedef struct {
+  int64_t nnz;          /* nonzeros carried by the plan (after drop_zeros) */
+  int64_t plan_bytes;   /* device bytes of the packed plan (read by every call) */
+  int32_t M, K, dtype, kind;
+  int32_t panels;       /* row panels (thread-block rows, Fig. 2b) */
+  int32_t warps;        /* warps per CTA */
+  int32_t rows_per_warp;
+  int32_t cols_per_lane;
+  int32_t n_tile;       /* columns per CTA */
+  int32_t k_chunk;      /* K rows per stage (conv: input channels per stage) */
+  int32_t chunks;
+  int32_t split_k;
+  int32_t smem_bytes;   /* dynamic shared memory per CTA */
+  int32_t device;
+  int32_t conv_rows_per_tile, conv_images_per_tile; /* conv tiling */
+  int64_t max_panel_nnz, min_panel_nnz;            /* load-balance metrics */
+  double build_ms;      /* host inspector wall time */
+  uint64_t digest;      /* FNV-1a of the packed plan: equal digests <=> identical replicas */
+} sparse_plan_info_t;
+
+int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out);
+
+/* Decode the packed plan back into one record per carried nonzero, in the
+ * plan's storage order (test/inspection aid).  Arrays of length >= nnz (any may
+ * be NULL): row and column of the nonzero, its stored value widened to fp32,
+ * the panel, K-chunk and row slot (warp*R + r) it lives in, and the split-K
+ * group that processes it.  Errors: EINVAL if cap < nnz. */
+int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col,
+                     float* value, int32_t* panel, int32_t* chunk, int32_t* slot,
+                     int32_t* group);
+
+/* Thread-local detail of the last failing call on this thread ("" if none). */
+const char* sparse_last_error(void);
+
+/* Library version string, e.g. "sparsert-b200 0.1 sm_100a". */
+const char* sparse_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSERT_H_ */

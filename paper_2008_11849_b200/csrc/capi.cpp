@@ -1,0 +1,240 @@
+// C ABI (include/sparsert.h): argument validation, error reporting and plan
+// ownership around the inspector (inspector.cpp) and executors (kernels.cu).
+// No exception crosses this boundary; nothing here computes on the CPU.
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/sparsert.h"
+#include "plan.h"
+
+struct sparse_plan_s {
+  srt::Plan p;
+  bool host_only = false;
+};
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int ok() {
+  g_err.clear();
+  return SPARSE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+void sparse_plan_opts_init(sparse_plan_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->kind = SPARSE_SPMM;
+  o->device = -1;
+}
+
+int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
+                       const int32_t* row_ptr, const int32_t* col_idx, const float* values,
+                       int32_t dtype, const sparse_plan_opts* opts) {
+  if (!out) return fail(SPARSE_EINVAL, "out is NULL");
+  *out = nullptr;
+  sparse_plan_opts d;
+  sparse_plan_opts_init(&d);
+  const sparse_plan_opts& o = opts ? *opts : d;
+  if (o.tune != 0 && o.tune != 1) return fail(SPARSE_EINVAL, "tune must be 0 or 1");
+  srt::BuildOpts bo;
+  bo.kind = o.kind;
+  bo.c_in = o.c_in;
+  bo.h = o.h;
+  bo.w = o.w;
+  bo.n_hint = o.n_hint;
+  bo.drop_zeros = o.drop_zeros;
+  bo.warps = o.warps;
+  bo.rows_per_warp = o.rows_per_warp;
+  bo.k_chunk = o.k_chunk;
+  bo.split_k = o.split_k;
+  sparse_plan_s* h = nullptr;
+  try {
+    h = new sparse_plan_s();
+  } catch (const std::bad_alloc&) {
+    return fail(SPARSE_ENOMEM, "host allocation failed");
+  }
+  std::string err;
+  int rc;
+  try {
+    rc = srt::build_plan(h->p, M, K, nnz, row_ptr, col_idx, values, dtype, bo, err);
+  } catch (const std::bad_alloc&) {
+    rc = SPARSE_ENOMEM;
+    err = "host allocation failed in inspector";
+  } catch (...) {
+    rc = SPARSE_EINTERNAL;
+    err = "unexpected exception in inspector";
+  }
+  if (rc != SPARSE_OK) {
+    delete h;
+    return fail(rc, err);
+  }
+  if (o.device == SPARSE_DEVICE_HOST_ONLY) {
+    h->host_only = true;
+    h->p.device = SPARSE_DEVICE_HOST_ONLY;
+  } else {
+    if (o.device < -1) {
+      delete h;
+      return fail(SPARSE_EINVAL, "device must be >= -1 or SPARSE_DEVICE_HOST_ONLY");
+    }
+    h->p.device = o.device;
+    rc = srt::upload_plan(h->p, err);
+    if (rc != SPARSE_OK) {
+      delete h;
+      return fail(rc, err);
+    }
+  }
+  *out = h;
+  return ok();
+}
+
+int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                sparse_stream_t stream) {
+  if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
+  if (plan->p.kind != SPARSE_SPMM) return fail(SPARSE_EINVAL, "sparse_spmm on a conv plan");
+  if (plan->host_only) return fail(SPARSE_EINVAL, "host-only plan cannot compute");
+  if (N < 0) return fail(SPARSE_EINVAL, "N < 0");
+  if (N == 0) return ok();
+  if (!X || !Y) return fail(SPARSE_EINVAL, "X or Y is NULL");
+  if (ldx < N || ldy < N) return fail(SPARSE_EINVAL, "ldx and ldy must be >= N");
+  std::string err;
+  const int rc = srt::launch_spmm(plan->p, N, X, ldx, Y, ldy, stream, err);
+  return rc == SPARSE_OK ? ok() : fail(rc, err);
+}
+
+int sparse_conv3x3(sparse_plan_t plan, int64_t batch, const void* x, void* y,
+                   sparse_stream_t stream) {
+  if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
+  if (plan->p.kind != SPARSE_CONV3X3) return fail(SPARSE_EINVAL, "sparse_conv3x3 on an SpMM plan");
+  if (plan->host_only) return fail(SPARSE_EINVAL, "host-only plan cannot compute");
+  if (batch < 0) return fail(SPARSE_EINVAL, "batch < 0");
+  if (batch == 0) return ok();
+  if (!x || !y) return fail(SPARSE_EINVAL, "x or y is NULL");
+  std::string err;
+  const int rc = srt::launch_conv3x3(plan->p, batch, x, y, stream, err);
+  return rc == SPARSE_OK ? ok() : fail(rc, err);
+}
+
+int plan_destroy(sparse_plan_t plan) {
+  if (!plan) return ok();
+  srt::free_plan_device(plan->p);
+  delete plan;
+  return ok();
+}
+
+int sparse_plan_destroy(sparse_plan_t plan) { return plan_destroy(plan); }
+
+int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
+  if (!plan || !out) return fail(SPARSE_EINVAL, "plan or out is NULL");
+  const srt::Plan& p = plan->p;
+  std::memset(out, 0, sizeof *out);
+  out->nnz = p.nnz;
+  out->plan_bytes = p.plan_bytes;
+  out->M = p.M;
+  out->K = p.K;
+  out->dtype = p.dtype;
+  out->kind = p.kind;
+  out->panels = p.npanels;
+  out->warps = p.warps;
+  out->rows_per_warp = p.R;
+  out->cols_per_lane = p.C;
+  out->n_tile = p.n_tile;
+  out->k_chunk = p.kind == SPARSE_CONV3X3 ? p.cc : p.kc;
+  out->chunks = p.nchunks;
+  out->split_k = p.gk;
+  out->smem_bytes = p.smem_bytes;
+  out->device = p.device;
+  out->conv_rows_per_tile = p.conv_rb;
+  out->conv_images_per_tile = p.conv_ipt;
+  out->max_panel_nnz = p.max_panel_nnz;
+  out->min_panel_nnz = p.min_panel_nnz;
+  out->build_ms = p.build_ms;
+  out->digest = p.digest;
+  return ok();
+}
+
+int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col, float* value,
+                     int32_t* panel, int32_t* chunk, int32_t* slot, int32_t* group) {
+  if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
+  const srt::Plan& p = plan->p;
+  if (cap < p.nnz) return fail(SPARSE_EINVAL, "cap < nnz");
+  const int hdr = ((p.Mp + 1) * 2 + 15) & ~15;
+  const bool f16 = p.dtype == SPARSE_F16;
+  int64_t out = 0;
+  for (int32_t q = 0; q < p.npanels; ++q) {
+    for (int32_t c = 0; c < p.nchunks; ++c) {
+      const uint8_t* blk = p.blob.data() + p.blk_off[(size_t)q * p.nchunks + c];
+      const uint16_t* soff = (const uint16_t*)blk;
+      const uint8_t* ents = blk + hdr;
+      for (int s = 0; s < p.Mp; ++s) {
+        const int beg = soff[s], end = soff[s + 1];
+        const int cnt = end - beg;
+        const int per = (cnt + p.gk - 1) / (p.gk > 0 ? p.gk : 1);
+        const int32_t m = p.row_id[(size_t)q * p.Mp + s];
+        for (int e = beg; e < end; ++e) {
+          if (out >= cap) return fail(SPARSE_EINTERNAL, "plan carries more entries than nnz");
+          const uint8_t* rec = ents + (size_t)e * p.entry_bytes;
+          int32_t k;
+          float w;
+          if (f16) {
+            uint16_t a, wh;
+            std::memcpy(&a, rec, 2);
+            std::memcpy(&wh, rec + 2, 2);
+            w = srt::f16_to_f32(wh);
+            if (p.kind == SPARSE_SPMM) {
+              k = c * p.kc + a;
+            } else {
+              k = -1;  // decoded below
+              const int off = (int16_t)a;
+              (void)off;
+            }
+          } else {
+            uint32_t a;
+            std::memcpy(&a, rec, 4);
+            std::memcpy(&w, rec + 4, 4);
+            k = p.kind == SPARSE_SPMM ? (int32_t)(c * p.kc + a) : -1;
+          }
+          if (p.kind == SPARSE_CONV3X3) {
+            int32_t off;
+            if (f16) {
+              int16_t o16;
+              std::memcpy(&o16, rec, 2);
+              off = o16;
+            } else {
+              std::memcpy(&off, rec, 4);
+            }
+            // invert off = ci*sci + (dy-1)*wp + (dx-1), |(dy-1)*wp + (dx-1)| <= wp + 1 < sci / 2
+            const int base = off + p.conv_wp + 1;  // = ci*sci + dy*wp + dx
+            const int ci = base / p.conv_sci;
+            const int rem = base - ci * p.conv_sci;
+            const int dy = rem / p.conv_wp, dx = rem % p.conv_wp;
+            k = (c * p.cc + ci) * 9 + dy * 3 + dx;
+          }
+          if (row) row[out] = m;
+          if (col) col[out] = k;
+          if (value) value[out] = w;
+          if (panel) panel[out] = q;
+          if (chunk) chunk[out] = c;
+          if (slot) slot[out] = s;
+          if (group) group[out] = per > 0 ? (e - beg) / per : 0;
+          ++out;
+        }
+      }
+    }
+  }
+  if (out != p.nnz) return fail(SPARSE_EINTERNAL, "plan entry count != nnz");
+  return ok();
+}
+
+const char* sparse_last_error(void) { return g_err.c_str(); }
+
+const char* sparse_version(void) { return "sparsert-b200 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,483 @@
+// Host-side inspector (offline; Sec. 2.3 P:71 "it can be done offline
+// at compile time as the sparse weight matrix is fully known").
+//
+// Steps:
+//  a1  CSR ingest + validation
+//  a2  row grouping + nnz-balanced row panels: the paper's block-level
+//      strategy (b) "assign different number of elements in M to different
+//      thread blocks to balance the number of nonzero values" (Fig. 2b).
+//      B200 variant: fixed panel height (Mp row slots), variable membership:
+//      rows sorted by nnz (desc, stable by id) are LPT-binned into panels, so
+//      no accumulator registers are wasted (the drawback named in P:165).
+//      Inside a panel the rows are LPT-binned again across the warps (thread
+//      groups).
+//  a3  split-K groups: each row's nonzeros of a chunk are cut into G_k
+//      contiguous k-ascending pieces, "each thread group except the last one
+//      processes the same number of non-zeros" (Fig. 3b); the cut is
+//      computed on device from the slot offsets, identically for every call.
+//  a4  K-chunking + packing: per (panel, chunk) one 16-byte aligned block
+//      (see plan.h) staged into shared memory beside its X tile.
+//  a5  tile-parameter selection (heuristic; the paper's autotuned parameters
+//      M_blocks, N_blocks, Gy).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <string>
+
+#include "plan.h"
+#include "../../include/sparsert.h"
+
+namespace srt {
+
+uint16_t f32_to_f16_rn(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const uint32_t sign = (x >> 16) & 0x8000u;
+  const uint32_t ax = x & 0x7fffffffu;
+  if (ax >= 0x7f800000u) {  // inf / nan
+    return (uint16_t)(sign | 0x7c00u | (ax > 0x7f800000u ? 0x200u : 0u));
+  }
+  if (ax >= 0x477ff000u) return (uint16_t)(sign | 0x7c00u);  // >= 65520 -> inf
+  if (ax < 0x33000000u) return (uint16_t)sign;               // < 2^-25 -> 0
+  int32_t e = (int32_t)(ax >> 23) - 127;
+  uint32_t m = (ax & 0x7fffffu) | 0x800000u;  // 24-bit significand
+  int32_t shift;
+  uint32_t base;
+  if (e < -14) {  // subnormal half: value = m * 2^(e-23); half unit = 2^-24
+    shift = -e - 14 + 13;  // bits to drop
+    base = 0;
+  } else {
+    shift = 13;
+    base = (uint32_t)(e + 15) << 10;
+    m &= 0x7fffffu;
+  }
+  uint32_t q = m >> shift;
+  const uint32_t rem = m & ((1u << shift) - 1u);
+  const uint32_t half = 1u << (shift - 1);
+  if (rem > half || (rem == half && (q & 1u))) q += 1;
+  return (uint16_t)(sign | (base + q));  // carry into exponent is correct IEEE behaviour
+}
+
+float f16_to_f32(uint16_t h) {
+  const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+  const uint32_t e = (h >> 10) & 0x1f, m = h & 0x3ffu;
+  float f;
+  if (e == 0) {
+    f = std::ldexp((float)m, -24);
+  } else if (e == 31) {
+    f = m ? NAN : INFINITY;
+  } else {
+    f = std::ldexp((float)(m | 0x400u), (int)e - 25);
+  }
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  x |= sign;
+  std::memcpy(&f, &x, 4);
+  return f;
+}
+
+static uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
+  const uint8_t* p = (const uint8_t*)data;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+static int pow2_ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+static int64_t align16(int64_t v) { return (v + 15) & ~int64_t(15); }
+
+namespace {
+struct Entry {
+  int32_t k;
+  float w;
+  uint16_t wh;
+};
+}  // namespace
+
+int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_ptr,
+               const int32_t* col_idx, const float* values, int32_t dtype,
+               const BuildOpts& o, std::string& err) {
+  const auto t0 = std::chrono::steady_clock::now();
+  char buf[256];
+  if (M < 1 || K < 1 || nnz < 0) {
+    err = "M and K must be >= 1 and nnz >= 0";
+    return SPARSE_EINVAL;
+  }
+  if (dtype != SPARSE_F32 && dtype != SPARSE_F16) {
+    err = "dtype must be SPARSE_F32 or SPARSE_F16";
+    return SPARSE_EINVAL;
+  }
+  if (o.kind != SPARSE_SPMM && o.kind != SPARSE_CONV3X3) {
+    err = "kind must be SPARSE_SPMM or SPARSE_CONV3X3";
+    return SPARSE_EINVAL;
+  }
+  if (!row_ptr || (nnz > 0 && (!col_idx || !values))) {
+    err = "null CSR array";
+    return SPARSE_EINVAL;
+  }
+  if (K > 65535) {
+    err = "K > 65535 is not supported";
+    return SPARSE_EUNSUPPORTED;
+  }
+  if (nnz > (int64_t)INT32_MAX) {
+    err = "nnz exceeds int32 range";
+    return SPARSE_EUNSUPPORTED;
+  }
+  if (o.kind == SPARSE_CONV3X3) {
+    if (o.c_in < 1 || o.h < 1 || o.w < 1) {
+      err = "conv plan needs c_in, h, w >= 1";
+      return SPARSE_EINVAL;
+    }
+    if ((int64_t)K != 9 * (int64_t)o.c_in) {
+      snprintf(buf, sizeof buf, "conv plan: K (%d) != 9*c_in (%d)", K, 9 * o.c_in);
+      err = buf;
+      return SPARSE_EUNSUPPORTED;
+    }
+  }
+
+  // ---------------- a1: validation ----------------
+  if (row_ptr[0] != 0) {
+    err = "row 0: row_ptr[0] != 0";
+    return SPARSE_EMATRIX;
+  }
+  for (int32_t m = 0; m < M; ++m) {
+    if (row_ptr[m + 1] < row_ptr[m]) {
+      snprintf(buf, sizeof buf, "row %d: row_ptr not monotone (%d > %d)", m, row_ptr[m],
+               row_ptr[m + 1]);
+      err = buf;
+      return SPARSE_EMATRIX;
+    }
+  }
+  if ((int64_t)row_ptr[M] != nnz) {
+    snprintf(buf, sizeof buf, "row %d: row_ptr[M] (%d) != nnz (%lld)", M, row_ptr[M],
+             (long long)nnz);
+    err = buf;
+    return SPARSE_EMATRIX;
+  }
+  std::vector<std::vector<Entry>> rows(M);
+  int64_t kept = 0;
+  for (int32_t m = 0; m < M; ++m) {
+    int32_t prev = -1;
+    for (int32_t e = row_ptr[m]; e < row_ptr[m + 1]; ++e) {
+      const int32_t k = col_idx[e];
+      const float v = values[e];
+      if (k < 0 || k >= K) {
+        snprintf(buf, sizeof buf, "row %d: col_idx %d out of [0,%d) at %d", m, k, K,
+                 e - row_ptr[m]);
+        err = buf;
+        return SPARSE_EMATRIX;
+      }
+      if (k <= prev) {
+        snprintf(buf, sizeof buf, "row %d: col_idx not strictly increasing at %d", m,
+                 e - row_ptr[m]);
+        err = buf;
+        return SPARSE_EMATRIX;
+      }
+      prev = k;
+      if (!std::isfinite(v)) {
+        snprintf(buf, sizeof buf, "row %d: non-finite value at %d", m, e - row_ptr[m]);
+        err = buf;
+        return SPARSE_EMATRIX;
+      }
+      uint16_t wh = 0;
+      float wv = v;
+      if (dtype == SPARSE_F16) {
+        wh = f32_to_f16_rn(v);
+        if ((wh & 0x7c00u) == 0x7c00u) {
+          snprintf(buf, sizeof buf, "row %d: value %g overflows fp16 at %d", m, (double)v,
+                   e - row_ptr[m]);
+          err = buf;
+          return SPARSE_EMATRIX;
+        }
+        wv = f16_to_f32(wh);
+      }
+      if (wv == 0.0f) {
+        if (o.drop_zeros) continue;
+        snprintf(buf, sizeof buf, "row %d: explicit zero%s at %d", m,
+                 v != 0.0f ? " (after fp16 rounding)" : "", e - row_ptr[m]);
+        err = buf;
+        return SPARSE_EMATRIX;
+      }
+      rows[m].push_back(Entry{k, wv, wh});
+      ++kept;
+    }
+  }
+
+  p = Plan();
+  p.M = M;
+  p.K = K;
+  p.dtype = dtype;
+  p.kind = o.kind;
+  p.nnz = kept;
+  p.n_hint = o.n_hint;
+  const bool f16 = dtype == SPARSE_F16;
+  const int S = f16 ? 2 : 4;
+  p.entry_bytes = f16 ? 4 : 8;
+
+  // ---------------- a5: tile parameters ----------------
+  const int kSM = 148;
+  if (o.kind == SPARSE_SPMM) {
+    p.C = f16 ? 8 : 4;  // 16 bytes of X per lane -> one 128-bit shared load
+    int gk = 1;
+    if (o.split_k) {
+      gk = o.split_k;
+    } else if (o.n_hint > 0) {
+      int L = pow2_ceil((int)((o.n_hint + p.C - 1) / p.C));
+      L = std::max(4, std::min(32, L));
+      gk = 32 / L;
+    }
+    if (gk != 1 && gk != 2 && gk != 4 && gk != 8) {
+      err = "split_k must be 1, 2, 4 or 8";
+      return SPARSE_EUNSUPPORTED;
+    }
+    p.gk = gk;
+    p.n_tile = (32 / gk) * p.C;
+    const int64_t nh = o.n_hint > 0 ? o.n_hint : 1024;
+    const int64_t ntiles = (nh + p.n_tile - 1) / p.n_tile;
+    p.warps = o.warps ? o.warps : 4;
+    if (o.rows_per_warp) {
+      p.R = o.rows_per_warp;
+    } else {
+      p.R = 1;
+      for (int R : {8, 4, 2}) {
+        const int64_t panels = (M + (int64_t)p.warps * R - 1) / ((int64_t)p.warps * R);
+        if (panels * ntiles >= 2 * kSM) {
+          p.R = R;
+          break;
+        }
+      }
+    }
+    if (o.k_chunk) {
+      if (o.k_chunk % 8 || o.k_chunk < 8 || o.k_chunk > 256) {
+        err = "k_chunk must be a multiple of 8 in [8, 256]";
+        return SPARSE_EUNSUPPORTED;
+      }
+      p.kc = o.k_chunk;
+    } else {
+      p.kc = 64;
+    }
+    if (K <= p.kc + p.kc / 2) p.kc = (int)std::min<int64_t>(256, (K + 7) / 8 * 8);
+    if (p.kc > 256) p.kc = 256;
+    p.nchunks = (K + p.kc - 1) / p.kc;
+    p.x_stage_bytes = p.kc * p.n_tile * S;
+  } else {
+    // implicit im2col conv: padded-position tiles
+    p.c_in = o.c_in;
+    p.h = o.h;
+    p.w = o.w;
+    p.gk = 1;
+    const int wp = o.w + 2;
+    p.conv_wp = wp;
+    const int kMaxPos = 256;  // 32 lanes x up to 8 positions
+    if (o.h * wp <= kMaxPos) {
+      p.conv_rb = o.h;
+      int ipt = std::max(1, kMaxPos / (o.h * wp));
+      if (o.n_hint > 0) ipt = (int)std::min<int64_t>(ipt, o.n_hint);
+      p.conv_ipt = ipt;
+    } else {
+      int rb = 0;
+      for (int d = 1; d <= o.h; ++d)
+        if (o.h % d == 0 && d * wp <= kMaxPos) rb = d;
+      if (rb == 0) {
+        snprintf(buf, sizeof buf, "conv: image width %d too large (W+2 > %d)", o.w, kMaxPos);
+        err = buf;
+        return SPARSE_EUNSUPPORTED;
+      }
+      p.conv_rb = rb;
+      p.conv_ipt = 1;
+    }
+    p.n_tile = p.conv_ipt * p.conv_rb * wp;
+    {
+      const int cp = (p.n_tile + 31) / 32;  // positions per lane, instantiated as 2, 4, 7 or 8
+      p.C = cp <= 2 ? 2 : cp <= 4 ? 4 : cp <= 7 ? 7 : 8;
+    }
+    p.conv_simg = (p.conv_rb + 2) * wp;
+    p.conv_sci = p.conv_ipt * p.conv_simg;
+    p.conv_guard = wp + 1;
+    int cc = o.k_chunk;
+    if (cc) {
+      if (cc < 1 || cc > 64) {
+        err = "conv k_chunk (channels per stage) must be in [1, 64]";
+        return SPARSE_EUNSUPPORTED;
+      }
+    } else {
+      cc = std::max(1, std::min(o.c_in, (f16 ? 16384 : 8192) / p.conv_sci));
+      cc = std::min(cc, 64);
+    }
+    if ((int64_t)cc * p.conv_sci + 2 * p.conv_guard > 32000) cc = std::max(1, (32000 - 2 * p.conv_guard) / p.conv_sci);
+    p.cc = cc;
+    p.kc = 9 * cc;
+    p.nchunks = (o.c_in + cc - 1) / cc;
+    p.conv_stage_elems = cc * p.conv_sci + 2 * p.conv_guard;
+    p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
+    const int64_t nb = o.n_hint > 0 ? o.n_hint : 64;
+    const int64_t ntiles = ((nb + p.conv_ipt - 1) / p.conv_ipt) * (o.h / p.conv_rb);
+    p.warps = o.warps ? o.warps : 4;
+    if (o.rows_per_warp) {
+      p.R = o.rows_per_warp;
+    } else {
+      p.R = 1;
+      for (int R : {8, 4, 2}) {
+        const int64_t panels = (M + (int64_t)p.warps * R - 1) / ((int64_t)p.warps * R);
+        if (panels * ntiles >= 2 * kSM) {
+          p.R = R;
+          break;
+        }
+      }
+    }
+  }
+  if (p.warps < 1 || p.warps > kMaxWarps) {
+    err = "warps must be in [1, 8]";
+    return SPARSE_EUNSUPPORTED;
+  }
+  if (p.R != 1 && p.R != 2 && p.R != 4 && p.R != 8) {
+    err = "rows_per_warp must be 1, 2, 4 or 8";
+    return SPARSE_EUNSUPPORTED;
+  }
+  p.Mp = p.warps * p.R;
+  p.npanels = (M + p.Mp - 1) / p.Mp;
+
+  // ---------------- a2: row grouping + LPT panels ----------------
+  std::vector<int32_t> order(M);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    return rows[a].size() > rows[b].size();
+  });
+  // min-heap over (panel nnz, panel id) among panels with free slots
+  using PI = std::pair<int64_t, int32_t>;
+  std::priority_queue<PI, std::vector<PI>, std::greater<PI>> heap;
+  for (int32_t q = 0; q < p.npanels; ++q) heap.push({0, q});
+  std::vector<std::vector<int32_t>> panel_rows(p.npanels);
+  std::vector<int64_t> panel_nnz(p.npanels, 0);
+  for (int32_t m : order) {
+    PI top = heap.top();
+    heap.pop();
+    const int32_t q = top.second;
+    panel_rows[q].push_back(m);
+    panel_nnz[q] += (int64_t)rows[m].size();
+    if ((int)panel_rows[q].size() < p.Mp) heap.push({panel_nnz[q], q});
+  }
+  p.max_panel_nnz = *std::max_element(panel_nnz.begin(), panel_nnz.end());
+  p.min_panel_nnz = *std::min_element(panel_nnz.begin(), panel_nnz.end());
+
+  // within a panel: LPT across warps (R slots each)
+  p.row_id.assign((size_t)p.npanels * p.Mp, -1);
+  for (int32_t q = 0; q < p.npanels; ++q) {
+    std::vector<int64_t> wl(p.warps, 0);
+    std::vector<int> wfill(p.warps, 0);
+    for (int32_t m : panel_rows[q]) {  // already in descending nnz order
+      int best = -1;
+      for (int wi = 0; wi < p.warps; ++wi) {
+        if (wfill[wi] >= p.R) continue;
+        if (best < 0 || wl[wi] < wl[best]) best = wi;
+      }
+      p.row_id[(size_t)q * p.Mp + best * p.R + wfill[best]] = m;
+      wfill[best]++;
+      wl[best] += (int64_t)rows[m].size();
+    }
+  }
+
+  // ---------------- a4: chunking + packing ----------------
+  const int hdr = (int)align16((int64_t)(p.Mp + 1) * 2);
+  p.blk_off.assign((size_t)p.npanels * p.nchunks + 1, 0);
+  p.blob.clear();
+  p.blob.reserve((size_t)(kept * p.entry_bytes + (int64_t)p.npanels * p.nchunks * (hdr + 16)));
+  std::vector<int32_t> cursor(M, 0);
+  std::vector<uint16_t> soff(p.Mp + 1);
+  std::vector<uint8_t> ents;
+  int64_t maxblk = 0;
+  for (int32_t q = 0; q < p.npanels; ++q) {
+    for (int32_t m : panel_rows[q]) cursor[m] = 0;
+    for (int32_t c = 0; c < p.nchunks; ++c) {
+      const int32_t k0 = c * p.kc, k1 = std::min(K, k0 + p.kc);
+      ents.clear();
+      int32_t cnt = 0;
+      for (int s = 0; s < p.Mp; ++s) {
+        soff[s] = (uint16_t)cnt;
+        const int32_t m = p.row_id[(size_t)q * p.Mp + s];
+        if (m < 0) continue;
+        auto& rr = rows[m];
+        int32_t& cur = cursor[m];
+        while (cur < (int32_t)rr.size() && rr[cur].k < k1) {
+          const Entry& en = rr[cur];
+          const int32_t kl = en.k - k0;
+          uint8_t rec[8];
+          if (o.kind == SPARSE_SPMM) {
+            if (f16) {
+              const uint16_t k16 = (uint16_t)kl;
+              std::memcpy(rec, &k16, 2);
+              std::memcpy(rec + 2, &en.wh, 2);
+            } else {
+              const uint32_t k32 = (uint32_t)kl;
+              std::memcpy(rec, &k32, 4);
+              std::memcpy(rec + 4, &en.w, 4);
+            }
+          } else {
+            const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
+            const int32_t off = ci * p.conv_sci + (dy - 1) * p.conv_wp + (dx - 1);
+            if (f16) {
+              const int16_t o16 = (int16_t)off;
+              std::memcpy(rec, &o16, 2);
+              std::memcpy(rec + 2, &en.wh, 2);
+            } else {
+              std::memcpy(rec, &off, 4);
+              std::memcpy(rec + 4, &en.w, 4);
+            }
+          }
+          ents.insert(ents.end(), rec, rec + p.entry_bytes);
+          ++cnt;
+          ++cur;
+        }
+      }
+      soff[p.Mp] = (uint16_t)cnt;
+      if (cnt > 65535) {
+        err = "internal: block entry count overflow";
+        return SPARSE_EINTERNAL;
+      }
+      const size_t start = p.blob.size();
+      p.blk_off[(size_t)q * p.nchunks + c] = (int64_t)start;
+      p.blob.resize(start + hdr, 0);
+      std::memcpy(p.blob.data() + start, soff.data(), (p.Mp + 1) * 2);
+      p.blob.insert(p.blob.end(), ents.begin(), ents.end());
+      p.blob.resize((size_t)align16((int64_t)p.blob.size()), 0);
+      maxblk = std::max<int64_t>(maxblk, (int64_t)(p.blob.size() - start));
+    }
+  }
+  p.blk_off[(size_t)p.npanels * p.nchunks] = (int64_t)p.blob.size();
+  if (p.blob.empty()) p.blob.resize(16, 0);
+  p.max_blk_bytes = (int32_t)maxblk;
+  p.stages = 2;
+  p.smem_bytes = p.stages * (p.x_stage_bytes + p.max_blk_bytes);
+  if (p.smem_bytes > 227 * 1024) {
+    snprintf(buf, sizeof buf, "plan needs %d bytes of shared memory (> 227 KB); lower k_chunk",
+             p.smem_bytes);
+    err = buf;
+    return SPARSE_EUNSUPPORTED;
+  }
+  p.plan_bytes = (int64_t)p.blob.size() + (int64_t)p.row_id.size() * 4 +
+                 (int64_t)p.blk_off.size() * 8;
+
+  uint64_t h = 1469598103934665603ull;
+  const int32_t cfg[] = {p.M, p.K, p.dtype, p.kind, p.c_in, p.h, p.w, p.warps, p.R, p.gk,
+                         p.C, p.n_tile, p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt};
+  h = fnv1a(h, cfg, sizeof cfg);
+  h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
+  h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);
+  h = fnv1a(h, p.blob.data(), p.blob.size());
+  p.digest = h;
+  p.build_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return SPARSE_OK;
+}
+
+}  // namespace srt

@@ -1,0 +1,108 @@
+// Internal plan representation shared by the host inspector (inspector.cpp),
+// the C ABI (capi.cpp) and the executor kernels (kernels.cu).
+//
+// A plan is the paper's compile-time artefact (Sec. 2.3, Sec. 3.4):
+// the sparse weight matrix after block-level load balancing (row panels,
+// strategy (b) of Fig. 2b), thread-group assignment (rows per warp,
+// optional split-K groups) and K-chunking, packed so that one
+// (panel, chunk) block is a single contiguous, 16-byte aligned byte range that
+// a CTA stages into shared memory next to the X tile it multiplies.
+//
+// Block layout (byte offsets relative to blob + blk_off[panel*nchunks+chunk]):
+//   uint16 slot_off[Mp+1]      entry index of each row slot's first entry,
+//                              relative to the block's entry array; slot s =
+//                              warp*R + r; padded to 16 bytes
+//   entries[slot_off[Mp]]      row-slot-major, k ascending within a slot
+//                              fp32 SpMM : {uint32 k_local; float w}     (8 B)
+//                              fp16 SpMM : {uint16 k_local; half  w}     (4 B)
+//                              fp32 conv : {int32 smem_off; float w}     (8 B)
+//                              fp16 conv : {int16 smem_off; half  w}     (4 B)
+//   zero padding to 16 bytes
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace srt {
+
+constexpr int kMaxWarps = 8;
+
+struct Plan {
+  // problem
+  int32_t M = 0, K = 0, dtype = 0, kind = 0;
+  int32_t c_in = 0, h = 0, w = 0;
+  int64_t nnz = 0;
+  int64_t n_hint = 0;
+
+  // tiling (thread block = `warps` thread groups of 32/gk lanes x gk groups)
+  int32_t warps = 4;     // warps per CTA
+  int32_t R = 4;         // row slots per warp
+  int32_t Mp = 16;       // rows per panel = warps * R
+  int32_t gk = 1;        // split-K groups per warp
+  int32_t C = 4;         // columns (SpMM) / positions (conv) per lane
+  int32_t n_tile = 128;  // columns per CTA (SpMM) / tile positions (conv)
+  int32_t kc = 64;       // K rows per chunk (SpMM) ; conv: K rows = 9 * cc
+  int32_t cc = 0;        // conv: input channels per chunk
+  int32_t nchunks = 1;
+  int32_t npanels = 1;
+  int32_t entry_bytes = 8;
+
+  // conv geometry (kind == CONV3X3)
+  int32_t conv_rb = 0;    // output rows per tile
+  int32_t conv_ipt = 0;   // images per tile
+  int32_t conv_wp = 0;    // padded row length W + 2
+  int32_t conv_simg = 0;  // smem elements per (ci, image) = (rb + 2) * wp
+  int32_t conv_sci = 0;   // smem elements per ci = ipt * simg
+  int32_t conv_guard = 0; // guard elements before/after the stage
+  int32_t conv_stage_elems = 0;
+
+  // packed plan (host copy)
+  std::vector<int32_t> row_id;   // npanels * Mp, -1 = empty slot
+  std::vector<int64_t> blk_off;  // npanels * nchunks + 1 byte offsets into blob
+  std::vector<uint8_t> blob;
+  int32_t max_blk_bytes = 0;
+  int32_t x_stage_bytes = 0;     // bytes of the staged X tile per stage
+  int32_t smem_bytes = 0;        // dynamic smem per CTA (all stages)
+  int32_t stages = 2;
+
+  // stats
+  int64_t max_panel_nnz = 0, min_panel_nnz = 0;
+  double build_ms = 0.0;
+  uint64_t digest = 0;
+
+  // device copy
+  int device = -1;
+  void* d_mem = nullptr;
+  const int32_t* d_row_id = nullptr;
+  const int64_t* d_blk_off = nullptr;
+  const uint8_t* d_blob = nullptr;
+  int64_t plan_bytes = 0;
+};
+
+struct BuildOpts {
+  int32_t kind = 0, c_in = 0, h = 0, w = 0;
+  int64_t n_hint = 0;
+  int32_t drop_zeros = 0;
+  int32_t warps = 0, rows_per_warp = 0, k_chunk = 0, split_k = 0;
+};
+
+// Inspector: validate the CSR (a1), group rows into nnz-balanced panels (a2),
+// choose split-K / chunking (a3, a5) and pack (a4).  Returns a sparse_status
+// code; on error `err` holds the detail.
+int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_ptr,
+               const int32_t* col_idx, const float* values, int32_t dtype,
+               const BuildOpts& o, std::string& err);
+
+// fp32 -> fp16 bits, round-to-nearest-even (host side, exact IEEE semantics).
+uint16_t f32_to_f16_rn(float f);
+float f16_to_f32(uint16_t h);
+
+// Device side (kernels.cu)
+int upload_plan(Plan& p, std::string& err);
+void free_plan_device(Plan& p);
+int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                void* stream, std::string& err);
+int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
+                   std::string& err);
+
+}  // namespace srt

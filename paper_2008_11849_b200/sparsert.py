@@ -1,0 +1,271 @@
+"""Thin ctypes binding of libsparsert.so (include/sparsert.h).
+
+Argument marshalling only: every step of the hot path runs in the library's CUDA
+kernels.  PyTorch is used for device memory and streams (tensors are passed as raw
+device pointers).  There is no CPU fallback: if the library is missing or fails to
+load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsparsert.so")
+
+SPARSE_OK, SPARSE_EINVAL, SPARSE_EMATRIX, SPARSE_EUNSUPPORTED = 0, 1, 2, 3
+SPARSE_ENOMEM, SPARSE_ECUDA, SPARSE_EINTERNAL = 4, 5, 6
+SPARSE_F32, SPARSE_F16 = 0, 1
+SPARSE_SPMM, SPARSE_CONV3X3 = 0, 1
+SPARSE_DEVICE_HOST_ONLY = -2
+
+STATUS_NAMES = {0: "SPARSE_OK", 1: "SPARSE_EINVAL", 2: "SPARSE_EMATRIX", 3: "SPARSE_EUNSUPPORTED",
+                4: "SPARSE_ENOMEM", 5: "SPARSE_ECUDA", 6: "SPARSE_EINTERNAL"}
+
+# every symbol include/sparsert.h declares (checked by tests/test_capi_host.py)
+EXPORTED = ["sparse_plan_opts_init", "sparse_plan_create", "sparse_spmm", "sparse_conv3x3",
+            "plan_destroy", "sparse_plan_destroy", "sparse_plan_info", "sparse_plan_dump",
+            "sparse_last_error", "sparse_version"]
+
+
+class SparseRTError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+class sparse_plan_opts(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("c_in", ctypes.c_int32), ("h", ctypes.c_int32),
+                ("w", ctypes.c_int32), ("n_hint", ctypes.c_int64), ("tune", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("drop_zeros", ctypes.c_int32),
+                ("warps", ctypes.c_int32), ("rows_per_warp", ctypes.c_int32),
+                ("k_chunk", ctypes.c_int32), ("split_k", ctypes.c_int32)]
+
+
+class sparse_plan_info_t(ctypes.Structure):
+    _fields_ = [("nnz", ctypes.c_int64), ("plan_bytes", ctypes.c_int64),
+                ("M", ctypes.c_int32), ("K", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("kind", ctypes.c_int32), ("panels", ctypes.c_int32), ("warps", ctypes.c_int32),
+                ("rows_per_warp", ctypes.c_int32), ("cols_per_lane", ctypes.c_int32),
+                ("n_tile", ctypes.c_int32), ("k_chunk", ctypes.c_int32),
+                ("chunks", ctypes.c_int32), ("split_k", ctypes.c_int32),
+                ("smem_bytes", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("conv_rows_per_tile", ctypes.c_int32), ("conv_images_per_tile", ctypes.c_int32),
+                ("max_panel_nnz", ctypes.c_int64), ("min_panel_nnz", ctypes.c_int64),
+                ("build_ms", ctypes.c_double), ("digest", ctypes.c_uint64)]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2008_11849_b200._build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.sparse_plan_opts_init.argtypes = [ctypes.POINTER(sparse_plan_opts)]
+    lib.sparse_plan_opts_init.restype = None
+    lib.sparse_plan_create.argtypes = [ctypes.POINTER(P), i32, i32, i64, P, P, P, i32,
+                                       ctypes.POINTER(sparse_plan_opts)]
+    lib.sparse_plan_create.restype = ctypes.c_int
+    lib.sparse_spmm.argtypes = [P, i64, P, i64, P, i64, P]
+    lib.sparse_spmm.restype = ctypes.c_int
+    lib.sparse_conv3x3.argtypes = [P, i64, P, P, P]
+    lib.sparse_conv3x3.restype = ctypes.c_int
+    lib.plan_destroy.argtypes = [P]
+    lib.plan_destroy.restype = ctypes.c_int
+    lib.sparse_plan_destroy.argtypes = [P]
+    lib.sparse_plan_destroy.restype = ctypes.c_int
+    lib.sparse_plan_info.argtypes = [P, ctypes.POINTER(sparse_plan_info_t)]
+    lib.sparse_plan_info.restype = ctypes.c_int
+    lib.sparse_plan_dump.argtypes = [P, i64, P, P, P, P, P, P, P]
+    lib.sparse_plan_dump.restype = ctypes.c_int
+    lib.sparse_last_error.argtypes = []
+    lib.sparse_last_error.restype = ctypes.c_char_p
+    lib.sparse_version.argtypes = []
+    lib.sparse_version.restype = ctypes.c_char_p
+    return lib
+
+
+lib = _load()
+
+
+def _check(rc: int):
+    if rc != SPARSE_OK:
+        raise SparseRTError(rc, lib.sparse_last_error().decode())
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ----------------------------------------------------------------------------- C names
+
+def sparse_plan_create(M, K, row_ptr, col_idx, values, dtype=SPARSE_F32, **opts) -> ctypes.c_void_p:
+    """Run the inspector and upload the plan; returns the opaque handle."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    o = sparse_plan_opts()
+    lib.sparse_plan_opts_init(ctypes.byref(o))
+    for k, val in opts.items():
+        if not hasattr(o, k):
+            raise TypeError(f"unknown plan option {k}")
+        setattr(o, k, int(val))
+    h = ctypes.c_void_p()
+    nnz = int(rp[-1]) if rp.size else 0
+    _check(lib.sparse_plan_create(ctypes.byref(h), int(M), int(K), nnz, _ptr(rp),
+                                  _ptr(ci) if ci.size else None, _ptr(v) if v.size else None,
+                                  int(dtype), ctypes.byref(o)))
+    return h
+
+
+def sparse_spmm(plan, N, X_ptr, ldx, Y_ptr, ldy, stream=0):
+    _check(lib.sparse_spmm(plan, int(N), X_ptr, int(ldx), Y_ptr, int(ldy), stream))
+
+
+def sparse_conv3x3(plan, batch, x_ptr, y_ptr, stream=0):
+    _check(lib.sparse_conv3x3(plan, int(batch), x_ptr, y_ptr, stream))
+
+
+def plan_destroy(plan):
+    _check(lib.plan_destroy(plan))
+
+
+def sparse_plan_info(plan) -> dict:
+    info = sparse_plan_info_t()
+    _check(lib.sparse_plan_info(plan, ctypes.byref(info)))
+    return {name: getattr(info, name) for name, _ in info._fields_}
+
+
+@dataclass
+class PlanDump:
+    row: np.ndarray
+    col: np.ndarray
+    value: np.ndarray
+    panel: np.ndarray
+    chunk: np.ndarray
+    slot: np.ndarray
+    group: np.ndarray
+
+
+def sparse_plan_dump(plan) -> PlanDump:
+    nnz = sparse_plan_info(plan)["nnz"]
+    arrs = [np.zeros(max(nnz, 1), np.int32) for _ in range(2)]
+    val = np.zeros(max(nnz, 1), np.float32)
+    more = [np.zeros(max(nnz, 1), np.int32) for _ in range(4)]
+    _check(lib.sparse_plan_dump(plan, max(nnz, 1), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(val),
+                                *[_ptr(a) for a in more]))
+    return PlanDump(arrs[0][:nnz], arrs[1][:nnz], val[:nnz], *[a[:nnz] for a in more])
+
+
+def version() -> str:
+    return lib.sparse_version().decode()
+
+
+# ----------------------------------------------------------------------------- torch API
+
+_TORCH_DT = {}
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t == torch.float32:
+        return SPARSE_F32
+    if t == torch.float16:
+        return SPARSE_F16
+    raise TypeError(f"unsupported dtype {t}")
+
+
+class Plan:
+    """Owning wrapper: Plan(csr_or_arrays, dtype=torch.float32, **opts).
+
+    `opts` are sparse_plan_opts fields (kind, c_in, h, w, n_hint, device, drop_zeros,
+    warps, rows_per_warp, k_chunk, split_k).  Use device=SPARSE_DEVICE_HOST_ONLY for an
+    inspect-only plan on a machine without a GPU.
+    """
+
+    def __init__(self, M, K, row_ptr, col_idx, values, dtype=None, **opts):
+        import torch
+        dtype = torch.float32 if dtype is None else dtype
+        self.dtype = dtype
+        self.M, self.K = int(M), int(K)
+        self.kind = int(opts.get("kind", SPARSE_SPMM))
+        self.conv_geom = (opts.get("c_in", 0), opts.get("h", 0), opts.get("w", 0))
+        self._h = sparse_plan_create(M, K, row_ptr, col_idx, values, _dtype_code(dtype), **opts)
+        self.info = sparse_plan_info(self._h)
+
+    @classmethod
+    def from_csr(cls, csr, dtype=None, **opts):
+        return cls(csr.M, csr.K, csr.row_ptr, csr.col_idx, csr.values, dtype=dtype, **opts)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            plan_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def dump(self) -> PlanDump:
+        return sparse_plan_dump(self._h)
+
+    def _check_tensor(self, t, name):
+        import torch
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.dtype != self.dtype:
+            raise TypeError(f"{name} dtype {t.dtype} != plan dtype {self.dtype}")
+        dev = self.info["device"]
+        if t.device.index != dev:
+            raise ValueError(f"{name} on {t.device}, plan on cuda:{dev}")
+
+    def spmm(self, X, Y=None, stream=None):
+        """Y[:, :N] = W @ X.  X: (K, N) CUDA tensor with unit column stride (row stride = ldx)."""
+        import torch
+        if self.kind != SPARSE_SPMM:
+            raise ValueError("spmm on a conv plan")
+        self._check_tensor(X, "X")
+        if X.dim() != 2 or X.shape[0] != self.K or (X.shape[1] > 1 and X.stride(1) != 1):
+            raise ValueError("X must be (K, N) with unit column stride")
+        N = X.shape[1]
+        if Y is None:
+            Y = torch.empty((self.M, N), dtype=self.dtype, device=X.device)
+        self._check_tensor(Y, "Y")
+        if Y.dim() != 2 or Y.shape[0] != self.M or Y.shape[1] != N or (N > 1 and Y.stride(1) != 1):
+            raise ValueError("Y must be (M, N) with unit column stride")
+        s = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        ldx = X.stride(0) if N > 0 else max(N, 1)
+        ldy = Y.stride(0) if N > 0 else max(N, 1)
+        sparse_spmm(self._h, N, ctypes.c_void_p(X.data_ptr()), max(ldx, N),
+                    ctypes.c_void_p(Y.data_ptr()), max(ldy, N), ctypes.c_void_p(s))
+        return Y
+
+    def conv3x3(self, x, y=None, stream=None):
+        """y = conv3x3(x), x: (C_in, B, H, W) contiguous CUDA tensor (CNHW)."""
+        import torch
+        if self.kind != SPARSE_CONV3X3:
+            raise ValueError("conv3x3 on an SpMM plan")
+        self._check_tensor(x, "x")
+        c_in, h, w = self.conv_geom
+        if x.dim() != 4 or tuple(x.shape[0:1]) + tuple(x.shape[2:]) != (c_in, h, w) or not x.is_contiguous():
+            raise ValueError(f"x must be contiguous (C_in={c_in}, B, H={h}, W={w})")
+        B = x.shape[1]
+        if y is None:
+            y = torch.empty((self.M, B, h, w), dtype=self.dtype, device=x.device)
+        self._check_tensor(y, "y")
+        if tuple(y.shape) != (self.M, B, h, w) or not y.is_contiguous():
+            raise ValueError("y must be contiguous (C_out, B, H, W)")
+        s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
+        sparse_conv3x3(self._h, B, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                       ctypes.c_void_p(s))
+        return y

@@ -1,0 +1,325 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (north star): rel-L2 <= 1e-5 for fp32 and <= 1e-2 for fp16 on
+generated inputs at 80/90/95/98% sparsity; BITWISE equality on integer-valued inputs
+(every fp32 partial sum exact) at the full BASELINE sizes; bitwise closed forms and
+invariances (W = 0, W = I, row selection, X = I_K, permutations, N-sharding).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import gen
+from sparsert_testutil import as_f16_f64
+
+import paper_2008_11849_b200 as srt
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-5
+F16_TOL = 1e-2
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _tdt(f16):
+    return torch.float16 if f16 else torch.float32
+
+
+def _w64(w, f16):
+    return as_f16_f64(w.values) if f16 else w.values.astype(np.float64)
+
+
+def _x64(x, f16):
+    return as_f16_f64(x) if f16 else x.astype(np.float64)
+
+
+def _run_spmm(w, X_np, f16, N=None, ld=None, ldy=None, **opts):
+    dev = _dev()
+    K, Ncols = X_np.shape
+    N = Ncols if N is None else N
+    plan = srt.Plan.from_csr(w, dtype=_tdt(f16), n_hint=opts.pop("n_hint", N), **opts)
+    X = torch.from_numpy(X_np).to(dev).to(_tdt(f16))
+    if ld is not None and ld != Ncols:
+        buf = torch.zeros((K, ld), dtype=_tdt(f16), device=dev)
+        buf[:, :Ncols] = X
+        X = buf[:, :N]
+    else:
+        X = X[:, :N]
+    if ldy is not None:
+        Ybuf = torch.full((w.M, ldy), float("nan"), dtype=_tdt(f16), device=dev)
+        Y = Ybuf[:, :N]
+    else:
+        Y = torch.full((w.M, N), float("nan"), dtype=_tdt(f16), device=dev)
+    plan.spmm(X, Y)
+    torch.cuda.synchronize()
+    return Y.float().cpu().numpy().astype(np.float64), plan
+
+
+def _ref(w, X_np, f16, N=None):
+    X = _x64(X_np, f16)
+    if N is not None:
+        X = X[:, :N]
+    y = oracle.spmm(w.M, w.K, w.row_ptr, w.col_idx, _w64(w, f16), X)
+    return y
+
+
+def _f16_round(y):
+    return y.astype(np.float16).astype(np.float64)
+
+
+# --------------------------------------------------------------------------- tolerance
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("p", [80, 90, 95, 98])
+@pytest.mark.parametrize("M,K,N", [(64, 64, 128), (300, 200, 517), (1000, 64, 49), (77, 1111, 300)])
+def test_spmm_rel_l2(M, K, N, p, f16):
+    w = gen.pruned_weights(M, K, p, seed=gen.case_seed(f"{M}x{K}x{N}", p))
+    X = gen.uniform_x(K, N, seed=N + p)
+    y, _ = _run_spmm(w, X, f16)
+    ref = _ref(w, X, f16)
+    err = oracle.rel_l2(y, ref)
+    assert err <= (F16_TOL if f16 else F32_TOL), err
+    if not f16:
+        assert err < 2e-6  # expected ~3e-7; catches gross order bugs
+
+
+# --------------------------------------------------------------------------- exactness
+
+def _exact_case(M, K, N, p, f16, seed, **kw):
+    vmax_w, vmax_x = (2, 4) if f16 else (3, 3)
+    w = gen.int_weights(M, K, p, seed=seed, vmax=vmax_w)
+    X = gen.int_x(K, N, seed=seed + 1, vmax=vmax_x)
+    y, plan = _run_spmm(w, X, f16, **kw)
+    ref = _ref(w, X, f16)
+    if f16:
+        ref = _f16_round(ref)
+    assert np.array_equal(y, ref), (np.argwhere(y != ref)[:5], plan.info)
+    return plan
+
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("case", [
+    (64, 256, 3136), (256, 64, 3136), (128, 512, 784), (512, 128, 784), (256, 1024, 196),
+    (1024, 256, 196), (512, 2048, 49), (2048, 512, 49),          # RN50 Table 1, batch 1
+    (2048, 512, 392), (512, 2048, 392),                           # RN50 p7/p8 batch 8
+    (64, 32, 12544), (1024, 1024, 49), (512, 512, 196),           # MobileNetV1
+    (3072, 768, 512), (768, 3072, 512),                           # BERT FC, 1x512
+])
+@pytest.mark.parametrize("p", [90, 95])
+def test_spmm_integer_exact_table_shapes(case, p, f16):
+    M, K, N = case
+    _exact_case(M, K, N, p, f16, seed=gen.case_seed(str(case), p))
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_spmm_integer_exact_bert_full(f16):
+    # BERT FC at N = 32 x 512 = 16384 (BASELINE configs[3] maximum), both orientations
+    for M, K in [(3072, 768), (768, 3072)]:
+        _exact_case(M, K, 16384, 90, f16, seed=M)
+
+
+# --------------------------------------------------------------------------- closed forms
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_closed_forms(f16):
+    dev = _dev()
+    K, N = 300, 777
+    X = gen.uniform_x(K, N, seed=3)
+    # W = 0 (nnz = 0) -> Y identically +0
+    z = gen.stress_pattern("empty", 50, K, seed=1)
+    y, _ = _run_spmm(z, X, f16)
+    assert np.array_equal(y, np.zeros_like(y)) and not np.signbit(y).any()
+    # W = I -> Y = X exactly
+    y, _ = _run_spmm(gen.identity_csr(K), X, f16)
+    assert np.array_equal(y, _x64(X, f16))
+    # row selection -> Y[m] = X[sigma(m)] exactly, with ragged N and ldx > N
+    s = gen.row_selection_csr(1000, K, seed=5)
+    y, _ = _run_spmm(s, X, f16, N=701, ld=777)
+    assert np.array_equal(y, _x64(X, f16)[s.col_idx][:, :701])
+    # X = I_K -> Y = dense(W) exactly: pins the position and value of every carried nonzero
+    w = gen.pruned_weights(513, K, 90, seed=6)
+    y, _ = _run_spmm(w, np.eye(K, dtype=np.float32), f16)
+    wd = gen.to_dense(w.with_values(_w64(w, f16).astype(np.float32)))
+    assert np.array_equal(y, wd)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_identity_full_size(f16):
+    # X = I_K tiled along N at a BERT size: every nonzero of a 3072 x 768 plan checked
+    w = gen.pruned_weights(3072, 768, 90, seed=7)
+    X = np.tile(np.eye(768, dtype=np.float32), (1, 3))
+    y, _ = _run_spmm(w, X, f16)
+    wd = gen.to_dense(w.with_values(_w64(w, f16).astype(np.float32)))
+    assert np.array_equal(y, np.tile(wd, (1, 3)))
+
+
+# --------------------------------------------------------------------------- invariances
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_permutation_and_sharding_invariance(f16):
+    rng = np.random.default_rng(0)
+    M, K, N = 700, 500, 1000
+    w = gen.pruned_weights(M, K, 90, seed=11)
+    X = gen.uniform_x(K, N, seed=12)
+    y, plan = _run_spmm(w, X, f16)
+    # column permutation of X -> column permutation of Y, bitwise
+    pc = rng.permutation(N)
+    y2, _ = _run_spmm(w, np.ascontiguousarray(X[:, pc]), f16, n_hint=N)
+    assert np.array_equal(y2, y[:, pc])
+    # row permutation of W -> row permutation of Y, bitwise
+    pr = rng.permutation(M)
+    d = gen.to_dense(w)[pr]
+    wp = gen.csr_from_mask(M, K, np.flatnonzero(d), d.astype(np.float32))
+    y3, _ = _run_spmm(wp, X, f16, n_hint=N)
+    assert np.array_equal(y3, y[pr])
+    # N-sharding: column slabs with the same plan -> concatenation bitwise equal
+    dev = _dev()
+    Xt = torch.from_numpy(X).to(dev).to(_tdt(f16))
+    parts = []
+    for a, b in [(0, 256), (256, 640), (640, 1000)]:
+        parts.append(plan.spmm(Xt[:, a:b].contiguous()).float().cpu().numpy())
+    assert np.array_equal(np.concatenate(parts, axis=1).astype(np.float64), y)
+    # determinism: repeated call bitwise identical
+    assert np.array_equal(plan.spmm(Xt).float().cpu().numpy().astype(np.float64), y)
+
+
+# --------------------------------------------------------------------------- edge cases
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("kind", ["zipf", "empty_rows", "dense_row", "block_dense", "one_column"])
+def test_stress_patterns(kind, f16):
+    M, K, N = 400, 600, 333
+    w = gen.stress_pattern(kind, M, K, seed=21)
+    X = gen.uniform_x(K, N, seed=22)
+    y, _ = _run_spmm(w, X, f16)
+    ref = _ref(w, X, f16)
+    assert oracle.rel_l2(y, ref) <= (F16_TOL if f16 else F32_TOL)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("N,ld,ldy", [(49, 49, 49), (49, 53, 51), (196, 196, 197), (1, 1, 1),
+                                      (130, 131, 130), (7, 8, 9)])
+def test_unaligned_and_tiny_n(N, ld, ldy, f16):
+    w = gen.int_weights(300, 257, 85, seed=N)
+    X = gen.int_x(257, ld, seed=N + 1, vmax=2)
+    y, _ = _run_spmm(w, X, f16, N=N, ld=ld, ldy=ldy)
+    ref = _ref(w, X, f16, N=N)
+    if f16:
+        ref = _f16_round(ref)
+    assert np.array_equal(y, ref)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("R,warps,kc,gk", [(1, 1, 8, 1), (2, 8, 16, 2), (8, 4, 256, 8), (4, 2, 40, 4)])
+def test_tile_overrides_exact(R, warps, kc, gk, f16):
+    _exact_case(333, 700, 250, 90, f16, seed=R * 10 + gk, rows_per_warp=R, warps=warps,
+                k_chunk=kc, split_k=gk)
+
+
+def test_api_errors_on_device():
+    dev = _dev()
+    w = gen.pruned_weights(64, 64, 90, seed=1)
+    plan = srt.Plan.from_csr(w)
+    with pytest.raises(ValueError):
+        plan.conv3x3(torch.zeros(1, 1, 3, 3, device=dev))
+    with pytest.raises(TypeError):
+        plan.spmm(torch.zeros(64, 8, device=dev, dtype=torch.float16))
+    # N = 0 is a no-op
+    plan.spmm(torch.zeros(64, 0, device=dev))
+    info = plan.info
+    assert info["device"] == 0 and info["plan_bytes"] > 0
+
+
+# --------------------------------------------------------------------------- conv
+
+def _conv_run(w, cin, x_np, f16, **opts):
+    dev = _dev()
+    C, B, H, W = x_np.shape
+    plan = srt.Plan.from_csr(w, dtype=_tdt(f16), kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W,
+                             n_hint=opts.pop("n_hint", B), **opts)
+    x = torch.from_numpy(x_np).to(dev).to(_tdt(f16)).contiguous()
+    y = plan.conv3x3(x)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy().astype(np.float64), plan
+
+
+def _conv_ref(w, x_np, f16):
+    return oracle.conv3x3(w.M, w.row_ptr, w.col_idx, _w64(w, f16), _x64(x_np, f16))
+
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("cin,cout,B,H,W,p", [(64, 64, 2, 56, 56, 90), (128, 128, 2, 28, 28, 90),
+                                              (256, 256, 3, 14, 14, 90), (512, 512, 2, 7, 7, 95),
+                                              (3, 5, 3, 5, 9, 50), (16, 40, 1, 1, 1, 80),
+                                              (8, 8, 5, 2, 3, 80)])
+def test_conv_rel_l2(cin, cout, B, H, W, p, f16):
+    w = gen.pruned_weights(cout, 9 * cin, p, seed=cin + H)
+    x = gen.relu_normal_x((cin, B, H, W), seed=B * H)
+    y, _ = _conv_run(w, cin, x, f16)
+    err = oracle.rel_l2(y, _conv_ref(w, x, f16))
+    assert err <= (F16_TOL if f16 else F32_TOL), err
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_conv_integer_exact_and_delta(f16):
+    cin, cout, B, H, W = 32, 48, 3, 14, 14
+    w = gen.int_weights(cout, 9 * cin, 80, seed=3, vmax=2)
+    x = gen.int_x(cin, B * H * W, seed=4, vmax=3).reshape(cin, B, H, W)
+    y, _ = _conv_run(w, cin, x, f16)
+    ref = _conv_ref(w, x, f16)
+    if f16:
+        ref = _f16_round(ref)
+    assert np.array_equal(y, ref)
+    # delta inputs at corners / edges / interior: exact taps (orientation + zero halo)
+    wd = gen.to_dense(w)
+    for (ci, b, y0, x0) in [(0, 0, 0, 0), (5, 2, H - 1, W - 1), (31, 1, 0, 7), (7, 0, 6, 0),
+                            (9, 1, 7, 8)]:
+        xd = np.zeros((cin, B, H, W), np.float32)
+        xd[ci, b, y0, x0] = 1.0
+        y, _ = _conv_run(w, cin, xd, f16)
+        exp = np.zeros((cout, B, H, W))
+        for dy in range(3):
+            for dx in range(3):
+                oy, ox = y0 - dy + 1, x0 - dx + 1
+                if 0 <= oy < H and 0 <= ox < W:
+                    exp[:, b, oy, ox] = wd[:, (ci * 3 + dy) * 3 + dx]
+        assert np.array_equal(y, exp)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_conv_center_tap_equals_spmm(f16):
+    # a W using only the center tap (dy = dx = 1) is a 1x1 conv: conv3x3 == spmm bitwise
+    cin, cout, B, H, W = 64, 96, 4, 14, 14
+    base = gen.pruned_weights(cout, cin, 80, seed=8)
+    w = gen.Csr(cout, 9 * cin, base.row_ptr, (base.col_idx * 9 + 4).astype(np.int32), base.values)
+    x = gen.relu_normal_x((cin, B, H, W), seed=9)
+    y, _ = _conv_run(w, cin, x, f16)
+    ys, _ = _run_spmm(base, x.reshape(cin, -1), f16)
+    assert np.array_equal(y.reshape(cout, -1), ys)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_conv_c5_full_batch_sampled(f16):
+    # BASELINE configs[4] at full size (256 ch, 14x14, batch 256, 90%), in the bench's launch
+    # configuration; integer data, images {0, 101, 255} checked bitwise against the oracle,
+    # and image-slab sharding (the N-sharded multi-GPU split) checked bitwise.
+    cin = cout = 256
+    B, H, W = 256, 14, 14
+    w = gen.int_weights(cout, 9 * cin, 90, seed=5, vmax=2)
+    x = gen.int_x(cin, B * H * W, seed=6, vmax=2).reshape(cin, B, H, W)
+    y, plan = _conv_run(w, cin, x, f16)
+    idx = [0, 101, 255]
+    ref = _conv_ref(w, np.ascontiguousarray(x[:, idx]), f16)
+    if f16:
+        ref = _f16_round(ref)
+    assert np.array_equal(y[:, idx], ref)
+    dev = _dev()
+    xt = torch.from_numpy(x).to(dev).to(_tdt(f16))
+    half = plan.conv3x3(xt[:, 128:].contiguous()).float().cpu().numpy()
+    assert np.array_equal(half.astype(np.float64), y[:, 128:])
