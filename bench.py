@@ -246,6 +246,9 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/dense/cpu legs (for ncu runs)")
+    ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--executor", type=int, default=1, choices=[0, 1],
+                    help="SpMM executor: 1 = JIT code generator (the paper's method), 0 = plan-driven")
     args = ap.parse_args()
     if args.warmup < 3 and not args.quick:
         args.warmup = 3
@@ -273,11 +276,11 @@ def main():
     for L in layers:
         w, x = make_inputs(L, args.sparsity, rank)
         if L["kind"] == "spmm":
-            p = srt.Plan.from_csr(w, dtype=tdt, n_hint=L["N"], device=local)
+            p = srt.Plan.from_csr(w, dtype=tdt, n_hint=L["N"], device=local, executor=args.executor)
         else:
             p = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=L["c_in"],
                                   h=L["H"], w=L["W"], n_hint=L["B"], device=local)
-        build_ms.append(p.info["build_ms"])
+        build_ms.append(round(p.info["build_ms"] + p.info["jit_compile_ms"], 1))
         X = torch.from_numpy(x).to(dev).to(tdt).contiguous()
         if L["kind"] == "spmm":
             Y = torch.empty((L["M"], L["N"]), dtype=tdt, device=dev)
@@ -289,7 +292,7 @@ def main():
         host.append(x)
     stream = torch.cuda.current_stream(dev)
 
-    def call(i, X=None, Y=None):
+    def call(i, X=None, Y=None, stream=stream):
         p, _ = plans[i]
         if layers[i]["kind"] == "spmm":
             p.spmm(xs[i] if X is None else X, ys[i] if Y is None else Y, stream=stream)
@@ -307,31 +310,60 @@ def main():
         for i in range(nl):
             call(i)
     torch.cuda.synchronize()
+
+    # One step = the nl executor launches, captured once in a CUDA graph (launch-bound layers
+    # would otherwise time the host), with external timing events between the launches so
+    # every kernel's duration is measured inside the timed region.
+    graph = None
+    gev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(nl + 1)]
+    if not args.eager:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            cur = torch.cuda.current_stream(dev)
+            gev[0].record(cur)
+            for i in range(nl):
+                call(i, stream=cur)
+                gev[i + 1].record(cur)
+        for _ in range(max(1, args.warmup // 2)):
+            flush.zero_()
+            graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
-    for s in range(args.steps):
-        flush.zero_()
-        ev[s][0].record(stream)
-        for i in range(nl):
-            call(i)
-            ev[s][i + 1].record(stream)
-    torch.cuda.synchronize()
+    step_ms, layer_acc = [], [0.0] * nl
+    if graph is not None:
+        for s in range(args.steps):
+            flush.zero_()
+            graph.replay()
+            torch.cuda.synchronize()
+            step_ms.append(gev[0].elapsed_time(gev[nl]))
+            for i in range(nl):
+                layer_acc[i] += gev[i].elapsed_time(gev[i + 1])
+    else:
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
+        for s in range(args.steps):
+            flush.zero_()
+            ev[s][0].record(stream)
+            for i in range(nl):
+                call(i)
+                ev[s][i + 1].record(stream)
+        torch.cuda.synchronize()
+        step_ms = [ev[s][0].elapsed_time(ev[s][nl]) for s in range(args.steps)]
+        for s in range(args.steps):
+            for i in range(nl):
+                layer_acc[i] += ev[s][i].elapsed_time(ev[s][i + 1])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
-    step_ms = [ev[s][0].elapsed_time(ev[s][nl]) for s in range(args.steps)]
-    layer_ms = [statistics.fmean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(args.steps))
-                for i in range(nl)]
+    layer_ms = [v / args.steps for v in layer_acc]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max = float(t.item())
-    value = flops_step * world * args.steps / (total_ms_max * 1e-3) / 1e9 if scaling == "weak" \
-        else flops_step * world * args.steps / (total_ms_max * 1e-3) / 1e9
+    value = flops_step * world * args.steps / (total_ms_max * 1e-3) / 1e9
     launches = args.steps * nl
 
     # ---------------- roofline of the dominant kernel (longest layer)
@@ -465,7 +497,9 @@ def main():
                        "description": desc, "sparsity_pct": args.sparsity,
                        "layers": [f"{L['M']}x{L['K']}xN{layer_N(L)}" for L in layers],
                        "l2": "flushed (256 MiB write) before every timed step, outside the events",
+                       "launch": "eager" if args.eager else "cuda-graph replay of the step",
                        "plan_build_ms": build_ms,
+                       "executor": "jit" if args.executor == 1 else "plan-driven",
                        "parallelism": f"N-sharded x{world}, replicated plan, no collective"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "layers": per_layer, "dense_baseline": dense,

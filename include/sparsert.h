@@ -40,7 +40,8 @@ enum sparse_status {
   SPARSE_EMATRIX = 2,      /* invalid CSR: row_ptr[0] != 0, row_ptr not monotone, row_ptr[M] != nnz,
                               col_idx out of [0,K), columns not strictly increasing within a row
                               (unsorted or duplicate), non-finite value, explicit zero (unless
-                              opts->drop_zeros), |value| > 65504 for an fp16 plan.  The detail
+                              opts->drop_zeros), a value that rounds to fp16 infinity
+                              (|value| >= 65520) for an fp16 plan.  The detail
                               names the row. */
   SPARSE_EUNSUPPORTED = 3, /* e.g. K > 65535, conv with K != 9*c_in, tile override out of range */
   SPARSE_ENOMEM = 4,       /* host or device allocation failed */
@@ -68,13 +69,24 @@ typedef struct {
                          requires a device and n_hint > 0 */
   int32_t device;     /* CUDA ordinal; -1 = current device; SPARSE_DEVICE_HOST_ONLY = no upload */
   int32_t drop_zeros; /* 0 = reject explicit zeros; 1 = drop them */
-  /* Tile overrides (0 = automatic).  None of these changes a result except split_k and
-     k_chunk, which fix the per-row summation order. */
+  /* Tile overrides (0 = automatic).  None of these changes a result except split_k,
+     k_chunk and k_split, which fix the per-row summation order. */
   int32_t warps;         /* warps per CTA (thread groups of the paper's block): 1..8 */
-  int32_t rows_per_warp; /* R: 1, 2, 4 or 8 */
+  int32_t rows_per_warp; /* R: 1, 2, 4, 8 or 16 (R * cols_per_lane <= 128) */
   int32_t k_chunk;       /* Kc: K rows staged per pipeline stage (SpMM: multiple of 8, 8..256);
                             conv: input channels per stage (1..64) */
   int32_t split_k;       /* G_k thread groups splitting each row's nonzeros: 1,2,4,8 */
+  int32_t k_split;       /* SpMM: CTAs of a thread-block cluster splitting the K chunks, partial
+                            tiles reduced in fixed rank order through distributed shared
+                            memory (the paper's strategy (a), Fig. 2a): 1,2,4,8 */
+  int32_t stages;        /* SpMM: X/plan pipeline stages (TMA + mbarrier ring): 1..4 */
+  int32_t executor;      /* SpMM: 0 = plan-driven kernels (default); 1 = JIT: the paper's code
+                            generator (Sec. 3.5) - per row panel, straight-line PTX with
+                            the weights as FFMA immediates, assembled in-process at plan creation
+                            (slow to create: seconds for 10^5 nonzeros).  X that is not 16-byte
+                            aligned falls back to the plan-driven kernels (same results, bitwise). */
+  int32_t jit_rows;      /* JIT: rows per panel (accumulator registers per thread), 0 = auto */
+  int32_t jit_warps;     /* JIT: warps per CTA (each owns 32 columns), 0 = auto */
 } sparse_plan_opts;
 
 /* Fill *opts with defaults (kind SPMM, device -1, everything else 0). */
@@ -127,11 +139,18 @@ typedef struct {
   int32_t k_chunk;      /* K rows per stage (conv: input channels per stage) */
   int32_t chunks;
   int32_t split_k;
+  int32_t k_split;      /* CTAs per cluster splitting K */
+  int32_t stages;
   int32_t smem_bytes;   /* dynamic shared memory per CTA */
   int32_t device;
   int32_t conv_rows_per_tile, conv_images_per_tile; /* conv tiling */
   int64_t max_panel_nnz, min_panel_nnz;            /* load-balance metrics */
   double build_ms;      /* host inspector wall time */
+  int32_t executor;     /* 0 plan-driven, 1 JIT */
+  int32_t jit_modules;  /* JIT: compiled modules (launches per call) */
+  int32_t jit_rows, jit_warps;
+  int64_t jit_cubin_bytes;
+  double jit_compile_ms;
   uint64_t digest;      /* FNV-1a of the packed plan: equal digests <=> identical replicas */
 } sparse_plan_info_t;
 

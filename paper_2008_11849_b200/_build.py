@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsparsert.so")
-SOURCES = ["inspector.cpp", "capi.cpp", "kernels.cu"]
+SOURCES = ["inspector.cpp", "capi.cpp", "kernels.cu", "jit.cpp"]
 HEADERS = [os.path.join(CSRC, "plan.h"), os.path.join(ROOT, "include", "sparsert.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -54,7 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(tmpdir, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
+                           "-L/usr/local/cuda/lib64", "-lnvptxcompiler_static", "-lpthread"])
     os.replace(tmp, LIB)
     return LIB
 

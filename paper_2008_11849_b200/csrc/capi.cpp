@@ -55,6 +55,12 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   bo.rows_per_warp = o.rows_per_warp;
   bo.k_chunk = o.k_chunk;
   bo.split_k = o.split_k;
+  bo.k_split = o.k_split;
+  bo.stages = o.stages;
+  bo.executor = o.executor;
+  bo.jit_rows = o.jit_rows;
+  bo.jit_warps = o.jit_warps;
+  if (o.stages < 0 || o.stages > 4) return fail(SPARSE_EUNSUPPORTED, "stages must be in [0, 4]");
   sparse_plan_s* h = nullptr;
   try {
     h = new sparse_plan_s();
@@ -72,6 +78,7 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
     rc = SPARSE_EINTERNAL;
     err = "unexpected exception in inspector";
   }
+  if (rc == SPARSE_OK && h->p.executor == 1) rc = srt::jit_compile(h->p, err);
   if (rc != SPARSE_OK) {
     delete h;
     return fail(rc, err);
@@ -86,7 +93,10 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
     }
     h->p.device = o.device;
     rc = srt::upload_plan(h->p, err);
+    if (rc == SPARSE_OK && h->p.executor == 1) rc = srt::jit_load(h->p, err);
     if (rc != SPARSE_OK) {
+      srt::jit_unload(h->p);
+      srt::free_plan_device(h->p);
       delete h;
       return fail(rc, err);
     }
@@ -105,7 +115,9 @@ int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void*
   if (!X || !Y) return fail(SPARSE_EINVAL, "X or Y is NULL");
   if (ldx < N || ldy < N) return fail(SPARSE_EINVAL, "ldx and ldy must be >= N");
   std::string err;
-  const int rc = srt::launch_spmm(plan->p, N, X, ldx, Y, ldy, stream, err);
+  const int rc = srt::jit_can_launch(plan->p, X, ldx)
+                     ? srt::jit_launch(plan->p, N, X, ldx, Y, ldy, stream, err)
+                     : srt::launch_spmm(plan->p, N, X, ldx, Y, ldy, stream, err);
   return rc == SPARSE_OK ? ok() : fail(rc, err);
 }
 
@@ -124,6 +136,7 @@ int sparse_conv3x3(sparse_plan_t plan, int64_t batch, const void* x, void* y,
 
 int plan_destroy(sparse_plan_t plan) {
   if (!plan) return ok();
+  srt::jit_unload(plan->p);
   srt::free_plan_device(plan->p);
   delete plan;
   return ok();
@@ -149,6 +162,8 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->k_chunk = p.kind == SPARSE_CONV3X3 ? p.cc : p.kc;
   out->chunks = p.nchunks;
   out->split_k = p.gk;
+  out->k_split = p.ks;
+  out->stages = p.stages;
   out->smem_bytes = p.smem_bytes;
   out->device = p.device;
   out->conv_rows_per_tile = p.conv_rb;
@@ -157,6 +172,12 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->min_panel_nnz = p.min_panel_nnz;
   out->build_ms = p.build_ms;
   out->digest = p.digest;
+  out->executor = p.executor;
+  out->jit_modules = (int32_t)p.jit.size();
+  out->jit_rows = p.jit_mp;
+  out->jit_warps = p.jit_warps;
+  out->jit_cubin_bytes = p.jit_cubin_bytes;
+  out->jit_compile_ms = p.jit_compile_ms;
   return ok();
 }
 
@@ -165,36 +186,32 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
   if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
   const srt::Plan& p = plan->p;
   if (cap < p.nnz) return fail(SPARSE_EINVAL, "cap < nnz");
-  const int hdr = ((p.Mp + 1) * 2 + 15) & ~15;
   const bool f16 = p.dtype == SPARSE_F16;
+  const int A = p.entry_align;
   int64_t out = 0;
   for (int32_t q = 0; q < p.npanels; ++q) {
     for (int32_t c = 0; c < p.nchunks; ++c) {
       const uint8_t* blk = p.blob.data() + p.blk_off[(size_t)q * p.nchunks + c];
-      const uint16_t* soff = (const uint16_t*)blk;
-      const uint8_t* ents = blk + hdr;
+      const uint32_t* shdr = (const uint32_t*)blk;
+      const uint8_t* ents = blk + p.hdr_bytes;
       for (int s = 0; s < p.Mp; ++s) {
-        const int beg = soff[s], end = soff[s + 1];
-        const int cnt = end - beg;
-        const int per = (cnt + p.gk - 1) / (p.gk > 0 ? p.gk : 1);
+        const int beg = (int)(shdr[s] & 0xffffu), cnt = (int)(shdr[s] >> 16);
+        const int end = beg + cnt;
+        // same cut as the executor: all groups but the last take per (a multiple of A)
+        int per = (cnt + p.gk - 1) / (p.gk > 0 ? p.gk : 1);
+        per = (per + A - 1) / A * A;
         const int32_t m = p.row_id[(size_t)q * p.Mp + s];
         for (int e = beg; e < end; ++e) {
           if (out >= cap) return fail(SPARSE_EINTERNAL, "plan carries more entries than nnz");
           const uint8_t* rec = ents + (size_t)e * p.entry_bytes;
-          int32_t k;
+          int32_t k = -1;  // conv: decoded below
           float w;
           if (f16) {
             uint16_t a, wh;
             std::memcpy(&a, rec, 2);
             std::memcpy(&wh, rec + 2, 2);
             w = srt::f16_to_f32(wh);
-            if (p.kind == SPARSE_SPMM) {
-              k = c * p.kc + a;
-            } else {
-              k = -1;  // decoded below
-              const int off = (int16_t)a;
-              (void)off;
-            }
+            if (p.kind == SPARSE_SPMM) k = c * p.kc + a;
           } else {
             uint32_t a;
             std::memcpy(&a, rec, 4);

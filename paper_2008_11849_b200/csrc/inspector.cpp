@@ -225,7 +225,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   p.entry_bytes = f16 ? 4 : 8;
 
   // ---------------- a5: tile parameters ----------------
-  const int kSM = 148;
+  const int kTargetCtas = 2 * 148;  // >= 2 waves on 148 SMs
+  p.entry_align = 16 / p.entry_bytes;
   if (o.kind == SPARSE_SPMM) {
     p.C = f16 ? 8 : 4;  // 16 bytes of X per lane -> one 128-bit shared load
     int gk = 1;
@@ -242,21 +243,6 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     }
     p.gk = gk;
     p.n_tile = (32 / gk) * p.C;
-    const int64_t nh = o.n_hint > 0 ? o.n_hint : 1024;
-    const int64_t ntiles = (nh + p.n_tile - 1) / p.n_tile;
-    p.warps = o.warps ? o.warps : 4;
-    if (o.rows_per_warp) {
-      p.R = o.rows_per_warp;
-    } else {
-      p.R = 1;
-      for (int R : {8, 4, 2}) {
-        const int64_t panels = (M + (int64_t)p.warps * R - 1) / ((int64_t)p.warps * R);
-        if (panels * ntiles >= 2 * kSM) {
-          p.R = R;
-          break;
-        }
-      }
-    }
     if (o.k_chunk) {
       if (o.k_chunk % 8 || o.k_chunk < 8 || o.k_chunk > 256) {
         err = "k_chunk must be a multiple of 8 in [8, 256]";
@@ -265,9 +251,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       p.kc = o.k_chunk;
     } else {
       p.kc = 64;
+      if (K <= 96) p.kc = (K + 7) / 8 * 8;
     }
-    if (K <= p.kc + p.kc / 2) p.kc = (int)std::min<int64_t>(256, (K + 7) / 8 * 8);
-    if (p.kc > 256) p.kc = 256;
     p.nchunks = (K + p.kc - 1) / p.kc;
     p.x_stage_bytes = p.kc * p.n_tile * S;
   } else {
@@ -311,39 +296,72 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
         return SPARSE_EUNSUPPORTED;
       }
     } else {
-      cc = std::max(1, std::min(o.c_in, (f16 ? 16384 : 8192) / p.conv_sci));
+      cc = std::max(1, std::min(o.c_in, (f16 ? 8192 : 4096) / p.conv_sci));
       cc = std::min(cc, 64);
     }
-    if ((int64_t)cc * p.conv_sci + 2 * p.conv_guard > 32000) cc = std::max(1, (32000 - 2 * p.conv_guard) / p.conv_sci);
+    if ((int64_t)cc * p.conv_sci + 2 * p.conv_guard > 32000)
+      cc = std::max(1, (32000 - 2 * p.conv_guard) / p.conv_sci);
     p.cc = cc;
     p.kc = 9 * cc;
     p.nchunks = (o.c_in + cc - 1) / cc;
     p.conv_stage_elems = cc * p.conv_sci + 2 * p.conv_guard;
     p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
-    const int64_t nb = o.n_hint > 0 ? o.n_hint : 64;
-    const int64_t ntiles = ((nb + p.conv_ipt - 1) / p.conv_ipt) * (o.h / p.conv_rb);
-    p.warps = o.warps ? o.warps : 4;
-    if (o.rows_per_warp) {
-      p.R = o.rows_per_warp;
-    } else {
-      p.R = 1;
-      for (int R : {8, 4, 2}) {
-        const int64_t panels = (M + (int64_t)p.warps * R - 1) / ((int64_t)p.warps * R);
-        if (panels * ntiles >= 2 * kSM) {
-          p.R = R;
-          break;
-        }
-      }
-    }
   }
+  p.warps = o.warps ? o.warps : 8;
   if (p.warps < 1 || p.warps > kMaxWarps) {
     err = "warps must be in [1, 8]";
     return SPARSE_EUNSUPPORTED;
   }
-  if (p.R != 1 && p.R != 2 && p.R != 4 && p.R != 8) {
-    err = "rows_per_warp must be 1, 2, 4 or 8";
+  {
+    int64_t ntiles;
+    if (o.kind == SPARSE_SPMM) {
+      const int64_t nh = o.n_hint > 0 ? o.n_hint : 4096;
+      ntiles = (nh + p.n_tile - 1) / p.n_tile;
+    } else {
+      const int64_t nb = o.n_hint > 0 ? o.n_hint : 64;
+      ntiles = ((nb + p.conv_ipt - 1) / p.conv_ipt) * (o.h / p.conv_rb);
+    }
+    // accumulators per thread: R * C fp32 registers; keep <= 64
+    const int rmax = 8;  // R * C <= 64 accumulators; Mp = 64 rows amortises X staging
+    const int max_ks = o.kind == SPARSE_SPMM ? std::min(8, p.nchunks) : 1;
+    int bestR = 1, bestKs = 1;
+    bool found = false;
+    for (int R = rmax; R >= 1 && !found; R /= 2) {
+      const int64_t panels = (M + (int64_t)p.warps * R - 1) / ((int64_t)p.warps * R);
+      for (int ks = 1; ks <= max_ks; ks *= 2) {
+        if (panels * ntiles * ks >= kTargetCtas) {
+          bestR = R;
+          bestKs = ks;
+          found = true;
+          break;
+        }
+      }
+    }
+    if (!found) {  // not enough work for two waves: maximise CTAs
+      bestR = 1;
+      bestKs = 1;
+      while (bestKs * 2 <= max_ks) bestKs *= 2;
+    }
+    p.R = o.rows_per_warp ? o.rows_per_warp : bestR;
+    p.ks = o.k_split ? o.k_split : (o.rows_per_warp ? 1 : bestKs);
+  }
+  if (p.R != 1 && p.R != 2 && p.R != 4 && p.R != 8 && p.R != 16) {
+    err = "rows_per_warp must be 1, 2, 4, 8 or 16";
     return SPARSE_EUNSUPPORTED;
   }
+  if (p.R * p.C > 128) {
+    err = "rows_per_warp too large for this dtype (accumulator registers)";
+    return SPARSE_EUNSUPPORTED;
+  }
+  if (p.ks != 1 && p.ks != 2 && p.ks != 4 && p.ks != 8) {
+    err = "k_split must be 1, 2, 4 or 8";
+    return SPARSE_EUNSUPPORTED;
+  }
+  if (p.ks > 1 && o.kind != SPARSE_SPMM) {
+    err = "k_split is only supported for SpMM plans";
+    return SPARSE_EUNSUPPORTED;
+  }
+  if (p.ks > p.nchunks) p.ks = 1 << (31 - __builtin_clz((unsigned)p.nchunks));
   p.Mp = p.warps * p.R;
   p.npanels = (M + p.Mp - 1) / p.Mp;
 
@@ -388,12 +406,18 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   }
 
   // ---------------- a4: chunking + packing ----------------
-  const int hdr = (int)align16((int64_t)(p.Mp + 1) * 2);
+  // header: uint32 per slot = start | count << 16 (entry indices relative to the block's
+  // entry array); every slot's entries start on a multiple of entry_align so that one
+  // 128-bit broadcast load yields entry_align entries.
+  const int hdr = (int)align16((int64_t)p.Mp * 4);
+  p.hdr_bytes = hdr;
+  const int A = p.entry_align;
   p.blk_off.assign((size_t)p.npanels * p.nchunks + 1, 0);
   p.blob.clear();
-  p.blob.reserve((size_t)(kept * p.entry_bytes + (int64_t)p.npanels * p.nchunks * (hdr + 16)));
+  p.blob.reserve((size_t)(kept * p.entry_bytes +
+                          (int64_t)p.npanels * p.nchunks * (hdr + 16 + p.Mp * 16)));
   std::vector<int32_t> cursor(M, 0);
-  std::vector<uint16_t> soff(p.Mp + 1);
+  std::vector<uint32_t> shdr(p.Mp);
   std::vector<uint8_t> ents;
   int64_t maxblk = 0;
   for (int32_t q = 0; q < p.npanels; ++q) {
@@ -403,61 +427,83 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       ents.clear();
       int32_t cnt = 0;
       for (int s = 0; s < p.Mp; ++s) {
-        soff[s] = (uint16_t)cnt;
-        const int32_t m = p.row_id[(size_t)q * p.Mp + s];
-        if (m < 0) continue;
-        auto& rr = rows[m];
-        int32_t& cur = cursor[m];
-        while (cur < (int32_t)rr.size() && rr[cur].k < k1) {
-          const Entry& en = rr[cur];
-          const int32_t kl = en.k - k0;
-          uint8_t rec[8];
-          if (o.kind == SPARSE_SPMM) {
-            if (f16) {
-              const uint16_t k16 = (uint16_t)kl;
-              std::memcpy(rec, &k16, 2);
-              std::memcpy(rec + 2, &en.wh, 2);
-            } else {
-              const uint32_t k32 = (uint32_t)kl;
-              std::memcpy(rec, &k32, 4);
-              std::memcpy(rec + 4, &en.w, 4);
-            }
-          } else {
-            const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
-            const int32_t off = ci * p.conv_sci + (dy - 1) * p.conv_wp + (dx - 1);
-            if (f16) {
-              const int16_t o16 = (int16_t)off;
-              std::memcpy(rec, &o16, 2);
-              std::memcpy(rec + 2, &en.wh, 2);
-            } else {
-              std::memcpy(rec, &off, 4);
-              std::memcpy(rec + 4, &en.w, 4);
-            }
-          }
-          ents.insert(ents.end(), rec, rec + p.entry_bytes);
+        while (cnt % A) {  // align the slot's first entry
+          ents.insert(ents.end(), (size_t)p.entry_bytes, (uint8_t)0);
           ++cnt;
-          ++cur;
         }
+        const int32_t start = cnt;
+        const int32_t m = p.row_id[(size_t)q * p.Mp + s];
+        if (m >= 0) {
+          auto& rr = rows[m];
+          int32_t& cur = cursor[m];
+          while (cur < (int32_t)rr.size() && rr[cur].k < k1) {
+            const Entry& en = rr[cur];
+            const int32_t kl = en.k - k0;
+            uint8_t rec[8];
+            if (o.kind == SPARSE_SPMM) {
+              if (f16) {
+                const uint16_t k16 = (uint16_t)kl;
+                std::memcpy(rec, &k16, 2);
+                std::memcpy(rec + 2, &en.wh, 2);
+              } else {
+                const uint32_t k32 = (uint32_t)kl;
+                std::memcpy(rec, &k32, 4);
+                std::memcpy(rec + 4, &en.w, 4);
+              }
+            } else {
+              const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
+              const int32_t off = ci * p.conv_sci + (dy - 1) * p.conv_wp + (dx - 1);
+              if (f16) {
+                const int16_t o16 = (int16_t)off;
+                std::memcpy(rec, &o16, 2);
+                std::memcpy(rec + 2, &en.wh, 2);
+              } else {
+                std::memcpy(rec, &off, 4);
+                std::memcpy(rec + 4, &en.w, 4);
+              }
+            }
+            ents.insert(ents.end(), rec, rec + p.entry_bytes);
+            ++cnt;
+            ++cur;
+          }
+        }
+        if (cnt > 65535) {
+          err = "internal: block entry count overflow (lower k_chunk)";
+          return SPARSE_EUNSUPPORTED;
+        }
+        shdr[s] = (uint32_t)start | ((uint32_t)(cnt - start) << 16);
       }
-      soff[p.Mp] = (uint16_t)cnt;
-      if (cnt > 65535) {
-        err = "internal: block entry count overflow";
-        return SPARSE_EINTERNAL;
-      }
-      const size_t start = p.blob.size();
-      p.blk_off[(size_t)q * p.nchunks + c] = (int64_t)start;
-      p.blob.resize(start + hdr, 0);
-      std::memcpy(p.blob.data() + start, soff.data(), (p.Mp + 1) * 2);
+      const size_t st = p.blob.size();
+      p.blk_off[(size_t)q * p.nchunks + c] = (int64_t)st;
+      p.blob.resize(st + hdr, 0);
+      std::memcpy(p.blob.data() + st, shdr.data(), (size_t)p.Mp * 4);
       p.blob.insert(p.blob.end(), ents.begin(), ents.end());
       p.blob.resize((size_t)align16((int64_t)p.blob.size()), 0);
-      maxblk = std::max<int64_t>(maxblk, (int64_t)(p.blob.size() - start));
+      maxblk = std::max<int64_t>(maxblk, (int64_t)(p.blob.size() - st));
     }
   }
   p.blk_off[(size_t)p.npanels * p.nchunks] = (int64_t)p.blob.size();
   if (p.blob.empty()) p.blob.resize(16, 0);
   p.max_blk_bytes = (int32_t)maxblk;
-  p.stages = 2;
-  p.smem_bytes = p.stages * (p.x_stage_bytes + p.max_blk_bytes);
+
+  // pipeline depth and shared memory
+  int stage_bytes = p.x_stage_bytes + p.max_blk_bytes;
+  if (o.kind == SPARSE_SPMM) {
+    stage_bytes = (stage_bytes + 127) & ~127;  // TMA destinations 128-byte aligned
+    // k_split == 1: persistent CTAs, the ring runs across tiles; k_split > 1: one tile
+    // per CTA, no point in more stages than chunks
+    const int per_chunks = (p.nchunks + p.ks - 1) / p.ks;
+    int stages = o.stages ? o.stages : 3;
+    if (p.ks > 1) stages = std::min(stages, per_chunks);
+    stages = std::max(1, stages);
+    p.stages = stages;
+    p.red_bytes = p.ks > 1 ? p.Mp * p.n_tile * 4 : 0;
+    p.smem_bytes = std::max(p.stages * stage_bytes, p.red_bytes) + 128;  // + mbarriers
+  } else {
+    p.stages = 2;
+    p.red_bytes = 0;
+    p.smem_bytes = p.stages * stage_bytes;
+  }
   if (p.smem_bytes > 227 * 1024) {
     snprintf(buf, sizeof buf, "plan needs %d bytes of shared memory (> 227 KB); lower k_chunk",
              p.smem_bytes);
@@ -467,9 +513,27 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   p.plan_bytes = (int64_t)p.blob.size() + (int64_t)p.row_id.size() * 4 +
                  (int64_t)p.blk_off.size() * 8;
 
+  if (o.executor == 1) {
+    if (o.kind != SPARSE_SPMM) {
+      err = "executor = JIT is only supported for SpMM plans";
+      return SPARSE_EUNSUPPORTED;
+    }
+    std::vector<std::vector<RowEntry>> re(M);
+    for (int32_t m = 0; m < M; ++m) {
+      re[m].reserve(rows[m].size());
+      for (const Entry& en : rows[m]) re[m].push_back(RowEntry{en.k, en.w});
+    }
+    const int rc = jit_generate(p, re, o, err);
+    if (rc != SPARSE_OK) return rc;
+  } else if (o.executor != 0) {
+    err = "executor must be 0 (plan-driven) or 1 (JIT)";
+    return SPARSE_EINVAL;
+  }
+
   uint64_t h = 1469598103934665603ull;
-  const int32_t cfg[] = {p.M, p.K, p.dtype, p.kind, p.c_in, p.h, p.w, p.warps, p.R, p.gk,
-                         p.C, p.n_tile, p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt};
+  const int32_t cfg[] = {p.M,  p.K,      p.dtype,   p.kind,    p.c_in,   p.h,
+                         p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
+                         p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

@@ -3,28 +3,41 @@
 // implicit-im2col 3x3 convolution variant (Sec. 3.6).
 //
 // Mapping of the paper's tiling (Sec. 3.3) onto the B200 kernel:
-//   thread block (M_blocks x N_blocks grid)  -> CTA (row panel, N tile)
+//   thread block (M_blocks x N_blocks grid)  -> CTA (row panel, N tile); with
+//        k_split > 1 a thread-block CLUSTER of k_split CTAs shares one
+//        (panel, N tile) and splits its K chunks ("different thread blocks can
+//        have different portions of the reduction axis", Fig. 2a)
 //   thread group of Gsy threads               -> warp (or 32/G_k-lane group)
 //   Gsy = N / N_blocks ("inner loop fixed to 1") -> lane owns C contiguous
 //        columns so every X access is one 128-bit shared-memory load
 //   ACC register array                        -> acc[R][C] fp32 registers,
 //        statically indexed (R unrolled), never local memory
-//   "Cache B[b, N_list]"                       -> X chunk staged in smem by
-//        cp.async (double buffered), shared by all rows of the panel
+//   "Cache B[b, N_list]"                       -> X chunk [Kc x N tile] staged
+//        in smem by TMA (cp.async.bulk.tensor) with the chunk's packed plan
+//        block (cp.async.bulk), an mbarrier ring filled by a producer warp
 //   A values "broadcast across the thread group" -> packed plan
-//        entries staged in smem and read with warp-uniform (broadcast) loads
+//        entries read with warp-uniform 128-bit broadcast shared loads
 //   reduction of group accumulators   -> fixed-order __shfl_xor tree
+//        inside a warp; fixed-rank-order sum over distributed shared memory
+//        across the CTAs of a cluster
 //   C written once per tile           -> one store per output, no atomics
+#include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <cstdio>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <string>
 
 #include "../../include/sparsert.h"
 #include "plan.h"
+
+namespace cg = cooperative_groups;
 
 namespace srt {
 
@@ -50,6 +63,51 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// mbarrier (shared::cta) primitives
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// TMA: 2-D tile of X (coordinates {n, k}) -> smem, completion on an mbarrier
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+// 1-D bulk copy global -> smem (16-byte multiple), completion on an mbarrier
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 // acc += w * x for fp16 w, x with the product exact in fp32 and an fp32
 // accumulator: mixed-precision FMA (sm_100 "fma.rn.f32.f16", SASS FHFMA).
 __device__ __forceinline__ void fma_h(float& acc, uint16_t w, uint16_t x) {
@@ -62,6 +120,82 @@ __device__ __forceinline__ void fma_h2(float& a0, float& a1, uint16_t w, uint32_
       : "h"(w), "r"(x2));
 }
 
+template <bool F16>
+struct EntryOps;
+
+template <>
+struct EntryOps<false> {  // {uint32 k_local, float w}; 2 per 16 bytes
+  static constexpr int EB = 8;
+  static constexpr int A = 2;
+  template <int C, int ROWB>
+  __device__ __forceinline__ static void run(float (&acc)[C], const uint8_t* ents, int beg,
+                                             int cnt, const uint8_t* xs) {
+    int e = 0;
+    for (; e + 4 <= cnt; e += 4) {
+      const uint4 p0 = *(const uint4*)(ents + (beg + e) * EB);
+      const uint4 p1 = *(const uint4*)(ents + (beg + e + 2) * EB);
+      const uint32_t k[4] = {p0.x, p0.z, p1.x, p1.z};
+      const uint32_t w[4] = {p0.y, p0.w, p1.y, p1.w};
+      float4 xv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) xv[j] = *(const float4*)(xs + k[j] * ROWB);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float wf = __uint_as_float(w[j]);
+        acc[0] = fmaf(wf, xv[j].x, acc[0]);
+        acc[1] = fmaf(wf, xv[j].y, acc[1]);
+        acc[2] = fmaf(wf, xv[j].z, acc[2]);
+        acc[3] = fmaf(wf, xv[j].w, acc[3]);
+      }
+    }
+    for (; e < cnt; ++e) {
+      const uint2 en = *(const uint2*)(ents + (beg + e) * EB);
+      const float4 xv = *(const float4*)(xs + en.x * ROWB);
+      const float wf = __uint_as_float(en.y);
+      acc[0] = fmaf(wf, xv.x, acc[0]);
+      acc[1] = fmaf(wf, xv.y, acc[1]);
+      acc[2] = fmaf(wf, xv.z, acc[2]);
+      acc[3] = fmaf(wf, xv.w, acc[3]);
+    }
+  }
+};
+
+template <>
+struct EntryOps<true> {  // {uint16 k_local, half w}; 4 per 16 bytes
+  static constexpr int EB = 4;
+  static constexpr int A = 4;
+  __device__ __forceinline__ static void one(float (&acc)[8], uint32_t en, const uint8_t* xs,
+                                             int ROWB) {
+    const uint4 xv = *(const uint4*)(xs + (en & 0xffffu) * ROWB);
+    const uint16_t w = (uint16_t)(en >> 16);
+    fma_h2(acc[0], acc[1], w, xv.x);
+    fma_h2(acc[2], acc[3], w, xv.y);
+    fma_h2(acc[4], acc[5], w, xv.z);
+    fma_h2(acc[6], acc[7], w, xv.w);
+  }
+  template <int C, int ROWB>
+  __device__ __forceinline__ static void run(float (&acc)[C], const uint8_t* ents, int beg,
+                                             int cnt, const uint8_t* xs) {
+    int e = 0;
+    for (; e + 4 <= cnt; e += 4) {
+      const uint4 q = *(const uint4*)(ents + (beg + e) * EB);
+      const uint32_t en[4] = {q.x, q.y, q.z, q.w};
+      uint4 xv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) xv[j] = *(const uint4*)(xs + (en[j] & 0xffffu) * ROWB);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint16_t w = (uint16_t)(en[j] >> 16);
+        fma_h2(acc[0], acc[1], w, xv[j].x);
+        fma_h2(acc[2], acc[3], w, xv[j].y);
+        fma_h2(acc[4], acc[5], w, xv[j].z);
+        fma_h2(acc[6], acc[7], w, xv[j].w);
+      }
+    }
+    for (; e < cnt; ++e) one(acc, *(const uint32_t*)(ents + (beg + e) * EB), xs, ROWB);
+  }
+};
+
 // ------------------------------------------------------------------ SpMM
 struct SpmmArgs {
   const uint8_t* blob;
@@ -70,192 +204,260 @@ struct SpmmArgs {
   const uint8_t* X;
   uint8_t* Y;
   int64_t ldx, ldy, N;
-  int32_t K, kc, nchunks, Mp;
-  int32_t x_stage_bytes, stage_bytes, hdr_bytes;
-  int32_t vec_x, vec_y;
+  int32_t K, kc, nchunks, Mp, ks, stages, npanels;
+  int32_t x_stage_bytes, stage_bytes, hdr_bytes, bar_off;
+  int32_t use_tma, vec_y;
 };
 
 template <int R, int GK, bool F16>
-__global__ void __launch_bounds__(256) spmm_kernel(const SpmmArgs a) {
-  constexpr int C = F16 ? 8 : 4;   // columns per lane (16 bytes of X)
-  constexpr int S = F16 ? 2 : 4;   // element bytes
-  constexpr int L = 32 / GK;       // lanes per thread group
-  constexpr int NT = L * C;        // columns per CTA
-  constexpr int ROWB = NT * S;     // bytes per staged X row
-  constexpr int SEG = ROWB / 16;   // 16-byte segments per staged X row
-  constexpr int EB = F16 ? 4 : 8;  // plan entry bytes
-  extern __shared__ __align__(16) uint8_t smem[];
+__global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                   const SpmmArgs a) {
+  constexpr int C = F16 ? 8 : 4;  // columns per lane (16 bytes of X)
+  constexpr int S = F16 ? 2 : 4;  // element bytes
+  constexpr int L = 32 / GK;      // lanes per thread group
+  constexpr int NT = L * C;       // columns per CTA
+  constexpr int ROWB = NT * S;    // bytes per staged X row
+  using E = EntryOps<F16>;
+  extern __shared__ __align__(1024) uint8_t smem[];
 
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const int nwarps = (blockDim.x >> 5) - 1;  // consumer warps; warp `nwarps` is the producer
   const int g = lane / L, li = lane % L;
-  const int panel = blockIdx.x;
-  const int64_t n0 = (int64_t)blockIdx.y * NT;
-  const int ncol = (int)min((int64_t)NT, a.N - n0);
+  const int col = li * C;
+  // Work decomposition.  k_split == 1: persistent CTAs walk the (panel, N tile) tiles
+  // t = blockIdx.x + j * gridDim.x with the panel index fastest, so CTAs running together
+  // read the same X tile (L2 reuse) and the producer prefetches across tile boundaries.
+  // k_split > 1: one tile per cluster; CTA rank r of the cluster takes chunk slice r.
+  const bool persistent = a.ks == 1;
+  const int rank = persistent ? 0 : (int)(blockIdx.x % a.ks);
+  const int64_t ntn = (a.N + NT - 1) / NT;
+  const int64_t ntiles = persistent ? (int64_t)a.npanels * ntn : 1;
+  const int64_t t_begin = persistent ? (int64_t)blockIdx.x : 0;
+  const int64_t t_step = persistent ? (int64_t)gridDim.x : 1;
+  const int cps = (a.nchunks + a.ks - 1) / a.ks;
+  const int c_begin = rank * cps;
+  const int nloc = max(0, min(a.nchunks, c_begin + cps) - c_begin);
+  auto tile_coords = [&](int64_t t, int& panel, int64_t& n0) {
+    if (persistent) {
+      panel = (int)(t % a.npanels);
+      n0 = (t / a.npanels) * NT;
+    } else {
+      panel = (int)(blockIdx.x / a.ks);
+      n0 = (int64_t)blockIdx.y * NT;
+    }
+  };
+  const uint32_t full0 = smem_u32(smem + a.bar_off);
+  const uint32_t empty0 = full0 + 8 * 4;
+
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(full0 + 8 * s, a.use_tma ? 1 : 33);
+      mbar_init(empty0 + 8 * s, nwarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
 
   float acc[R][C];
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
 
-  auto stage = [&](int chunk, int buf) {
-    uint8_t* st = smem + buf * a.stage_bytes;
-    const int64_t bi = (int64_t)panel * a.nchunks + chunk;
-    const int64_t b0 = a.blk_off[bi];
-    const int nb = (int)((a.blk_off[bi + 1] - b0) >> 4);
-    const uint32_t dblk = smem_u32(st + a.x_stage_bytes);
-    for (int i = tid; i < nb; i += nthr) cp_async16(dblk + 16 * i, a.blob + b0 + 16 * i, 16);
-    const int k0 = chunk * a.kc;
-    const int kr = min(a.kc, a.K - k0);
-    if (a.vec_x) {
-      const int total = kr * SEG;
-      for (int i = tid; i < total; i += nthr) {
-        const int r = i / SEG, s = i % SEG;
-        const int64_t n = n0 + s * (16 / S);
-        const int64_t rem = (a.N - n) * S;
-        const int bytes = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
-        const uint8_t* gp = bytes > 0 ? a.X + ((int64_t)(k0 + r) * a.ldx + n) * S : a.X;
-        cp_async16(smem_u32(st + r * ROWB + s * 16), gp, bytes);
-      }
-    } else {
-      const int total = kr * NT;
-      for (int i = tid; i < total; i += nthr) {
-        const int r = i / NT, cc = i % NT;
-        const int64_t n = n0 + cc;
-        const uint8_t* gp = a.X + ((int64_t)(k0 + r) * a.ldx + n) * S;
-        if (F16) {
-          uint16_t v = 0;
-          if (n < a.N) v = __ldg((const unsigned short*)gp);
-          *(uint16_t*)(st + r * ROWB + cc * 2) = v;
+  // Y[row][n0 + col ...] <- acc (fp16: RN once), group-0 lanes only
+  auto store_tile = [&](int panel, int64_t n0, const int (&rows)[R]) {
+    const int ncol = (int)min((int64_t)NT, a.N - n0);
+    if (g != 0 || col >= ncol) return;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = rows[r];
+      if (row < 0) continue;
+      uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + col) * S;
+      if (F16) {
+        __half h[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) h[c] = __float2half_rn(acc[r][c]);
+        if (a.vec_y && col + C <= ncol) {
+          *(uint4*)yp = *(const uint4*)h;
         } else {
-          cp_async4(smem_u32(st + r * ROWB + cc * 4), n < a.N ? gp : a.X, n < a.N ? 4 : 0);
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (col + c < ncol) ((__half*)yp)[c] = h[c];
+        }
+      } else {
+        if (a.vec_y && col + C <= ncol) {
+          *(float4*)yp = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (col + c < ncol) ((float*)yp)[c] = acc[r][c];
         }
       }
     }
   };
 
-  stage(0, 0);
-  cp_async_commit();
-  for (int c = 0; c < a.nchunks; ++c) {
-    if (c + 1 < a.nchunks) {
-      stage(c + 1, (c + 1) & 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+  if (warp == nwarps) {
+    // ---------------- producer warp: TMA X tile + bulk plan block per chunk, running
+    // ahead of the consumers by up to `stages` chunks (across tile boundaries)
+    int i = 0;
+    for (int64_t t = t_begin; t < ntiles; t += t_step) {
+      int panel;
+      int64_t n0;
+      tile_coords(t, panel, n0);
+      for (int j = 0; j < nloc; ++j, ++i) {
+        const int c = c_begin + j;
+        const int s = i % a.stages;
+        if (i >= a.stages) mbar_wait(empty0 + 8 * s, ((i / a.stages) - 1) & 1);
+        uint8_t* st = smem + s * a.stage_bytes;
+        const int64_t bi = (int64_t)panel * a.nchunks + c;
+        const int64_t b0 = a.blk_off[bi];
+        const uint32_t bbytes = (uint32_t)(a.blk_off[bi + 1] - b0);
+        const uint32_t fb = full0 + 8 * s;
+        if (a.use_tma) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(fb, (uint32_t)a.x_stage_bytes + bbytes);
+            tma_load_2d(smem_u32(st), &tmap, (int)n0, c * a.kc, fb);
+            bulk_load(smem_u32(st + a.x_stage_bytes), a.blob + b0, bbytes, fb);
+          }
+        } else {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(fb, bbytes);
+            bulk_load(smem_u32(st + a.x_stage_bytes), a.blob + b0, bbytes, fb);
+          }
+          const int k0 = c * a.kc;
+          const int kr = min(a.kc, a.K - k0);
+          const int total = kr * NT;
+          for (int idx = lane; idx < total; idx += 32) {
+            const int r = idx / NT, cc = idx % NT;
+            const int64_t n = n0 + cc;
+            const uint8_t* gp = a.X + ((int64_t)(k0 + r) * a.ldx + n) * S;
+            if (F16) {
+              uint16_t v = 0;
+              if (n < a.N) v = __ldg((const unsigned short*)gp);
+              *(uint16_t*)(st + r * ROWB + cc * 2) = v;
+            } else {
+              cp_async4(smem_u32(st + r * ROWB + cc * 4), n < a.N ? gp : a.X, n < a.N ? 4 : 0);
+            }
+          }
+          if (F16)
+            mbar_arrive(fb);
+          else
+            cp_async_mbar_arrive_noinc(fb);
+        }
+      }
     }
-    __syncthreads();
-    const uint8_t* st = smem + (c & 1) * a.stage_bytes;
-    const uint8_t* xs = st + li * (C * S);
-    const uint16_t* soff = (const uint16_t*)(st + a.x_stage_bytes);
-    const uint8_t* ents = st + a.x_stage_bytes + a.hdr_bytes;
+  } else {
+    // ---------------- consumer warps: Alg. 3 over each staged chunk
+    int i = 0;
+    for (int64_t t = t_begin; t < ntiles; t += t_step) {
+      int panel;
+      int64_t n0;
+      tile_coords(t, panel, n0);
+      int rows[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) rows[r] = a.row_id[(int64_t)panel * a.Mp + warp * R + r];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+      for (int j = 0; j < nloc; ++j, ++i) {
+        const int s = i % a.stages;
+        mbar_wait(full0 + 8 * s, (i / a.stages) & 1);
+        const uint8_t* st = smem + s * a.stage_bytes;
+        const uint8_t* xs = st + li * (C * S);
+        const uint32_t* shdr = (const uint32_t*)(st + a.x_stage_bytes);
+        const uint8_t* ents = st + a.x_stage_bytes + a.hdr_bytes;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t h = shdr[warp * R + r];
+          int beg = (int)(h & 0xffffu);
+          int cnt = (int)(h >> 16);
+          if (GK > 1) {  // contiguous k-ascending pieces, all but the last of equal size
+            int per = (cnt + GK - 1) / GK;
+            per = (per + E::A - 1) / E::A * E::A;
+            const int lo = min(g * per, cnt);
+            const int hi = min(lo + per, cnt);
+            beg += lo;
+            cnt = hi - lo;
+          }
+          E::template run<C, ROWB>(acc[r], ents, beg, cnt, xs);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * s);
+      }
+      // cross-group reduction inside the warp: fixed binary tree over group index
+      if (GK > 1) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int off = 16; off >= L; off >>= 1)
+              acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], off);
+      }
+      if (persistent) store_tile(panel, n0, rows);
+    }
+  }
+  if (persistent) return;
+
+  int panel;
+  int64_t n0;
+  tile_coords(0, panel, n0);
+  const int ncol = (int)min((int64_t)NT, a.N - n0);
+  // ---------------- k_split > 1: partial tiles reduced across the cluster through DSMEM,
+  // summed in rank order 0, 1, ..., ks-1 for every output (deterministic).
+  __syncthreads();  // every consumer is done with the stage buffers that `red` overlays
+  float* red = (float*)smem;  // [Mp][NT] fp32
+  if (warp < nwarps && g == 0) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int slot = warp * R + r;
-      int beg = soff[slot];
-      int end = soff[slot + 1];
-      if (GK > 1) {  // contiguous k-ascending pieces, all but the last of equal size
-        const int cnt = end - beg;
-        const int per = (cnt + GK - 1) / GK;
-        const int lo = min(g * per, cnt);
-        const int hi = min(lo + per, cnt);
-        end = beg + hi;
-        beg = beg + lo;
-      }
-      int e = beg;
-      if (!F16) {
-        for (; e + 4 <= end; e += 4) {
-          uint2 en[4];
-          float4 xv[4];
+      float* dst = red + (warp * R + r) * NT + col;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) en[j] = *(const uint2*)(ents + (e + j) * EB);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) xv[j] = *(const float4*)(xs + en[j].x * ROWB);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float w = __uint_as_float(en[j].y);
-            acc[r][0] = fmaf(w, xv[j].x, acc[r][0]);
-            acc[r][1] = fmaf(w, xv[j].y, acc[r][1]);
-            acc[r][2] = fmaf(w, xv[j].z, acc[r][2]);
-            acc[r][3] = fmaf(w, xv[j].w, acc[r][3]);
-          }
-        }
-        for (; e < end; ++e) {
-          const uint2 en = *(const uint2*)(ents + e * EB);
-          const float4 xv = *(const float4*)(xs + en.x * ROWB);
-          const float w = __uint_as_float(en.y);
-          acc[r][0] = fmaf(w, xv.x, acc[r][0]);
-          acc[r][1] = fmaf(w, xv.y, acc[r][1]);
-          acc[r][2] = fmaf(w, xv.z, acc[r][2]);
-          acc[r][3] = fmaf(w, xv.w, acc[r][3]);
-        }
-      } else {
-        for (; e + 4 <= end; e += 4) {
-          uint32_t en[4];
-          uint4 xv[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) en[j] = *(const uint32_t*)(ents + (e + j) * EB);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) xv[j] = *(const uint4*)(xs + (en[j] & 0xffffu) * ROWB);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint16_t w = (uint16_t)(en[j] >> 16);
-            fma_h2(acc[r][0], acc[r][1], w, xv[j].x);
-            fma_h2(acc[r][2], acc[r][3], w, xv[j].y);
-            fma_h2(acc[r][4], acc[r][5], w, xv[j].z);
-            fma_h2(acc[r][6], acc[r][7], w, xv[j].w);
-          }
-        }
-        for (; e < end; ++e) {
-          const uint32_t en = *(const uint32_t*)(ents + e * EB);
-          const uint4 xv = *(const uint4*)(xs + (en & 0xffffu) * ROWB);
-          const uint16_t w = (uint16_t)(en >> 16);
-          fma_h2(acc[r][0], acc[r][1], w, xv.x);
-          fma_h2(acc[r][2], acc[r][3], w, xv.y);
-          fma_h2(acc[r][4], acc[r][5], w, xv.z);
-          fma_h2(acc[r][6], acc[r][7], w, xv.w);
-        }
-      }
+      for (int c = 0; c < C; c += 4)
+        *(float4*)(dst + c) = make_float4(acc[r][c], acc[r][c + 1], acc[r][c + 2], acc[r][c + 3]);
     }
-    __syncthreads();
   }
-
-  // cross-group reduction: fixed binary tree over group index, no atomics
-  if (GK > 1) {
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < C; ++c)
-#pragma unroll
-        for (int off = 16; off >= L; off >>= 1)
-          acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], off);
-  }
-  if (g != 0) return;
-  const int col = li * C;
-  if (col >= ncol) return;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int row = a.row_id[(int64_t)panel * a.Mp + warp * R + r];
-    if (row < 0) continue;
-    uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + col) * S;
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();
+  const int rows_per_rank = (a.Mp + a.ks - 1) / a.ks;
+  const int s0 = rank * rows_per_rank;
+  const int s1 = min(a.Mp, s0 + rows_per_rank);
+  const int items = (s1 - s0) * (NT / 4);
+  for (int it = tid; it < items; it += blockDim.x) {
+    const int slot = s0 + it / (NT / 4);
+    const int c4 = (it % (NT / 4)) * 4;
+    const int row = a.row_id[(int64_t)panel * a.Mp + slot];
+    if (row < 0 || c4 >= ncol) continue;
+    float4 v = *(const float4*)(cluster.map_shared_rank(red, 0) + slot * NT + c4);
+    for (int q = 1; q < a.ks; ++q) {
+      const float4 u = *(const float4*)(cluster.map_shared_rank(red, q) + slot * NT + c4);
+      v.x += u.x;
+      v.y += u.y;
+      v.z += u.z;
+      v.w += u.w;
+    }
+    uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + c4) * S;
+    const float vv[4] = {v.x, v.y, v.z, v.w};
     if (F16) {
-      __half h[C];
+      __half h[4];
 #pragma unroll
-      for (int c = 0; c < C; ++c) h[c] = __float2half_rn(acc[r][c]);
-      if (a.vec_y && col + C <= ncol) {
-        *(uint4*)yp = *(const uint4*)h;
+      for (int c = 0; c < 4; ++c) h[c] = __float2half_rn(vv[c]);
+      if (a.vec_y && c4 + 4 <= ncol) {
+        *(uint2*)yp = *(const uint2*)h;
       } else {
-        for (int c = 0; c < C && col + c < ncol; ++c) ((__half*)yp)[c] = h[c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c4 + c < ncol) ((__half*)yp)[c] = h[c];
       }
     } else {
-      if (a.vec_y && col + C <= ncol) {
-        *(float4*)yp = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+      if (a.vec_y && c4 + 4 <= ncol) {
+        *(float4*)yp = v;
       } else {
-        for (int c = 0; c < C && col + c < ncol; ++c) ((float*)yp)[c] = acc[r][c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c4 + c < ncol) ((float*)yp)[c] = vv[c];
       }
     }
   }
+  cluster.sync();  // keep every CTA's smem alive until all remote reads are done
 }
 
 // ------------------------------------------------------------------ conv 3x3
@@ -274,7 +476,7 @@ template <int R, int CP, bool F16>
 __global__ void __launch_bounds__(256) conv3x3_kernel(const ConvArgs a) {
   constexpr int S = F16 ? 2 : 4;
   constexpr int EB = F16 ? 4 : 8;
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int panel = blockIdx.x;
@@ -353,31 +555,59 @@ __global__ void __launch_bounds__(256) conv3x3_kernel(const ConvArgs a) {
     }
     __syncthreads();
     const uint8_t* st = smem + (c & 1) * a.stage_bytes;
-    const uint16_t* soff = (const uint16_t*)(st + a.x_stage_bytes);
+    const uint32_t* shdr = (const uint32_t*)(st + a.x_stage_bytes);
     const uint8_t* ents = st + a.x_stage_bytes + a.hdr_bytes;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int slot = warp * R + r;
-      const int beg = soff[slot], end = soff[slot + 1];
-      for (int e = beg; e < end; ++e) {
-        if (F16) {
-          const uint32_t en = *(const uint32_t*)(ents + e * EB);
+      const uint32_t h = shdr[warp * R + r];
+      const int beg = (int)(h & 0xffffu), cnt = (int)(h >> 16);
+      int e = 0;
+      if (F16) {
+        for (; e + 4 <= cnt; e += 4) {  // 4 entries per 128-bit broadcast load
+          const uint4 q = *(const uint4*)(ents + (beg + e) * EB);
+          const uint32_t en[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int off = (int)(int16_t)(en[u] & 0xffffu);
+            const uint16_t w = (uint16_t)(en[u] >> 16);
+            uint16_t xv[CP];
+#pragma unroll
+            for (int j = 0; j < CP; ++j) xv[j] = *(const uint16_t*)(st + (pos[j] + off) * 2);
+#pragma unroll
+            for (int j = 0; j < CP; ++j) fma_h(acc[r][j], w, xv[j]);
+          }
+        }
+        for (; e < cnt; ++e) {
+          const uint32_t en = *(const uint32_t*)(ents + (beg + e) * EB);
           const int off = (int)(int16_t)(en & 0xffffu);
           const uint16_t w = (uint16_t)(en >> 16);
 #pragma unroll
+          for (int j = 0; j < CP; ++j) fma_h(acc[r][j], w, *(const uint16_t*)(st + (pos[j] + off) * 2));
+        }
+      } else {
+        for (; e + 2 <= cnt; e += 2) {  // 2 entries per 128-bit broadcast load
+          const uint4 q = *(const uint4*)(ents + (beg + e) * EB);
+          const int off0 = (int)q.x, off1 = (int)q.z;
+          const float w0 = __uint_as_float(q.y), w1 = __uint_as_float(q.w);
+          float x0[CP], x1[CP];
+#pragma unroll
           for (int j = 0; j < CP; ++j) {
-            const uint16_t xv = *(const uint16_t*)(st + (pos[j] + off) * 2);
-            fma_h(acc[r][j], w, xv);
+            x0[j] = *(const float*)(st + (pos[j] + off0) * 4);
+            x1[j] = *(const float*)(st + (pos[j] + off1) * 4);
           }
-        } else {
-          const uint2 en = *(const uint2*)(ents + e * EB);
+#pragma unroll
+          for (int j = 0; j < CP; ++j) {
+            acc[r][j] = fmaf(w0, x0[j], acc[r][j]);
+            acc[r][j] = fmaf(w1, x1[j], acc[r][j]);
+          }
+        }
+        for (; e < cnt; ++e) {
+          const uint2 en = *(const uint2*)(ents + (beg + e) * EB);
           const int off = (int)en.x;
           const float w = __uint_as_float(en.y);
 #pragma unroll
-          for (int j = 0; j < CP; ++j) {
-            const float xv = *(const float*)(st + (pos[j] + off) * 4);
-            acc[r][j] = fmaf(w, xv, acc[r][j]);
-          }
+          for (int j = 0; j < CP; ++j)
+            acc[r][j] = fmaf(w, *(const float*)(st + (pos[j] + off) * 4), acc[r][j]);
         }
       }
     }
@@ -401,7 +631,7 @@ __global__ void __launch_bounds__(256) conv3x3_kernel(const ConvArgs a) {
 }
 
 // ------------------------------------------------------------------ dispatch
-using SpmmFn = void (*)(const SpmmArgs);
+using SpmmFn = void (*)(const __grid_constant__ CUtensorMap, const SpmmArgs);
 using ConvFn = void (*)(const ConvArgs);
 
 template <bool F16>
@@ -410,6 +640,7 @@ static SpmmFn pick_spmm(int R, int GK) {
   if (R == RR && GK == GG) return spmm_kernel<RR, GG, F16>;
 #define SRT_SR(RR) SRT_S(RR, 1) SRT_S(RR, 2) SRT_S(RR, 4) SRT_S(RR, 8)
   SRT_SR(1) SRT_SR(2) SRT_SR(4) SRT_SR(8)
+  if constexpr (!F16) { SRT_SR(16) }
 #undef SRT_SR
 #undef SRT_S
   return nullptr;
@@ -430,11 +661,19 @@ static std::mutex g_attr_mu;
 
 template <typename Fn>
 static cudaError_t ensure_smem_attr(Fn fn, int bytes) {
-  // Opt in to > 48 KB dynamic shared memory once per kernel (idempotent).
+  // Opt in to > 48 KB dynamic shared memory once per (kernel, device); cached so that
+  // launches inside CUDA-graph capture make no driver calls.
   if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::set<std::pair<const void*, int>> done;
   std::lock_guard<std::mutex> lk(g_attr_mu);
-  return cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              227 * 1024);
+  const auto key = std::make_pair((const void*)fn, dev);
+  if (done.count(key)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute((const void*)fn,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
 }
 
 struct DeviceGuard {
@@ -458,10 +697,27 @@ static int cuda_fail(cudaError_t e, const char* what, std::string& err) {
   return SPARSE_ECUDA;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
+}
+
 int upload_plan(Plan& p, std::string& err) {
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
-  if (e != cudaSuccess || ndev == 0) return cuda_fail(e == cudaSuccess ? cudaErrorNoDevice : e, "no CUDA device", err);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return cuda_fail(e == cudaSuccess ? cudaErrorNoDevice : e, "no CUDA device", err);
+  }
   if (p.device < 0) {
     e = cudaGetDevice(&p.device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice", err);
@@ -528,22 +784,76 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
   a.kc = p.kc;
   a.nchunks = p.nchunks;
   a.Mp = p.Mp;
+  a.ks = p.ks;
+  a.stages = p.stages;
   a.x_stage_bytes = p.x_stage_bytes;
-  a.stage_bytes = p.x_stage_bytes + p.max_blk_bytes;
-  a.hdr_bytes = ((p.Mp + 1) * 2 + 15) & ~15;
-  a.vec_x = ((uintptr_t)X % 16 == 0) && ((ldx * S) % 16 == 0);
+  a.stage_bytes = (p.x_stage_bytes + p.max_blk_bytes + 127) & ~127;
+  a.hdr_bytes = p.hdr_bytes;
+  a.bar_off = p.smem_bytes - 128;
+  const int smem = p.smem_bytes;
+  const bool vec_x = ((uintptr_t)X % 16 == 0) && ((ldx * S) % 16 == 0);
   a.vec_y = ((uintptr_t)Y % 16 == 0) && ((ldy * S) % 16 == 0);
-  const int64_t ntiles = (N + p.n_tile - 1) / p.n_tile;
+  a.npanels = p.npanels;
+  auto encode = tensor_map_encoder();
+  const int threads = (p.warps + 1) * 32;
+  auto make_map = [&](CUtensorMap& tmap) {
+    std::memset(&tmap, 0, sizeof tmap);
+    a.use_tma = 0;
+    if (vec_x && encode) {
+      cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)p.K};
+      cuuint64_t strides[1] = {(cuuint64_t)(ldx * S)};
+      cuuint32_t box[2] = {(cuuint32_t)p.n_tile, (cuuint32_t)p.kc};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult r = encode(&tmap, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                          2, (void*)a.X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      a.use_tma = r == CUDA_SUCCESS ? 1 : 0;
+    }
+  };
+  const int64_t ntn = (N + p.n_tile - 1) / p.n_tile;
+  if (p.ks == 1) {
+    // persistent: one wave of CTAs, each walking tiles blockIdx.x + j * gridDim.x
+    a.X = (const uint8_t*)X;
+    a.Y = (uint8_t*)Y;
+    a.N = N;
+    CUtensorMap tmap;
+    make_map(tmap);
+    const int64_t ntiles = (int64_t)p.npanels * ntn;
+    int per_sm = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
+    fn<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tmap, a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "spmm launch", err);
+    return SPARSE_OK;
+  }
   const int64_t kMaxY = 65535;
-  for (int64_t t0 = 0; t0 < ntiles; t0 += kMaxY) {
-    const int64_t nt = std::min(kMaxY, ntiles - t0);
+  for (int64_t t0 = 0; t0 < ntn; t0 += kMaxY) {
+    const int64_t nt = std::min(kMaxY, ntn - t0);
     const int64_t c0 = t0 * p.n_tile;
     a.X = (const uint8_t*)X + c0 * S;
     a.Y = (uint8_t*)Y + c0 * S;
     a.N = N - c0;
-    dim3 grid((unsigned)p.npanels, (unsigned)nt);
-    fn<<<grid, p.warps * 32, p.smem_bytes, (cudaStream_t)stream>>>(a);
-    e = cudaGetLastError();
+    CUtensorMap tmap;
+    make_map(tmap);
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3((unsigned)(p.npanels * p.ks), (unsigned)nt, 1);
+    cfg.blockDim = dim3((unsigned)threads, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.ks;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
     if (e != cudaSuccess) return cuda_fail(e, "spmm launch", err);
   }
   return SPARSE_OK;
@@ -580,7 +890,7 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
   a.Mp = p.Mp;
   a.x_stage_bytes = p.x_stage_bytes;
   a.stage_bytes = p.x_stage_bytes + p.max_blk_bytes;
-  a.hdr_bytes = ((p.Mp + 1) * 2 + 15) & ~15;
+  a.hdr_bytes = p.hdr_bytes;
   a.rb = p.conv_rb;
   a.ipt = p.conv_ipt;
   a.wp = p.conv_wp;

@@ -9,10 +9,12 @@
 // a CTA stages into shared memory next to the X tile it multiplies.
 //
 // Block layout (byte offsets relative to blob + blk_off[panel*nchunks+chunk]):
-//   uint16 slot_off[Mp+1]      entry index of each row slot's first entry,
-//                              relative to the block's entry array; slot s =
-//                              warp*R + r; padded to 16 bytes
-//   entries[slot_off[Mp]]      row-slot-major, k ascending within a slot
+//   uint32 slot_hdr[Mp]        start | count << 16: first entry index (relative
+//                              to the block's entry array, a multiple of
+//                              entry_align = 16 / entry_bytes) and number of
+//                              entries of row slot s = warp*R + r; padded to 16 B
+//   entries[...]               row-slot-major, k ascending within a slot; gaps
+//                              between slots are zero padding
 //                              fp32 SpMM : {uint32 k_local; float w}     (8 B)
 //                              fp16 SpMM : {uint16 k_local; half  w}     (4 B)
 //                              fp32 conv : {int32 smem_off; float w}     (8 B)
@@ -46,6 +48,9 @@ struct Plan {
   int32_t nchunks = 1;
   int32_t npanels = 1;
   int32_t entry_bytes = 8;
+  int32_t entry_align = 2;  // entries per 16-byte broadcast load
+  int32_t hdr_bytes = 16;   // block header bytes (slot table)
+  int32_t ks = 1;           // cluster K-split: CTAs of a cluster take disjoint chunk ranges
 
   // conv geometry (kind == CONV3X3)
   int32_t conv_rb = 0;    // output rows per tile
@@ -64,11 +69,32 @@ struct Plan {
   int32_t x_stage_bytes = 0;     // bytes of the staged X tile per stage
   int32_t smem_bytes = 0;        // dynamic smem per CTA (all stages)
   int32_t stages = 2;
+  int32_t red_bytes = 0;         // smem for the cross-CTA (DSMEM) reduction tile
 
   // stats
   int64_t max_panel_nnz = 0, min_panel_nnz = 0;
   double build_ms = 0.0;
   uint64_t digest = 0;
+
+  // JIT executor (the paper's unrolled, value-baked code generator, Sec. 3.5
+  // P:183-185): per row panel, straight-line PTX that walks the panel's K
+  // union in ascending order, loads X[k, lane column] once and issues one FFMA
+  // with the weight as an immediate per nonzero of column k (Alg. 3).
+  int32_t executor = 0;      // 0 = plan-driven kernels, 1 = JIT
+  struct JitModule {
+    std::string ptx;
+    std::vector<char> cubin;
+    int32_t panel_begin = 0, npanels = 0;
+    int64_t fmas = 0;
+    void* mod = nullptr;  // CUmodule
+    void* fn = nullptr;   // CUfunction
+  };
+  std::vector<JitModule> jit;
+  int32_t jit_mp = 0, jit_warps = 0, jit_kc = 0, jit_stages = 0, jit_npanels = 0;
+  int32_t jit_smem = 0;
+  std::vector<int32_t> jit_row_id;  // jit_npanels * jit_mp
+  double jit_compile_ms = 0.0;
+  int64_t jit_cubin_bytes = 0;
 
   // device copy
   int device = -1;
@@ -84,7 +110,24 @@ struct BuildOpts {
   int64_t n_hint = 0;
   int32_t drop_zeros = 0;
   int32_t warps = 0, rows_per_warp = 0, k_chunk = 0, split_k = 0;
+  int32_t k_split = 0, stages = 0;
+  int32_t executor = 0, jit_rows = 0, jit_warps = 0;
 };
+
+// JIT executor (jit.cpp).  Row entries per row (k ascending) as validated by the
+// inspector; builds jit_row_id and one PTX module per group of panels.
+struct RowEntry {
+  int32_t k;
+  float w;
+};
+int jit_generate(Plan& p, const std::vector<std::vector<RowEntry>>& rows, const BuildOpts& o,
+                 std::string& err);
+int jit_compile(Plan& p, std::string& err);  // PTX -> cubin (host only, no GPU needed)
+int jit_load(Plan& p, std::string& err);     // cubin -> CUmodule on p.device
+void jit_unload(Plan& p);
+int jit_launch(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
+               void* stream, std::string& err);
+bool jit_can_launch(const Plan& p, const void* X, int64_t ldx);
 
 // Inspector: validate the CSR (a1), group rows into nnz-balanced panels (a2),
 // choose split-K / chunking (a3, a5) and pack (a4).  Returns a sparse_status

@@ -43,7 +43,10 @@ class sparse_plan_opts(ctypes.Structure):
                 ("w", ctypes.c_int32), ("n_hint", ctypes.c_int64), ("tune", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("drop_zeros", ctypes.c_int32),
                 ("warps", ctypes.c_int32), ("rows_per_warp", ctypes.c_int32),
-                ("k_chunk", ctypes.c_int32), ("split_k", ctypes.c_int32)]
+                ("k_chunk", ctypes.c_int32), ("split_k", ctypes.c_int32),
+                ("k_split", ctypes.c_int32), ("stages", ctypes.c_int32),
+                ("executor", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
+                ("jit_warps", ctypes.c_int32)]
 
 
 class sparse_plan_info_t(ctypes.Structure):
@@ -53,10 +56,14 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("rows_per_warp", ctypes.c_int32), ("cols_per_lane", ctypes.c_int32),
                 ("n_tile", ctypes.c_int32), ("k_chunk", ctypes.c_int32),
                 ("chunks", ctypes.c_int32), ("split_k", ctypes.c_int32),
+                ("k_split", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("conv_rows_per_tile", ctypes.c_int32), ("conv_images_per_tile", ctypes.c_int32),
                 ("max_panel_nnz", ctypes.c_int64), ("min_panel_nnz", ctypes.c_int64),
-                ("build_ms", ctypes.c_double), ("digest", ctypes.c_uint64)]
+                ("build_ms", ctypes.c_double), ("executor", ctypes.c_int32),
+                ("jit_modules", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
+                ("jit_warps", ctypes.c_int32), ("jit_cubin_bytes", ctypes.c_int64),
+                ("jit_compile_ms", ctypes.c_double), ("digest", ctypes.c_uint64)]
 
 
 def _load() -> ctypes.CDLL:

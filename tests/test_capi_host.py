@@ -86,7 +86,8 @@ def test_panel_balance_and_group_split():
     max_row = np.diff(w.row_ptr).max()
     assert info["max_panel_nnz"] <= mean + max_row
     assert info["min_panel_nnz"] >= mean - max_row
-    # split-K groups: all non-trailing groups hold exactly ceil(cnt/G) nonzeros
+    # split-K groups: all non-trailing groups hold exactly the same number of nonzeros
+    # (P:167): ceil(cnt/G) rounded up to the 2-entry broadcast-load width of fp32 entries
     pl = _plan(w, n_hint=49, split_k=4)
     d = pl.dump()
     assert pl.info["split_k"] == 4
@@ -94,6 +95,7 @@ def test_panel_balance_and_group_split():
         sel = (d.row == r) & (d.chunk == c)
         cnt = int(sel.sum())
         per = -(-cnt // 4)
+        per = -(-per // 2) * 2
         sizes = [int(((d.group == g) & sel).sum()) for g in range(4)]
         assert sizes == [min(per, max(0, cnt - g * per)) for g in range(4)]
 
@@ -200,3 +202,17 @@ def test_fp16_rounding_matches_ieee():
     got = np.empty(M, np.float32)
     got[d.row] = d.value
     assert np.array_equal(got, v.astype(np.float16).astype(np.float32))
+
+
+def test_jit_codegen_compiles_on_host():
+    # the JIT executor generates PTX per row panel and assembles it in-process;
+    # both steps run without a GPU
+    import torch
+    w = gen.pruned_weights(200, 96, 90, seed=3)
+    pl = _plan(w, n_hint=300, executor=1)
+    i = pl.info
+    assert i["executor"] == 1 and i["jit_modules"] >= 1 and i["jit_cubin_bytes"] > 0
+    pl16 = _plan(w, torch.float16, n_hint=300, executor=1)
+    assert pl16.info["jit_cubin_bytes"] > 0
+    with pytest.raises(S.SparseRTError):
+        _plan(w, kind=srt.SPARSE_CONV3X3, c_in=w.K // 9, h=4, w=4, executor=1)

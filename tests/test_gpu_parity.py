@@ -216,10 +216,30 @@ def test_unaligned_and_tiny_n(N, ld, ldy, f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
-@pytest.mark.parametrize("R,warps,kc,gk", [(1, 1, 8, 1), (2, 8, 16, 2), (8, 4, 256, 8), (4, 2, 40, 4)])
-def test_tile_overrides_exact(R, warps, kc, gk, f16):
+@pytest.mark.parametrize("R,warps,kc,gk,ks,st", [(1, 1, 8, 1, 1, 1), (2, 8, 16, 2, 8, 2),
+                                                 (8, 4, 256, 8, 1, 3), (4, 2, 40, 4, 2, 4),
+                                                 (8, 3, 64, 1, 4, 2), (16, 8, 32, 1, 8, 3)])
+def test_tile_overrides_exact(R, warps, kc, gk, ks, st, f16):
+    if f16 and R == 16:
+        pytest.skip("R=16 exceeds the fp16 accumulator budget")
     _exact_case(333, 700, 250, 90, f16, seed=R * 10 + gk, rows_per_warp=R, warps=warps,
-                k_chunk=kc, split_k=gk)
+                k_chunk=kc, split_k=gk, k_split=ks, stages=st)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_k_split_changes_order_not_value(f16):
+    # k_split fixes a different (still deterministic) summation order: equal within tolerance,
+    # bitwise on integer data, and repeated calls are bitwise identical.
+    w = gen.pruned_weights(256, 2048, 90, seed=31)
+    X = gen.uniform_x(2048, 392, seed=32)
+    ys = []
+    for ks in (1, 2, 4, 8):
+        y, plan = _run_spmm(w, X, f16, k_split=ks, rows_per_warp=4)
+        assert plan.info["k_split"] == ks
+        ys.append(y)
+        assert oracle.rel_l2(y, _ref(w, X, f16)) <= (F16_TOL if f16 else F32_TOL)
+    for ks in (1, 8):
+        _exact_case(256, 2048, 392, 90, f16, seed=33, k_split=ks, rows_per_warp=4)
 
 
 def test_api_errors_on_device():
@@ -323,3 +343,44 @@ def test_conv_c5_full_batch_sampled(f16):
     xt = torch.from_numpy(x).to(dev).to(_tdt(f16))
     half = plan.conv3x3(xt[:, 128:].contiguous()).float().cpu().numpy()
     assert np.array_equal(half.astype(np.float64), y[:, 128:])
+
+
+# --------------------------------------------------------------------------- JIT executor
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("case", [(64, 64, 128), (300, 200, 517), (2048, 512, 392), (512, 2048, 49),
+                                  (256, 64, 25088), (1000, 333, 1001)])
+def test_jit_integer_exact(case, f16):
+    M, K, N = case
+    plan = _exact_case(M, K, N, 90, f16, seed=M + K + N, executor=1)
+    assert plan.info["executor"] == 1 and plan.info["jit_modules"] >= 1
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_jit_bitwise_equals_plan_driven(f16):
+    # same per-output summation order (k ascending, sequential) -> bitwise identical
+    w = gen.pruned_weights(768, 512, 90, seed=41)
+    X = gen.uniform_x(512, 3000, seed=42)
+    y_jit, pj = _run_spmm(w, X, f16, executor=1)
+    y_ref, pr = _run_spmm(w, X, f16, split_k=1, k_split=1)
+    assert pj.info["executor"] == 1 and pr.info["executor"] == 0
+    assert np.array_equal(y_jit, y_ref)
+    assert oracle.rel_l2(y_jit, _ref(w, X, f16)) <= (F16_TOL if f16 else F32_TOL)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_jit_closed_forms_and_fallback(f16):
+    K = 300
+    w = gen.pruned_weights(513, K, 90, seed=6)
+    y, _ = _run_spmm(w, np.eye(K, dtype=np.float32), f16, executor=1)
+    wd = gen.to_dense(w.with_values(_w64(w, f16).astype(np.float32)))
+    assert np.array_equal(y, wd)
+    # unaligned X (ld = 301, odd) -> plan-driven fallback, still exact
+    s = gen.row_selection_csr(700, K, seed=5)
+    X = gen.uniform_x(K, 301, seed=9)
+    y, _ = _run_spmm(s, X, f16, N=299, ld=301, executor=1)
+    assert np.array_equal(y, _x64(X, f16)[s.col_idx][:, :299])
+    # empty matrix
+    z = gen.stress_pattern("empty", 50, K, seed=1)
+    y, _ = _run_spmm(z, gen.uniform_x(K, 64, seed=3), f16, executor=1)
+    assert np.array_equal(y, np.zeros_like(y))
