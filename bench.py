@@ -247,8 +247,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/dense/cpu legs (for ncu runs)")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA graph")
-    ap.add_argument("--executor", type=int, default=1, choices=[0, 1],
-                    help="SpMM executor: 1 = JIT code generator (the paper's method), 0 = plan-driven")
+    ap.add_argument("--executor", type=int, default=2, choices=[0, 1, 2],
+                    help="SpMM executor: 0 plan-driven, 1 JIT code generator (the paper's method), "
+                         "2 auto")
+    ap.add_argument("--no-tune", action="store_true",
+                    help="skip the offline autotuner (P:259-263); use the heuristic tile choice")
     args = ap.parse_args()
     if args.warmup < 3 and not args.quick:
         args.warmup = 3
@@ -272,14 +275,30 @@ def main():
 
     layers, scaling, desc = workload_layers(args.workload, args.sparsity, world)
     plans, xs, ys, host = [], [], [], []
-    build_ms = []
+    build_ms, chosen, tuned_us = [], [], []
     for L in layers:
         w, x = make_inputs(L, args.sparsity, rank)
         if L["kind"] == "spmm":
-            p = srt.Plan.from_csr(w, dtype=tdt, n_hint=L["N"], device=local, executor=args.executor)
+            base = dict(n_hint=L["N"], executor=args.executor)
         else:
-            p = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=L["c_in"],
-                                  h=L["H"], w=L["W"], n_hint=L["B"], device=local)
+            base = dict(kind=srt.SPARSE_CONV3X3, c_in=L["c_in"], h=L["H"], w=L["W"], n_hint=L["B"])
+        if args.no_tune:
+            p = srt.Plan.from_csr(w, dtype=tdt, device=local, **base)
+        else:
+            # offline autotuning on rank 0; every rank then builds the chosen
+            # configuration explicitly, so the replicated plans are identical (digests)
+            opts = [None]
+            if rank == 0:
+                tuned = srt.Plan.from_csr(w, dtype=tdt, device=local, tune=1, **base)
+                opts = [tuned.chosen_opts()]
+                tuned_us.append(round(tuned.info["tuned_us"], 2))
+                tuned.close()
+            if world > 1:
+                dist.broadcast_object_list(opts, src=0)
+            chosen.append(opts[0])
+            kw = dict(base)
+            kw.update(opts[0])
+            p = srt.Plan.from_csr(w, dtype=tdt, device=local, **kw)
         build_ms.append(round(p.info["build_ms"] + p.info["jit_compile_ms"], 1))
         X = torch.from_numpy(x).to(dev).to(tdt).contiguous()
         if L["kind"] == "spmm":
@@ -291,6 +310,12 @@ def main():
         ys.append(Y)
         host.append(x)
     stream = torch.cuda.current_stream(dev)
+    digests = [int(p.info["digest"]) for p, _ in plans]
+    replicas_equal = True
+    if world > 1:
+        allds = [None] * world
+        dist.all_gather_object(allds, digests)
+        replicas_equal = all(d == allds[0] for d in allds)
 
     def call(i, X=None, Y=None, stream=stream):
         p, _ = plans[i]
@@ -499,8 +524,11 @@ def main():
                        "l2": "flushed (256 MiB write) before every timed step, outside the events",
                        "launch": "eager" if args.eager else "cuda-graph replay of the step",
                        "plan_build_ms": build_ms,
-                       "executor": "jit" if args.executor == 1 else "plan-driven",
-                       "parallelism": f"N-sharded x{world}, replicated plan, no collective"},
+                       "executor": {0: "plan-driven", 1: "jit", 2: "auto"}[args.executor],
+                       "tuned": None if args.no_tune else chosen,
+                       "tuned_us": None if args.no_tune else tuned_us,
+                       "parallelism": f"N-sharded x{world}, replicated plan, no collective",
+                       "replica_digests_equal": replicas_equal},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "layers": per_layer, "dense_baseline": dense,
         }

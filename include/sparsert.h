@@ -65,8 +65,12 @@ typedef struct {
   int32_t c_in, h, w; /* conv only: K must equal 9*c_in; H, W fixed at plan time (the paper
                          specialises each kernel to its problem shape) */
   int64_t n_hint;     /* expected N (SpMM) or batch (conv); 0 = unknown.  Drives the tile heuristic. */
-  int32_t tune;       /* 0 = heuristic; 1 = timed search over <= 100 candidates —
-                         requires a device and n_hint > 0 */
+  int32_t tune;       /* 0 = heuristic; 1 = timed search over <= 100 candidates on the
+                         plan's device with synthetic X of n_hint columns (tile parameters,
+                         cluster K-split, split-K groups, JIT executor); requires n_hint > 0.
+                         The choice depends on measured times, so two tuned plans of one matrix
+                         may differ in summation order (pass the chosen options explicitly to
+                         build identical replicas). */
   int32_t device;     /* CUDA ordinal; -1 = current device; SPARSE_DEVICE_HOST_ONLY = no upload */
   int32_t drop_zeros; /* 0 = reject explicit zeros; 1 = drop them */
   /* Tile overrides (0 = automatic).  None of these changes a result except split_k,
@@ -80,7 +84,8 @@ typedef struct {
                             tiles reduced in fixed rank order through distributed shared
                             memory (the paper's strategy (a), Fig. 2a): 1,2,4,8 */
   int32_t stages;        /* SpMM: X/plan pipeline stages (TMA + mbarrier ring): 1..4 */
-  int32_t executor;      /* SpMM: 0 = plan-driven kernels (default); 1 = JIT: the paper's code
+  int32_t executor;      /* SpMM: 0 = plan-driven kernels (default); 2 = auto (JIT where each
+                            panel's code is <= 24 KB, else plan-driven); 1 = JIT: the paper's code
                             generator (Sec. 3.5) - per row panel, straight-line PTX with
                             the weights as FFMA immediates, assembled in-process at plan creation
                             (slow to create: seconds for 10^5 nonzeros).  X that is not 16-byte
@@ -151,6 +156,7 @@ typedef struct {
   int32_t jit_rows, jit_warps;
   int64_t jit_cubin_bytes;
   double jit_compile_ms;
+  double tuned_us;      /* tune = 1: measured time of the chosen configuration (us) */
   uint64_t digest;      /* FNV-1a of the packed plan: equal digests <=> identical replicas */
 } sparse_plan_info_t;
 

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsparsert.so")
-SOURCES = ["inspector.cpp", "capi.cpp", "kernels.cu", "jit.cpp"]
+SOURCES = ["inspector.cpp", "capi.cpp", "kernels.cu", "jit.cpp", "tune.cu"]
 HEADERS = [os.path.join(CSRC, "plan.h"), os.path.join(ROOT, "include", "sparsert.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

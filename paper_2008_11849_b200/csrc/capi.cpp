@@ -8,6 +8,8 @@
 #include "../../include/sparsert.h"
 #include "plan.h"
 
+#include <cuda_runtime.h>
+
 struct sparse_plan_s {
   srt::Plan p;
   bool host_only = false;
@@ -69,8 +71,39 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   }
   std::string err;
   int rc;
+  if (o.tune == 1) {
+    if (o.device == SPARSE_DEVICE_HOST_ONLY) {
+      delete h;
+      return fail(SPARSE_EINVAL, "tune = 1 needs a device");
+    }
+    int dev = o.device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+      delete h;
+      return fail(SPARSE_ECUDA, "no CUDA device");
+    }
+    try {
+      rc = srt::tune_plan(h->p, M, K, nnz, row_ptr, col_idx, values, dtype, bo, dev, err);
+    } catch (const std::bad_alloc&) {
+      rc = SPARSE_ENOMEM;
+      err = "host allocation failed in tuner";
+    }
+    if (rc != SPARSE_OK) {
+      delete h;
+      return fail(rc, err);
+    }
+    *out = h;
+    return ok();
+  }
+  const bool auto_exec = bo.executor == 2;
+  if (auto_exec) bo.executor = 1;
   try {
     rc = srt::build_plan(h->p, M, K, nnz, row_ptr, col_idx, values, dtype, bo, err);
+    if (rc == SPARSE_OK && auto_exec && h->p.executor == 1 &&
+        srt::jit_panel_code_bytes(h->p) > 24 * 1024) {
+      // auto: the JIT executor only where each panel's code fits the instruction cache
+      bo.executor = 0;
+      rc = srt::build_plan(h->p, M, K, nnz, row_ptr, col_idx, values, dtype, bo, err);
+    }
   } catch (const std::bad_alloc&) {
     rc = SPARSE_ENOMEM;
     err = "host allocation failed in inspector";
@@ -178,6 +211,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->jit_warps = p.jit_warps;
   out->jit_cubin_bytes = p.jit_cubin_bytes;
   out->jit_compile_ms = p.jit_compile_ms;
+  out->tuned_us = p.tuned_us;
   return ok();
 }
 

@@ -322,7 +322,9 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       ntiles = ((nb + p.conv_ipt - 1) / p.conv_ipt) * (o.h / p.conv_rb);
     }
     // accumulators per thread: R * C fp32 registers; keep <= 64
-    const int rmax = 8;  // R * C <= 64 accumulators; Mp = 64 rows amortises X staging
+    // R = 4 rows per warp x 8 warps: Mp = 32 rows; measured best on B200 for both dtypes
+    // (R = 8 halves occupancy through registers, scripts/sweep.py)
+    const int rmax = 4;
     const int max_ks = o.kind == SPARSE_SPMM ? std::min(8, p.nchunks) : 1;
     int bestR = 1, bestKs = 1;
     bool found = false;
@@ -493,7 +495,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // k_split == 1: persistent CTAs, the ring runs across tiles; k_split > 1: one tile
     // per CTA, no point in more stages than chunks
     const int per_chunks = (p.nchunks + p.ks - 1) / p.ks;
-    int stages = o.stages ? o.stages : 3;
+    int stages = o.stages ? o.stages : 2;
     if (p.ks > 1) stages = std::min(stages, per_chunks);
     stages = std::max(1, stages);
     p.stages = stages;
@@ -526,7 +528,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     const int rc = jit_generate(p, re, o, err);
     if (rc != SPARSE_OK) return rc;
   } else if (o.executor != 0) {
-    err = "executor must be 0 (plan-driven) or 1 (JIT)";
+    err = "executor must be 0 (plan-driven), 1 (JIT) or 2 (auto)";
     return SPARSE_EINVAL;
   }
 

@@ -425,6 +425,12 @@ void jit_unload(Plan& p) {
   }
 }
 
+int64_t jit_panel_code_bytes(const Plan& p) {
+  int64_t maxf = 0;
+  for (const auto& jm : p.jit) maxf = std::max<int64_t>(maxf, jm.fmas / std::max(1, jm.npanels));
+  return maxf * 16;  // one 16-byte FFMA per nonzero dominates the code
+}
+
 bool jit_can_launch(const Plan& p, const void* X, int64_t ldx) {
   const int S = p.dtype == SPARSE_F16 ? 2 : 4;
   return p.executor == 1 && !p.jit.empty() && p.jit[0].fn != nullptr && driver().ok &&

@@ -231,20 +231,43 @@ __global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUten
   // k_split > 1: one tile per cluster; CTA rank r of the cluster takes chunk slice r.
   const bool persistent = a.ks == 1;
   const int rank = persistent ? 0 : (int)(blockIdx.x % a.ks);
-  const int64_t ntn = (a.N + NT - 1) / NT;
-  const int64_t ntiles = persistent ? (int64_t)a.npanels * ntn : 1;
-  const int64_t t_begin = persistent ? (int64_t)blockIdx.x : 0;
-  const int64_t t_step = persistent ? (int64_t)gridDim.x : 1;
+  const int ntn = (int)((a.N + NT - 1) / NT);
+  const int np = a.npanels;
+  const int ntiles = persistent ? np * ntn : 1;
   const int cps = (a.nchunks + a.ks - 1) / a.ks;
   const int c_begin = rank * cps;
   const int nloc = max(0, min(a.nchunks, c_begin + cps) - c_begin);
-  auto tile_coords = [&](int64_t t, int& panel, int64_t& n0) {
+  // tile walker without divisions in the loop (64-bit / runtime-divisor division is
+  // emulated on the GPU and used to dominate small-K layers)
+  struct TileIter {
+    int t, panel, nt, step, sd, sm;
+  };
+  auto tile_begin = [&]() {
+    TileIter it;
     if (persistent) {
-      panel = (int)(t % a.npanels);
-      n0 = (t / a.npanels) * NT;
+      it.t = (int)blockIdx.x;
+      it.panel = it.t % np;
+      it.nt = it.t / np;
+      it.step = (int)gridDim.x;
+      it.sd = it.step / np;
+      it.sm = it.step % np;
     } else {
-      panel = (int)(blockIdx.x / a.ks);
-      n0 = (int64_t)blockIdx.y * NT;
+      it.t = 0;
+      it.panel = (int)(blockIdx.x / a.ks);
+      it.nt = (int)blockIdx.y;
+      it.step = 1;
+      it.sd = 0;
+      it.sm = 0;
+    }
+    return it;
+  };
+  auto tile_next = [&](TileIter& it) {
+    it.t += it.step;
+    it.nt += it.sd;
+    it.panel += it.sm;
+    if (it.panel >= np) {
+      it.panel -= np;
+      it.nt += 1;
     }
   };
   const uint32_t full0 = smem_u32(smem + a.bar_off);
@@ -297,15 +320,14 @@ __global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUten
   if (warp == nwarps) {
     // ---------------- producer warp: TMA X tile + bulk plan block per chunk, running
     // ahead of the consumers by up to `stages` chunks (across tile boundaries)
-    int i = 0;
-    for (int64_t t = t_begin; t < ntiles; t += t_step) {
-      int panel;
-      int64_t n0;
-      tile_coords(t, panel, n0);
-      for (int j = 0; j < nloc; ++j, ++i) {
+    int s = 0, uses = 0;  // ring slot and how many times it has been filled (phase)
+    uint32_t ph = 0;
+    for (TileIter it = tile_begin(); it.t < ntiles; tile_next(it)) {
+      const int panel = it.panel;
+      const int64_t n0 = (int64_t)it.nt * NT;
+      for (int j = 0; j < nloc; ++j) {
         const int c = c_begin + j;
-        const int s = i % a.stages;
-        if (i >= a.stages) mbar_wait(empty0 + 8 * s, ((i / a.stages) - 1) & 1);
+        if (uses > 0) mbar_wait(empty0 + 8 * s, ph ^ 1u);
         uint8_t* st = smem + s * a.stage_bytes;
         const int64_t bi = (int64_t)panel * a.nchunks + c;
         const int64_t b0 = a.blk_off[bi];
@@ -342,15 +364,20 @@ __global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUten
           else
             cp_async_mbar_arrive_noinc(fb);
         }
+        if (++s == a.stages) {
+          s = 0;
+          ph ^= 1u;
+          uses = 1;
+        }
       }
     }
   } else {
     // ---------------- consumer warps: Alg. 3 over each staged chunk
-    int i = 0;
-    for (int64_t t = t_begin; t < ntiles; t += t_step) {
-      int panel;
-      int64_t n0;
-      tile_coords(t, panel, n0);
+    int s = 0;
+    uint32_t ph = 0;
+    for (TileIter it = tile_begin(); it.t < ntiles; tile_next(it)) {
+      const int panel = it.panel;
+      const int64_t n0 = (int64_t)it.nt * NT;
       int rows[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) rows[r] = a.row_id[(int64_t)panel * a.Mp + warp * R + r];
@@ -358,9 +385,8 @@ __global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUten
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
-      for (int j = 0; j < nloc; ++j, ++i) {
-        const int s = i % a.stages;
-        mbar_wait(full0 + 8 * s, (i / a.stages) & 1);
+      for (int j = 0; j < nloc; ++j) {
+        mbar_wait(full0 + 8 * s, ph);
         const uint8_t* st = smem + s * a.stage_bytes;
         const uint8_t* xs = st + li * (C * S);
         const uint32_t* shdr = (const uint32_t*)(st + a.x_stage_bytes);
@@ -382,6 +408,10 @@ __global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUten
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * s);
+        if (++s == a.stages) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
       // cross-group reduction inside the warp: fixed binary tree over group index
       if (GK > 1) {
@@ -398,9 +428,9 @@ __global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUten
   }
   if (persistent) return;
 
-  int panel;
-  int64_t n0;
-  tile_coords(0, panel, n0);
+  const TileIter it0 = tile_begin();
+  const int panel = it0.panel;
+  const int64_t n0 = (int64_t)it0.nt * NT;
   const int ncol = (int)min((int64_t)NT, a.N - n0);
   // ---------------- k_split > 1: partial tiles reduced across the cluster through DSMEM,
   // summed in rank order 0, 1, ..., ks-1 for every output (deterministic).

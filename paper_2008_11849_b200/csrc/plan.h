@@ -94,6 +94,7 @@ struct Plan {
   int32_t jit_smem = 0;
   std::vector<int32_t> jit_row_id;  // jit_npanels * jit_mp
   double jit_compile_ms = 0.0;
+  double tuned_us = 0.0;  // autotuner: measured time of the chosen configuration
   int64_t jit_cubin_bytes = 0;
 
   // device copy
@@ -128,6 +129,14 @@ void jit_unload(Plan& p);
 int jit_launch(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
                void* stream, std::string& err);
 bool jit_can_launch(const Plan& p, const void* X, int64_t ldx);
+// Per-panel straight-line code size (bytes) of a JIT plan, max over modules.
+int64_t jit_panel_code_bytes(const Plan& p);
+
+// Autotuner (tune.cu): builds, uploads and times every candidate on `device` and
+// leaves the fastest (uploaded, JIT loaded) in `best`.
+int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_ptr,
+              const int32_t* col_idx, const float* values, int32_t dtype, const BuildOpts& base,
+              int device, std::string& err);
 
 // Inspector: validate the CSR (a1), group rows into nnz-balanced panels (a2),
 // choose split-K / chunking (a3, a5) and pack (a4).  Returns a sparse_status

@@ -1,0 +1,193 @@
+// Offline autotuner (Sec. 3.7 "Autotuning"): "we perform
+// exhaustive grid search over a list of hand picked choices for each SpMM problem
+// according to a couple of simple heuristics ... This typically resulted in less
+// than 100 parameter combinations for each problem."
+//
+// Here: sparse_plan_create(..., opts.tune = 1) times every candidate tile
+// configuration (and the JIT executor when its per-panel code is small) on the
+// plan's device with synthetic X of the hinted size, and keeps the fastest.  The
+// candidate grid stays under 100 entries.  Timing: 2 warm-up launches, then the
+// median of 3 trials of 5 back-to-back launches, CUDA events on a private stream.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sparsert.h"
+#include "plan.h"
+
+namespace srt {
+
+namespace {
+
+constexpr int64_t kJitMaxPanelCode = 24 * 1024;
+
+__global__ void fill_uniform(uint8_t* p, int64_t n, int f16, uint32_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ seed;
+    h ^= h >> 16;
+    h *= 0x7feb352du;
+    h ^= h >> 15;
+    const float v = (float)(h & 0xffffff) * (2.0f / 16777216.0f) - 1.0f;
+    if (f16)
+      reinterpret_cast<__half*>(p)[i] = __float2half_rn(v);
+    else
+      reinterpret_cast<float*>(p)[i] = v;
+  }
+}
+
+void release(Plan& p) {
+  jit_unload(p);
+  free_plan_device(p);
+}
+
+}  // namespace
+
+int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_ptr,
+              const int32_t* col_idx, const float* values, int32_t dtype, const BuildOpts& base,
+              int device, std::string& err) {
+  if (base.n_hint <= 0) {
+    err = "tune = 1 needs n_hint > 0 (N for SpMM, batch for conv)";
+    return SPARSE_EINVAL;
+  }
+  const bool f16 = dtype == SPARSE_F16;
+  const int S = f16 ? 2 : 4;
+  // candidate grid (hand-picked): warps per CTA, rows per warp, pipeline depth,
+  // cluster K-split, split-K groups (small N); plus the JIT executor
+  std::vector<BuildOpts> cands;
+  if (base.kind == SPARSE_SPMM) {
+    const int nch = (K + 63) / 64;
+    for (int R : {2, 4})
+      for (int st : {2, 4})
+        for (int ks : {1, 2, 4, 8})
+          for (int gk : {1, 2}) {
+            if (ks > nch) continue;
+            if (gk == 2 && base.n_hint > 512) continue;
+            BuildOpts o = base;
+            o.warps = 8;
+            o.rows_per_warp = R;
+            o.stages = st;
+            o.k_split = ks;
+            o.split_k = gk;
+            o.executor = 0;
+            cands.push_back(o);
+          }
+    BuildOpts j = base;
+    j.executor = 1;
+    cands.push_back(j);
+  } else {
+    for (int R : {2, 4, 8})
+      for (int w : {4, 8})
+        for (int cc : {8, 16, 32}) {
+          BuildOpts o = base;
+          o.rows_per_warp = R;
+          o.warps = w;
+          o.k_chunk = cc;
+          cands.push_back(o);
+        }
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+    return SPARSE_ECUDA;
+  }
+  int64_t xe, ye, N = base.n_hint;
+  if (base.kind == SPARSE_SPMM) {
+    xe = (int64_t)K * N;
+    ye = (int64_t)M * N;
+  } else {
+    xe = (int64_t)base.c_in * N * base.h * base.w;
+    ye = (int64_t)M * N * base.h * base.w;
+  }
+  uint8_t *X = nullptr, *Y = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (cudaMalloc(&X, (size_t)xe * S + 16) != cudaSuccess ||
+      cudaMalloc(&Y, (size_t)ye * S + 16) != cudaSuccess) {
+    cudaFree(X);
+    cudaGetLastError();
+    err = "tune: cannot allocate the synthetic X / Y";
+    return SPARSE_ENOMEM;
+  }
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaEventCreate(&ev[0]);
+  cudaEventCreate(&ev[1]);
+  fill_uniform<<<1024, 256, 0, st>>>(X, xe, f16 ? 1 : 0, 12345u);
+  float best_ms = 1e30f;
+  bool have = false;
+  std::string last_err;
+  for (const BuildOpts& o : cands) {
+    Plan p;
+    std::string e2;
+    int rc = build_plan(p, M, K, nnz, row_ptr, col_idx, values, dtype, o, e2);
+    if (rc != SPARSE_OK) continue;
+    if (p.executor == 1) {
+      // JIT only where each panel's straight-line code stays instruction-cache sized
+      // (the instruction-fetch limit of P:379, measured on B200: DESIGN.md)
+      if (jit_panel_code_bytes(p) > kJitMaxPanelCode) continue;
+      if (jit_compile(p, e2) != SPARSE_OK) continue;
+    }
+    p.device = device;
+    if (upload_plan(p, e2) != SPARSE_OK) continue;
+    if (p.executor == 1 && jit_load(p, e2) != SPARSE_OK) {
+      release(p);
+      continue;
+    }
+    auto run = [&]() -> int {
+      if (base.kind == SPARSE_SPMM) {
+        if (p.executor == 1 && jit_can_launch(p, X, N)) return jit_launch(p, N, X, N, Y, N, st, e2);
+        return launch_spmm(p, N, X, N, Y, N, st, e2);
+      }
+      return launch_conv3x3(p, N, X, Y, st, e2);
+    };
+    // back-to-back launches keep the device busy, so host launch cost is not timed
+    bool ok = run() == SPARSE_OK && run() == SPARSE_OK;
+    std::vector<float> ms;
+    for (int r = 0; ok && r < 3; ++r) {
+      cudaEventRecord(ev[0], st);
+      for (int q = 0; ok && q < 5; ++q) ok = run() == SPARSE_OK;
+      cudaEventRecord(ev[1], st);
+      if (cudaEventSynchronize(ev[1]) != cudaSuccess) ok = false;
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[0], ev[1]);
+      ms.push_back(t / 5.0f);
+    }
+    if (!ok) {
+      last_err = e2;
+      cudaGetLastError();
+      release(p);
+      continue;
+    }
+    std::sort(ms.begin(), ms.end());
+    const float med = ms[ms.size() / 2];
+    if (med < best_ms) {
+      if (have) release(best);
+      best = std::move(p);
+      // `p` no longer owns the device state
+      p.d_mem = nullptr;
+      for (auto& jm : p.jit) jm.mod = jm.fn = nullptr;
+      best_ms = med;
+      have = true;
+    } else {
+      release(p);
+    }
+  }
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  cudaStreamDestroy(st);
+  cudaFree(X);
+  cudaFree(Y);
+  if (!have) {
+    err = "tune: no candidate ran" + (last_err.empty() ? std::string() : ": " + last_err);
+    return SPARSE_EINTERNAL;
+  }
+  best.tuned_us = best_ms * 1000.0;
+  return SPARSE_OK;
+}
+
+}  // namespace srt

@@ -63,7 +63,8 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("build_ms", ctypes.c_double), ("executor", ctypes.c_int32),
                 ("jit_modules", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
                 ("jit_warps", ctypes.c_int32), ("jit_cubin_bytes", ctypes.c_int64),
-                ("jit_compile_ms", ctypes.c_double), ("digest", ctypes.c_uint64)]
+                ("jit_compile_ms", ctypes.c_double), ("tuned_us", ctypes.c_double),
+                ("digest", ctypes.c_uint64)]
 
 
 def _load() -> ctypes.CDLL:
@@ -225,6 +226,22 @@ class Plan:
 
     def dump(self) -> PlanDump:
         return sparse_plan_dump(self._h)
+
+    def chosen_opts(self) -> dict:
+        """The tile options this plan was built with (e.g. after tune=1): passing them to
+        another Plan of the same matrix rebuilds an identical replica (same digest)."""
+        i = self.info
+        o = dict(warps=i["warps"], rows_per_warp=i["rows_per_warp"], split_k=i["split_k"],
+                 stages=i["stages"], executor=i["executor"])
+        if self.kind == SPARSE_SPMM:
+            o.update(k_chunk=i["k_chunk"], k_split=i["k_split"])
+            if i["executor"] == 1:
+                o.update(jit_rows=i["jit_rows"], jit_warps=i["jit_warps"])
+        else:
+            o.update(k_chunk=i["k_chunk"])
+            o.pop("split_k")
+            o.pop("stages")
+        return o
 
     def _check_tensor(self, t, name):
         import torch

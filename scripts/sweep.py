@@ -34,7 +34,7 @@ def main():
     ap.add_argument("--grid", default="")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--conv", default="", help="c_in,h,w,batch for a conv layer")
-    ap.add_argument("--flush", default="write", choices=["none", "write", "writeread"])
+    ap.add_argument("--flush", default="write", choices=["none", "write", "writeread", "b2b"])
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     tdt = torch.float16 if args.dtype == "f16" else torch.float32
@@ -65,7 +65,16 @@ def main():
         for _ in range(3):
             fn()
         ms = []
-        for _ in range(args.reps):
+        if args.flush == "b2b":  # back-to-back launches, warm L2: intrinsic kernel duration
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.zero_()
+            e0.record()
+            for _ in range(args.reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = [e0.elapsed_time(e1) / args.reps]
+        for _ in range(args.reps if args.flush != "b2b" else 0):
             if args.flush != "none":
                 flush.zero_()
             if args.flush == "writeread":

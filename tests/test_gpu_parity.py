@@ -384,3 +384,25 @@ def test_jit_closed_forms_and_fallback(f16):
     z = gen.stress_pattern("empty", 50, K, seed=1)
     y, _ = _run_spmm(z, gen.uniform_x(K, 64, seed=3), f16, executor=1)
     assert np.array_equal(y, np.zeros_like(y))
+
+
+# --------------------------------------------------------------------------- autotuner
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("case", [(2048, 512, 392), (256, 64, 3136)])
+def test_tuned_plan_exact_and_replicable(case, f16):
+    # tune=1 picks a configuration by measurement; whatever it picks is exact on
+    # integer data, and its chosen options rebuild an identical replica (same digest)
+    M, K, N = case
+    plan = _exact_case(M, K, N, 90, f16, seed=M + N, tune=1)
+    assert plan.info["tuned_us"] > 0
+    w = gen.int_weights(M, K, 90, seed=M + N, vmax=2 if f16 else 3)
+    rep = srt.Plan.from_csr(w, dtype=_tdt(f16), n_hint=N, **plan.chosen_opts())
+    assert rep.info["digest"] == plan.info["digest"]
+
+
+def test_auto_executor_choice():
+    # auto: JIT for small per-panel code (RN50 p2), plan-driven for large (BERT)
+    small = srt.Plan.from_csr(gen.pruned_weights(256, 64, 90, seed=1), n_hint=25088, executor=2)
+    big = srt.Plan.from_csr(gen.pruned_weights(768, 3072, 90, seed=1), n_hint=16384, executor=2)
+    assert small.info["executor"] == 1 and big.info["executor"] == 0
