@@ -250,6 +250,8 @@ def main():
     ap.add_argument("--executor", type=int, default=2, choices=[0, 1, 2],
                     help="SpMM executor: 0 plan-driven, 1 JIT code generator (the paper's method), "
                          "2 auto")
+    ap.add_argument("--retune", action="store_true", help="re-run the autotuner even if "
+                    "profiles/tuned_<workload>.json exists")
     ap.add_argument("--no-tune", action="store_true",
                     help="skip the offline autotuner (P:259-263); use the heuristic tile choice")
     args = ap.parse_args()
@@ -276,6 +278,12 @@ def main():
     layers, scaling, desc = workload_layers(args.workload, args.sparsity, world)
     plans, xs, ys, host = [], [], [], []
     build_ms, chosen, tuned_us = [], [], []
+    tuned_path = os.path.join(ROOT, "profiles",
+                              f"tuned_{args.workload}_{args.dtype}_s{args.sparsity}_x{args.executor}.json")
+    saved = None
+    if not args.no_tune and not args.retune and os.path.exists(tuned_path):
+        saved = json.load(open(tuned_path))
+    retuned = {}
     for L in layers:
         w, x = make_inputs(L, args.sparsity, rank)
         if L["kind"] == "spmm":
@@ -285,14 +293,17 @@ def main():
         if args.no_tune:
             p = srt.Plan.from_csr(w, dtype=tdt, device=local, **base)
         else:
-            # offline autotuning on rank 0; every rank then builds the chosen
-            # configuration explicitly, so the replicated plans are identical (digests)
-            opts = [None]
-            if rank == 0:
+            # offline autotuning: the configuration chosen by tune=1 is stored in
+            # profiles/tuned_<workload>.json and reused (deterministic, same plans under ncu);
+            # --retune re-runs the timed search on rank 0.  Every rank then builds the chosen
+            # configuration explicitly, so the replicated plans are identical (digests).
+            opts = [saved.get(L["name"]) if saved else None]
+            if opts[0] is None and rank == 0:
                 tuned = srt.Plan.from_csr(w, dtype=tdt, device=local, tune=1, **base)
                 opts = [tuned.chosen_opts()]
                 tuned_us.append(round(tuned.info["tuned_us"], 2))
                 tuned.close()
+                retuned[L["name"]] = opts[0]
             if world > 1:
                 dist.broadcast_object_list(opts, src=0)
             chosen.append(opts[0])
@@ -309,6 +320,10 @@ def main():
         xs.append(X)
         ys.append(Y)
         host.append(x)
+    if retuned and rank == 0 and not saved:
+        os.makedirs(os.path.dirname(tuned_path), exist_ok=True)
+        with open(tuned_path, "w") as f:
+            json.dump(retuned, f, indent=1)
     stream = torch.cuda.current_stream(dev)
     digests = [int(p.info["digest"]) for p, _ in plans]
     replicas_equal = True
@@ -360,7 +375,9 @@ def main():
     if graph is not None:
         for s in range(args.steps):
             flush.zero_()
+            torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" selects these
             graph.replay()
+            torch.cuda.nvtx.range_pop()
             torch.cuda.synchronize()
             step_ms.append(gev[0].elapsed_time(gev[nl]))
             for i in range(nl):
@@ -369,10 +386,12 @@ def main():
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
         for s in range(args.steps):
             flush.zero_()
+            torch.cuda.nvtx.range_push("timed")
             ev[s][0].record(stream)
             for i in range(nl):
                 call(i)
                 ev[s][i + 1].record(stream)
+            torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         step_ms = [ev[s][0].elapsed_time(ev[s][nl]) for s in range(args.steps)]
         for s in range(args.steps):
@@ -415,7 +434,8 @@ def main():
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_{args.dtype}_s{args.sparsity}.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(d["name"])
+        t = json.load(open(tpath)).get(d["name"])
+        traffic = t and t.get("traffic_bytes_per_launch")
     if d["bound"] == "hbm":
         roof = {"bound": "hbm", "achieved": d["alg_bytes"] / sec / 1e9, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s"}
@@ -527,6 +547,8 @@ def main():
                        "executor": {0: "plan-driven", 1: "jit", 2: "auto"}[args.executor],
                        "tuned": None if args.no_tune else chosen,
                        "tuned_us": None if args.no_tune else tuned_us,
+                       "tuned_from": None if args.no_tune else (
+                           os.path.relpath(tuned_path, ROOT) if saved else "timed search in this run"),
                        "parallelism": f"N-sharded x{world}, replicated plan, no collective",
                        "replica_digests_equal": replicas_equal},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -148,9 +148,25 @@ int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void*
   if (!X || !Y) return fail(SPARSE_EINVAL, "X or Y is NULL");
   if (ldx < N || ldy < N) return fail(SPARSE_EINVAL, "ldx and ldy must be >= N");
   std::string err;
-  const int rc = srt::jit_can_launch(plan->p, X, ldx)
-                     ? srt::jit_launch(plan->p, N, X, ldx, Y, ldy, stream, err)
-                     : srt::launch_spmm(plan->p, N, X, ldx, Y, ldy, stream, err);
+  const srt::Plan& p = plan->p;
+  const int S = p.dtype == SPARSE_F16 ? 2 : 4;
+  const void* Xa = X;
+  int64_t lda = ldx;
+  void* scratch = nullptr;
+  if (((uintptr_t)X % 16) != 0 || ((ldx * S) % 16) != 0) {
+    // TMA needs a 16-byte aligned base and row stride: repack on the device (never on the
+    // host); if no scratch can be had, the kernels' element-wise staging path is used
+    if (srt::launch_repack(p.device, p.K, N, S, X, ldx, &scratch, &lda, stream, err) == SPARSE_OK) {
+      Xa = scratch;
+    } else {
+      lda = ldx;
+      scratch = nullptr;
+    }
+  }
+  const int rc = srt::jit_can_launch(p, Xa, lda)
+                     ? srt::jit_launch(p, N, Xa, lda, Y, ldy, stream, err)
+                     : srt::launch_spmm(p, N, Xa, lda, Y, ldy, stream, err);
+  if (scratch) srt::free_repack(p.device, scratch, stream);
   return rc == SPARSE_OK ? ok() : fail(rc, err);
 }
 

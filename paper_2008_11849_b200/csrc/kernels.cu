@@ -741,6 +741,50 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// Row repack of an X whose base or row stride is not 16-byte aligned (TMA needs both):
+// Xp[k][0..N) = X[k][0..N), Xp with a padded row stride.  Pure data movement.
+__global__ void repack_rows(const uint8_t* __restrict__ X, int64_t ldx_b, uint8_t* __restrict__ Xp,
+                            int64_t ldp_b, int64_t N, int S) {
+  const int64_t k = blockIdx.y;
+  const uint8_t* src = X + k * ldx_b;
+  uint8_t* dst = Xp + k * ldp_b;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    if (S == 2)
+      ((uint16_t*)dst)[n] = __ldg((const unsigned short*)src + n);
+    else
+      ((float*)dst)[n] = __ldg((const float*)src + n);
+  }
+}
+
+int launch_repack(int device, int64_t K, int64_t N, int S, const void* X, int64_t ldx, void** Xp,
+                  int64_t* ldp, void* stream, std::string& err) {
+  DeviceGuard dg(device);
+  if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
+  const int64_t per16 = 16 / S;
+  *ldp = (N + per16 - 1) / per16 * per16;
+  cudaError_t e = cudaMallocAsync(Xp, (size_t)(K * *ldp * S), (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *Xp = nullptr;
+    return cuda_fail(e, "cudaMallocAsync(repack)", err);
+  }
+  const unsigned gx = (unsigned)std::min<int64_t>((N + 255) / 256, 64);
+  for (int64_t k0 = 0; k0 < K; k0 += 65535) {
+    const int64_t kk = std::min<int64_t>(65535, K - k0);
+    repack_rows<<<dim3(gx, (unsigned)kk), 256, 0, (cudaStream_t)stream>>>(
+        (const uint8_t*)X + k0 * ldx * S, ldx * S, (uint8_t*)*Xp + k0 * *ldp * S, *ldp * S, N, S);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "repack launch", err);
+  return SPARSE_OK;
+}
+
+void free_repack(int device, void* Xp, void* stream) {
+  DeviceGuard dg(device);
+  cudaFreeAsync(Xp, (cudaStream_t)stream);
+}
+
 int upload_plan(Plan& p, std::string& err) {
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);

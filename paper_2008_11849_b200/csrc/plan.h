@@ -156,5 +156,10 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
                 void* stream, std::string& err);
 int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
                    std::string& err);
+// Unaligned X (base or row stride not a 16-byte multiple): stream-ordered copy into a
+// padded scratch buffer so the TMA paths apply; free_repack releases it (stream-ordered).
+int launch_repack(int device, int64_t K, int64_t N, int S, const void* X, int64_t ldx, void** Xp,
+                  int64_t* ldp, void* stream, std::string& err);
+void free_repack(int device, void* Xp, void* stream);
 
 }  // namespace srt

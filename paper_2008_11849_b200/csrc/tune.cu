@@ -97,9 +97,12 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     return SPARSE_ECUDA;
   }
   int64_t xe, ye, N = base.n_hint;
+  // at run time unaligned X is repacked to a 16-byte row stride first, so time that layout
+  const int64_t per16 = 16 / S;
+  const int64_t ldt = (N + per16 - 1) / per16 * per16;
   if (base.kind == SPARSE_SPMM) {
-    xe = (int64_t)K * N;
-    ye = (int64_t)M * N;
+    xe = (int64_t)K * ldt;
+    ye = (int64_t)M * ldt;
   } else {
     xe = (int64_t)base.c_in * N * base.h * base.w;
     ye = (int64_t)M * N * base.h * base.w;
@@ -140,8 +143,8 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     }
     auto run = [&]() -> int {
       if (base.kind == SPARSE_SPMM) {
-        if (p.executor == 1 && jit_can_launch(p, X, N)) return jit_launch(p, N, X, N, Y, N, st, e2);
-        return launch_spmm(p, N, X, N, Y, N, st, e2);
+        if (p.executor == 1 && jit_can_launch(p, X, ldt)) return jit_launch(p, N, X, ldt, Y, ldt, st, e2);
+        return launch_spmm(p, N, X, ldt, Y, ldt, st, e2);
       }
       return launch_conv3x3(p, N, X, Y, st, e2);
     };

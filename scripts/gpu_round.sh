@@ -16,3 +16,4 @@ for wl in ${WORKLOADS:-rn50_b8}; do
   done
 done
 done
+cp profiles/tuned_*.json gpurun_out/ 2>/dev/null || true
