@@ -486,9 +486,13 @@ def main():
     if not (args.no_dense or args.quick) and rank == 0:
         dense = {}
         prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+        prev_cudnn_tf32 = torch.backends.cudnn.allow_tf32
         torch.backends.cudnn.benchmark = True
+        # fp32 dense context = true fp32 (SGEMM / fp32 cuDNN conv, TF32 off), the paper's
+        # cuBLAS / cuDNN fp32 baselines; fp16 = tensor cores
         for label, ddt, tf32 in [("fp32_sgemm", torch.float32, False), ("fp16_tc", torch.float16, False)]:
             torch.backends.cuda.matmul.allow_tf32 = tf32
+            torch.backends.cudnn.allow_tf32 = tf32
             tot = 0.0
             for i, L in enumerate(layers):
                 w = plans[i][1]
@@ -517,6 +521,7 @@ def main():
             sparse_step = statistics.median(step_ms)
             dense[label] = {"ms_per_step": tot, "speedup_of_sparse": tot / sparse_step}
         torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+        torch.backends.cudnn.allow_tf32 = prev_cudnn_tf32
 
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
