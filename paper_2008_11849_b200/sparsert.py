@@ -69,7 +69,7 @@ class sparse_plan_info_t(ctypes.Structure):
 
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2008_11849_b200._build` "
+        raise ImportError(f"{LIB_PATH} is missing: run `python __graft_entry__.py` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
