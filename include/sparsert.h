@@ -75,7 +75,7 @@ typedef struct {
   int32_t drop_zeros; /* 0 = reject explicit zeros; 1 = drop them */
   /* Tile overrides (0 = automatic).  None of these changes a result except split_k,
      k_chunk and k_split, which fix the per-row summation order. */
-  int32_t warps;         /* warps per CTA (thread groups of the paper's block): 1..8 */
+  int32_t warps;         /* warps per CTA (thread groups of the paper's block): 1..16 */
   int32_t rows_per_warp; /* R: 1, 2, 4, 8 or 16 (R * cols_per_lane <= 128) */
   int32_t k_chunk;       /* Kc: K rows staged per pipeline stage (SpMM: multiple of 8, 8..256);
                             conv: input channels per stage (1..64) */
@@ -83,7 +83,7 @@ typedef struct {
   int32_t k_split;       /* SpMM: CTAs of a thread-block cluster splitting the K chunks, partial
                             tiles reduced in fixed rank order through distributed shared
                             memory (the paper's strategy (a), Fig. 2a): 1,2,4,8 */
-  int32_t stages;        /* SpMM: X/plan pipeline stages (TMA + mbarrier ring): 1..4 */
+  int32_t stages;        /* SpMM: X/plan pipeline stages (TMA + mbarrier ring): 1..8 */
   int32_t executor;      /* SpMM: 0 = plan-driven kernels (default); 2 = auto (JIT where each
                             panel's code is <= 24 KB, else plan-driven); 1 = JIT: the paper's code
                             generator (Sec. 3.5) - per row panel, straight-line PTX with
@@ -92,6 +92,16 @@ typedef struct {
                             aligned falls back to the plan-driven kernels (same results, bitwise). */
   int32_t jit_rows;      /* JIT: rows per panel (accumulator registers per thread), 0 = auto */
   int32_t jit_warps;     /* JIT: warps per CTA (each owns 32 columns), 0 = auto */
+  int32_t x_multicast;   /* SpMM, k_split == 1: CTAs of a thread-block cluster (consecutive row
+                            panels, same N tile) that share every staged X tile through one TMA
+                            multicast load, dividing the L2 -> SM traffic of X: 1, 2, 4 or 8;
+                            0 = 1.  Result-neutral. */
+  int32_t x_source;      /* SpMM: where the executor's FMA loop reads X from.  0 = shared memory
+                            (LDS.128, default); 1 = tensor memory: every staged X chunk is copied
+                            smem -> TMEM (tcgen05.cp, replicated to the 4 lane quarters) and read
+                            with warp-uniform tcgen05.ld, which has ~2x the shared-memory
+                            bandwidth.  Needs split_k = 1, k_split = 1,
+                            x_multicast = 1, k_chunk <= 56 (default 56).  Result-neutral. */
 } sparse_plan_opts;
 
 /* Fill *opts with defaults (kind SPMM, device -1, everything else 0). */
@@ -158,6 +168,8 @@ typedef struct {
   double jit_compile_ms;
   double tuned_us;      /* tune = 1: measured time of the chosen configuration (us) */
   uint64_t digest;      /* FNV-1a of the packed plan: equal digests <=> identical replicas */
+  int32_t x_multicast;  /* CTAs per cluster sharing X tiles (TMA multicast) */
+  int32_t x_source;     /* 0 shared memory, 1 tensor memory */
 } sparse_plan_info_t;
 
 int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out);

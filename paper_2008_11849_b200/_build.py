@@ -29,16 +29,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libsparsert.so (or, for A/B experiments, a variant with extra -D defines
+    into `out`)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     objs = []
-    tmpdir = os.path.join(PKG, "build")
+    tmpdir = os.path.join(PKG, "build" if out is None else "build_variant")
     os.makedirs(tmpdir, exist_ok=True)
     procs = []
     for s in SOURCES:
         obj = os.path.join(tmpdir, s + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c",
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, s), "-o", obj]
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
@@ -53,11 +56,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write("\n".join(logs))
     with open(os.path.join(tmpdir, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
                            "-L/usr/local/cuda/lib64", "-lnvptxcompiler_static", "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

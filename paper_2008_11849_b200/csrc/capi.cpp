@@ -1,6 +1,7 @@
 // C ABI (include/sparsert.h): argument validation, error reporting and plan
 // ownership around the inspector (inspector.cpp) and executors (kernels.cu).
 // No exception crosses this boundary; nothing here computes on the CPU.
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <string>
@@ -62,7 +63,10 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   bo.executor = o.executor;
   bo.jit_rows = o.jit_rows;
   bo.jit_warps = o.jit_warps;
-  if (o.stages < 0 || o.stages > 4) return fail(SPARSE_EUNSUPPORTED, "stages must be in [0, 4]");
+  bo.cm = o.x_multicast;
+  bo.tm = o.x_source;
+  if (o.stages < 0 || o.stages > srt::kMaxStages)
+    return fail(SPARSE_EUNSUPPORTED, "stages must be in [0, 8]");
   sparse_plan_s* h = nullptr;
   try {
     h = new sparse_plan_s();
@@ -228,6 +232,8 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->jit_cubin_bytes = p.jit_cubin_bytes;
   out->jit_compile_ms = p.jit_compile_ms;
   out->tuned_us = p.tuned_us;
+  out->x_multicast = p.cm;
+  out->x_source = p.tm;
   return ok();
 }
 
@@ -239,59 +245,83 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
   const bool f16 = p.dtype == SPARSE_F16;
   const int A = p.entry_align;
   int64_t out = 0;
+  auto emit = [&](int32_t m, int32_t k, float w, int32_t q, int32_t c, int32_t s, int32_t g) {
+    if (out >= cap) return false;
+    if (row) row[out] = m;
+    if (col) col[out] = k;
+    if (value) value[out] = w;
+    if (panel) panel[out] = q;
+    if (chunk) chunk[out] = c;
+    if (slot) slot[out] = s;
+    if (group) group[out] = g;
+    ++out;
+    return true;
+  };
+  const int64_t rowb = (int64_t)p.n_tile * (f16 ? 2 : 4);
   for (int32_t q = 0; q < p.npanels; ++q) {
     for (int32_t c = 0; c < p.nchunks; ++c) {
       const uint8_t* blk = p.blob.data() + p.blk_off[(size_t)q * p.nchunks + c];
       const uint32_t* shdr = (const uint32_t*)blk;
       const uint8_t* ents = blk + p.hdr_bytes;
       for (int s = 0; s < p.Mp; ++s) {
-        const int beg = (int)(shdr[s] & 0xffffu), cnt = (int)(shdr[s] >> 16);
-        const int end = beg + cnt;
-        // same cut as the executor: all groups but the last take per (a multiple of A)
-        int per = (cnt + p.gk - 1) / (p.gk > 0 ? p.gk : 1);
-        per = (per + A - 1) / A * A;
         const int32_t m = p.row_id[(size_t)q * p.Mp + s];
-        for (int e = beg; e < end; ++e) {
-          if (out >= cap) return fail(SPARSE_EINTERNAL, "plan carries more entries than nnz");
-          const uint8_t* rec = ents + (size_t)e * p.entry_bytes;
-          int32_t k = -1;  // conv: decoded below
-          float w;
-          if (f16) {
-            uint16_t a, wh;
-            std::memcpy(&a, rec, 2);
-            std::memcpy(&wh, rec + 2, 2);
-            w = srt::f16_to_f32(wh);
-            if (p.kind == SPARSE_SPMM) k = c * p.kc + a;
-          } else {
-            uint32_t a;
-            std::memcpy(&a, rec, 4);
-            std::memcpy(&w, rec + 4, 4);
-            k = p.kind == SPARSE_SPMM ? (int32_t)(c * p.kc + a) : -1;
-          }
-          if (p.kind == SPARSE_CONV3X3) {
-            int32_t off;
-            if (f16) {
-              int16_t o16;
-              std::memcpy(&o16, rec, 2);
-              off = o16;
-            } else {
-              std::memcpy(&off, rec, 4);
+        if (p.kind == SPARSE_SPMM) {
+          for (int g = 0; g < p.gk; ++g) {
+            const uint32_t h = shdr[s * p.gk + g];
+            const int64_t u0 = h & 0xffffu, nu = h >> 16;
+            for (int64_t e = u0 * A; e < (u0 + nu) * A; ++e) {
+              const uint8_t* rec = ents + e * p.entry_bytes;
+              int64_t xoff;
+              float w;
+              if (f16) {
+                uint16_t a, wh;
+                std::memcpy(&a, rec, 2);
+                std::memcpy(&wh, rec + 2, 2);
+                xoff = (int64_t)a * 16;
+                w = srt::f16_to_f32(wh);
+              } else {
+                uint32_t a;
+                std::memcpy(&a, rec, 4);
+                std::memcpy(&w, rec + 4, 4);
+                xoff = a;
+              }
+              if (xoff % rowb) return fail(SPARSE_EINTERNAL, "plan entry offset not a row multiple");
+              const int64_t kl = xoff / rowb;
+              if (kl == p.kc) {  // neutral padding entry (zero row, -0 weight)
+                if (!(w == 0.0f && std::signbit(w)))
+                  return fail(SPARSE_EINTERNAL, "padding entry with a nonzero weight");
+                continue;
+              }
+              if (m < 0) return fail(SPARSE_EINTERNAL, "entry in an empty row slot");
+              if (!emit(m, (int32_t)(c * p.kc + kl), w, q, c, s, g))
+                return fail(SPARSE_EINTERNAL, "plan carries more entries than nnz");
             }
-            // invert off = ci*sci + (dy-1)*wp + (dx-1), |(dy-1)*wp + (dx-1)| <= wp + 1 < sci / 2
-            const int base = off + p.conv_wp + 1;  // = ci*sci + dy*wp + dx
-            const int ci = base / p.conv_sci;
-            const int rem = base - ci * p.conv_sci;
-            const int dy = rem / p.conv_wp, dx = rem % p.conv_wp;
-            k = (c * p.cc + ci) * 9 + dy * 3 + dx;
           }
-          if (row) row[out] = m;
-          if (col) col[out] = k;
-          if (value) value[out] = w;
-          if (panel) panel[out] = q;
-          if (chunk) chunk[out] = c;
-          if (slot) slot[out] = s;
-          if (group) group[out] = per > 0 ? (e - beg) / per : 0;
-          ++out;
+          continue;
+        }
+        const int beg = (int)(shdr[s] & 0xffffu), cnt = (int)(shdr[s] >> 16);
+        for (int e = beg; e < beg + cnt; ++e) {
+          const uint8_t* rec = ents + (size_t)e * p.entry_bytes;
+          float w;
+          int32_t off;
+          if (f16) {
+            int16_t o16;
+            uint16_t wh;
+            std::memcpy(&o16, rec, 2);
+            std::memcpy(&wh, rec + 2, 2);
+            off = o16;
+            w = srt::f16_to_f32(wh);
+          } else {
+            std::memcpy(&off, rec, 4);
+            std::memcpy(&w, rec + 4, 4);
+          }
+          // invert off = ci*sci + (dy-1)*wp + (dx-1), |(dy-1)*wp + (dx-1)| <= wp + 1 < sci / 2
+          const int base = off + p.conv_wp + 1;  // = ci*sci + dy*wp + dx
+          const int ci = base / p.conv_sci;
+          const int rem = base - ci * p.conv_sci;
+          const int dy = rem / p.conv_wp, dx = rem % p.conv_wp;
+          if (!emit(m, (c * p.cc + ci) * 9 + dy * 3 + dx, w, q, c, s, 0))
+            return fail(SPARSE_EINTERNAL, "plan carries more entries than nnz");
         }
       }
     }

@@ -243,6 +243,14 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     }
     p.gk = gk;
     p.n_tile = (32 / gk) * p.C;
+    if (o.tm != 0 && o.tm != 1) {
+      err = "x_source must be 0 (shared memory) or 1 (tensor memory)";
+      return SPARSE_EINVAL;
+    }
+    if (o.tm && (gk != 1 || o.k_chunk > 56)) {
+      err = "x_source = 1 (tensor memory) needs split_k = 1 and k_chunk <= 56";
+      return SPARSE_EUNSUPPORTED;
+    }
     if (o.k_chunk) {
       if (o.k_chunk % 8 || o.k_chunk < 8 || o.k_chunk > 256) {
         err = "k_chunk must be a multiple of 8 in [8, 256]";
@@ -250,11 +258,12 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       }
       p.kc = o.k_chunk;
     } else {
-      p.kc = 64;
-      if (K <= 96) p.kc = (K + 7) / 8 * 8;
+      p.kc = o.tm ? 56 : 64;  // tensor memory: two 256-column buffers of kc rows + a zero row
+      if (K <= (o.tm ? 56 : 96)) p.kc = (K + 7) / 8 * 8;
     }
     p.nchunks = (K + p.kc - 1) / p.kc;
-    p.x_stage_bytes = p.kc * p.n_tile * S;
+    // kc X rows plus one zero row (target of the neutral padding entries), 128-byte aligned
+    p.x_stage_bytes = (int)(((int64_t)(p.kc + 1) * p.n_tile * S + 127) & ~int64_t(127));
   } else {
     // implicit im2col conv: padded-position tiles
     p.c_in = o.c_in;
@@ -309,7 +318,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   }
   p.warps = o.warps ? o.warps : 8;
   if (p.warps < 1 || p.warps > kMaxWarps) {
-    err = "warps must be in [1, 8]";
+    err = "warps must be in [1, 16]";
     return SPARSE_EUNSUPPORTED;
   }
   {
@@ -364,8 +373,25 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     return SPARSE_EUNSUPPORTED;
   }
   if (p.ks > p.nchunks) p.ks = 1 << (31 - __builtin_clz((unsigned)p.nchunks));
+  p.cm = o.cm ? o.cm : 1;
+  if (p.cm != 1 && p.cm != 2 && p.cm != 4 && p.cm != 8) {
+    err = "x_multicast must be 1, 2, 4 or 8";
+    return SPARSE_EUNSUPPORTED;
+  }
+  if (p.cm > 1 && (o.kind != SPARSE_SPMM || p.ks > 1)) {
+    err = "x_multicast > 1 needs an SpMM plan with k_split = 1";
+    return SPARSE_EUNSUPPORTED;
+  }
+  p.tm = o.kind == SPARSE_SPMM ? o.tm : 0;
+  if (p.tm && (p.ks > 1 || p.cm > 1 || p.R > 8 || p.warps % 4)) {
+    err = "x_source = 1 (tensor memory) needs k_split = 1, x_multicast = 1, rows_per_warp <= 8 "
+          "and warps a multiple of 4";
+    return SPARSE_EUNSUPPORTED;
+  }
   p.Mp = p.warps * p.R;
   p.npanels = (M + p.Mp - 1) / p.Mp;
+  // a multicast cluster takes cm consecutive panels: pad with empty panels (no rows)
+  p.npanels = (p.npanels + p.cm - 1) / p.cm * p.cm;
 
   // ---------------- a2: row grouping + LPT panels ----------------
   std::vector<int32_t> order(M);
@@ -408,77 +434,101 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   }
 
   // ---------------- a4: chunking + packing ----------------
-  // header: uint32 per slot = start | count << 16 (entry indices relative to the block's
-  // entry array); every slot's entries start on a multiple of entry_align so that one
-  // 128-bit broadcast load yields entry_align entries.
-  const int hdr = (int)align16((int64_t)p.Mp * 4);
-  p.hdr_bytes = hdr;
+  // (block layouts in plan.h)
   const int A = p.entry_align;
+  const int G = o.kind == SPARSE_SPMM ? p.gk : 1;
+  const int hdr = (int)align16((int64_t)p.Mp * G * 4);
+  p.hdr_bytes = hdr;
   p.blk_off.assign((size_t)p.npanels * p.nchunks + 1, 0);
   p.blob.clear();
   p.blob.reserve((size_t)(kept * p.entry_bytes +
-                          (int64_t)p.npanels * p.nchunks * (hdr + 16 + p.Mp * 16)));
+                          (int64_t)p.npanels * p.nchunks * (hdr + 16 + p.Mp * G * 16)));
   std::vector<int32_t> cursor(M, 0);
-  std::vector<uint32_t> shdr(p.Mp);
+  std::vector<uint32_t> shdr((size_t)p.Mp * G);
   std::vector<uint8_t> ents;
+  const int64_t rowb = (int64_t)p.n_tile * S;  // bytes of one staged X row (SpMM)
+  auto put_spmm = [&](int32_t kl, float w, uint16_t wh) {
+    uint8_t rec[8];
+    if (f16) {
+      const uint16_t o16 = (uint16_t)((int64_t)kl * rowb / 16);
+      std::memcpy(rec, &o16, 2);
+      std::memcpy(rec + 2, &wh, 2);
+    } else {
+      const uint32_t o32 = (uint32_t)((int64_t)kl * rowb);
+      std::memcpy(rec, &o32, 4);
+      std::memcpy(rec + 4, &w, 4);
+    }
+    ents.insert(ents.end(), rec, rec + p.entry_bytes);
+  };
   int64_t maxblk = 0;
   for (int32_t q = 0; q < p.npanels; ++q) {
     for (int32_t m : panel_rows[q]) cursor[m] = 0;
     for (int32_t c = 0; c < p.nchunks; ++c) {
       const int32_t k0 = c * p.kc, k1 = std::min(K, k0 + p.kc);
       ents.clear();
-      int32_t cnt = 0;
+      int32_t cnt = 0;  // entries (conv) / units (SpMM) so far
       for (int s = 0; s < p.Mp; ++s) {
-        while (cnt % A) {  // align the slot's first entry
-          ents.insert(ents.end(), (size_t)p.entry_bytes, (uint8_t)0);
-          ++cnt;
-        }
-        const int32_t start = cnt;
         const int32_t m = p.row_id[(size_t)q * p.Mp + s];
+        int32_t e0 = 0, e1 = 0;  // this row's entries in [k0, k1): rows[m][e0, e1)
         if (m >= 0) {
-          auto& rr = rows[m];
           int32_t& cur = cursor[m];
-          while (cur < (int32_t)rr.size() && rr[cur].k < k1) {
-            const Entry& en = rr[cur];
+          e0 = cur;
+          while (cur < (int32_t)rows[m].size() && rows[m][cur].k < k1) ++cur;
+          e1 = cur;
+        }
+        if (o.kind == SPARSE_SPMM) {
+          // G contiguous k-ascending pieces, all but the last of `per` entries
+          const int32_t n = e1 - e0;
+          int32_t per = (n + G - 1) / G;
+          per = (per + A - 1) / A * A;
+          for (int g = 0; g < G; ++g) {
+            const int32_t lo = std::min(g * per, n), hi = std::min(lo + per, n);
+            const int32_t units = (hi - lo + A - 1) / A;
+            for (int32_t e = e0 + lo; e < e0 + hi; ++e)
+              put_spmm(rows[m][e].k - k0, rows[m][e].w, rows[m][e].wh);
+            for (int32_t e = hi - lo; e < units * A; ++e)  // neutral: -0 * (zero row)
+              put_spmm(p.kc, -0.0f, (uint16_t)0x8000u);
+            if (cnt > 65535 || units > 65535) {
+              err = "internal: block unit count overflow (lower k_chunk)";
+              return SPARSE_EUNSUPPORTED;
+            }
+            shdr[(size_t)s * G + g] = (uint32_t)cnt | ((uint32_t)units << 16);
+            cnt += units;
+          }
+        } else {
+          while (cnt % A) {  // align the slot's first entry
+            ents.insert(ents.end(), (size_t)p.entry_bytes, (uint8_t)0);
+            ++cnt;
+          }
+          const int32_t start = cnt;
+          for (int32_t e = e0; e < e1; ++e) {
+            const Entry& en = rows[m][e];
             const int32_t kl = en.k - k0;
+            const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
+            const int32_t off = ci * p.conv_sci + (dy - 1) * p.conv_wp + (dx - 1);
             uint8_t rec[8];
-            if (o.kind == SPARSE_SPMM) {
-              if (f16) {
-                const uint16_t k16 = (uint16_t)kl;
-                std::memcpy(rec, &k16, 2);
-                std::memcpy(rec + 2, &en.wh, 2);
-              } else {
-                const uint32_t k32 = (uint32_t)kl;
-                std::memcpy(rec, &k32, 4);
-                std::memcpy(rec + 4, &en.w, 4);
-              }
+            if (f16) {
+              const int16_t o16 = (int16_t)off;
+              std::memcpy(rec, &o16, 2);
+              std::memcpy(rec + 2, &en.wh, 2);
             } else {
-              const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
-              const int32_t off = ci * p.conv_sci + (dy - 1) * p.conv_wp + (dx - 1);
-              if (f16) {
-                const int16_t o16 = (int16_t)off;
-                std::memcpy(rec, &o16, 2);
-                std::memcpy(rec + 2, &en.wh, 2);
-              } else {
-                std::memcpy(rec, &off, 4);
-                std::memcpy(rec + 4, &en.w, 4);
-              }
+              std::memcpy(rec, &off, 4);
+              std::memcpy(rec + 4, &en.w, 4);
             }
             ents.insert(ents.end(), rec, rec + p.entry_bytes);
             ++cnt;
-            ++cur;
           }
+          if (cnt > 65535) {
+            err = "internal: block entry count overflow (lower k_chunk)";
+            return SPARSE_EUNSUPPORTED;
+          }
+          shdr[s] = (uint32_t)start | ((uint32_t)(cnt - start) << 16);
         }
-        if (cnt > 65535) {
-          err = "internal: block entry count overflow (lower k_chunk)";
-          return SPARSE_EUNSUPPORTED;
-        }
-        shdr[s] = (uint32_t)start | ((uint32_t)(cnt - start) << 16);
       }
       const size_t st = p.blob.size();
       p.blk_off[(size_t)q * p.nchunks + c] = (int64_t)st;
       p.blob.resize(st + hdr, 0);
-      std::memcpy(p.blob.data() + st, shdr.data(), (size_t)p.Mp * 4);
+      std::memcpy(p.blob.data() + st, shdr.data(), (size_t)p.Mp * G * 4);
       p.blob.insert(p.blob.end(), ents.begin(), ents.end());
       p.blob.resize((size_t)align16((int64_t)p.blob.size()), 0);
       maxblk = std::max<int64_t>(maxblk, (int64_t)(p.blob.size() - st));
@@ -487,6 +537,17 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   p.blk_off[(size_t)p.npanels * p.nchunks] = (int64_t)p.blob.size();
   if (p.blob.empty()) p.blob.resize(16, 0);
   p.max_blk_bytes = (int32_t)maxblk;
+  if (o.kind == SPARSE_SPMM) {
+    // fixed block stride: block bi lives at bi * max_blk_bytes, so the executor computes a
+    // chunk's plan address without a dependent global load on its pipeline refill path
+    const int64_t nb = (int64_t)p.npanels * p.nchunks;
+    std::vector<uint8_t> fixed((size_t)std::max<int64_t>(16, nb * maxblk), 0);
+    for (int64_t bi = 0; bi < nb; ++bi)
+      std::memcpy(fixed.data() + bi * maxblk, p.blob.data() + p.blk_off[bi],
+                  (size_t)(p.blk_off[bi + 1] - p.blk_off[bi]));
+    for (int64_t bi = 0; bi <= nb; ++bi) p.blk_off[bi] = bi * maxblk;
+    p.blob.swap(fixed);
+  }
 
   // pipeline depth and shared memory
   int stage_bytes = p.x_stage_bytes + p.max_blk_bytes;
@@ -495,12 +556,23 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // k_split == 1: persistent CTAs, the ring runs across tiles; k_split > 1: one tile
     // per CTA, no point in more stages than chunks
     const int per_chunks = (p.nchunks + p.ks - 1) / p.ks;
-    int stages = o.stages ? o.stages : 2;
+    // default depth (stages = 0, or -1 from the tuner): as many stages as fit in ~200 KB
+    // (one CTA per SM, the deepest X pipeline); stages = -2 (tuner): ~100 KB, two CTAs per
+    // SM.  At least 2 (1 if a single stage needs more than half of the budget), at most 8.
+    int stages = o.stages;
+    if (stages <= 0) {
+      const int budget = (stages == -2 ? 100 : 200) * 1024;
+      stages = std::max(1, std::min(kMaxStages, budget / stage_bytes));
+      if (stages == 1 && 2 * stage_bytes + 128 <= 227 * 1024) stages = 2;
+    }
     if (p.ks > 1) stages = std::min(stages, per_chunks);
     stages = std::max(1, stages);
     p.stages = stages;
     p.red_bytes = p.ks > 1 ? p.Mp * p.n_tile * 4 : 0;
+    if (p.tm) p.stages = std::max(p.stages, std::min(3, 227 * 1024 / stage_bytes));
     p.smem_bytes = std::max(p.stages * stage_bytes, p.red_bytes) + 128;  // + mbarriers
+    // tensor memory plans allocate all 512 TMEM columns: one CTA per SM (> half the smem)
+    if (p.tm) p.smem_bytes = std::max(p.smem_bytes, 116 * 1024);
   } else {
     p.stages = 2;
     p.red_bytes = 0;
@@ -535,7 +607,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   uint64_t h = 1469598103934665603ull;
   const int32_t cfg[] = {p.M,  p.K,      p.dtype,   p.kind,    p.c_in,   p.h,
                          p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
-                         p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks};
+                         p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

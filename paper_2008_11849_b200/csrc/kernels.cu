@@ -108,6 +108,43 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
       : "memory");
 }
 
+// ---- thread-block-cluster helpers (X multicast clusters)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cta address of this CTA -> shared::cluster address of the same offset in CTA `rank`
+__device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
+                   bar_cluster), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_cluster(uint32_t addr_cluster, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr_cluster), "r"(v)
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// TMA 2-D box multicast to the CTAs of `mask` (same smem offset and mbarrier offset in each)
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                               uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+      : "memory");
+}
+
 // acc += w * x for fp16 w, x with the product exact in fp32 and an fp32
 // accumulator: mixed-precision FMA (sm_100 "fma.rn.f32.f16", SASS FHFMA).
 __device__ __forceinline__ void fma_h(float& acc, uint16_t w, uint16_t x) {
@@ -120,81 +157,205 @@ __device__ __forceinline__ void fma_h2(float& a0, float& a1, uint16_t w, uint32_
       : "h"(w), "r"(x2));
 }
 
+// Inner loop of Alg. 3 for one thread group, one row and one staged chunk: `cnt`
+// 16-byte units of packed entries (plan.h), each one warp-uniform broadcast load;
+// per entry one 128-bit shared load of the lane's C columns of X row k and C FMAs.
+// Entries are applied in storage (k-ascending) order; neutral padding entries
+// (-0 times the zero row) leave acc unchanged bit for bit.
+__device__ __forceinline__ void fma4(float (&acc)[4], uint32_t wbits, const float4 x) {
+  const float w = __uint_as_float(wbits);
+  acc[0] = fmaf(w, x.x, acc[0]);
+  acc[1] = fmaf(w, x.y, acc[1]);
+  acc[2] = fmaf(w, x.z, acc[2]);
+  acc[3] = fmaf(w, x.w, acc[3]);
+}
+__device__ __forceinline__ void fma8h(float (&acc)[8], uint32_t en, const uint4 xv) {
+  const uint16_t w = (uint16_t)(en >> 16);
+  fma_h2(acc[0], acc[1], w, xv.x);
+  fma_h2(acc[2], acc[3], w, xv.y);
+  fma_h2(acc[4], acc[5], w, xv.z);
+  fma_h2(acc[6], acc[7], w, xv.w);
+}
+
 template <bool F16>
 struct EntryOps;
 
 template <>
-struct EntryOps<false> {  // {uint32 k_local, float w}; 2 per 16 bytes
-  static constexpr int EB = 8;
-  static constexpr int A = 2;
-  template <int C, int ROWB>
-  __device__ __forceinline__ static void run(float (&acc)[C], const uint8_t* ents, int beg,
-                                             int cnt, const uint8_t* xs) {
-    int e = 0;
-    for (; e + 4 <= cnt; e += 4) {
-      const uint4 p0 = *(const uint4*)(ents + (beg + e) * EB);
-      const uint4 p1 = *(const uint4*)(ents + (beg + e + 2) * EB);
-      const uint32_t k[4] = {p0.x, p0.z, p1.x, p1.z};
-      const uint32_t w[4] = {p0.y, p0.w, p1.y, p1.w};
-      float4 xv[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) xv[j] = *(const float4*)(xs + k[j] * ROWB);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float wf = __uint_as_float(w[j]);
-        acc[0] = fmaf(wf, xv[j].x, acc[0]);
-        acc[1] = fmaf(wf, xv[j].y, acc[1]);
-        acc[2] = fmaf(wf, xv[j].z, acc[2]);
-        acc[3] = fmaf(wf, xv[j].w, acc[3]);
-      }
-    }
-    for (; e < cnt; ++e) {
-      const uint2 en = *(const uint2*)(ents + (beg + e) * EB);
-      const float4 xv = *(const float4*)(xs + en.x * ROWB);
-      const float wf = __uint_as_float(en.y);
-      acc[0] = fmaf(wf, xv.x, acc[0]);
-      acc[1] = fmaf(wf, xv.y, acc[1]);
-      acc[2] = fmaf(wf, xv.z, acc[2]);
-      acc[3] = fmaf(wf, xv.w, acc[3]);
-    }
+struct EntryOps<false> {  // unit = 2 x {uint32 xoff (bytes), float w}
+  static constexpr int C = 4;
+  __device__ __forceinline__ static void unit(float (&acc)[4], const uint4 p, const uint8_t* xs) {
+    const float4 x0 = *(const float4*)(xs + p.x);
+    const float4 x1 = *(const float4*)(xs + p.z);
+    fma4(acc, p.y, x0);
+    fma4(acc, p.w, x1);
   }
 };
 
 template <>
-struct EntryOps<true> {  // {uint16 k_local, half w}; 4 per 16 bytes
-  static constexpr int EB = 4;
-  static constexpr int A = 4;
-  __device__ __forceinline__ static void one(float (&acc)[8], uint32_t en, const uint8_t* xs,
-                                             int ROWB) {
-    const uint4 xv = *(const uint4*)(xs + (en & 0xffffu) * ROWB);
-    const uint16_t w = (uint16_t)(en >> 16);
-    fma_h2(acc[0], acc[1], w, xv.x);
-    fma_h2(acc[2], acc[3], w, xv.y);
-    fma_h2(acc[4], acc[5], w, xv.z);
-    fma_h2(acc[6], acc[7], w, xv.w);
+struct EntryOps<true> {  // unit = 4 x {uint16 xoff (16-byte units), half w}
+  static constexpr int C = 8;
+  __device__ __forceinline__ static const uint8_t* xrow(const uint8_t* xs, uint32_t en) {
+    return xs + ((en & 0xffffu) << 4);
   }
-  template <int C, int ROWB>
-  __device__ __forceinline__ static void run(float (&acc)[C], const uint8_t* ents, int beg,
-                                             int cnt, const uint8_t* xs) {
-    int e = 0;
-    for (; e + 4 <= cnt; e += 4) {
-      const uint4 q = *(const uint4*)(ents + (beg + e) * EB);
-      const uint32_t en[4] = {q.x, q.y, q.z, q.w};
-      uint4 xv[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) xv[j] = *(const uint4*)(xs + (en[j] & 0xffffu) * ROWB);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint16_t w = (uint16_t)(en[j] >> 16);
-        fma_h2(acc[0], acc[1], w, xv[j].x);
-        fma_h2(acc[2], acc[3], w, xv[j].y);
-        fma_h2(acc[4], acc[5], w, xv[j].z);
-        fma_h2(acc[6], acc[7], w, xv[j].w);
-      }
-    }
-    for (; e < cnt; ++e) one(acc, *(const uint32_t*)(ents + (beg + e) * EB), xs, ROWB);
+  __device__ __forceinline__ static void unit(float (&acc)[8], const uint4 q, const uint8_t* xs) {
+    const uint4 x0 = *(const uint4*)xrow(xs, q.x);
+    const uint4 x1 = *(const uint4*)xrow(xs, q.y);
+    const uint4 x2 = *(const uint4*)xrow(xs, q.z);
+    const uint4 x3 = *(const uint4*)xrow(xs, q.w);
+    fma8h(acc, q.x, x0);
+    fma8h(acc, q.y, x1);
+    fma8h(acc, q.z, x2);
+    fma8h(acc, q.w, x3);
   }
 };
+
+// One thread group's R rows over one staged chunk.  The rows are walked jointly for
+// their common unit count (R independent load->FMA chains per step: the latency of the
+// broadcast plan load and of the X load of one row hides behind the others), then each
+// row's remaining units.  Every row still applies its own entries in storage
+// (k-ascending) order, so the result is the same as walking the rows one by one.
+#ifndef SRT_JOINT
+#define SRT_JOINT 1
+#endif
+template <bool F16>
+__device__ __forceinline__ void run_one_row(float (&acc)[F16 ? 8 : 4], const uint4* up, int u, int cnt,
+                                            const uint8_t* xs) {
+  using E = EntryOps<F16>;
+#pragma unroll 1
+  for (; u + 2 <= cnt; u += 2) {
+    const uint4 q0 = up[u], q1 = up[u + 1];
+    E::unit(acc, q0, xs);
+    E::unit(acc, q1, xs);
+  }
+  if (u < cnt) E::unit(acc, up[u], xs);
+}
+
+template <bool F16, int R>
+__device__ __forceinline__ void run_rows(float (&acc)[R][F16 ? 8 : 4], const uint32_t (&h)[R],
+                                         const uint4* ents, const uint8_t* xs) {
+  using E = EntryOps<F16>;
+#if SRT_JOINT == 0
+#pragma unroll
+  for (int r = 0; r < R; ++r) run_one_row<F16>(acc[r], ents + (h[r] & 0xffffu), 0, (int)(h[r] >> 16), xs);
+#else
+  constexpr int P = (SRT_JOINT == 2 && R > 2) ? 2 : R;  // rows walked jointly
+#pragma unroll
+  for (int r0 = 0; r0 < R; r0 += P) {
+    int mn = (int)(h[r0] >> 16);
+#pragma unroll
+    for (int r = 1; r < P; ++r) mn = min(mn, (int)(h[r0 + r] >> 16));
+#pragma unroll 1
+    for (int u = 0; u < mn; ++u) {
+      uint4 q[P];
+#pragma unroll
+      for (int r = 0; r < P; ++r) q[r] = ents[(h[r0 + r] & 0xffffu) + u];
+#pragma unroll
+      for (int r = 0; r < P; ++r) E::unit(acc[r0 + r], q[r], xs);
+    }
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+      run_one_row<F16>(acc[r0 + r], ents + (h[r0 + r] & 0xffffu), mn, (int)(h[r0 + r] >> 16), xs);
+  }
+#endif
+}
+
+// ---- TMEM X source (tcgen05): X rows of a chunk live in tensor memory, replicated to the
+// four 32-lane quarters, so every warp reads row k of its 32 lanes with one warp-uniform
+// tcgen05.ld (X row k of a 512-byte staged row -> TMEM columns 4k..4k+3 of each lane).
+__device__ __forceinline__ void ldtm4(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tm_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// shared-memory matrix descriptor (sm_100, SWIZZLE_NONE) of one 512-byte X row seen as a
+// 32 x 16-byte matrix: 8-row core matrices 128 bytes apart (stride byte offset)
+__device__ __forceinline__ uint64_t tm_row_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128u >> 4) << 32) | ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void tm_cp_row(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+}
+__device__ __forceinline__ void tm_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+template <bool F16>
+struct TmOps;
+template <>
+struct TmOps<false> {  // unit = 2 x {uint32 xoff = 512 k, float w}: TMEM column 4k = xoff >> 7
+  __device__ __forceinline__ static void load(const uint4 q, uint32_t tq, uint32_t (&x)[2][4]) {
+    ldtm4(tq + (q.x >> 7), x[0]);
+    ldtm4(tq + (q.z >> 7), x[1]);
+  }
+  __device__ __forceinline__ static void fma(float (&acc)[4], const uint4 q, const uint32_t (&x)[2][4]) {
+    fma4(acc, q.y, make_float4(__uint_as_float(x[0][0]), __uint_as_float(x[0][1]),
+                               __uint_as_float(x[0][2]), __uint_as_float(x[0][3])));
+    fma4(acc, q.w, make_float4(__uint_as_float(x[1][0]), __uint_as_float(x[1][1]),
+                               __uint_as_float(x[1][2]), __uint_as_float(x[1][3])));
+  }
+  static constexpr int NL = 2;
+};
+template <>
+struct TmOps<true> {  // unit = 4 x {uint16 xoff16 = 32 k, half w}: TMEM column 4k = xoff16 >> 3
+  __device__ __forceinline__ static void load(const uint4 q, uint32_t tq, uint32_t (&x)[4][4]) {
+    ldtm4(tq + ((q.x & 0xffffu) >> 3), x[0]);
+    ldtm4(tq + ((q.y & 0xffffu) >> 3), x[1]);
+    ldtm4(tq + ((q.z & 0xffffu) >> 3), x[2]);
+    ldtm4(tq + ((q.w & 0xffffu) >> 3), x[3]);
+  }
+  __device__ __forceinline__ static void fma(float (&acc)[8], const uint4 q, const uint32_t (&x)[4][4]) {
+    fma8h(acc, q.x, make_uint4(x[0][0], x[0][1], x[0][2], x[0][3]));
+    fma8h(acc, q.y, make_uint4(x[1][0], x[1][1], x[1][2], x[1][3]));
+    fma8h(acc, q.z, make_uint4(x[2][0], x[2][1], x[2][2], x[2][3]));
+    fma8h(acc, q.w, make_uint4(x[3][0], x[3][1], x[3][2], x[3][3]));
+  }
+  static constexpr int NL = 4;
+};
+
+// run_rows with X from TMEM (tq = this warp's lane quarter + the chunk's buffer column): the
+// R rows are walked jointly for their common unit count (one tcgen05.wait::ld per step of R
+// rows), then each row's remaining units.
+template <bool F16, int R>
+__device__ __forceinline__ void run_rows_tm(float (&acc)[R][F16 ? 8 : 4], const uint32_t (&h)[R],
+                                            const uint4* ents, uint32_t tq) {
+  using T = TmOps<F16>;
+  int mn = (int)(h[0] >> 16);
+#pragma unroll
+  for (int r = 1; r < R; ++r) mn = min(mn, (int)(h[r] >> 16));
+#pragma unroll 1
+  for (int u = 0; u < mn; ++u) {
+    uint4 q[R];
+    uint32_t x[R][T::NL][4];
+#pragma unroll
+    for (int r = 0; r < R; ++r) q[r] = ents[(h[r] & 0xffffu) + u];
+#pragma unroll
+    for (int r = 0; r < R; ++r) T::load(q[r], tq, x[r]);
+    tm_wait_ld();
+#pragma unroll
+    for (int r = 0; r < R; ++r) T::fma(acc[r], q[r], x[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint4* up = ents + (h[r] & 0xffffu);
+    const int cnt = (int)(h[r] >> 16);
+#pragma unroll 1
+    for (int u = mn; u < cnt; ++u) {
+      const uint4 q = up[u];
+      uint32_t x[T::NL][4];
+      T::load(q, tq, x);
+      tm_wait_ld();
+      T::fma(acc[r], q, x);
+    }
+  }
+}
 
 // ------------------------------------------------------------------ SpMM
 struct SpmmArgs {
@@ -205,88 +366,185 @@ struct SpmmArgs {
   uint8_t* Y;
   int64_t ldx, ldy, N;
   int32_t K, kc, nchunks, Mp, ks, stages, npanels;
-  int32_t x_stage_bytes, stage_bytes, hdr_bytes, bar_off;
-  int32_t use_tma, vec_y;
+  int32_t x_stage_bytes, stage_bytes, hdr_bytes, bar_off, blk_bytes;
+  int32_t use_tma, vec_y, cm;
 };
 
-template <int R, int GK, bool F16>
-__global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUtensorMap tmap,
+template <int R, int GK, bool F16, bool TM>
+__global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUtensorMap tmap,
                                                    const SpmmArgs a) {
   constexpr int C = F16 ? 8 : 4;  // columns per lane (16 bytes of X)
   constexpr int S = F16 ? 2 : 4;  // element bytes
   constexpr int L = 32 / GK;      // lanes per thread group
   constexpr int NT = L * C;       // columns per CTA
   constexpr int ROWB = NT * S;    // bytes per staged X row
-  using E = EntryOps<F16>;
   extern __shared__ __align__(1024) uint8_t smem[];
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int nwarps = (blockDim.x >> 5) - 1;  // consumer warps; warp `nwarps` is the producer
+  const int nwarps = blockDim.x >> 5;  // every warp consumes (no dedicated producer warp)
   const int g = lane / L, li = lane % L;
   const int col = li * C;
   // Work decomposition.  k_split == 1: persistent CTAs walk the (panel, N tile) tiles
-  // t = blockIdx.x + j * gridDim.x with the panel index fastest, so CTAs running together
-  // read the same X tile (L2 reuse) and the producer prefetches across tile boundaries.
+  // t = blockIdx.x + i * gridDim.x with the panel index fastest, so CTAs running together
+  // read the same X tile (L2 reuse); the ring of stages runs across tile boundaries.
   // k_split > 1: one tile per cluster; CTA rank r of the cluster takes chunk slice r.
   const bool persistent = a.ks == 1;
   const int rank = persistent ? 0 : (int)(blockIdx.x % a.ks);
-  const int ntn = (int)((a.N + NT - 1) / NT);
   const int np = a.npanels;
-  const int ntiles = persistent ? np * ntn : 1;
+  // X multicast cluster (persistent only): cm CTAs take panels pg*cm + crank of the same tile
+  const int cm = a.cm;
+  const uint32_t crank = cm > 1 ? cluster_rank() : 0u;
+  const int cid = (int)blockIdx.x / cm, ncl = (int)gridDim.x / cm;
+  const int npg = np / cm;
+  const int ntiles = persistent ? npg * (int)((a.N + NT - 1) / NT) : 1;
+  const int my_tiles = !persistent ? 1 : (ntiles > cid ? (ntiles - 1 - cid) / ncl + 1 : 0);
   const int cps = (a.nchunks + a.ks - 1) / a.ks;
   const int c_begin = rank * cps;
   const int nloc = max(0, min(a.nchunks, c_begin + cps) - c_begin);
-  // tile walker without divisions in the loop (64-bit / runtime-divisor division is
-  // emulated on the GPU and used to dominate small-K layers)
-  struct TileIter {
-    int t, panel, nt, step, sd, sm;
-  };
-  auto tile_begin = [&]() {
-    TileIter it;
+  const int total = my_tiles * nloc;  // chunks this CTA consumes, in ring order
+  // tile ti of this CTA (cluster): panel group fastest, so clusters running together read
+  // the same X tile (L2 reuse); the ring of stages runs across tile boundaries
+  auto tile_of = [&](int ti, int& pg, int64_t& n0) {
     if (persistent) {
-      it.t = (int)blockIdx.x;
-      it.panel = it.t % np;
-      it.nt = it.t / np;
-      it.step = (int)gridDim.x;
-      it.sd = it.step / np;
-      it.sm = it.step % np;
+      const int t = cid + ti * ncl;
+      pg = t % npg;
+      n0 = (int64_t)(t / npg) * NT;
     } else {
-      it.t = 0;
-      it.panel = (int)(blockIdx.x / a.ks);
-      it.nt = (int)blockIdx.y;
-      it.step = 1;
-      it.sd = 0;
-      it.sm = 0;
-    }
-    return it;
-  };
-  auto tile_next = [&](TileIter& it) {
-    it.t += it.step;
-    it.nt += it.sd;
-    it.panel += it.sm;
-    if (it.panel >= np) {
-      it.panel -= np;
-      it.nt += 1;
+      pg = (int)(blockIdx.x / a.ks);
+      n0 = (int64_t)blockIdx.y * NT;
     }
   };
   const uint32_t full0 = smem_u32(smem + a.bar_off);
-  const uint32_t empty0 = full0 + 8 * 4;
+  uint32_t* ctr = (uint32_t*)(smem + a.bar_off + 8 * kMaxStages);  // releases per ring slot
 
+  // the zero row after the kc X rows of every stage (target of neutral padding entries)
+  for (int s = 0; s < a.stages; ++s)
+    for (int i = tid; i < ROWB / 16; i += blockDim.x)
+      *(uint4*)(smem + s * a.stage_bytes + a.kc * ROWB + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
+  if (tid < kMaxStages) ctr[tid] = 0u;
+  // TMEM X source: chunk q lives in TMEM buffer q & 1 (columns 256 b .. 256 b + 4 kc, zero
+  // row at column 256 b + 4 kc), replicated in the four 32-lane quarters
+  uint32_t* tslot = (uint32_t*)(smem + a.bar_off + 8 * kMaxStages + 4 * kMaxStages + 16);
+  if (TM && warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
   if (tid == 0) {
-    for (int s = 0; s < a.stages; ++s) {
-      mbar_init(full0 + 8 * s, a.use_tma ? 1 : 33);
-      mbar_init(empty0 + 8 * s, nwarps);
-    }
+    for (int s = 0; s < a.stages; ++s) mbar_init(full0 + 8 * s, a.use_tma ? 1 : 33);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
+  if (TM) tm_fence_before();
   __syncthreads();
+  if (TM) tm_fence_after();
+  if (cm > 1) cluster_sync_all();  // every CTA's barriers exist before anyone fills them
+  const uint32_t tbase = TM ? *tslot : 0u;
+  if (TM && warp < 4) {  // zero rows of both TMEM buffers, one lane quarter per warp
+    const uint32_t tz = tbase + (((uint32_t)warp * 32u) << 16) + 4u * (uint32_t)a.kc;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %1, %1, %1};" ::"r"(tz + 256u * b),
+                   "r"(0u)
+                   : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  if (TM) {
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+  }
+  // TMEM fill of staged chunk q (smem ring slot) into buffer q & 1 of this warp's lane
+  // quarter: the nwarps / 4 warps of a quarter split the kc X rows (LDS.128 of the lane's
+  // 16 bytes -> tcgen05.st), then meet at the quarter's named barrier.
+  const int tq_id = warp & 3, tq_idx = warp >> 2, tq_n = nwarps >> 2;
+  const uint32_t tq_base = TM ? tbase + (((uint32_t)tq_id * 32u) << 16) : 0u;
+  auto tm_fill = [&](const uint8_t* st, int q) {
+    const uint32_t dst = tq_base + 256u * (uint32_t)(q & 1);
+    for (int k = tq_idx; k < a.kc; k += tq_n) {
+      const uint4 v = *(const uint4*)(st + k * ROWB + lane * 16);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 4u * k),
+                   "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tm_fence_before();
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + tq_id), "r"(tq_n * 32) : "memory");
+    tm_fence_after();
+  };
+  // Stage chunk q of the (cluster's) sequence into ring slot q % stages of every CTA of the
+  // cluster: one TMA 2-D box of X (kc rows x NT columns, OOB zero-filled), multicast to the
+  // cm CTAs when cm > 1, and each CTA's own plan block (1-D bulk copy), all completing on
+  // the slot's mbarrier of the receiving CTA.  Called by one whole warp.
+  auto refill = [&](int q) {
+    const int slot = q % a.stages;
+    const int ti = q / nloc, j = q - ti * nloc;
+    int pg;
+    int64_t n0;
+    tile_of(ti, pg, n0);
+    const int c = c_begin + j;
+    const uint32_t bbytes = (uint32_t)a.blk_bytes;  // fixed block stride (plan.h)
+    uint8_t* st = smem + slot * a.stage_bytes;
+    const uint32_t fb = full0 + 8 * slot;
+    if (a.use_tma && cm > 1) {
+      if (lane < cm) {  // lane d serves cluster rank d (its panel's plan block)
+        const int64_t bi = (int64_t)(pg * cm + lane) * a.nchunks + c;
+        const uint32_t bar_d = map_rank(fb, (uint32_t)lane);
+        mbar_arrive_expect_tx_cluster(bar_d, (uint32_t)(a.kc * ROWB) + bbytes);
+        bulk_load(map_rank(smem_u32(st + a.x_stage_bytes), (uint32_t)lane), a.blob + bi * a.blk_bytes,
+                  bbytes, bar_d);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_load_2d_mc(smem_u32(st), &tmap, (int)n0, c * a.kc, fb, (uint16_t)((1u << cm) - 1u));
+      }
+      return;
+    }
+    const int64_t bi = (int64_t)(persistent ? pg * cm + (int)crank : pg) * a.nchunks + c;
+    const int64_t b0 = bi * a.blk_bytes;
+    if (a.use_tma) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(fb, (uint32_t)(a.kc * ROWB) + bbytes);
+        tma_load_2d(smem_u32(st), &tmap, (int)n0, c * a.kc, fb);
+        bulk_load(smem_u32(st + a.x_stage_bytes), a.blob + b0, bbytes, fb);
+      }
+      return;
+    }
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(fb, bbytes);
+      bulk_load(smem_u32(st + a.x_stage_bytes), a.blob + b0, bbytes, fb);
+    }
+    const int k0 = c * a.kc;
+    const int kr = min(a.kc, a.K - k0);
+    const int cnt = kr * NT;
+    for (int idx = lane; idx < cnt; idx += 32) {
+      const int r = idx / NT, cc = idx % NT;
+      const int64_t n = n0 + cc;
+      const uint8_t* gp = a.X + ((int64_t)(k0 + r) * a.ldx + n) * S;
+      if (F16) {
+        uint16_t v = 0;
+        if (n < a.N) v = __ldg((const unsigned short*)gp);
+        *(uint16_t*)(st + r * ROWB + cc * 2) = v;
+      } else {
+        cp_async4(smem_u32(st + r * ROWB + cc * 4), n < a.N ? gp : a.X, n < a.N ? 4 : 0);
+      }
+    }
+    if (F16)
+      mbar_arrive(fb);
+    else
+      cp_async_mbar_arrive_noinc(fb);
+  };
+  if (warp == 0 && crank == 0)
+    for (int q = 0; q < min(a.stages, total); ++q) refill(q);
 
   float acc[R][C];
 
   // Y[row][n0 + col ...] <- acc (fp16: RN once), group-0 lanes only
-  auto store_tile = [&](int panel, int64_t n0, const int (&rows)[R]) {
+  auto store_tile = [&](int64_t n0, const int (&rows)[R]) {
     const int ncol = (int)min((int64_t)NT, a.N - n0);
     if (g != 0 || col >= ncol) return;
 #pragma unroll
@@ -317,126 +575,91 @@ __global__ void __launch_bounds__(288) spmm_kernel(const __grid_constant__ CUten
     }
   };
 
-  if (warp == nwarps) {
-    // ---------------- producer warp: TMA X tile + bulk plan block per chunk, running
-    // ahead of the consumers by up to `stages` chunks (across tile boundaries)
-    int s = 0, uses = 0;  // ring slot and how many times it has been filled (phase)
-    uint32_t ph = 0;
-    for (TileIter it = tile_begin(); it.t < ntiles; tile_next(it)) {
-      const int panel = it.panel;
-      const int64_t n0 = (int64_t)it.nt * NT;
-      for (int j = 0; j < nloc; ++j) {
-        const int c = c_begin + j;
-        if (uses > 0) mbar_wait(empty0 + 8 * s, ph ^ 1u);
-        uint8_t* st = smem + s * a.stage_bytes;
-        const int64_t bi = (int64_t)panel * a.nchunks + c;
-        const int64_t b0 = a.blk_off[bi];
-        const uint32_t bbytes = (uint32_t)(a.blk_off[bi + 1] - b0);
-        const uint32_t fb = full0 + 8 * s;
-        if (a.use_tma) {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(fb, (uint32_t)a.x_stage_bytes + bbytes);
-            tma_load_2d(smem_u32(st), &tmap, (int)n0, c * a.kc, fb);
-            bulk_load(smem_u32(st + a.x_stage_bytes), a.blob + b0, bbytes, fb);
-          }
-        } else {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(fb, bbytes);
-            bulk_load(smem_u32(st + a.x_stage_bytes), a.blob + b0, bbytes, fb);
-          }
-          const int k0 = c * a.kc;
-          const int kr = min(a.kc, a.K - k0);
-          const int total = kr * NT;
-          for (int idx = lane; idx < total; idx += 32) {
-            const int r = idx / NT, cc = idx % NT;
-            const int64_t n = n0 + cc;
-            const uint8_t* gp = a.X + ((int64_t)(k0 + r) * a.ldx + n) * S;
-            if (F16) {
-              uint16_t v = 0;
-              if (n < a.N) v = __ldg((const unsigned short*)gp);
-              *(uint16_t*)(st + r * ROWB + cc * 2) = v;
-            } else {
-              cp_async4(smem_u32(st + r * ROWB + cc * 4), n < a.N ? gp : a.X, n < a.N ? 4 : 0);
-            }
-          }
-          if (F16)
-            mbar_arrive(fb);
-          else
-            cp_async_mbar_arrive_noinc(fb);
-        }
-        if (++s == a.stages) {
-          s = 0;
-          ph ^= 1u;
-          uses = 1;
+  // ---------------- Alg. 3 over each staged chunk; the last warp to release a ring slot
+  // refills it with chunk q + stages (no producer warp, no blocking wait on an empty barrier)
+  int q = 0, slot = 0;
+  uint32_t ph = 0;
+  int panel = 0;
+  int64_t n0 = 0;
+  const uint32_t releases = (uint32_t)(cm * nwarps);  // per slot and round, cluster-wide
+  for (int ti = 0; ti < my_tiles; ++ti) {
+    tile_of(ti, panel, n0);
+    if (persistent) panel = panel * cm + (int)crank;
+    int rows[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rows[r] = __ldg(a.row_id + (int64_t)panel * a.Mp + warp * R + r);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+    for (int j = 0; j < nloc; ++j) {
+      mbar_wait(full0 + 8 * slot, ph);
+      const uint8_t* st = smem + slot * a.stage_bytes;
+      if (TM) tm_fill(st, q);
+      const uint8_t* xs = st + li * (C * S);
+      const uint32_t* shdr = (const uint32_t*)(st + a.x_stage_bytes);
+      const uint4* ents = (const uint4*)(st + a.x_stage_bytes + a.hdr_bytes);
+      uint32_t h[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) h[r] = shdr[(warp * R + r) * GK + g];
+      if (TM) {
+        run_rows_tm<F16, R>(acc, h, ents, tq_base + 256u * (uint32_t)(q & 1));
+        tm_fence_before();
+      } else {
+        run_rows<F16, R>(acc, h, ents, xs);
+      }
+      __syncwarp();
+      uint32_t old = 0;
+      if (lane == 0) {  // release the slot; the last of the cluster's warps refills it
+        if (cm > 1) {
+          asm volatile("fence.acq_rel.cluster;" ::: "memory");
+          old = atom_add_cluster(map_rank(smem_u32(ctr + slot), 0u), 1u);
+        } else {  // release: this warp's reads of the slot precede the count
+          asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                       : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
         }
       }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if ((old + 1u) % releases == 0u && q + a.stages < total) {
+        if (cm > 1) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        refill(q + a.stages);
+      }
+
+      ++q;
+      if (++slot == a.stages) {
+        slot = 0;
+        ph ^= 1u;
+      }
     }
-  } else {
-    // ---------------- consumer warps: Alg. 3 over each staged chunk
-    int s = 0;
-    uint32_t ph = 0;
-    for (TileIter it = tile_begin(); it.t < ntiles; tile_next(it)) {
-      const int panel = it.panel;
-      const int64_t n0 = (int64_t)it.nt * NT;
-      int rows[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) rows[r] = a.row_id[(int64_t)panel * a.Mp + warp * R + r];
+    // cross-group reduction inside the warp: fixed binary tree over group index
+    if (GK > 1) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
-      for (int j = 0; j < nloc; ++j) {
-        mbar_wait(full0 + 8 * s, ph);
-        const uint8_t* st = smem + s * a.stage_bytes;
-        const uint8_t* xs = st + li * (C * S);
-        const uint32_t* shdr = (const uint32_t*)(st + a.x_stage_bytes);
-        const uint8_t* ents = st + a.x_stage_bytes + a.hdr_bytes;
+        for (int c = 0; c < C; ++c)
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const uint32_t h = shdr[warp * R + r];
-          int beg = (int)(h & 0xffffu);
-          int cnt = (int)(h >> 16);
-          if (GK > 1) {  // contiguous k-ascending pieces, all but the last of equal size
-            int per = (cnt + GK - 1) / GK;
-            per = (per + E::A - 1) / E::A * E::A;
-            const int lo = min(g * per, cnt);
-            const int hi = min(lo + per, cnt);
-            beg += lo;
-            cnt = hi - lo;
-          }
-          E::template run<C, ROWB>(acc[r], ents, beg, cnt, xs);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * s);
-        if (++s == a.stages) {
-          s = 0;
-          ph ^= 1u;
-        }
-      }
-      // cross-group reduction inside the warp: fixed binary tree over group index
-      if (GK > 1) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-          for (int c = 0; c < C; ++c)
-#pragma unroll
-            for (int off = 16; off >= L; off >>= 1)
-              acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], off);
-      }
-      if (persistent) store_tile(panel, n0, rows);
+          for (int off = 16; off >= L; off >>= 1)
+            acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], off);
     }
+    if (persistent) store_tile(n0, rows);
   }
-  if (persistent) return;
+  if (persistent) {
+    if (cm > 1) cluster_sync_all();  // no CTA leaves while peers may still touch its smem
+    if (TM) {
+      tm_fence_before();
+      __syncthreads();
+      if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+    }
+    return;
+  }
 
-  const TileIter it0 = tile_begin();
-  const int panel = it0.panel;
-  const int64_t n0 = (int64_t)it0.nt * NT;
   const int ncol = (int)min((int64_t)NT, a.N - n0);
   // ---------------- k_split > 1: partial tiles reduced across the cluster through DSMEM,
   // summed in rank order 0, 1, ..., ks-1 for every output (deterministic).
   __syncthreads();  // every consumer is done with the stage buffers that `red` overlays
   float* red = (float*)smem;  // [Mp][NT] fp32
-  if (warp < nwarps && g == 0) {
+  if (g == 0) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       float* dst = red + (warp * R + r) * NT + col;
@@ -665,9 +888,17 @@ using SpmmFn = void (*)(const __grid_constant__ CUtensorMap, const SpmmArgs);
 using ConvFn = void (*)(const ConvArgs);
 
 template <bool F16>
-static SpmmFn pick_spmm(int R, int GK) {
+static SpmmFn pick_spmm(int R, int GK, bool tm) {
+  if (tm) {  // TMEM X source: split_k = 1 only
+    if (GK != 1) return nullptr;
+    if (R == 1) return spmm_kernel<1, 1, F16, true>;
+    if (R == 2) return spmm_kernel<2, 1, F16, true>;
+    if (R == 4) return spmm_kernel<4, 1, F16, true>;
+    if (R == 8) return spmm_kernel<8, 1, F16, true>;
+    return nullptr;
+  }
 #define SRT_S(RR, GG) \
-  if (R == RR && GK == GG) return spmm_kernel<RR, GG, F16>;
+  if (R == RR && GK == GG) return spmm_kernel<RR, GG, F16, false>;
 #define SRT_SR(RR) SRT_S(RR, 1) SRT_S(RR, 2) SRT_S(RR, 4) SRT_S(RR, 8)
   SRT_SR(1) SRT_SR(2) SRT_SR(4) SRT_SR(8)
   if constexpr (!F16) { SRT_SR(16) }
@@ -820,6 +1051,13 @@ int upload_plan(Plan& p, std::string& err) {
     cudaFree(mem);
     return cuda_fail(e, "cudaMemcpy(plan)", err);
   }
+  // A cudaMemcpy from pageable memory may return before the DMA has landed; it is ordered
+  // only with the legacy default stream.  Executors may run on any (non-blocking) stream,
+  // so the plan must be complete in device memory when create returns.
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+    cudaFree(mem);
+    return cuda_fail(e, "cudaDeviceSynchronize(plan upload)", err);
+  }
   p.d_mem = mem;
   p.d_blk_off = (const int64_t*)(b + o_off);
   p.d_row_id = (const int32_t*)(b + o_row);
@@ -839,7 +1077,7 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
                 void* stream, std::string& err) {
   const bool f16 = p.dtype == SPARSE_F16;
   const int S = f16 ? 2 : 4;
-  SpmmFn fn = f16 ? pick_spmm<true>(p.R, p.gk) : pick_spmm<false>(p.R, p.gk);
+  SpmmFn fn = f16 ? pick_spmm<true>(p.R, p.gk, p.tm) : pick_spmm<false>(p.R, p.gk, p.tm);
   if (!fn) {
     err = "internal: no kernel instance for this tile configuration";
     return SPARSE_EINTERNAL;
@@ -863,13 +1101,14 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
   a.x_stage_bytes = p.x_stage_bytes;
   a.stage_bytes = (p.x_stage_bytes + p.max_blk_bytes + 127) & ~127;
   a.hdr_bytes = p.hdr_bytes;
+  a.blk_bytes = p.max_blk_bytes;
   a.bar_off = p.smem_bytes - 128;
   const int smem = p.smem_bytes;
   const bool vec_x = ((uintptr_t)X % 16 == 0) && ((ldx * S) % 16 == 0);
   a.vec_y = ((uintptr_t)Y % 16 == 0) && ((ldy * S) % 16 == 0);
   a.npanels = p.npanels;
   auto encode = tensor_map_encoder();
-  const int threads = (p.warps + 1) * 32;
+  const int threads = p.warps * 32;
   auto make_map = [&](CUtensorMap& tmap) {
     std::memset(&tmap, 0, sizeof tmap);
     a.use_tma = 0;
@@ -887,21 +1126,50 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
   };
   const int64_t ntn = (N + p.n_tile - 1) / p.n_tile;
   if (p.ks == 1) {
-    // persistent: one wave of CTAs, each walking tiles blockIdx.x + j * gridDim.x
+    // persistent: one wave of CTAs (clusters of cm CTAs when X is multicast), each walking
+    // tiles (panel group, N tile) cluster_id + j * clusters
     a.X = (const uint8_t*)X;
     a.Y = (uint8_t*)Y;
     a.N = N;
+    a.cm = p.cm;
     CUtensorMap tmap;
     make_map(tmap);
-    const int64_t ntiles = (int64_t)p.npanels * ntn;
-    int per_sm = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
-    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
-    fn<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tmap, a);
-    e = cudaGetLastError();
+    if (!a.use_tma && p.cm > 1) {
+      err = "internal: x_multicast needs the TMA path (16-byte aligned X)";
+      return SPARSE_EINTERNAL;
+    }
+    const int64_t ntiles = (int64_t)(p.npanels / p.cm) * ntn;
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.blockDim = dim3((unsigned)threads, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.cm;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (p.grid_cache <= 0) {  // resident clusters (CTAs) in one wave; cached per plan
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+      int per_sm = 1;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+      if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+      int64_t clusters = (int64_t)sms * per_sm / p.cm;
+      if (p.cm > 1) {
+        int nc = 0;
+        cfg.gridDim = dim3((unsigned)(p.cm * clusters), 1, 1);
+        if (cudaOccupancyMaxActiveClusters(&nc, (const void*)fn, &cfg) == cudaSuccess && nc > 0)
+          clusters = nc;
+        cudaGetLastError();
+      }
+      p.grid_cache = (int32_t)std::max<int64_t>(1, clusters);
+    }
+    const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(ntiles, p.grid_cache));
+    cfg.gridDim = dim3((unsigned)(clusters * p.cm), 1, 1);
+    e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
     if (e != cudaSuccess) return cuda_fail(e, "spmm launch", err);
     return SPARSE_OK;
   }
@@ -916,6 +1184,7 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
     make_map(tmap);
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof cfg);
+    a.cm = 1;
     cfg.gridDim = dim3((unsigned)(p.npanels * p.ks), (unsigned)nt, 1);
     cfg.blockDim = dim3((unsigned)threads, 1, 1);
     cfg.dynamicSmemBytes = (size_t)smem;

@@ -8,17 +8,35 @@
 // (panel, chunk) block is a single contiguous, 16-byte aligned byte range that
 // a CTA stages into shared memory next to the X tile it multiplies.
 //
-// Block layout (byte offsets relative to blob + blk_off[panel*nchunks+chunk]):
-//   uint32 slot_hdr[Mp]        start | count << 16: first entry index (relative
-//                              to the block's entry array, a multiple of
-//                              entry_align = 16 / entry_bytes) and number of
-//                              entries of row slot s = warp*R + r; padded to 16 B
-//   entries[...]               row-slot-major, k ascending within a slot; gaps
-//                              between slots are zero padding
-//                              fp32 SpMM : {uint32 k_local; float w}     (8 B)
-//                              fp16 SpMM : {uint16 k_local; half  w}     (4 B)
-//                              fp32 conv : {int32 smem_off; float w}     (8 B)
-//                              fp16 conv : {int16 smem_off; half  w}     (4 B)
+// Block layout (byte offsets relative to blob + blk_off[panel*nchunks+chunk]).
+//
+// SpMM plans (kernel spmm_kernel): every block occupies max_blk_bytes (fixed stride,
+// block bi at bi * max_blk_bytes, zero padded) so its address needs no table lookup.
+//   uint32 hdr[Mp * gk]        unit_start | unit_count << 16 of thread group g of
+//                              row slot s = warp*R + r at index s*gk + g; a "unit"
+//                              is one 16-byte broadcast load = entry_align entries;
+//                              unit_start is relative to the block's entry array;
+//                              padded to 16 B
+//   units[...]                 slot-major, group-major inside a slot, k ascending
+//                              fp32: {uint32 xoff; float w} x 2 per unit, xoff =
+//                                    k_local * n_tile * 4 (byte offset of X row k
+//                                    inside the staged tile)
+//                              fp16: {uint16 xoff16; half w} x 4 per unit, xoff16 =
+//                                    k_local * n_tile * 2 / 16 (16-byte units)
+//                              a group's last unit is completed with neutral
+//                              entries {xoff of row k_local = kc (the zero row
+//                              every stage carries after its kc X rows), w = -0.0}:
+//                              fma(-0, +0, acc) == acc bit for bit, so padding
+//                              never changes a result
+//   The split of a row's chunk entries into gk groups: every group but the last
+//   takes per = ceil(cnt / gk) rounded up to entry_align entries (Fig. 3b).
+//
+// Conv plans (kernel conv3x3_kernel):
+//   uint32 slot_hdr[Mp]        start | count << 16 in entries, start a multiple of
+//                              entry_align; padded to 16 B
+//   entries[...]               fp32 {int32 smem_off; float w} (8 B),
+//                              fp16 {int16 smem_off; half w} (4 B), row-slot-major,
+//                              k ascending, zero padding between slots
 //   zero padding to 16 bytes
 #pragma once
 #include <cstdint>
@@ -27,7 +45,8 @@
 
 namespace srt {
 
-constexpr int kMaxWarps = 8;
+constexpr int kMaxWarps = 16;
+constexpr int kMaxStages = 8;
 
 struct Plan {
   // problem
@@ -37,7 +56,7 @@ struct Plan {
   int64_t n_hint = 0;
 
   // tiling (thread block = `warps` thread groups of 32/gk lanes x gk groups)
-  int32_t warps = 4;     // warps per CTA
+  int32_t warps = 4;     // consumer warps per CTA (SpMM adds one producer warp)
   int32_t R = 4;         // row slots per warp
   int32_t Mp = 16;       // rows per panel = warps * R
   int32_t gk = 1;        // split-K groups per warp
@@ -51,6 +70,8 @@ struct Plan {
   int32_t entry_align = 2;  // entries per 16-byte broadcast load
   int32_t hdr_bytes = 16;   // block header bytes (slot table)
   int32_t ks = 1;           // cluster K-split: CTAs of a cluster take disjoint chunk ranges
+  int32_t cm = 1;           // X multicast cluster: CTAs (consecutive panels) sharing X tiles
+  int32_t tm = 0;           // X source: 0 = shared memory, 1 = tensor memory (tcgen05.ld)
 
   // conv geometry (kind == CONV3X3)
   int32_t conv_rb = 0;    // output rows per tile
@@ -104,6 +125,7 @@ struct Plan {
   const int64_t* d_blk_off = nullptr;
   const uint8_t* d_blob = nullptr;
   int64_t plan_bytes = 0;
+  mutable int32_t grid_cache = 0;  // resident CTAs (clusters) of the persistent launch
 };
 
 struct BuildOpts {
@@ -113,6 +135,8 @@ struct BuildOpts {
   int32_t warps = 0, rows_per_warp = 0, k_chunk = 0, split_k = 0;
   int32_t k_split = 0, stages = 0;
   int32_t executor = 0, jit_rows = 0, jit_warps = 0;
+  int32_t cm = 0;
+  int32_t tm = 0;
 };
 
 // JIT executor (jit.cpp).  Row entries per row (k ascending) as validated by the

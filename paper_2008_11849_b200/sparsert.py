@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsparsert.so")
+# SPARSERT_LIB: load an alternative build of the same library (A/B experiments, scripts/)
+LIB_PATH = os.environ.get("SPARSERT_LIB") or os.path.join(_PKG, "libsparsert.so")
 
 SPARSE_OK, SPARSE_EINVAL, SPARSE_EMATRIX, SPARSE_EUNSUPPORTED = 0, 1, 2, 3
 SPARSE_ENOMEM, SPARSE_ECUDA, SPARSE_EINTERNAL = 4, 5, 6
@@ -46,7 +47,8 @@ class sparse_plan_opts(ctypes.Structure):
                 ("k_chunk", ctypes.c_int32), ("split_k", ctypes.c_int32),
                 ("k_split", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("executor", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
-                ("jit_warps", ctypes.c_int32)]
+                ("jit_warps", ctypes.c_int32), ("x_multicast", ctypes.c_int32),
+                ("x_source", ctypes.c_int32)]
 
 
 class sparse_plan_info_t(ctypes.Structure):
@@ -64,7 +66,8 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("jit_modules", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
                 ("jit_warps", ctypes.c_int32), ("jit_cubin_bytes", ctypes.c_int64),
                 ("jit_compile_ms", ctypes.c_double), ("tuned_us", ctypes.c_double),
-                ("digest", ctypes.c_uint64)]
+                ("digest", ctypes.c_uint64), ("x_multicast", ctypes.c_int32),
+                ("x_source", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -234,7 +237,8 @@ class Plan:
         o = dict(warps=i["warps"], rows_per_warp=i["rows_per_warp"], split_k=i["split_k"],
                  stages=i["stages"], executor=i["executor"])
         if self.kind == SPARSE_SPMM:
-            o.update(k_chunk=i["k_chunk"], k_split=i["k_split"])
+            o.update(k_chunk=i["k_chunk"], k_split=i["k_split"], x_multicast=i["x_multicast"],
+                     x_source=i["x_source"])
             if i["executor"] == 1:
                 o.update(jit_rows=i["jit_rows"], jit_warps=i["jit_warps"])
         else:

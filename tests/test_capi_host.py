@@ -179,6 +179,10 @@ def test_validation_errors():
     assert _rc(lambda: S.sparse_plan_create(1, 70000, [0, 0], [], [], 0, **HOST))[0] == S.SPARSE_EUNSUPPORTED
     assert _rc(lambda: mk(kind=srt.SPARSE_CONV3X3, c_in=1, h=3, w=3))[0] == S.SPARSE_EUNSUPPORTED
     assert _rc(lambda: mk(rows_per_warp=3))[0] == S.SPARSE_EUNSUPPORTED
+    assert _rc(lambda: mk(x_multicast=3))[0] == S.SPARSE_EUNSUPPORTED
+    assert _rc(lambda: mk(x_multicast=2, k_split=2, K=256))[0] == S.SPARSE_EUNSUPPORTED
+    assert _rc(lambda: mk(warps=17))[0] == S.SPARSE_EUNSUPPORTED
+    assert _rc(lambda: mk(stages=9))[0] == S.SPARSE_EUNSUPPORTED
     # compute calls on a host-only plan are rejected (never computed on the CPU)
     h = mk()
     assert S.lib.sparse_spmm(h, 4, ctypes.c_void_p(16), 4, ctypes.c_void_p(16), 4, None) == S.SPARSE_EINVAL

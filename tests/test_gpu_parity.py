@@ -227,6 +227,59 @@ def test_tile_overrides_exact(R, warps, kc, gk, ks, st, f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("warps,R,kc,st,cm", [(16, 4, 32, 8, 1), (16, 2, 128, 0, 2), (8, 4, 64, 3, 4),
+                                              (16, 1, 32, 6, 8), (5, 2, 48, 2, 2), (16, 8, 64, 0, 1)])
+def test_wide_ctas_deep_rings_and_multicast_exact(warps, R, kc, st, cm, f16):
+    # 16-warp CTAs, rings up to 8 stages, X multicast clusters of 2-8 CTAs (one TMA box
+    # feeds every CTA of the cluster): exact on integer data, incl. ragged M / N / K, and
+    # x_multicast never changes a result (it only changes who loads X)
+    if f16 and R * 8 > 64:
+        pytest.skip("accumulator budget")
+    for M, K, N in [(333, 700, 250), (2048, 512, 392), (64, 256, 3136)]:
+        plan = _exact_case(M, K, N, 90, f16, seed=warps + R + cm, rows_per_warp=R, warps=warps,
+                           k_chunk=kc, stages=st, x_multicast=cm)
+        assert plan.info["x_multicast"] == cm and plan.info["warps"] == warps
+        assert plan.info["panels"] % cm == 0
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_multicast_bitwise_equals_unicast(f16):
+    w = gen.pruned_weights(1024, 768, 90, seed=41)
+    X = gen.uniform_x(768, 1000, seed=42)
+    y1, _ = _run_spmm(w, X, f16, warps=8, rows_per_warp=4, x_multicast=1)
+    for cm in (2, 4, 8):
+        y, _ = _run_spmm(w, X, f16, warps=8, rows_per_warp=4, x_multicast=cm)
+        assert np.array_equal(y, y1)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("warps,R,kc", [(16, 4, 56), (8, 8, 56), (8, 2, 32), (4, 1, 16), (12, 8, 48)])
+def test_tmem_x_source_exact(warps, R, kc, f16):
+    # X read from tensor memory (tcgen05.cp smem -> TMEM, tcgen05.ld): exact on integer data
+    # for ragged shapes and the Table-1 / BERT shapes, including neutral padding entries
+    # (zero row of each TMEM buffer) and K not a multiple of k_chunk
+    if f16 and R * 8 > 64:
+        pytest.skip("accumulator budget")
+    for M, K, N in [(333, 700, 250), (2048, 512, 392), (64, 256, 3136), (3072, 768, 512)]:
+        plan = _exact_case(M, K, N, 90, f16, seed=warps * R + kc, rows_per_warp=R, warps=warps,
+                           k_chunk=kc, x_source=1)
+        assert plan.info["x_source"] == 1
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_tmem_bitwise_equals_smem(f16):
+    # the X source never changes the arithmetic: same plan options, bitwise equal outputs
+    w = gen.pruned_weights(1024, 768, 90, seed=51)
+    X = gen.uniform_x(768, 1000, seed=52)
+    kw = dict(warps=8, rows_per_warp=4, k_chunk=56)
+    y0, _ = _run_spmm(w, X, f16, x_source=0, **kw)
+    y1, p1 = _run_spmm(w, X, f16, x_source=1, **kw)
+    assert p1.info["x_source"] == 1
+    assert np.array_equal(y0, y1)
+    assert oracle.rel_l2(y1, _ref(w, X, f16)) <= (F16_TOL if f16 else F32_TOL)
+
+
+@pytest.mark.parametrize("f16", [False, True])
 def test_k_split_changes_order_not_value(f16):
     # k_split fixes a different (still deterministic) summation order: equal within tolerance,
     # bitwise on integer data, and repeated calls are bitwise identical.
