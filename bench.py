@@ -9,7 +9,7 @@ A "step" is one pass of the executor over one batch of synthetic input for every
 the workload (the plans are built once, offline, like the paper's inspector; their
 build time is reported in config.plan_build_ms).  Default workload (BASELINE.json
 configs[1]): the eight ResNet-50 1x1 layers of PAPER.md Table 1, 90% sparsity,
-batch 8 per GPU, fp32 (the paper's precision).  L2 is flushed (256 MiB write)
+batch 8 per GPU, fp32 (the paper's precision).  L2 is flushed (256 MiB write + 256 MiB read)
 before every timed step, outside the timed events, so every layer reads cold HBM.
 
 Multi-GPU: one process per GPU, each with a replicated plan and its own batch (weak
@@ -339,7 +339,21 @@ def main():
         else:
             p.conv3x3(xs[i] if X is None else X, ys[i] if Y is None else Y, stream=stream)
 
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # L2 flush: write a 256 MiB buffer (evicts everything), then read a second 256 MiB buffer
+    # so the write-back of the dirty flush lines also happens here, outside the timed events,
+    # and the timed step starts from a cold and clean L2 (HBM-honest inputs, no write-back of
+    # flush data charged to the first kernels)
+    flush_w = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush_r = torch.zeros(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush_sink = torch.empty(1, dtype=torch.float32, device=dev)
+
+    class _Flush:
+        @staticmethod
+        def zero_():
+            flush_w.zero_()
+            torch.sum(flush_r, dim=0, out=flush_sink[0])
+
+    flush = _Flush()
     nl = len(layers)
     flops_step = sum(2 * plans[i][1].nnz * layer_N(layers[i]) for i in range(nl))
 
@@ -352,13 +366,24 @@ def main():
     torch.cuda.synchronize()
 
     # One step = the nl executor launches, captured once in a CUDA graph (launch-bound layers
-    # would otherwise time the host), with external timing events between the launches so
-    # every kernel's duration is measured inside the timed region.
-    graph = None
+    # would otherwise time the host).  The step graph has events only at its two ends, so
+    # consecutive kernels chain directly (programmatic dependent launch overlaps one layer's
+    # prologue with the previous layer's tail); the `value` is timed on it.  A second graph of
+    # the same launches with an event between every two kernels is replayed for the same
+    # number of steps to measure each kernel's duration (roofline, per-layer breakdown).
+    graph = graph_l = None
     gev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(nl + 1)]
+    sev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
     if not args.eager:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
+            cur = torch.cuda.current_stream(dev)
+            sev[0].record(cur)
+            for i in range(nl):
+                call(i, stream=cur)
+            sev[1].record(cur)
+        graph_l = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_l):
             cur = torch.cuda.current_stream(dev)
             gev[0].record(cur)
             for i in range(nl):
@@ -367,6 +392,8 @@ def main():
         for _ in range(max(1, args.warmup // 2)):
             flush.zero_()
             graph.replay()
+            flush.zero_()
+            graph_l.replay()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -379,7 +406,11 @@ def main():
             graph.replay()
             torch.cuda.nvtx.range_pop()
             torch.cuda.synchronize()
-            step_ms.append(gev[0].elapsed_time(gev[nl]))
+            step_ms.append(sev[0].elapsed_time(sev[1]))
+        for s in range(args.steps):
+            flush.zero_()
+            graph_l.replay()
+            torch.cuda.synchronize()
             for i in range(nl):
                 layer_acc[i] += gev[i].elapsed_time(gev[i + 1])
     else:
@@ -546,8 +577,11 @@ def main():
             "config": {"workload": f"{args.workload}_s{args.sparsity}_{args.dtype}",
                        "description": desc, "sparsity_pct": args.sparsity,
                        "layers": [f"{L['M']}x{L['K']}xN{layer_N(L)}" for L in layers],
-                       "l2": "flushed (256 MiB write) before every timed step, outside the events",
+                       "l2": "flushed before every timed step, outside the events: 256 MiB write, then a 256 MiB read (cold, clean L2; inputs > L2 not needed)",
                        "launch": "eager" if args.eager else "cuda-graph replay of the step",
+                       "layer_times": "eager, events between launches" if args.eager else
+                       "second graph of the same launches with an event between kernels, replayed "
+                       "for the same number of steps (the step graph has events only at its ends)",
                        "plan_build_ms": build_ms,
                        "executor": {0: "plan-driven", 1: "jit", 2: "auto"}[args.executor],
                        "tuned": None if args.no_tune else chosen,

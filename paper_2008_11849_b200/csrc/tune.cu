@@ -7,8 +7,9 @@
 // configuration (and the JIT executor when its per-panel code is small) on the
 // plan's device with synthetic X of the hinted size, and keeps the fastest.  The
 // candidate grid stays under 100 entries.  Timing: 2 warm-up launches, then the
-// median of 5 single launches, each after a 256 MiB memset that evicts the L2 (cold
-// inputs, as bench.py measures), CUDA events on a private stream.
+// median of 5 single launches, each after a 256 MiB memset that evicts the L2 and a 256 MiB
+// read that leaves it clean (cold inputs, as bench.py measures), CUDA events on a private
+// stream.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -43,6 +44,17 @@ __global__ void fill_uniform(uint8_t* p, int64_t n, int f16, uint32_t seed) {
     else
       reinterpret_cast<float*>(p)[i] = v;
   }
+}
+
+// reads a buffer (so that L2 holds clean lines: no write-back of the memset flush is
+// charged to the timed launch)
+__global__ void read_sink(const uint4* p, int64_t n, uint32_t* sink) {
+  uint32_t a = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = p[i];
+    a ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (a == 0x9e3779b9u) *sink = a;
 }
 
 void release(Plan& p) {
@@ -141,7 +153,7 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
   cudaEventCreate(&ev[1]);
   fill_uniform<<<1024, 256, 0, st>>>(X, xe, f16 ? 1 : 0, 12345u);
   void* flush = nullptr;
-  if (cudaMalloc(&flush, kFlushBytes) != cudaSuccess) {
+  if (cudaMalloc(&flush, 2 * kFlushBytes) != cudaSuccess) {
     cudaGetLastError();
     flush = nullptr;  // warm-L2 timing only
   }
@@ -178,7 +190,11 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     bool ok = run() == SPARSE_OK && run() == SPARSE_OK;
     std::vector<float> ms;
     for (int r = 0; ok && r < 5; ++r) {
-      if (flush) cudaMemsetAsync(flush, r, kFlushBytes, st);
+      if (flush) {  // write 256 MiB (evicts the L2), then read another 256 MiB (cleans it)
+        cudaMemsetAsync(flush, r, kFlushBytes, st);
+        read_sink<<<1184, 256, 0, st>>>((const uint4*)((uint8_t*)flush + kFlushBytes),
+                                        (int64_t)(kFlushBytes / 16), (uint32_t*)flush);
+      }
       cudaEventRecord(ev[0], st);
       ok = run() == SPARSE_OK;
       cudaEventRecord(ev[1], st);
