@@ -258,8 +258,10 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       }
       p.kc = o.k_chunk;
     } else {
-      p.kc = o.tm ? 56 : 64;  // tensor memory: two 256-column buffers of kc rows + a zero row
-      if (K <= (o.tm ? 56 : 96)) p.kc = (K + 7) / 8 * 8;
+      // 128 rows per stage (fewer, larger chunks measured fastest on B200);
+      // tensor memory: 56 (two 256-column buffers of kc rows + a zero row each)
+      p.kc = o.tm ? 56 : 128;
+      if (K <= p.kc) p.kc = (K + 7) / 8 * 8;
     }
     p.nchunks = (K + p.kc - 1) / p.kc;
     // kc X rows plus one zero row (target of the neutral padding entries), 128-byte aligned
@@ -316,7 +318,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     p.conv_stage_elems = cc * p.conv_sci + 2 * p.conv_guard;
     p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
   }
-  p.warps = o.warps ? o.warps : 8;
+  p.warps = o.warps ? o.warps : (o.kind == SPARSE_SPMM ? 16 : 8);
   if (p.warps < 1 || p.warps > kMaxWarps) {
     err = "warps must be in [1, 16]";
     return SPARSE_EUNSUPPORTED;
@@ -333,14 +335,16 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // accumulators per thread: R * C fp32 registers; keep <= 64
     // R = 4 rows per warp x 8 warps: Mp = 32 rows; measured best on B200 for both dtypes
     // (R = 8 halves occupancy through registers, scripts/sweep.py)
+    // SpMM executors are persistent: one wave of 148 CTAs is the target
     const int rmax = 4;
-    const int max_ks = o.kind == SPARSE_SPMM ? std::min(8, p.nchunks) : 1;
+    const int max_ks = o.kind == SPARSE_SPMM ? std::min(4, p.nchunks) : 1;
+    const int64_t target = o.kind == SPARSE_SPMM ? 148 : kTargetCtas;
     int bestR = 1, bestKs = 1;
     bool found = false;
     for (int R = rmax; R >= 1 && !found; R /= 2) {
       const int64_t panels = (M + (int64_t)p.warps * R - 1) / ((int64_t)p.warps * R);
       for (int ks = 1; ks <= max_ks; ks *= 2) {
-        if (panels * ntiles * ks >= kTargetCtas) {
+        if (panels * ntiles * ks >= target) {
           bestR = R;
           bestKs = ks;
           found = true;

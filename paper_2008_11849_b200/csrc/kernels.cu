@@ -244,13 +244,28 @@ __device__ __forceinline__ void run_rows(float (&acc)[R][F16 ? 8 : 4], const uin
     int mn = (int)(h[r0] >> 16);
 #pragma unroll
     for (int r = 1; r < P; ++r) mn = min(mn, (int)(h[r0 + r] >> 16));
-#pragma unroll 1
-    for (int u = 0; u < mn; ++u) {
-      uint4 q[P];
+    const uint4* pr[P];
 #pragma unroll
-      for (int r = 0; r < P; ++r) q[r] = ents[(h[r0 + r] & 0xffffu) + u];
+    for (int r = 0; r < P; ++r) pr[r] = ents + (h[r0 + r] & 0xffffu);
+    int u = 0;
+#pragma unroll 1
+    for (; u + 2 <= mn; u += 2) {  // two steps per trip: both steps' loads in flight
+      uint4 q[P], q2[P];
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        q[r] = pr[r][0];
+        q2[r] = pr[r][1];
+        pr[r] += 2;
+      }
 #pragma unroll
       for (int r = 0; r < P; ++r) E::unit(acc[r0 + r], q[r], xs);
+#pragma unroll
+      for (int r = 0; r < P; ++r) E::unit(acc[r0 + r], q2[r], xs);
+    }
+    if (u < mn) {
+#pragma unroll
+      for (int r = 0; r < P; ++r) E::unit(acc[r0 + r], pr[r][0], xs);
+      ++u;
     }
 #pragma unroll
     for (int r = 0; r < P; ++r)
