@@ -102,6 +102,10 @@ typedef struct {
                             with warp-uniform tcgen05.ld, which has ~2x the shared-memory
                             bandwidth.  Needs split_k = 1, k_split = 1,
                             x_multicast = 1, k_chunk <= 56 (default 56).  Result-neutral. */
+  int32_t conv_kernel;   /* conv: 0 = auto (the vectorised kernel - three dx-shifted copies of the
+                            staged input, 128-bit loads of C consecutive positions - when a padded
+                            row of W + 2 positions fits twice in 32 * C positions, else the
+                            position-strided kernel); 1 = position-strided kernel */
 } sparse_plan_opts;
 
 /* Fill *opts with defaults (kind SPMM, device -1, everything else 0). */
@@ -170,6 +174,8 @@ typedef struct {
   uint64_t digest;      /* FNV-1a of the packed plan: equal digests <=> identical replicas */
   int32_t x_multicast;  /* CTAs per cluster sharing X tiles (TMA multicast) */
   int32_t x_source;     /* 0 shared memory, 1 tensor memory */
+  int32_t conv_kernel;  /* conv: 0 vectorised, 1 position-strided */
+  int32_t reserved2;
 } sparse_plan_info_t;
 
 int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out);

@@ -65,6 +65,9 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   bo.jit_warps = o.jit_warps;
   bo.cm = o.x_multicast;
   bo.tm = o.x_source;
+  if (o.conv_kernel != 0 && o.conv_kernel != 1)
+    return fail(SPARSE_EINVAL, "conv_kernel must be 0 (auto) or 1 (position-strided)");
+  bo.conv_vec = o.conv_kernel == 0;
   if (o.stages < 0 || o.stages > srt::kMaxStages)
     return fail(SPARSE_EUNSUPPORTED, "stages must be in [0, 8]");
   sparse_plan_s* h = nullptr;
@@ -234,6 +237,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->tuned_us = p.tuned_us;
   out->x_multicast = p.cm;
   out->x_source = p.tm;
+  out->conv_kernel = p.kind == SPARSE_CONV3X3 && !p.conv_vec ? 1 : 0;
   return ok();
 }
 
@@ -265,7 +269,7 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
       const uint8_t* ents = blk + p.hdr_bytes;
       for (int s = 0; s < p.Mp; ++s) {
         const int32_t m = p.row_id[(size_t)q * p.Mp + s];
-        if (p.kind == SPARSE_SPMM) {
+        if (p.kind == SPARSE_SPMM || p.conv_vec) {
           for (int g = 0; g < p.gk; ++g) {
             const uint32_t h = shdr[s * p.gk + g];
             const int64_t u0 = h & 0xffffu, nu = h >> 16;
@@ -285,15 +289,30 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
                 std::memcpy(&w, rec + 4, 4);
                 xoff = a;
               }
-              if (xoff % rowb) return fail(SPARSE_EINTERNAL, "plan entry offset not a row multiple");
-              const int64_t kl = xoff / rowb;
+              int64_t kl;
+              if (p.kind == SPARSE_SPMM) {
+                if (xoff % rowb) return fail(SPARSE_EINTERNAL, "plan entry offset not a row multiple");
+                kl = xoff / rowb;
+              } else {  // vectorised conv: elems = dx * cs + ci * sci + dy * wp, or the zero block
+                const int64_t el = xoff / (f16 ? 2 : 4);
+                if (el == 3 * (int64_t)p.conv_cs) {
+                  kl = p.kc;
+                } else {
+                  const int64_t dx = el / p.conv_cs, rem = el % p.conv_cs;
+                  const int64_t ci = rem / p.conv_sci, dy = (rem % p.conv_sci) / p.conv_wp;
+                  if (dx > 2 || dy > 2 || (rem % p.conv_sci) % p.conv_wp)
+                    return fail(SPARSE_EINTERNAL, "conv plan entry offset does not decode");
+                  kl = ci * 9 + dy * 3 + dx;
+                }
+              }
               if (kl == p.kc) {  // neutral padding entry (zero row, -0 weight)
                 if (!(w == 0.0f && std::signbit(w)))
                   return fail(SPARSE_EINTERNAL, "padding entry with a nonzero weight");
                 continue;
               }
               if (m < 0) return fail(SPARSE_EINTERNAL, "entry in an empty row slot");
-              if (!emit(m, (int32_t)(c * p.kc + kl), w, q, c, s, g))
+              const int32_t kg = p.kind == SPARSE_SPMM ? (int32_t)(c * p.kc + kl) : (int32_t)(c * p.cc * 9 + kl);
+              if (!emit(m, kg, w, q, c, s, g))
                 return fail(SPARSE_EINTERNAL, "plan carries more entries than nnz");
             }
           }

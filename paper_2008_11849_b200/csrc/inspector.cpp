@@ -317,8 +317,38 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     p.nchunks = (o.c_in + cc - 1) / cc;
     p.conv_stage_elems = cc * p.conv_sci + 2 * p.conv_guard;
     p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
+    // Vectorised variant (conv3x3_vec_kernel) when a padded row fits twice in a warp's
+    // positions: lane owns C consecutive output positions (16 bytes), rows padded to wp
+    // (a multiple of C), and the staged input is kept as three copies shifted by dx - 1 so
+    // every tap is one aligned 128-bit shared load; entries use the SpMM unit format.
+    {
+      const int Cv = f16 ? 8 : 4, NTv = 32 * Cv;
+      const int wpv = (o.w + 2 + Cv - 1) / Cv * Cv;
+      if (o.conv_vec && 2 * wpv <= NTv) {
+        const int threads = 32 * (o.warps ? o.warps : 16);
+        p.conv_vec = 1;
+        p.C = Cv;
+        p.n_tile = NTv;
+        p.conv_wp = wpv;
+        p.conv_rb = std::min(o.h, NTv / wpv);
+        p.conv_ipt = 1;
+        p.conv_guard = 8;
+        p.conv_sci = (p.conv_guard + (p.conv_rb + 2) * wpv + 8 + 7) / 8 * 8;  // per channel
+        const int per_ch = 3 * p.conv_sci * S;
+        int ccv = o.k_chunk ? o.k_chunk : std::max(1, std::min(o.c_in, (48 * 1024) / per_ch));
+        // register-staged fill: at most 8 input elements per thread and chunk
+        ccv = std::max(1, std::min(ccv, 8 * threads / ((p.conv_rb + 2) * o.w)));
+        ccv = std::min(ccv, 64);
+        p.cc = ccv;
+        p.kc = 9 * ccv;
+        p.nchunks = (o.c_in + ccv - 1) / ccv;
+        p.conv_cs = ccv * p.conv_sci;  // elements per shifted copy
+        p.conv_stage_elems = 3 * p.conv_cs + NTv + 16;  // + zero block
+        p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
+      }
+    }
   }
-  p.warps = o.warps ? o.warps : (o.kind == SPARSE_SPMM ? 16 : 8);
+  p.warps = o.warps ? o.warps : (o.kind == SPARSE_SPMM || p.conv_vec ? 16 : 8);
   if (p.warps < 1 || p.warps > kMaxWarps) {
     err = "warps must be in [1, 16]";
     return SPARSE_EUNSUPPORTED;
@@ -362,6 +392,10 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   }
   if (p.R != 1 && p.R != 2 && p.R != 4 && p.R != 8 && p.R != 16) {
     err = "rows_per_warp must be 1, 2, 4, 8 or 16";
+    return SPARSE_EUNSUPPORTED;
+  }
+  if (p.conv_vec && p.R > 8) {
+    err = "rows_per_warp must be <= 8 for the vectorised conv kernel";
     return SPARSE_EUNSUPPORTED;
   }
   if (p.R * p.C > 128) {
@@ -440,6 +474,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   // ---------------- a4: chunking + packing ----------------
   // (block layouts in plan.h)
   const int A = p.entry_align;
+  const bool units = o.kind == SPARSE_SPMM || p.conv_vec;  // SpMM unit format (plan.h)
   const int G = o.kind == SPARSE_SPMM ? p.gk : 1;
   const int hdr = (int)align16((int64_t)p.Mp * G * 4);
   p.hdr_bytes = hdr;
@@ -450,15 +485,22 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   std::vector<int32_t> cursor(M, 0);
   std::vector<uint32_t> shdr((size_t)p.Mp * G);
   std::vector<uint8_t> ents;
-  const int64_t rowb = (int64_t)p.n_tile * S;  // bytes of one staged X row (SpMM)
+  // element offset of K row kl inside the staged tile (SpMM: X row kl; vectorised conv: tap
+  // (ci, dy, dx) = shifted copy dx, channel plane ci, row dy; kl == kc: the zero row/block)
+  auto elem_off = [&](int32_t kl) -> int64_t {
+    if (o.kind == SPARSE_SPMM) return (int64_t)kl * p.n_tile;
+    if (kl == p.kc) return 3 * (int64_t)p.conv_cs;
+    const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
+    return (int64_t)dx * p.conv_cs + (int64_t)ci * p.conv_sci + (int64_t)dy * p.conv_wp;
+  };
   auto put_spmm = [&](int32_t kl, float w, uint16_t wh) {
     uint8_t rec[8];
     if (f16) {
-      const uint16_t o16 = (uint16_t)((int64_t)kl * rowb / 16);
+      const uint16_t o16 = (uint16_t)(elem_off(kl) * 2 / 16);
       std::memcpy(rec, &o16, 2);
       std::memcpy(rec + 2, &wh, 2);
     } else {
-      const uint32_t o32 = (uint32_t)((int64_t)kl * rowb);
+      const uint32_t o32 = (uint32_t)(elem_off(kl) * 4);
       std::memcpy(rec, &o32, 4);
       std::memcpy(rec + 4, &w, 4);
     }
@@ -480,7 +522,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
           while (cur < (int32_t)rows[m].size() && rows[m][cur].k < k1) ++cur;
           e1 = cur;
         }
-        if (o.kind == SPARSE_SPMM) {
+        if (units) {
           // G contiguous k-ascending pieces, all but the last of `per` entries
           const int32_t n = e1 - e0;
           int32_t per = (n + G - 1) / G;
@@ -611,7 +653,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   uint64_t h = 1469598103934665603ull;
   const int32_t cfg[] = {p.M,  p.K,      p.dtype,   p.kind,    p.c_in,   p.h,
                          p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
-                         p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm};
+                         p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm,
+                         p.conv_vec};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

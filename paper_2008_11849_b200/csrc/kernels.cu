@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <mutex>
 #include <set>
+#include <type_traits>
 #include <utility>
 #include <string>
 
@@ -741,7 +742,7 @@ struct ConvArgs {
   uint8_t* y;
   int32_t B, H, W, c_in, cc, nchunks, Mp;
   int32_t x_stage_bytes, stage_bytes, hdr_bytes;
-  int32_t rb, ipt, wp, simg, sci, guard, stage_elems, T, bands;
+  int32_t rb, ipt, wp, simg, sci, guard, stage_elems, T, bands, cs;
 };
 
 template <int R, int CP, bool F16>
@@ -902,6 +903,126 @@ __global__ void __launch_bounds__(256) conv3x3_kernel(const ConvArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ conv 3x3, vectorised
+// Implicit im2col (Sec. 3.6) on the SpMM inner loop.  CTA = (panel of output
+// channels, image b, band of rb output rows).  Output positions p = r * wp + c (row r of the
+// band, padded column c, pixel x = c - 1); lane owns C consecutive positions (16 bytes).
+// The staged input of a chunk of cc channels is the zero-halo band (rows y0-1 .. y0+rb)
+// stored three times, copy d shifted by d - 1 elements, so tap (ci, dy, dx) of position p is
+// copy_dx[ci][G + p + dy * wp]: every entry is one aligned 128-bit shared load per lane
+// (plan entry offset = dx * cs + ci * sci + dy * wp elements).  Halo, guard and junk
+// positions are zero / discarded; no bounds checks in the FMA loop.
+template <int R, bool F16>
+__global__ void __launch_bounds__(512) conv3x3_vec_kernel(const ConvArgs a) {
+  constexpr int C = F16 ? 8 : 4;
+  constexpr int S = F16 ? 2 : 4;
+  constexpr int MAXE = 8;  // staged input elements per thread and chunk (inspector bound)
+  using T = typename std::conditional<F16, uint16_t, float>::type;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int panel = blockIdx.x;
+  const int b = (int)blockIdx.y / a.bands, band = (int)blockIdx.y % a.bands;
+  const int y0 = band * a.rb;
+  const int64_t plane = (int64_t)a.H * a.W;
+  const int per_ch = (a.rb + 2) * a.W;
+
+  for (int i = tid; i < 2 * a.stage_bytes / 16; i += nthr) ((uint4*)smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+
+  T v[MAXE];
+  auto load = [&](int chunk) {  // global -> registers (coalesced along x)
+    const int ci0 = chunk * a.cc, n = min(a.cc, a.c_in - ci0) * per_ch;
+#pragma unroll
+    for (int j = 0; j < MAXE; ++j) {
+      const int e = tid + j * nthr;
+      v[j] = T(0);
+      if (e < n) {
+        const int cl = e / per_ch, r = e - cl * per_ch;
+        const int hr = r / a.W, x = r - hr * a.W;
+        const int y = y0 - 1 + hr;
+        if (y >= 0 && y < a.H)
+          v[j] = ((const T*)a.x)[((int64_t)(ci0 + cl) * a.B + b) * plane + (int64_t)y * a.W + x];
+      }
+    }
+  };
+  auto store = [&](int buf, int chunk) {  // registers -> the three shifted copies
+    T* st = (T*)(smem + buf * a.stage_bytes);
+    const int n = min(a.cc, a.c_in - chunk * a.cc) * per_ch;
+#pragma unroll
+    for (int j = 0; j < MAXE; ++j) {
+      const int e = tid + j * nthr;
+      if (e < n) {
+        const int cl = e / per_ch, r = e - cl * per_ch;
+        const int hr = r / a.W, x = r - hr * a.W;
+        const int ebase = cl * a.sci + a.guard + hr * a.wp + x + 2;  // halo h + G + 1 - d, d = 0
+        st[ebase] = v[j];
+        st[a.cs + ebase - 1] = v[j];
+        st[2 * a.cs + ebase - 2] = v[j];
+      }
+    }
+  };
+  auto plan_copy = [&](int buf, int chunk) {
+    uint8_t* st = smem + buf * a.stage_bytes;
+    const int64_t bi = (int64_t)panel * a.nchunks + chunk;
+    const int64_t blk0 = a.blk_off[bi];
+    const int nb = (int)((a.blk_off[bi + 1] - blk0) >> 4);
+    const uint32_t dblk = smem_u32(st + a.x_stage_bytes);
+    for (int i = tid; i < nb; i += nthr) cp_async16(dblk + 16 * i, a.blob + blk0 + 16 * i, 16);
+  };
+
+  float acc[R][C];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+
+  load(0);
+  store(0, 0);
+  plan_copy(0, 0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int c = 0; c < a.nchunks; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < a.nchunks) {
+      load(c + 1);
+      plan_copy(buf ^ 1, c + 1);
+      cp_async_commit();
+    }
+    const uint8_t* st = smem + buf * a.stage_bytes;
+    const uint32_t* shdr = (const uint32_t*)(st + a.x_stage_bytes);
+    const uint4* ents = (const uint4*)(st + a.x_stage_bytes + a.hdr_bytes);
+    uint32_t h[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) h[r] = shdr[warp * R + r];
+    run_rows<F16, R>(acc, h, ents, st + (a.guard + lane * C) * S);
+    if (c + 1 < a.nchunks) {
+      store(buf ^ 1, c + 1);
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int row = a.row_id[(int64_t)panel * a.Mp + warp * R + r];
+    if (row < 0) continue;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int p = lane * C + c;
+      const int rr = p / a.wp, x = p - rr * a.wp - 1;
+      const int y = y0 + rr;
+      if (rr >= a.rb || y >= a.H || x < 0 || x >= a.W) continue;
+      const int64_t o = ((int64_t)row * a.B + b) * plane + (int64_t)y * a.W + x;
+      if (F16)
+        ((__half*)a.y)[o] = __float2half_rn(acc[r][c]);
+      else
+        ((float*)a.y)[o] = acc[r][c];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ dispatch
 using SpmmFn = void (*)(const __grid_constant__ CUtensorMap, const SpmmArgs);
 using ConvFn = void (*)(const ConvArgs);
@@ -923,6 +1044,15 @@ static SpmmFn pick_spmm(int R, int GK, bool tm) {
   if constexpr (!F16) { SRT_SR(16) }
 #undef SRT_SR
 #undef SRT_S
+  return nullptr;
+}
+
+template <bool F16>
+static ConvFn pick_conv_vec(int R) {
+  if (R == 1) return conv3x3_vec_kernel<1, F16>;
+  if (R == 2) return conv3x3_vec_kernel<2, F16>;
+  if (R == 4) return conv3x3_vec_kernel<4, F16>;
+  if (R == 8) return conv3x3_vec_kernel<8, F16>;
   return nullptr;
 }
 
@@ -1228,7 +1358,8 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
 int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
                    std::string& err) {
   const bool f16 = p.dtype == SPARSE_F16;
-  ConvFn fn = f16 ? pick_conv<true>(p.R, p.C) : pick_conv<false>(p.R, p.C);
+  ConvFn fn = p.conv_vec ? (f16 ? pick_conv_vec<true>(p.R) : pick_conv_vec<false>(p.R))
+                        : (f16 ? pick_conv<true>(p.R, p.C) : pick_conv<false>(p.R, p.C));
   if (!fn) {
     err = "internal: no conv kernel instance for this tile configuration";
     return SPARSE_EINTERNAL;
@@ -1265,7 +1396,8 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
   a.guard = p.conv_guard;
   a.stage_elems = p.conv_stage_elems;
   a.T = p.n_tile;
-  a.bands = p.h / p.conv_rb;
+  a.bands = p.conv_vec ? (p.h + p.conv_rb - 1) / p.conv_rb : p.h / p.conv_rb;
+  a.cs = p.conv_cs;
   const int64_t groups = (batch + p.conv_ipt - 1) / p.conv_ipt;
   const int64_t ntiles = groups * a.bands;
   if (ntiles > 65535) {

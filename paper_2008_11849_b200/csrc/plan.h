@@ -81,6 +81,8 @@ struct Plan {
   int32_t conv_sci = 0;   // smem elements per ci = ipt * simg
   int32_t conv_guard = 0; // guard elements before/after the stage
   int32_t conv_stage_elems = 0;
+  int32_t conv_vec = 0;   // 1: vectorised kernel (three dx-shifted copies, SpMM unit entries)
+  int32_t conv_cs = 0;    // vectorised: elements per shifted copy = cc * conv_sci
 
   // packed plan (host copy)
   std::vector<int32_t> row_id;   // npanels * Mp, -1 = empty slot
@@ -137,6 +139,7 @@ struct BuildOpts {
   int32_t executor = 0, jit_rows = 0, jit_warps = 0;
   int32_t cm = 0;
   int32_t tm = 0;
+  int32_t conv_vec = 1;   // allow the vectorised conv kernel
 };
 
 // JIT executor (jit.cpp).  Row entries per row (k ascending) as validated by the

@@ -112,15 +112,19 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     j.executor = 1;
     cands.push_back(j);
   } else {
-    for (int R : {2, 4, 8})
-      for (int w : {4, 8})
-        for (int cc : {8, 16, 32}) {
-          BuildOpts o = base;
-          o.rows_per_warp = R;
-          o.warps = w;
-          o.k_chunk = cc;
-          cands.push_back(o);
-        }
+    // vectorised kernel (16-byte loads of consecutive positions) and position-strided one
+    for (int vec : {1, 0})
+      for (int R : {2, 4, 8})
+        for (int w : {8, 16})
+          for (int cc : {8, 16, 32}) {
+            if (!vec && w == 16) continue;  // the position-strided kernel runs <= 8 warps
+            BuildOpts o = base;
+            o.rows_per_warp = R;
+            o.warps = w;
+            o.k_chunk = cc;
+            o.conv_vec = vec;
+            cands.push_back(o);
+          }
   }
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {

@@ -48,7 +48,7 @@ class sparse_plan_opts(ctypes.Structure):
                 ("k_split", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("executor", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
                 ("jit_warps", ctypes.c_int32), ("x_multicast", ctypes.c_int32),
-                ("x_source", ctypes.c_int32)]
+                ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32)]
 
 
 class sparse_plan_info_t(ctypes.Structure):
@@ -67,7 +67,8 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("jit_warps", ctypes.c_int32), ("jit_cubin_bytes", ctypes.c_int64),
                 ("jit_compile_ms", ctypes.c_double), ("tuned_us", ctypes.c_double),
                 ("digest", ctypes.c_uint64), ("x_multicast", ctypes.c_int32),
-                ("x_source", ctypes.c_int32)]
+                ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
+                ("reserved2", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -242,7 +243,7 @@ class Plan:
             if i["executor"] == 1:
                 o.update(jit_rows=i["jit_rows"], jit_warps=i["jit_warps"])
         else:
-            o.update(k_chunk=i["k_chunk"])
+            o.update(k_chunk=i["k_chunk"], conv_kernel=i["conv_kernel"])
             o.pop("split_k")
             o.pop("stages")
         return o

@@ -366,6 +366,34 @@ def test_conv_integer_exact_and_delta(f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("cin,cout,B,H,W,R,warps,cc", [
+    (16, 24, 3, 14, 14, 2, 16, 5), (256, 64, 2, 14, 14, 8, 16, 16), (8, 40, 2, 7, 7, 4, 8, 3),
+    (32, 16, 1, 56, 56, 2, 16, 8), (12, 20, 2, 28, 28, 8, 8, 4), (5, 9, 3, 5, 9, 1, 4, 2)])
+def test_conv_vectorised_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, f16):
+    # the vectorised conv kernel (three dx-shifted input copies, 128-bit position loads):
+    # exact on integer data, bitwise equal to the position-strided kernel (same k order)
+    dev = _dev()
+    vmax_w, vmax_x = (2, 4) if f16 else (3, 3)
+    w = gen.int_weights(cout, 9 * cin, 90, seed=cin + H, vmax=vmax_w)
+    x = gen.int_x(cin * B * H, W, seed=cout, vmax=vmax_x).reshape(cin, B, H, W)
+    xt = torch.from_numpy(x).to(dev).to(_tdt(f16))
+    ys = []
+    for ck in (0, 1):
+        kw = dict(rows_per_warp=R, warps=warps, k_chunk=cc) if ck == 0 else {}
+        plan = srt.Plan.from_csr(w, dtype=_tdt(f16), kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W,
+                                 n_hint=B, conv_kernel=ck, **kw)
+        assert plan.info["conv_kernel"] == ck
+        y = plan.conv3x3(xt)
+        torch.cuda.synchronize()
+        ys.append(y.float().cpu().numpy().astype(np.float64))
+    ref = oracle.conv3x3(cout, w.row_ptr, w.col_idx, _w64(w, f16), _x64(x, f16))
+    if f16:
+        ref = _f16_round(ref)
+    assert np.array_equal(ys[0], ref)
+    assert np.array_equal(ys[0], ys[1])
+
+
+@pytest.mark.parametrize("f16", [False, True])
 def test_conv_center_tap_equals_spmm(f16):
     # a W using only the center tap (dy = dx = 1) is a 1x1 conv: conv3x3 == spmm bitwise
     cin, cout, B, H, W = 64, 96, 4, 14, 14
