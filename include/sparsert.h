@@ -106,6 +106,9 @@ typedef struct {
                             staged input, 128-bit loads of C consecutive positions - when a padded
                             row of W + 2 positions fits twice in 32 * C positions, else the
                             position-strided kernel); 1 = position-strided kernel */
+  int32_t row_order;     /* 0 = load-balanced panels (rows sorted by nnz, LPT-binned, P:163-165;
+                            default); 1 = natural contiguous row ranges (the "no load balancing"
+                            ablation of P:385).  Result-neutral for split_k = k_split = 1. */
 } sparse_plan_opts;
 
 /* Fill *opts with defaults (kind SPMM, device -1, everything else 0). */
@@ -175,7 +178,7 @@ typedef struct {
   int32_t x_multicast;  /* CTAs per cluster sharing X tiles (TMA multicast) */
   int32_t x_source;     /* 0 shared memory, 1 tensor memory */
   int32_t conv_kernel;  /* conv: 0 vectorised, 1 position-strided */
-  int32_t reserved2;
+  int32_t row_order;    /* 0 LPT panels, 1 natural order */
 } sparse_plan_info_t;
 
 int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out);

@@ -68,6 +68,9 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   if (o.conv_kernel != 0 && o.conv_kernel != 1)
     return fail(SPARSE_EINVAL, "conv_kernel must be 0 (auto) or 1 (position-strided)");
   bo.conv_vec = o.conv_kernel == 0;
+  if (o.row_order != 0 && o.row_order != 1)
+    return fail(SPARSE_EINVAL, "row_order must be 0 (load balanced) or 1 (natural)");
+  bo.row_order = o.row_order;
   if (o.stages < 0 || o.stages > srt::kMaxStages)
     return fail(SPARSE_EUNSUPPORTED, "stages must be in [0, 8]");
   sparse_plan_s* h = nullptr;
@@ -238,6 +241,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->x_multicast = p.cm;
   out->x_source = p.tm;
   out->conv_kernel = p.kind == SPARSE_CONV3X3 && !p.conv_vec ? 1 : 0;
+  out->row_order = p.row_order;
   return ok();
 }
 

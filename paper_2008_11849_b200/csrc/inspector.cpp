@@ -443,20 +443,32 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   for (int32_t q = 0; q < p.npanels; ++q) heap.push({0, q});
   std::vector<std::vector<int32_t>> panel_rows(p.npanels);
   std::vector<int64_t> panel_nnz(p.npanels, 0);
-  for (int32_t m : order) {
-    PI top = heap.top();
-    heap.pop();
-    const int32_t q = top.second;
-    panel_rows[q].push_back(m);
-    panel_nnz[q] += (int64_t)rows[m].size();
-    if ((int)panel_rows[q].size() < p.Mp) heap.push({panel_nnz[q], q});
+  p.row_order = o.row_order;
+  if (o.row_order == 1) {
+    // ablation ("without load balancing"): panel q takes rows q*Mp .. q*Mp+Mp-1 and
+    // warp w of it the slots w*R .. w*R+R-1, in natural row order
+    for (int32_t m = 0; m < M; ++m) {
+      panel_rows[m / p.Mp].push_back(m);
+      panel_nnz[m / p.Mp] += (int64_t)rows[m].size();
+    }
+  } else {
+    for (int32_t m : order) {
+      PI top = heap.top();
+      heap.pop();
+      const int32_t q = top.second;
+      panel_rows[q].push_back(m);
+      panel_nnz[q] += (int64_t)rows[m].size();
+      if ((int)panel_rows[q].size() < p.Mp) heap.push({panel_nnz[q], q});
+    }
   }
   p.max_panel_nnz = *std::max_element(panel_nnz.begin(), panel_nnz.end());
   p.min_panel_nnz = *std::min_element(panel_nnz.begin(), panel_nnz.end());
 
   // within a panel: LPT across warps (R slots each)
   p.row_id.assign((size_t)p.npanels * p.Mp, -1);
-  for (int32_t q = 0; q < p.npanels; ++q) {
+  for (int32_t q = 0; o.row_order == 1 && q < p.npanels; ++q)
+    for (size_t i = 0; i < panel_rows[q].size(); ++i) p.row_id[(size_t)q * p.Mp + i] = panel_rows[q][i];
+  for (int32_t q = 0; o.row_order != 1 && q < p.npanels; ++q) {
     std::vector<int64_t> wl(p.warps, 0);
     std::vector<int> wfill(p.warps, 0);
     for (int32_t m : panel_rows[q]) {  // already in descending nnz order
@@ -654,7 +666,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   const int32_t cfg[] = {p.M,  p.K,      p.dtype,   p.kind,    p.c_in,   p.h,
                          p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
                          p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm,
-                         p.conv_vec};
+                         p.conv_vec, p.row_order};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

@@ -71,6 +71,7 @@ struct Plan {
   int32_t hdr_bytes = 16;   // block header bytes (slot table)
   int32_t ks = 1;           // cluster K-split: CTAs of a cluster take disjoint chunk ranges
   int32_t cm = 1;           // X multicast cluster: CTAs (consecutive panels) sharing X tiles
+  int32_t row_order = 0;    // 0 = LPT load balancing (default), 1 = natural order (ablation)
   int32_t tm = 0;           // X source: 0 = shared memory, 1 = tensor memory (tcgen05.ld)
 
   // conv geometry (kind == CONV3X3)
@@ -140,6 +141,7 @@ struct BuildOpts {
   int32_t cm = 0;
   int32_t tm = 0;
   int32_t conv_vec = 1;   // allow the vectorised conv kernel
+  int32_t row_order = 0;  // 0 = LPT panels (load balancing), 1 = natural contiguous rows
 };
 
 // JIT executor (jit.cpp).  Row entries per row (k ascending) as validated by the

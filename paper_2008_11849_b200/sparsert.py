@@ -48,7 +48,8 @@ class sparse_plan_opts(ctypes.Structure):
                 ("k_split", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("executor", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
                 ("jit_warps", ctypes.c_int32), ("x_multicast", ctypes.c_int32),
-                ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32)]
+                ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
+                ("row_order", ctypes.c_int32)]
 
 
 class sparse_plan_info_t(ctypes.Structure):
@@ -68,7 +69,7 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("jit_compile_ms", ctypes.c_double), ("tuned_us", ctypes.c_double),
                 ("digest", ctypes.c_uint64), ("x_multicast", ctypes.c_int32),
                 ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
-                ("reserved2", ctypes.c_int32)]
+                ("row_order", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -236,7 +237,7 @@ class Plan:
         another Plan of the same matrix rebuilds an identical replica (same digest)."""
         i = self.info
         o = dict(warps=i["warps"], rows_per_warp=i["rows_per_warp"], split_k=i["split_k"],
-                 stages=i["stages"], executor=i["executor"])
+                 stages=i["stages"], executor=i["executor"], row_order=i["row_order"])
         if self.kind == SPARSE_SPMM:
             o.update(k_chunk=i["k_chunk"], k_split=i["k_split"], x_multicast=i["x_multicast"],
                      x_source=i["x_source"])

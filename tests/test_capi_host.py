@@ -100,6 +100,21 @@ def test_panel_balance_and_group_split():
         assert sizes == [min(per, max(0, cnt - g * per)) for g in range(4)]
 
 
+def test_row_order_natural_panels():
+    # row_order = 1 (the "no load balancing" ablation): panel q holds rows q*Mp..,
+    # warp slots in natural order; default LPT panels are balanced within one max row
+    w = gen.stress_pattern("zipf", 512, 256, seed=5)
+    nat = _plan(w, n_hint=1024, warps=8, rows_per_warp=4, row_order=1)
+    assert nat.info["row_order"] == 1
+    d = nat.dump()
+    assert np.array_equal(d.panel, d.row // 32)
+    assert np.array_equal(d.slot, d.row % 32)
+    lpt = _plan(w, n_hint=1024, warps=8, rows_per_warp=4)
+    spread = lambda pl: pl.info["max_panel_nnz"] - pl.info["min_panel_nnz"]
+    assert spread(lpt) <= np.diff(w.row_ptr).max()
+    assert spread(nat) > spread(lpt)
+
+
 def test_spec_partition_examples():
     g = golden("spec_partition.json")
     # 4x4 example, 2 blocks -> balanced 2 / 2 (membership may differ: LPT)

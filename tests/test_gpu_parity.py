@@ -243,6 +243,16 @@ def test_wide_ctas_deep_rings_and_multicast_exact(warps, R, kc, st, cm, f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
+def test_row_order_natural_bitwise(f16):
+    # load balancing only moves rows between CTAs: bitwise the same output
+    w = gen.stress_pattern("zipf", 700, 300, seed=61)
+    X = gen.uniform_x(300, 333, seed=62)
+    y0, _ = _run_spmm(w, X, f16, warps=8, rows_per_warp=4)
+    y1, p1 = _run_spmm(w, X, f16, warps=8, rows_per_warp=4, row_order=1)
+    assert p1.info["row_order"] == 1 and np.array_equal(y0, y1)
+
+
+@pytest.mark.parametrize("f16", [False, True])
 def test_multicast_bitwise_equals_unicast(f16):
     w = gen.pruned_weights(1024, 768, 90, seed=41)
     X = gen.uniform_x(768, 1000, seed=42)
