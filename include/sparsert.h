@@ -144,6 +144,24 @@ int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void*
 int sparse_conv3x3(sparse_plan_t plan, int64_t batch, const void* x, void* y,
                    sparse_stream_t stream);
 
+/* Fused epilogue (NEXT #4; the paper leaves inter-op fusion to future work):
+ *   Y = act(W*X + bias + beta*Y)
+ * evaluated in fp32 on the plan-fixed accumulator (bias added after the last nonzero, then
+ * beta*Y_old, then the activation), rounded once to the output dtype.  beta == 0 never reads
+ * Y (NaN in Y is ignored); relu keeps NaN (x < 0 ? 0 : x). */
+typedef struct {
+  float beta;          /* 0 = overwrite */
+  const void* bias;    /* DEVICE, M values (SpMM) or C_out values (conv), plan dtype; NULL = none */
+  int32_t relu;        /* 0 = identity, 1 = ReLU */
+} sparse_epilogue;
+
+/* sparse_spmm / sparse_conv3x3 with an epilogue (ep == NULL: plain overwrite).  A JIT plan
+ * (executor 1) runs its plan-driven kernel when ep is non-trivial. */
+int sparse_spmm_ex(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y,
+                   int64_t ldy, const sparse_epilogue* ep, sparse_stream_t stream);
+int sparse_conv3x3_ex(sparse_plan_t plan, int64_t batch, const void* x, void* y,
+                      const sparse_epilogue* ep, sparse_stream_t stream);
+
 /* Free the plan and its device memory (north-star name).  Must not race with
  * work still enqueued that uses the plan.  NULL is a no-op. */
 int plan_destroy(sparse_plan_t plan);

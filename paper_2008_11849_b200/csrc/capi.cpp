@@ -148,8 +148,8 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   return ok();
 }
 
-int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                sparse_stream_t stream) {
+static int spmm_impl(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y,
+                     int64_t ldy, const sparse_epilogue* e, sparse_stream_t stream) {
   if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
   if (plan->p.kind != SPARSE_SPMM) return fail(SPARSE_EINVAL, "sparse_spmm on a conv plan");
   if (plan->host_only) return fail(SPARSE_EINVAL, "host-only plan cannot compute");
@@ -157,6 +157,13 @@ int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void*
   if (N == 0) return ok();
   if (!X || !Y) return fail(SPARSE_EINVAL, "X or Y is NULL");
   if (ldx < N || ldy < N) return fail(SPARSE_EINVAL, "ldx and ldy must be >= N");
+  srt::Epilogue ep;
+  if (e) {
+    if (e->relu != 0 && e->relu != 1) return fail(SPARSE_EINVAL, "epilogue relu must be 0 or 1");
+    ep.beta = e->beta;
+    ep.bias = e->bias;
+    ep.relu = e->relu;
+  }
   std::string err;
   const srt::Plan& p = plan->p;
   const int S = p.dtype == SPARSE_F16 ? 2 : 4;
@@ -173,24 +180,51 @@ int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void*
       scratch = nullptr;
     }
   }
-  const int rc = srt::jit_can_launch(p, Xa, lda)
+  const int rc = ep.trivial() && srt::jit_can_launch(p, Xa, lda)
                      ? srt::jit_launch(p, N, Xa, lda, Y, ldy, stream, err)
-                     : srt::launch_spmm(p, N, Xa, lda, Y, ldy, stream, err);
+                     : srt::launch_spmm(p, N, Xa, lda, Y, ldy, stream, err, ep);
   if (scratch) srt::free_repack(p.device, scratch, stream);
   return rc == SPARSE_OK ? ok() : fail(rc, err);
 }
 
-int sparse_conv3x3(sparse_plan_t plan, int64_t batch, const void* x, void* y,
-                   sparse_stream_t stream) {
+int sparse_spmm(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                sparse_stream_t stream) {
+  return spmm_impl(plan, N, X, ldx, Y, ldy, nullptr, stream);
+}
+
+int sparse_spmm_ex(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y,
+                   int64_t ldy, const sparse_epilogue* ep, sparse_stream_t stream) {
+  return spmm_impl(plan, N, X, ldx, Y, ldy, ep, stream);
+}
+
+static int conv_impl(sparse_plan_t plan, int64_t batch, const void* x, void* y,
+                     const sparse_epilogue* e, sparse_stream_t stream) {
   if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
   if (plan->p.kind != SPARSE_CONV3X3) return fail(SPARSE_EINVAL, "sparse_conv3x3 on an SpMM plan");
   if (plan->host_only) return fail(SPARSE_EINVAL, "host-only plan cannot compute");
   if (batch < 0) return fail(SPARSE_EINVAL, "batch < 0");
   if (batch == 0) return ok();
   if (!x || !y) return fail(SPARSE_EINVAL, "x or y is NULL");
+  srt::Epilogue ep;
+  if (e) {
+    if (e->relu != 0 && e->relu != 1) return fail(SPARSE_EINVAL, "epilogue relu must be 0 or 1");
+    ep.beta = e->beta;
+    ep.bias = e->bias;
+    ep.relu = e->relu;
+  }
   std::string err;
-  const int rc = srt::launch_conv3x3(plan->p, batch, x, y, stream, err);
+  const int rc = srt::launch_conv3x3(plan->p, batch, x, y, stream, err, ep);
   return rc == SPARSE_OK ? ok() : fail(rc, err);
+}
+
+int sparse_conv3x3(sparse_plan_t plan, int64_t batch, const void* x, void* y,
+                   sparse_stream_t stream) {
+  return conv_impl(plan, batch, x, y, nullptr, stream);
+}
+
+int sparse_conv3x3_ex(sparse_plan_t plan, int64_t batch, const void* x, void* y,
+                      const sparse_epilogue* ep, sparse_stream_t stream) {
+  return conv_impl(plan, batch, x, y, ep, stream);
 }
 
 int plan_destroy(sparse_plan_t plan) {

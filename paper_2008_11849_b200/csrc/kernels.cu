@@ -373,6 +373,16 @@ __device__ __forceinline__ void run_rows_tm(float (&acc)[R][F16 ? 8 : 4], const 
   }
 }
 
+// Fused epilogue on one output value: act(acc + bias[row] + beta * y_old), fp32.
+template <bool F16>
+__device__ __forceinline__ float epilogue_one(float v, const uint8_t* bias, int row, float beta,
+                                              const uint8_t* yold, int relu) {
+  if (bias) v += F16 ? __half2float(((const __half*)bias)[row]) : ((const float*)bias)[row];
+  if (beta != 0.0f) v = fmaf(beta, F16 ? __half2float(*(const __half*)yold) : *(const float*)yold, v);
+  if (relu) v = v < 0.0f ? 0.0f : v;
+  return v;
+}
+
 // ------------------------------------------------------------------ SpMM
 struct SpmmArgs {
   const uint8_t* blob;
@@ -384,6 +394,9 @@ struct SpmmArgs {
   int32_t K, kc, nchunks, Mp, ks, stages, npanels;
   int32_t x_stage_bytes, stage_bytes, hdr_bytes, bar_off, blk_bytes;
   int32_t use_tma, vec_y, cm;
+  const uint8_t* bias;  // fused epilogue (plan.h Epilogue)
+  float beta;
+  int32_t relu;
 };
 
 template <int R, int GK, bool F16, bool TM>
@@ -567,11 +580,18 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
   auto store_tile = [&](int64_t n0, const int (&rows)[R]) {
     const int ncol = (int)min((int64_t)NT, a.N - n0);
     if (g != 0 || col >= ncol) return;
+    const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int row = rows[r];
       if (row < 0) continue;
       uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + col) * S;
+      if (epi) {
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          if (col + c < ncol)
+            acc[r][c] = epilogue_one<F16>(acc[r][c], a.bias, row, a.beta, yp + c * S, a.relu);
+      }
       if (F16) {
         __half h[C];
 #pragma unroll
@@ -708,6 +728,12 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
       v.w += u.w;
     }
     uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + c4) * S;
+    if (a.bias != nullptr || a.beta != 0.0f || a.relu) {
+      if (c4 + 0 < ncol) v.x = epilogue_one<F16>(v.x, a.bias, row, a.beta, yp + 0 * S, a.relu);
+      if (c4 + 1 < ncol) v.y = epilogue_one<F16>(v.y, a.bias, row, a.beta, yp + 1 * S, a.relu);
+      if (c4 + 2 < ncol) v.z = epilogue_one<F16>(v.z, a.bias, row, a.beta, yp + 2 * S, a.relu);
+      if (c4 + 3 < ncol) v.w = epilogue_one<F16>(v.w, a.bias, row, a.beta, yp + 3 * S, a.relu);
+    }
     const float vv[4] = {v.x, v.y, v.z, v.w};
     if (F16) {
       __half h[4];
@@ -743,6 +769,9 @@ struct ConvArgs {
   int32_t B, H, W, c_in, cc, nchunks, Mp;
   int32_t x_stage_bytes, stage_bytes, hdr_bytes;
   int32_t rb, ipt, wp, simg, sci, guard, stage_elems, T, bands, cs;
+  const uint8_t* bias;  // fused epilogue (plan.h Epilogue)
+  float beta;
+  int32_t relu;
 };
 
 template <int R, int CP, bool F16>
@@ -895,10 +924,11 @@ __global__ void __launch_bounds__(256) conv3x3_kernel(const ConvArgs a) {
     for (int j = 0; j < CP; ++j) {
       if (out[j] < 0) continue;
       const int64_t o = (int64_t)row * plane + out[j];
+      const float v = epilogue_one<F16>(acc[r][j], a.bias, row, a.beta, a.y + o * S, a.relu);
       if (F16)
-        ((__half*)a.y)[o] = __float2half_rn(acc[r][j]);
+        ((__half*)a.y)[o] = __float2half_rn(v);
       else
-        ((float*)a.y)[o] = acc[r][j];
+        ((float*)a.y)[o] = v;
     }
   }
 }
@@ -1015,10 +1045,11 @@ __global__ void __launch_bounds__(512) conv3x3_vec_kernel(const ConvArgs a) {
       const int y = y0 + rr;
       if (rr >= a.rb || y >= a.H || x < 0 || x >= a.W) continue;
       const int64_t o = ((int64_t)row * a.B + b) * plane + (int64_t)y * a.W + x;
+      const float v = epilogue_one<F16>(acc[r][c], a.bias, row, a.beta, a.y + o * S, a.relu);
       if (F16)
-        ((__half*)a.y)[o] = __float2half_rn(acc[r][c]);
+        ((__half*)a.y)[o] = __float2half_rn(v);
       else
-        ((float*)a.y)[o] = acc[r][c];
+        ((float*)a.y)[o] = v;
     }
   }
 }
@@ -1223,7 +1254,7 @@ void free_plan_device(Plan& p) {
 }
 
 int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                void* stream, std::string& err) {
+                void* stream, std::string& err, const Epilogue& ep) {
   const bool f16 = p.dtype == SPARSE_F16;
   const int S = f16 ? 2 : 4;
   SpmmFn fn = f16 ? pick_spmm<true>(p.R, p.gk, p.tm) : pick_spmm<false>(p.R, p.gk, p.tm);
@@ -1252,6 +1283,9 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
   a.hdr_bytes = p.hdr_bytes;
   a.blk_bytes = p.max_blk_bytes;
   a.bar_off = p.smem_bytes - 128;
+  a.bias = (const uint8_t*)ep.bias;
+  a.beta = ep.beta;
+  a.relu = ep.relu;
   const int smem = p.smem_bytes;
   const bool vec_x = ((uintptr_t)X % 16 == 0) && ((ldx * S) % 16 == 0);
   a.vec_y = ((uintptr_t)Y % 16 == 0) && ((ldy * S) % 16 == 0);
@@ -1356,7 +1390,7 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
 }
 
 int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
-                   std::string& err) {
+                   std::string& err, const Epilogue& ep) {
   const bool f16 = p.dtype == SPARSE_F16;
   ConvFn fn = p.conv_vec ? (f16 ? pick_conv_vec<true>(p.R) : pick_conv_vec<false>(p.R))
                         : (f16 ? pick_conv<true>(p.R, p.C) : pick_conv<false>(p.R, p.C));
@@ -1398,6 +1432,9 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
   a.T = p.n_tile;
   a.bands = p.conv_vec ? (p.h + p.conv_rb - 1) / p.conv_rb : p.h / p.conv_rb;
   a.cs = p.conv_cs;
+  a.bias = (const uint8_t*)ep.bias;
+  a.beta = ep.beta;
+  a.relu = ep.relu;
   const int64_t groups = (batch + p.conv_ipt - 1) / p.conv_ipt;
   const int64_t ntiles = groups * a.bands;
   if (ntiles > 65535) {

@@ -181,10 +181,16 @@ float f16_to_f32(uint16_t h);
 // Device side (kernels.cu)
 int upload_plan(Plan& p, std::string& err);
 void free_plan_device(Plan& p);
+struct Epilogue {  // Y = act(acc + bias + beta * Y); see sparse_epilogue
+  float beta = 0.0f;
+  const void* bias = nullptr;
+  int32_t relu = 0;
+  bool trivial() const { return beta == 0.0f && bias == nullptr && relu == 0; }
+};
 int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                void* stream, std::string& err);
+                void* stream, std::string& err, const Epilogue& ep = Epilogue());
 int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
-                   std::string& err);
+                   std::string& err, const Epilogue& ep = Epilogue());
 // Unaligned X (base or row stride not a 16-byte multiple): stream-ordered copy into a
 // padded scratch buffer so the TMA paths apply; free_repack releases it (stream-ordered).
 int launch_repack(int device, int64_t K, int64_t N, int S, const void* X, int64_t ldx, void** Xp,

@@ -28,6 +28,7 @@ STATUS_NAMES = {0: "SPARSE_OK", 1: "SPARSE_EINVAL", 2: "SPARSE_EMATRIX", 3: "SPA
 
 # every symbol include/sparsert.h declares (checked by tests/test_capi_host.py)
 EXPORTED = ["sparse_plan_opts_init", "sparse_plan_create", "sparse_spmm", "sparse_conv3x3",
+            "sparse_spmm_ex", "sparse_conv3x3_ex",
             "plan_destroy", "sparse_plan_destroy", "sparse_plan_info", "sparse_plan_dump",
             "sparse_last_error", "sparse_version"]
 
@@ -50,6 +51,10 @@ class sparse_plan_opts(ctypes.Structure):
                 ("jit_warps", ctypes.c_int32), ("x_multicast", ctypes.c_int32),
                 ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
                 ("row_order", ctypes.c_int32)]
+
+
+class sparse_epilogue(ctypes.Structure):
+    _fields_ = [("beta", ctypes.c_float), ("bias", ctypes.c_void_p), ("relu", ctypes.c_int32)]
 
 
 class sparse_plan_info_t(ctypes.Structure):
@@ -87,6 +92,10 @@ def _load() -> ctypes.CDLL:
     lib.sparse_spmm.restype = ctypes.c_int
     lib.sparse_conv3x3.argtypes = [P, i64, P, P, P]
     lib.sparse_conv3x3.restype = ctypes.c_int
+    lib.sparse_spmm_ex.argtypes = [P, i64, P, i64, P, i64, ctypes.POINTER(sparse_epilogue), P]
+    lib.sparse_spmm_ex.restype = ctypes.c_int
+    lib.sparse_conv3x3_ex.argtypes = [P, i64, P, P, ctypes.POINTER(sparse_epilogue), P]
+    lib.sparse_conv3x3_ex.restype = ctypes.c_int
     lib.plan_destroy.argtypes = [P]
     lib.plan_destroy.restype = ctypes.c_int
     lib.sparse_plan_destroy.argtypes = [P]
@@ -141,6 +150,16 @@ def sparse_spmm(plan, N, X_ptr, ldx, Y_ptr, ldy, stream=0):
 
 def sparse_conv3x3(plan, batch, x_ptr, y_ptr, stream=0):
     _check(lib.sparse_conv3x3(plan, int(batch), x_ptr, y_ptr, stream))
+
+
+def sparse_spmm_ex(plan, N, X_ptr, ldx, Y_ptr, ldy, epilogue=None, stream=0):
+    ep = ctypes.byref(epilogue) if epilogue is not None else None
+    _check(lib.sparse_spmm_ex(plan, int(N), X_ptr, int(ldx), Y_ptr, int(ldy), ep, stream))
+
+
+def sparse_conv3x3_ex(plan, batch, x_ptr, y_ptr, epilogue=None, stream=0):
+    ep = ctypes.byref(epilogue) if epilogue is not None else None
+    _check(lib.sparse_conv3x3_ex(plan, int(batch), x_ptr, y_ptr, ep, stream))
 
 
 def plan_destroy(plan):
@@ -259,8 +278,19 @@ class Plan:
         if t.device.index != dev:
             raise ValueError(f"{name} on {t.device}, plan on cuda:{dev}")
 
-    def spmm(self, X, Y=None, stream=None):
-        """Y[:, :N] = W @ X.  X: (K, N) CUDA tensor with unit column stride (row stride = ldx)."""
+    def _epilogue(self, bias, beta, relu, n_out):
+        if bias is None and beta == 0.0 and not relu:
+            return None
+        if bias is not None:
+            self._check_tensor(bias, "bias")
+            if bias.dim() != 1 or bias.shape[0] != n_out or not bias.is_contiguous():
+                raise ValueError(f"bias must be a contiguous vector of {n_out} values")
+        return sparse_epilogue(float(beta), ctypes.c_void_p(bias.data_ptr()) if bias is not None else None,
+                               1 if relu else 0)
+
+    def spmm(self, X, Y=None, stream=None, bias=None, beta=0.0, relu=False):
+        """Y[:, :N] = act(W @ X + bias + beta * Y).  X: (K, N) CUDA tensor with unit column
+        stride (row stride = ldx); bias: (M,) plan dtype; relu: ReLU after the sum."""
         import torch
         if self.kind != SPARSE_SPMM:
             raise ValueError("spmm on a conv plan")
@@ -268,6 +298,8 @@ class Plan:
         if X.dim() != 2 or X.shape[0] != self.K or (X.shape[1] > 1 and X.stride(1) != 1):
             raise ValueError("X must be (K, N) with unit column stride")
         N = X.shape[1]
+        if beta != 0.0 and Y is None:
+            raise ValueError("beta != 0 needs Y")
         if Y is None:
             Y = torch.empty((self.M, N), dtype=self.dtype, device=X.device)
         self._check_tensor(Y, "Y")
@@ -276,12 +308,18 @@ class Plan:
         s = (stream or torch.cuda.current_stream(X.device)).cuda_stream
         ldx = X.stride(0) if N > 0 else max(N, 1)
         ldy = Y.stride(0) if N > 0 else max(N, 1)
-        sparse_spmm(self._h, N, ctypes.c_void_p(X.data_ptr()), max(ldx, N),
-                    ctypes.c_void_p(Y.data_ptr()), max(ldy, N), ctypes.c_void_p(s))
+        ep = self._epilogue(bias, beta, relu, self.M)
+        if ep is None:
+            sparse_spmm(self._h, N, ctypes.c_void_p(X.data_ptr()), max(ldx, N),
+                        ctypes.c_void_p(Y.data_ptr()), max(ldy, N), ctypes.c_void_p(s))
+        else:
+            sparse_spmm_ex(self._h, N, ctypes.c_void_p(X.data_ptr()), max(ldx, N),
+                           ctypes.c_void_p(Y.data_ptr()), max(ldy, N), ep, ctypes.c_void_p(s))
         return Y
 
-    def conv3x3(self, x, y=None, stream=None):
-        """y = conv3x3(x), x: (C_in, B, H, W) contiguous CUDA tensor (CNHW)."""
+    def conv3x3(self, x, y=None, stream=None, bias=None, beta=0.0, relu=False):
+        """y = act(conv3x3(x) + bias + beta * y), x: (C_in, B, H, W) contiguous CUDA tensor
+        (CNHW); bias: (C_out,) plan dtype."""
         import torch
         if self.kind != SPARSE_CONV3X3:
             raise ValueError("conv3x3 on an SpMM plan")
@@ -290,12 +328,19 @@ class Plan:
         if x.dim() != 4 or tuple(x.shape[0:1]) + tuple(x.shape[2:]) != (c_in, h, w) or not x.is_contiguous():
             raise ValueError(f"x must be contiguous (C_in={c_in}, B, H={h}, W={w})")
         B = x.shape[1]
+        if beta != 0.0 and y is None:
+            raise ValueError("beta != 0 needs y")
         if y is None:
             y = torch.empty((self.M, B, h, w), dtype=self.dtype, device=x.device)
         self._check_tensor(y, "y")
         if tuple(y.shape) != (self.M, B, h, w) or not y.is_contiguous():
             raise ValueError("y must be contiguous (C_out, B, H, W)")
         s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
-        sparse_conv3x3(self._h, B, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
-                       ctypes.c_void_p(s))
+        ep = self._epilogue(bias, beta, relu, self.M)
+        if ep is None:
+            sparse_conv3x3(self._h, B, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                           ctypes.c_void_p(s))
+        else:
+            sparse_conv3x3_ex(self._h, B, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                              ep, ctypes.c_void_p(s))
         return y

@@ -497,3 +497,59 @@ def test_auto_executor_choice():
     small = srt.Plan.from_csr(gen.pruned_weights(256, 64, 90, seed=1), n_hint=25088, executor=2)
     big = srt.Plan.from_csr(gen.pruned_weights(768, 3072, 90, seed=1), n_hint=16384, executor=2)
     assert small.info["executor"] == 1 and big.info["executor"] == 0
+
+
+# --------------------------------------------------------------------------- fused epilogue
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("opts", [dict(), dict(k_split=4, rows_per_warp=4), dict(executor=1),
+                                  dict(split_k=2, warps=8)])
+def test_spmm_epilogue_exact(opts, f16):
+    # Y = relu(W X + bias + beta Y0) on integer data: exact (fp32 accumulate, one rounding);
+    # also through the cluster (k_split) store, a JIT plan (falls back to plan-driven) and
+    # split-K groups
+    dev = _dev()
+    M, K, N = 300, 500, 260
+    vmax_w, vmax_x = (2, 4) if f16 else (3, 3)
+    w = gen.int_weights(M, K, 90, seed=71, vmax=vmax_w)
+    X = gen.int_x(K, N, seed=72, vmax=vmax_x)
+    rng = np.random.default_rng(73)
+    bias = rng.integers(-8, 9, M).astype(np.float32)
+    Y0 = rng.integers(-8, 9, (M, N)).astype(np.float32)
+    plan = srt.Plan.from_csr(w, dtype=_tdt(f16), n_hint=N, **opts)
+    Xd = torch.from_numpy(X).to(dev).to(_tdt(f16))
+    for beta, relu, use_bias in [(0.0, True, True), (2.0, False, True), (-1.0, True, False), (0.0, False, False)]:
+        Y = torch.from_numpy(Y0).to(dev).to(_tdt(f16))
+        b = torch.from_numpy(bias).to(dev).to(_tdt(f16)) if use_bias else None
+        plan.spmm(Xd, Y, bias=b, beta=beta, relu=relu)
+        torch.cuda.synchronize()
+        ref = _ref(w, X, f16) + (bias[:, None] if use_bias else 0.0) + beta * Y0
+        if relu:
+            ref = np.maximum(ref, 0.0)
+        if f16:
+            ref = _f16_round(ref)
+        assert np.array_equal(Y.double().cpu().numpy(), ref), (beta, relu, use_bias)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("ck", [0, 1])
+def test_conv_epilogue_exact(ck, f16):
+    dev = _dev()
+    cin, cout, B, H, W = 24, 40, 2, 14, 14
+    vmax_w, vmax_x = (2, 4) if f16 else (3, 3)
+    w = gen.int_weights(cout, 9 * cin, 90, seed=81, vmax=vmax_w)
+    x = gen.int_x(cin * B * H, W, seed=82, vmax=vmax_x).reshape(cin, B, H, W)
+    rng = np.random.default_rng(83)
+    bias = rng.integers(-8, 9, cout).astype(np.float32)
+    y0 = rng.integers(-8, 9, (cout, B, H, W)).astype(np.float32)
+    plan = srt.Plan.from_csr(w, dtype=_tdt(f16), kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W,
+                             n_hint=B, conv_kernel=ck)
+    y = torch.from_numpy(y0).to(dev).to(_tdt(f16))
+    plan.conv3x3(torch.from_numpy(x).to(dev).to(_tdt(f16)), y,
+                 bias=torch.from_numpy(bias).to(dev).to(_tdt(f16)), beta=0.5, relu=True)
+    torch.cuda.synchronize()
+    ref = oracle.conv3x3(cout, w.row_ptr, w.col_idx, _w64(w, f16), _x64(x, f16))
+    ref = np.maximum(ref + bias[:, None, None, None] + 0.5 * y0, 0.0)
+    if f16:
+        ref = _f16_round(ref)
+    assert np.array_equal(y.double().cpu().numpy(), ref)
