@@ -109,6 +109,12 @@ typedef struct {
   int32_t row_order;     /* 0 = load-balanced panels (rows sorted by nnz, LPT-binned, P:163-165;
                             default); 1 = natural contiguous row ranges (the "no load balancing"
                             ablation of P:385).  Result-neutral for split_k = k_split = 1. */
+  int32_t tc_min_density; /* fp16 SpMM plans (not JIT): aligned 16 x 16 tiles of W holding at least
+                            this % of nonzeros are multiplied as dense blocks on the tensor
+                            cores (mma.sync m16n8k16, fp32 accumulate) and added to the CUDA-core
+                            result before its single rounding.  0 = default
+                            (50 %), -1 = off, 1..100 = threshold.  Changes the summation order
+                            of the rows concerned (within tolerance; exact on integer data). */
 } sparse_plan_opts;
 
 /* Fill *opts with defaults (kind SPMM, device -1, everything else 0). */
@@ -197,6 +203,10 @@ typedef struct {
   int32_t x_source;     /* 0 shared memory, 1 tensor memory */
   int32_t conv_kernel;  /* conv: 0 vectorised, 1 position-strided */
   int32_t row_order;    /* 0 LPT panels, 1 natural order */
+  int32_t tc_min_density; /* effective threshold (%), 0 = no tensor-core sub-blocks */
+  int32_t tc_row_blocks;  /* 16-row blocks with >= 1 dense tile */
+  int64_t tc_tiles;       /* dense 16 x 16 tiles on the tensor cores */
+  int64_t tc_nnz;         /* nonzeros inside them (counted in nnz) */
 } sparse_plan_info_t;
 
 int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out);

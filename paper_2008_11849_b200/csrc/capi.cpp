@@ -71,6 +71,9 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   if (o.row_order != 0 && o.row_order != 1)
     return fail(SPARSE_EINVAL, "row_order must be 0 (load balanced) or 1 (natural)");
   bo.row_order = o.row_order;
+  if (o.tc_min_density < -1 || o.tc_min_density > 100)
+    return fail(SPARSE_EINVAL, "tc_min_density must be -1 (off), 0 (default) or 1..100");
+  bo.tc_min_pct = o.tc_min_density == 0 ? 50 : (o.tc_min_density < 0 ? 0 : o.tc_min_density);
   if (o.stages < 0 || o.stages > srt::kMaxStages)
     return fail(SPARSE_EUNSUPPORTED, "stages must be in [0, 8]");
   sparse_plan_s* h = nullptr;
@@ -276,6 +279,10 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->x_source = p.tm;
   out->conv_kernel = p.kind == SPARSE_CONV3X3 && !p.conv_vec ? 1 : 0;
   out->row_order = p.row_order;
+  out->tc_min_density = p.tc_ntiles > 0 || p.tc_min_pct > 0 ? p.tc_min_pct : 0;
+  out->tc_row_blocks = p.tc_nrb;
+  out->tc_tiles = p.tc_ntiles;
+  out->tc_nnz = p.tc_nnz;
   return ok();
 }
 
@@ -378,6 +385,22 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
           const int rem = base - ci * p.conv_sci;
           const int dy = rem / p.conv_wp, dx = rem % p.conv_wp;
           if (!emit(m, (c * p.cc + ci) * 9 + dy * 3 + dx, w, q, c, s, 0))
+            return fail(SPARSE_EINTERNAL, "plan carries more entries than nnz");
+        }
+      }
+    }
+  }
+  // tensor-core sub-blocks: the nonzero slots of every dense tile (panel/chunk/slot = -1,
+  // group = tile index)
+  for (size_t i = 0; i < p.tc_rb.size(); ++i) {
+    for (int32_t t = p.tc_tile_begin[i]; t < p.tc_tile_begin[i + 1]; ++t) {
+      for (int lane = 0; lane < 32; ++lane) {
+        for (int sl = 0; sl < 8; ++sl) {
+          const uint16_t wh = p.tc_a[(size_t)t * 256 + lane * 8 + sl];
+          if ((wh & 0x7fffu) == 0) continue;
+          const int g = lane / 4, tq = lane % 4;
+          const int r = g + 8 * ((sl >> 1) & 1), c = 2 * tq + (sl & 1) + 8 * (sl >> 2);
+          if (!emit(p.tc_rb[i] * 16 + r, p.tc_cb[t] * 16 + c, srt::f16_to_f32(wh), -1, -1, -1, t))
             return fail(SPARSE_EINTERNAL, "plan carries more entries than nnz");
         }
       }

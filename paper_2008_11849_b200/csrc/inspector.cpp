@@ -213,12 +213,87 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     }
   }
 
+  // ---------------- tensor-core sub-blocks (NEXT #1): fp16 SpMM plans only ----------------
+  // Aligned 16 x 16 tiles of W holding >= tc_min_pct % nonzeros are dense enough to be a
+  // real dense contraction: their nonzeros leave the CUDA-core rows and are packed as dense
+  // fp16 tiles in mma.m16n8k16 A-fragment order (lane l = 4 g + t holds rows g, g + 8 and
+  // columns 2t, 2t + 1, 2t + 8, 2t + 9).
+  std::vector<int32_t> tc_rb, tc_tile_begin, tc_cb, ws_row;
+  std::vector<uint16_t> tc_a;
+  int64_t tc_nnz = 0;
+  // (not with the JIT executor, which bakes every nonzero into its code)
+  const int tc_pct = (dtype == SPARSE_F16 && o.kind == SPARSE_SPMM && o.executor != 1) ? o.tc_min_pct : 0;
+  if (tc_pct < 0 || tc_pct > 100) {
+    err = "tc_min_density must be in [0, 100] (percent)";
+    return SPARSE_EINVAL;
+  }
+  const int64_t nrb = (M + 15) / 16, ncb = (K + 15) / 16;
+  if (tc_pct > 0 && nrb * ncb <= (int64_t)1 << 26) {
+    const int thr = std::max(1, (tc_pct * 256 + 99) / 100);
+    std::vector<uint16_t> cnt((size_t)(nrb * ncb), 0);
+    for (int32_t m = 0; m < M; ++m)
+      for (const Entry& en : rows[m]) cnt[(size_t)((m / 16) * ncb + en.k / 16)]++;
+    ws_row.assign(M, -1);
+    for (int64_t rb = 0; rb < nrb; ++rb) {
+      bool any = false;
+      for (int64_t cb = 0; cb < ncb; ++cb) {
+        if (cnt[(size_t)(rb * ncb + cb)] < thr) continue;
+        if (!any) {
+          tc_rb.push_back((int32_t)rb);
+          tc_tile_begin.push_back((int32_t)tc_cb.size());
+          any = true;
+        }
+        tc_cb.push_back((int32_t)cb);
+        tc_a.resize(tc_a.size() + 256, 0);
+      }
+    }
+    tc_tile_begin.push_back((int32_t)tc_cb.size());
+    if (!tc_cb.empty()) {
+      // dense tile index of (rb, cb), -1 if not dense
+      std::vector<int32_t> tile_of((size_t)(nrb * ncb), -1);
+      for (size_t i = 0; i + 1 < tc_tile_begin.size(); ++i)
+        for (int32_t t = tc_tile_begin[i]; t < tc_tile_begin[i + 1]; ++t)
+          tile_of[(size_t)(tc_rb[i] * ncb + tc_cb[t])] = t;
+      for (size_t i = 0; i < tc_rb.size(); ++i)
+        for (int r = 0; r < 16 && tc_rb[i] * 16 + r < M; ++r) ws_row[tc_rb[i] * 16 + r] = (int32_t)(i * 16 + r);
+      for (int32_t m = 0; m < M; ++m) {
+        std::vector<Entry> keep;
+        keep.reserve(rows[m].size());
+        for (const Entry& en : rows[m]) {
+          const int32_t t = tile_of[(size_t)((m / 16) * ncb + en.k / 16)];
+          if (t < 0) {
+            keep.push_back(en);
+            continue;
+          }
+          const int r = m % 16, c = en.k % 16;
+          const int g = r % 8, hi_r = r / 8, tq = (c % 8) / 2, hi_c = c / 8, lo = c % 2;
+          const int lane = 4 * g + tq;
+          const int slot = hi_c * 4 + hi_r * 2 + lo;  // a0..a7
+          tc_a[(size_t)t * 256 + lane * 8 + slot] = en.wh;
+          ++tc_nnz;
+        }
+        rows[m].swap(keep);
+      }
+    }
+  }
+
   p = Plan();
   p.M = M;
   p.K = K;
   p.dtype = dtype;
   p.kind = o.kind;
   p.nnz = kept;
+  p.tc_min_pct = tc_pct;
+  p.tc_nrb = (int32_t)tc_rb.size();
+  p.tc_ntiles = (int64_t)tc_cb.size();
+  p.tc_nnz = tc_nnz;
+  if (p.tc_ntiles > 0) {
+    p.tc_rb.swap(tc_rb);
+    p.tc_tile_begin.swap(tc_tile_begin);
+    p.tc_cb.swap(tc_cb);
+    p.tc_a.swap(tc_a);
+    p.ws_row.swap(ws_row);
+  }
   p.n_hint = o.n_hint;
   const bool f16 = dtype == SPARSE_F16;
   const int S = f16 ? 2 : 4;
@@ -643,7 +718,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     return SPARSE_EUNSUPPORTED;
   }
   p.plan_bytes = (int64_t)p.blob.size() + (int64_t)p.row_id.size() * 4 +
-                 (int64_t)p.blk_off.size() * 8;
+                 (int64_t)p.blk_off.size() * 8 + (int64_t)p.tc_a.size() * 2 +
+                 (int64_t)(p.tc_cb.size() + p.tc_rb.size() + p.tc_tile_begin.size() + p.ws_row.size()) * 4;
 
   if (o.executor == 1) {
     if (o.kind != SPARSE_SPMM) {
@@ -671,6 +747,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);
   h = fnv1a(h, p.blob.data(), p.blob.size());
+  h = fnv1a(h, p.tc_cb.data(), p.tc_cb.size() * 4);
+  h = fnv1a(h, p.tc_a.data(), p.tc_a.size() * 2);
   p.digest = h;
   p.build_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -397,6 +397,9 @@ struct SpmmArgs {
   const uint8_t* bias;  // fused epilogue (plan.h Epilogue)
   float beta;
   int32_t relu;
+  const float* tcws;    // tensor-core sub-block partial sums (fp32, ldws), or null
+  const int32_t* ws_row;
+  int64_t ldws;
 };
 
 template <int R, int GK, bool F16, bool TM>
@@ -586,6 +589,15 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
       const int row = rows[r];
       if (row < 0) continue;
       uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + col) * S;
+      if (a.tcws) {  // + the row's dense-tile contribution (tensor cores), before rounding
+        const int wr = a.ws_row[row];
+        if (wr >= 0) {
+          const float* wp = a.tcws + (int64_t)wr * a.ldws + n0 + col;
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (col + c < ncol) acc[r][c] += wp[c];
+        }
+      }
       if (epi) {
 #pragma unroll
         for (int c = 0; c < C; ++c)
@@ -728,6 +740,13 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
       v.w += u.w;
     }
     uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + c4) * S;
+    if (a.tcws && a.ws_row[row] >= 0) {
+      const float* wp = a.tcws + (int64_t)a.ws_row[row] * a.ldws + n0 + c4;
+      if (c4 + 0 < ncol) v.x += wp[0];
+      if (c4 + 1 < ncol) v.y += wp[1];
+      if (c4 + 2 < ncol) v.z += wp[2];
+      if (c4 + 3 < ncol) v.w += wp[3];
+    }
     if (a.bias != nullptr || a.beta != 0.0f || a.relu) {
       if (c4 + 0 < ncol) v.x = epilogue_one<F16>(v.x, a.bias, row, a.beta, yp + 0 * S, a.relu);
       if (c4 + 1 < ncol) v.y = epilogue_one<F16>(v.y, a.bias, row, a.beta, yp + 1 * S, a.relu);
@@ -1054,6 +1073,104 @@ __global__ void __launch_bounds__(512) conv3x3_vec_kernel(const ConvArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ tensor-core sub-blocks
+// the dense-enough 16 x 16 tiles of W (plan.h tc_*) as a dense contraction on
+// the tensor cores.  CTA = (row block, 128 columns of N), 4 warps x 32 columns; per tile of
+// the row block (k-block ascending): X rows 16 cb .. 16 cb + 15 of the CTA's columns are
+// staged in shared memory (272-byte row pitch: conflict-free ldmatrix), each warp loads its
+// A fragment (16 bytes per lane, pre-packed by the inspector) and issues 4 mma.m16n8k16
+// (fp16 x fp16, fp32 accumulate) with B fragments from ldmatrix.x2.trans.  The fp32 result
+// overwrites the workspace rows of the row block; the CUDA-core kernel adds them to its
+// accumulators before the single rounding (sparse part + dense part, then epilogue).
+struct TcArgs {
+  const uint16_t* A;
+  const int32_t *rb, *tile_begin, *cb;
+  const uint8_t* X;
+  float* ws;
+  int64_t ldx, ldws, N;
+  int32_t K, vec_x;
+};
+
+// COLS = columns of N per CTA (4 warps x COLS / 4): 512 for large N, 128 for small N
+template <int COLS>
+__global__ void __launch_bounds__(128) spmm_tc_kernel(const TcArgs a) {
+  constexpr int kTcCols = COLS, JW = COLS / 32;  // n8 tiles per warp
+  constexpr int kTcPitch = kTcCols + 8;  // smem row pitch in halves (conflict-free ldmatrix)
+  extern __shared__ __align__(128) uint16_t xs[];  // [2][16][kTcPitch]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i = blockIdx.x;
+  const int64_t n0 = (int64_t)blockIdx.y * kTcCols;
+  float acc[JW][4];
+#pragma unroll
+  for (int j = 0; j < JW; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[j][c] = 0.0f;
+  const int t0 = a.tile_begin[i], t1 = a.tile_begin[i + 1];
+  // stage X[k0 .. k0 + 16][n0 .. n0 + COLS) into buffer `buf`: 16 rows x COLS / 8 chunks
+  auto stage = [&](int t, int buf) {
+    const int k0 = a.cb[t] * 16;
+    uint16_t* dst = xs + buf * 16 * kTcPitch;
+    for (int q = tid; q < 16 * (kTcCols / 8); q += 128) {
+      const int r = q / (kTcCols / 8), ch = q % (kTcCols / 8);
+      const int64_t k = k0 + r, n = n0 + ch * 8;
+      uint16_t* d = dst + r * kTcPitch + ch * 8;
+      const uint16_t* src = (const uint16_t*)a.X + k * a.ldx + n;
+      if (k < a.K && a.vec_x && n + 8 <= a.N) {
+        cp_async16(smem_u32(d), src, 16);
+      } else {
+        uint16_t h[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) h[e] = (k < a.K && n + e < a.N) ? src[e] : (uint16_t)0;
+        *(uint4*)d = *(const uint4*)h;
+      }
+    }
+    cp_async_commit();
+  };
+  if (t0 < t1) stage(t0, 0);
+  for (int t = t0; t < t1; ++t) {
+    const int buf = (t - t0) & 1;
+    if (t + 1 < t1) {
+      stage(t + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const uint4 af = *((const uint4*)a.A + (int64_t)t * 32 + lane);
+    const uint16_t* xb = xs + buf * 16 * kTcPitch;
+#pragma unroll
+    for (int j = 0; j < JW; ++j) {
+      // lanes 0-7: K rows 0-7, lanes 8-15: rows 8-15, at column (COLS / 4) warp + 8 j
+      const uint32_t addr = smem_u32(xb + (lane & 15) * kTcPitch + warp * (COLS / 4) + j * 8);
+      uint32_t b0, b1;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                   : "=r"(b0), "=r"(b1)
+                   : "r"(addr));
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+          "{%8, %9}, {%0, %1, %2, %3};"
+          : "+f"(acc[j][0]), "+f"(acc[j][1]), "+f"(acc[j][2]), "+f"(acc[j][3])
+          : "r"(af.x), "r"(af.y), "r"(af.z), "r"(af.w), "r"(b0), "r"(b1));
+    }
+    __syncthreads();
+  }
+  // D fragment: lane (g, t): rows g and g + 8, columns 2 t, 2 t + 1 of each 16 x 8 tile
+  const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int j = 0; j < JW; ++j) {
+    const int64_t n = n0 + warp * (COLS / 4) + j * 8 + 2 * tq;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float* wp = a.ws + (int64_t)(i * 16 + g + 8 * h) * a.ldws + n;
+      if (n + 1 < a.N) {
+        *(float2*)wp = make_float2(acc[j][2 * h], acc[j][2 * h + 1]);
+      } else if (n < a.N) {
+        wp[0] = acc[j][2 * h];
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ dispatch
 using SpmmFn = void (*)(const __grid_constant__ CUtensorMap, const SpmmArgs);
 using ConvFn = void (*)(const ConvArgs);
@@ -1216,7 +1333,11 @@ int upload_plan(Plan& p, std::string& err) {
   const size_t nrow = p.row_id.size() * 4, noff = p.blk_off.size() * 8, nblob = p.blob.size();
   const size_t o_off = 0, o_row = (noff + 255) & ~size_t(255),
                o_blob = (o_row + nrow + 255) & ~size_t(255);
-  const size_t total = o_blob + nblob;
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  const size_t o_tca = al(o_blob + nblob), o_tcrb = al(o_tca + p.tc_a.size() * 2),
+               o_tctb = al(o_tcrb + p.tc_rb.size() * 4), o_tccb = al(o_tctb + p.tc_tile_begin.size() * 4),
+               o_wsr = al(o_tccb + p.tc_cb.size() * 4);
+  const size_t total = o_wsr + p.ws_row.size() * 4;
   void* mem = nullptr;
   e = cudaMalloc(&mem, total);
   if (e != cudaSuccess) {
@@ -1227,7 +1348,14 @@ int upload_plan(Plan& p, std::string& err) {
   uint8_t* b = (uint8_t*)mem;
   if ((e = cudaMemcpy(b + o_off, p.blk_off.data(), noff, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(b + o_row, p.row_id.data(), nrow, cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemcpy(b + o_blob, p.blob.data(), nblob, cudaMemcpyHostToDevice)) != cudaSuccess) {
+      (e = cudaMemcpy(b + o_blob, p.blob.data(), nblob, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (p.tc_ntiles > 0 &&
+       ((e = cudaMemcpy(b + o_tca, p.tc_a.data(), p.tc_a.size() * 2, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(b + o_tcrb, p.tc_rb.data(), p.tc_rb.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(b + o_tctb, p.tc_tile_begin.data(), p.tc_tile_begin.size() * 4,
+                        cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(b + o_tccb, p.tc_cb.data(), p.tc_cb.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(b + o_wsr, p.ws_row.data(), p.ws_row.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess))) {
     cudaFree(mem);
     return cuda_fail(e, "cudaMemcpy(plan)", err);
   }
@@ -1242,6 +1370,13 @@ int upload_plan(Plan& p, std::string& err) {
   p.d_blk_off = (const int64_t*)(b + o_off);
   p.d_row_id = (const int32_t*)(b + o_row);
   p.d_blob = b + o_blob;
+  if (p.tc_ntiles > 0) {
+    p.d_tc_a = (const uint16_t*)(b + o_tca);
+    p.d_tc_rb = (const int32_t*)(b + o_tcrb);
+    p.d_tc_tile_begin = (const int32_t*)(b + o_tctb);
+    p.d_tc_cb = (const int32_t*)(b + o_tccb);
+    p.d_ws_row = (const int32_t*)(b + o_wsr);
+  }
   return SPARSE_OK;
 }
 
@@ -1308,6 +1443,62 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
     }
   };
   const int64_t ntn = (N + p.n_tile - 1) / p.n_tile;
+  a.tcws = nullptr;
+  a.ws_row = nullptr;
+  a.ldws = 0;
+  float* tcws = nullptr;
+  if (p.tc_ntiles > 0) {
+    // dense 16 x 16 tiles on the tensor cores -> fp32 workspace (stream ordered)
+    const int64_t ldws = (N + 3) / 4 * 4;  // float2 stores stay 8-byte aligned
+    e = cudaMallocAsync((void**)&tcws, (size_t)p.tc_nrb * 16 * ldws * 4, (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cuda_fail(e, "cudaMallocAsync(tensor-core workspace)", err);
+    }
+    TcArgs t;
+    t.A = p.d_tc_a;
+    t.rb = p.d_tc_rb;
+    t.tile_begin = p.d_tc_tile_begin;
+    t.cb = p.d_tc_cb;
+    t.X = (const uint8_t*)X;
+    t.ws = tcws;
+    t.ldx = ldx;
+    t.ldws = ldws;
+    t.N = N;
+    t.K = p.K;
+    t.vec_x = vec_x ? 1 : 0;
+    const int cols = N >= 2048 ? 512 : 128;
+    auto tc_fn = cols == 512 ? spmm_tc_kernel<512> : spmm_tc_kernel<128>;
+    const int64_t nblk = (N + cols - 1) / cols;
+    const size_t tc_smem = 2 * 16 * (cols + 8) * 2;
+    e = ensure_smem_attr(tc_fn, (int)tc_smem);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(tcws, (cudaStream_t)stream);
+      return cuda_fail(e, "cudaFuncSetAttribute(tensor-core kernel)", err);
+    }
+    for (int64_t b0 = 0; b0 < nblk; b0 += 65535) {
+      const int64_t nb = std::min<int64_t>(65535, nblk - b0);
+      t.X = (const uint8_t*)X + b0 * cols * S;
+      t.ws = tcws + b0 * cols;
+      t.N = N - b0 * cols;
+      tc_fn<<<dim3((unsigned)p.tc_nrb, (unsigned)nb), 128, tc_smem, (cudaStream_t)stream>>>(t);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cudaFreeAsync(tcws, (cudaStream_t)stream);
+      return cuda_fail(e, "tensor-core sub-block launch", err);
+    }
+    a.tcws = tcws;
+    a.ws_row = p.d_ws_row;
+    a.ldws = ldws;
+  }
+  struct WsFree {
+    float* w;
+    void* st;
+    ~WsFree() {
+      if (w) cudaFreeAsync(w, (cudaStream_t)st);
+    }
+  } ws_free{tcws, stream};
   if (p.ks == 1) {
     // persistent: one wave of CTAs (clusters of cm CTAs when X is multicast), each walking
     // tiles (panel group, N tile) cluster_id + j * clusters
@@ -1365,6 +1556,7 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
     a.X = (const uint8_t*)X + c0 * S;
     a.Y = (uint8_t*)Y + c0 * S;
     a.N = N - c0;
+    a.tcws = tcws ? tcws + c0 : nullptr;
     CUtensorMap tmap;
     make_map(tmap);
     cudaLaunchConfig_t cfg;

@@ -129,6 +129,25 @@ struct Plan {
   const uint8_t* d_blob = nullptr;
   int64_t plan_bytes = 0;
   mutable int32_t grid_cache = 0;  // resident CTAs (clusters) of the persistent launch
+
+  // Tensor-core sub-block path (fp16 SpMM plans): aligned 16 x 16 tiles of W
+  // with at least tc_min_pct % nonzeros are taken out of the CUDA-core plan and multiplied
+  // as dense blocks with mma.sync m16n8k16 (fp16 x fp16 -> fp32) into an fp32 workspace that
+  // the CUDA-core kernel adds before its single rounding.
+  int32_t tc_min_pct = 0;
+  int32_t tc_nrb = 0;                // row blocks (16 rows) holding >= 1 dense tile
+  int64_t tc_ntiles = 0;
+  int64_t tc_nnz = 0;                // nonzeros carried by the dense tiles
+  std::vector<int32_t> tc_rb;        // [tc_nrb] row-block index (rows 16 rb .. 16 rb + 15)
+  std::vector<int32_t> tc_tile_begin;  // [tc_nrb + 1] tile ranges, k-block ascending
+  std::vector<int32_t> tc_cb;        // [tc_ntiles] k-block index (K columns 16 cb ..)
+  std::vector<uint16_t> tc_a;        // [tc_ntiles][32 lanes][8] fp16, mma A-fragment order
+  std::vector<int32_t> ws_row;       // [M] workspace row of W row m, or -1
+  const int32_t* d_tc_rb = nullptr;
+  const int32_t* d_tc_tile_begin = nullptr;
+  const int32_t* d_tc_cb = nullptr;
+  const uint16_t* d_tc_a = nullptr;
+  const int32_t* d_ws_row = nullptr;
 };
 
 struct BuildOpts {
@@ -142,6 +161,7 @@ struct BuildOpts {
   int32_t tm = 0;
   int32_t conv_vec = 1;   // allow the vectorised conv kernel
   int32_t row_order = 0;  // 0 = LPT panels (load balancing), 1 = natural contiguous rows
+  int32_t tc_min_pct = 50;  // tensor-core sub-blocks: min % of nonzeros in a 16x16 tile (0 = off)
 };
 
 // JIT executor (jit.cpp).  Row entries per row (k ascending) as validated by the

@@ -108,6 +108,17 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
                 o.executor = 0;
                 cands.push_back(o);
               }
+    if (f16) {  // tensor-core sub-blocks on / off (when the matrix has dense 16x16 tiles)
+      for (int tc : {50, 0}) {
+        BuildOpts o = base;
+        o.warps = 16;
+        o.rows_per_warp = 4;
+        o.k_chunk = 128;
+        o.tc_min_pct = tc;
+        o.executor = 0;
+        cands.push_back(o);
+      }
+    }
     BuildOpts j = base;
     j.executor = 1;
     cands.push_back(j);

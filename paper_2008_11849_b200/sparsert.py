@@ -50,7 +50,7 @@ class sparse_plan_opts(ctypes.Structure):
                 ("executor", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
                 ("jit_warps", ctypes.c_int32), ("x_multicast", ctypes.c_int32),
                 ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
-                ("row_order", ctypes.c_int32)]
+                ("row_order", ctypes.c_int32), ("tc_min_density", ctypes.c_int32)]
 
 
 class sparse_epilogue(ctypes.Structure):
@@ -74,7 +74,9 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("jit_compile_ms", ctypes.c_double), ("tuned_us", ctypes.c_double),
                 ("digest", ctypes.c_uint64), ("x_multicast", ctypes.c_int32),
                 ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
-                ("row_order", ctypes.c_int32)]
+                ("row_order", ctypes.c_int32), ("tc_min_density", ctypes.c_int32),
+                ("tc_row_blocks", ctypes.c_int32), ("tc_tiles", ctypes.c_int64),
+                ("tc_nnz", ctypes.c_int64)]
 
 
 def _load() -> ctypes.CDLL:
@@ -259,7 +261,7 @@ class Plan:
                  stages=i["stages"], executor=i["executor"], row_order=i["row_order"])
         if self.kind == SPARSE_SPMM:
             o.update(k_chunk=i["k_chunk"], k_split=i["k_split"], x_multicast=i["x_multicast"],
-                     x_source=i["x_source"])
+                     x_source=i["x_source"], tc_min_density=i["tc_min_density"] or -1)
             if i["executor"] == 1:
                 o.update(jit_rows=i["jit_rows"], jit_warps=i["jit_warps"])
         else:

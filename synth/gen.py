@@ -120,7 +120,9 @@ def random_pattern(M: int, K: int, nnz: int, seed: int, values: str = "normal") 
 
 def stress_pattern(kind: str, M: int, K: int, seed: int, density: float = 0.1) -> Csr:
     """Stress patterns for parity (SURVEY 8(d)): 'zipf', 'empty_rows', 'dense_row',
-    'block_dense', 'one_column', 'empty'."""
+    'block_dense', 'block16', 'one_column', 'empty'.  'block16': a fraction `density` of the
+    aligned 16x16 tiles fully dense plus uniform 5% background nonzeros (the structured case
+    of the tensor-core sub-block path, SURVEY NEXT #1)."""
     rng = np.random.default_rng(seed)
     v = rng.standard_normal((M, K)).astype(np.float32)
     v[v == 0] = 1.0
@@ -152,6 +154,14 @@ def stress_pattern(kind: str, M: int, K: int, seed: int, density: float = 0.1) -
         for b in bi:
             r, c = divmod(int(b), K // 8)
             mask[r * 8:(r + 1) * 8, c * 8:(c + 1) * 8] = True
+        return csr_from_mask(M, K, np.flatnonzero(mask), v)
+    if kind == "block16":
+        mask = rng.random((M, K)) < 0.05
+        nrb, ncb = M // 16, K // 16
+        nb = max(1, int(density * nrb * ncb))
+        for b in rng.choice(nrb * ncb, size=nb, replace=False):
+            r, c = divmod(int(b), ncb)
+            mask[r * 16:(r + 1) * 16, c * 16:(c + 1) * 16] = True
         return csr_from_mask(M, K, np.flatnonzero(mask), v)
     if kind == "one_column":
         mask = np.zeros((M, K), bool)

@@ -115,6 +115,31 @@ def test_row_order_natural_panels():
     assert spread(nat) > spread(lpt)
 
 
+def test_tensor_core_subblock_extraction():
+    # NEXT #1: aligned 16x16 tiles with >= 50% nonzeros leave the CUDA-core plan (fp16 only);
+    # the dump still carries every nonzero exactly once with its fp16 value
+    import torch
+    w = gen.stress_pattern("block16", 200, 300, seed=3, density=0.1)
+    pl = _plan(w, torch.float16, n_hint=512)
+    info = pl.info
+    assert info["tc_tiles"] > 0 and info["tc_min_density"] == 50
+    d = pl.dump()
+    key = np.sort(d.row.astype(np.int64) * 300 + d.col)
+    ref_rows = np.repeat(np.arange(200), np.diff(w.row_ptr)).astype(np.int64)
+    assert np.array_equal(key, np.sort(ref_rows * 300 + w.col_idx))
+    tc = d.panel == -1
+    assert tc.sum() == info["tc_nnz"] > 0
+    # every tensor-core nonzero lies in a 16x16 tile with >= 128 nonzeros of W
+    dense = np.zeros((13, 19), np.int64)
+    np.add.at(dense, (ref_rows // 16, w.col_idx // 16), 1)
+    assert np.all(dense[d.row[tc] // 16, d.col[tc] // 16] >= 128)
+    assert np.all(dense[d.row[~tc] // 16, d.col[~tc] // 16] < 128)
+    # off switches, fp32 and uniform 90% sparsity never take the path
+    assert _plan(w, torch.float16, n_hint=512, tc_min_density=-1).info["tc_tiles"] == 0
+    assert _plan(w, torch.float32, n_hint=512).info["tc_tiles"] == 0
+    assert _plan(gen.pruned_weights(512, 512, 90, seed=1), torch.float16, n_hint=512).info["tc_tiles"] == 0
+
+
 def test_spec_partition_examples():
     g = golden("spec_partition.json")
     # 4x4 example, 2 blocks -> balanced 2 / 2 (membership may differ: LPT)

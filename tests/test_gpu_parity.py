@@ -553,3 +553,38 @@ def test_conv_epilogue_exact(ck, f16):
     if f16:
         ref = _f16_round(ref)
     assert np.array_equal(y.double().cpu().numpy(), ref)
+
+
+# --------------------------------------------------------------------------- tensor-core sub-blocks
+
+@pytest.mark.parametrize("opts", [dict(), dict(k_split=2, rows_per_warp=4), dict(split_k=2, warps=8),
+                                  dict(tc_min_density=25)])
+@pytest.mark.parametrize("M,K,N", [(256, 512, 392), (200, 300, 131), (1024, 256, 3136)])
+def test_tensor_core_subblocks_exact(M, K, N, opts):
+    # dense 16x16 tiles on mma.sync (fp16 x fp16 -> fp32) + the rest on CUDA cores, summed in
+    # fp32 before one rounding: exact on integer data, also with the fused epilogue
+    dev = _dev()
+    w = gen.stress_pattern("block16", M, K, seed=M + K, density=0.1)
+    w = w.with_values((np.sign(w.values) * np.random.default_rng(1).integers(1, 3, w.nnz)).astype(np.float32))
+    X = gen.int_x(K, N, seed=N, vmax=4)
+    y, plan = _run_spmm(w, X, True, **opts)
+    assert plan.info["tc_tiles"] > 0
+    ref = _f16_round(_ref(w, X, True))
+    assert np.array_equal(y, ref)
+    bias = torch.arange(M, device=dev, dtype=torch.float16) % 7 - 3
+    Xd = torch.from_numpy(X).to(dev).half()
+    Y = torch.zeros((M, N), device=dev, dtype=torch.float16)
+    plan.spmm(Xd, Y, bias=bias, relu=True)
+    torch.cuda.synchronize()
+    ref2 = _f16_round(np.maximum(_ref(w, X, True) + bias.double().cpu().numpy()[:, None], 0))
+    assert np.array_equal(Y.double().cpu().numpy(), ref2)
+
+
+def test_tensor_core_subblocks_rel_l2():
+    w = gen.stress_pattern("block16", 768, 1024, seed=9, density=0.2)
+    X = gen.uniform_x(1024, 2000, seed=10)
+    y_tc, p_tc = _run_spmm(w, X, True)
+    y_cc, p_cc = _run_spmm(w, X, True, tc_min_density=-1)
+    assert p_tc.info["tc_tiles"] > 0 and p_cc.info["tc_tiles"] == 0
+    ref = _ref(w, X, True)
+    assert oracle.rel_l2(y_tc, ref) <= F16_TOL and oracle.rel_l2(y_cc, ref) <= F16_TOL
