@@ -481,6 +481,30 @@ def main():
     roof["alg_bytes_per_launch"] = d["alg_bytes"]
     roof["flops_per_launch"] = 2 * d["nnz"] * d["N"]
 
+    # ---------------- optional gather of Y over ranks: off the data path, NCCL
+    # all-gather (NVLink / NVSwitch) of every layer's output slab, timed separately
+    gather = None
+    if world > 1 and not args.quick:
+        outs = [torch.empty((world,) + tuple(y.shape), dtype=y.dtype, device=dev) for y in ys]
+        for _ in range(2):
+            for y, o in zip(ys, outs):
+                dist.all_gather_into_tensor(o, y.contiguous())
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        g0.record(stream)
+        for _ in range(reps):
+            for y, o in zip(ys, outs):
+                dist.all_gather_into_tensor(o, y.contiguous())
+        g1.record(stream)
+        torch.cuda.synchronize()
+        tg = torch.tensor([g0.elapsed_time(g1) / reps], dtype=torch.float64, device=dev)
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        gather = {"ms_per_step": float(tg.item()), "bytes_per_rank": sum(y.numel() * S for y in ys),
+                  "collective": "all_gather_into_tensor (NCCL), not part of the timed step"}
+        del outs
+
     # ---------------- e2e through the public API with host buffers
     e2e = None
     if not (args.no_e2e or args.quick):
@@ -615,7 +639,7 @@ def main():
                        "parallelism": f"N-sharded x{world}, replicated plan, no collective",
                        "replica_digests_equal": replicas_equal},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks, "layers": per_layer, "dense_baseline": dense,
+            "clocks": clocks, "layers": per_layer, "dense_baseline": dense, "gather": gather,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

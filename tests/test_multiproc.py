@@ -41,7 +41,7 @@ def _worker(rank, world, port, out):
         import oracle
         import paper_2008_11849_b200 as srt
         from synth import gen
-        M, K, N, unit = 96, 200, 6 * 49, 49
+        M, K, N, unit = 96, 200, 7 * 49, 49  # 7 samples over 2 ranks: uneven slabs
         w = gen.pruned_weights(M, K, 90, seed=5)
         X = gen.uniform_x(K, N, seed=6).astype(np.float64)
         # replicated plan: identical digests on every rank
@@ -54,12 +54,14 @@ def _worker(rank, world, port, out):
                         np.ascontiguousarray(X[:, n0:n1]))
         parts = [None] * world
         dist.all_gather_object(parts, y)
+        from paper_2008_11849_b200.shard import gather_columns
+        gathered = gather_columns(torch.from_numpy(y), N, world, unit).numpy()
         t = torch.tensor([float(rank + 1)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if rank == 0:
             full = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), X)
-            out.put((len(set(digs)) == 1, bool(np.array_equal(np.concatenate(parts, axis=1), full)),
-                     float(t.item())))
+            out.put((len(set(digs)) == 1, bool(np.array_equal(np.concatenate(parts, axis=1), full))
+                     and bool(np.array_equal(gathered, full)), float(t.item())))
     finally:
         dist.destroy_process_group()
 
