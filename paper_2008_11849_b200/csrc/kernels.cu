@@ -1025,6 +1025,7 @@ __global__ void __launch_bounds__(512) conv3x3_vec_kernel(const ConvArgs a) {
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+  const bool junk = (lane * C) / a.wp >= min(a.rb, a.H - y0);
 
   load(0);
   store(0, 0);
@@ -1045,7 +1046,9 @@ __global__ void __launch_bounds__(512) conv3x3_vec_kernel(const ConvArgs a) {
     uint32_t h[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) h[r] = shdr[warp * R + r];
-    run_rows<F16, R>(acc, h, ents, st + (a.guard + lane * C) * S);
+    // lanes whose C positions all lie below the band's last image row read lane 0's address:
+    // their loads merge into lane 0's wavefront (no shared-memory bandwidth for junk rows)
+    run_rows<F16, R>(acc, h, ents, st + (a.guard + (junk ? 0 : lane * C)) * S);
     if (c + 1 < a.nchunks) {
       store(buf ^ 1, c + 1);
       cp_async_wait<0>();
