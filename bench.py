@@ -480,6 +480,18 @@ def main():
         "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"
     roof["alg_bytes_per_launch"] = d["alg_bytes"]
     roof["flops_per_launch"] = 2 * d["nnz"] * d["N"]
+    # Design ceilings of the CUDA-core executor, context for `frac`: one shared-
+    # memory X load per lane-FMA caps it at 25% (fp32) / 50% (fp16) of the FMA peak, and every
+    # row panel re-reads its X tiles from L2 (measured L2 -> SM streaming: 4.7 TB/s).
+    pi = plans[dom][0].info
+    Ld = layers[dom]
+    xb = S * (Ld["K"] if Ld["kind"] == "spmm" else Ld["c_in"]) * d["N"]
+    t_smem = 2 * d["nnz"] * d["N"] / (alu * 1e9 * (0.5 if args.dtype == "f16" else 0.25))
+    t_l2 = pi["panels"] * xb / 4.7e12
+    t_ceil = max(t_smem, t_l2, max(d["alg_bytes"] / (peaks["hbm_gbs"] * 1e9), 0.0))
+    roof["design_ceiling"] = {"smem_fma_frac_max": 0.5 if args.dtype == "f16" else 0.25,
+                              "t_smem_us": t_smem * 1e6, "t_l2_reread_us": t_l2 * 1e6,
+                              "frac_of_design_ceiling": t_ceil / (d["ms"] * 1e-3)}
 
     # ---------------- optional gather of Y over ranks: off the data path, NCCL
     # all-gather (NVLink / NVSwitch) of every layer's output slab, timed separately

@@ -703,7 +703,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     p.stages = stages;
     p.red_bytes = p.ks > 1 ? p.Mp * p.n_tile * 4 : 0;
     if (p.tm) p.stages = std::max(p.stages, std::min(3, 227 * 1024 / stage_bytes));
-    p.smem_bytes = std::max(p.stages * stage_bytes, p.red_bytes) + 128;  // + mbarriers
+    p.smem_bytes = std::max(p.stages * stage_bytes, p.red_bytes) + 256;  // + mbarriers etc.
     // tensor memory plans allocate all 512 TMEM columns: one CTA per SM (> half the smem)
     if (p.tm) p.smem_bytes = std::max(p.smem_bytes, 116 * 1024);
   } else {

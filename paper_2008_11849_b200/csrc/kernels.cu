@@ -448,7 +448,10 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
     }
   };
   const uint32_t full0 = smem_u32(smem + a.bar_off);
-  uint32_t* ctr = (uint32_t*)(smem + a.bar_off + 8 * kMaxStages);  // releases per ring slot
+  // smem tail (256 B): full[8] mbarriers | cluster-empty[8] mbarriers (multicast leader) |
+  // release counters[8] | TMEM base
+  const uint32_t cempty0 = full0 + 8 * kMaxStages;
+  uint32_t* ctr = (uint32_t*)(smem + a.bar_off + 16 * kMaxStages);  // releases per ring slot
 
   // the zero row after the kc X rows of every stage (target of neutral padding entries)
   for (int s = 0; s < a.stages; ++s)
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
   if (tid < kMaxStages) ctr[tid] = 0u;
   // TMEM X source: chunk q lives in TMEM buffer q & 1 (columns 256 b .. 256 b + 4 kc, zero
   // row at column 256 b + 4 kc), replicated in the four 32-lane quarters
-  uint32_t* tslot = (uint32_t*)(smem + a.bar_off + 8 * kMaxStages + 4 * kMaxStages + 16);
+  uint32_t* tslot = (uint32_t*)(smem + a.bar_off + 16 * kMaxStages + 4 * kMaxStages);
   if (TM && warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(tslot)));
@@ -465,6 +468,7 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
   }
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) mbar_init(full0 + 8 * s, a.use_tma ? 1 : 33);
+    for (int s = 0; cm > 1 && s < a.stages; ++s) mbar_init(cempty0 + 8 * s, (uint32_t)cm);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -633,7 +637,6 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
   uint32_t ph = 0;
   int panel = 0;
   int64_t n0 = 0;
-  const uint32_t releases = (uint32_t)(cm * nwarps);  // per slot and round, cluster-wide
   for (int ti = 0; ti < my_tiles; ++ti) {
     tile_of(ti, panel, n0);
     if (persistent) panel = panel * cm + (int)crank;
@@ -662,19 +665,27 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
       }
       __syncwarp();
       uint32_t old = 0;
-      if (lane == 0) {  // release the slot; the last of the cluster's warps refills it
-        if (cm > 1) {
-          asm volatile("fence.acq_rel.cluster;" ::: "memory");
-          old = atom_add_cluster(map_rank(smem_u32(ctr + slot), 0u), 1u);
-        } else {  // release: this warp's reads of the slot precede the count
-          asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                       : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
-        }
-      }
+      if (lane == 0)  // release: this warp's reads of the slot precede the count
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
       old = __shfl_sync(0xffffffffu, old, 0);
-      if ((old + 1u) % releases == 0u && q + a.stages < total) {
-        if (cm > 1) asm volatile("fence.acq_rel.cluster;" ::: "memory");
-        refill(q + a.stages);
+      const bool last_local = (old + 1u) % (uint32_t)nwarps == 0u;
+      if (cm == 1) {  // the CTA's last releasing warp refills the slot
+        if (last_local && q + a.stages < total) refill(q + a.stages);
+      } else if (last_local) {
+        // multicast cluster: one remote arrive per CTA on the leader's cluster-empty barrier;
+        // the leader's last warp waits for all cm CTAs, then refills the slot cluster-wide
+        if (lane == 0) {
+          asm volatile("fence.acq_rel.cluster;" ::: "memory");
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           map_rank(cempty0 + 8 * slot, 0u))
+                       : "memory");
+        }
+        if (crank == 0 && q + a.stages < total) {
+          mbar_wait(cempty0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
+          asm volatile("fence.acq_rel.cluster;" ::: "memory");
+          refill(q + a.stages);
+        }
       }
 
       ++q;
@@ -1420,7 +1431,7 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
   a.stage_bytes = (p.x_stage_bytes + p.max_blk_bytes + 127) & ~127;
   a.hdr_bytes = p.hdr_bytes;
   a.blk_bytes = p.max_blk_bytes;
-  a.bar_off = p.smem_bytes - 128;
+  a.bar_off = p.smem_bytes - 256;
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
