@@ -218,6 +218,12 @@ struct EntryOps<true> {  // unit = 4 x {uint16 xoff (16-byte units), half w}
 #ifndef SRT_JOINT
 #define SRT_JOINT 1
 #endif
+#ifndef SRT_MINB
+#define SRT_MINB 1
+#endif
+#ifndef SRT_TAILMERGE
+#define SRT_TAILMERGE 1
+#endif
 template <bool F16>
 __device__ __forceinline__ void run_one_row(float (&acc)[F16 ? 8 : 4], const uint4* up, int u, int cnt,
                                             const uint8_t* xs) {
@@ -403,7 +409,7 @@ struct SpmmArgs {
 };
 
 template <int R, int GK, bool F16, bool TM>
-__global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(512, SRT_MINB) spmm_kernel(const __grid_constant__ CUtensorMap tmap,
                                                    const SpmmArgs a) {
   constexpr int C = F16 ? 8 : 4;  // columns per lane (16 bytes of X)
   constexpr int S = F16 ? 2 : 4;  // element bytes
@@ -647,11 +653,19 @@ __global__ void __launch_bounds__(512) spmm_kernel(const __grid_constant__ CUten
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+    // lanes past the ragged end of N read lane 0's columns (never stored): their loads
+    // merge into lane 0's wavefront, so a tile with n valid lanes costs ceil(n / 8)
+    // shared-memory wavefronts per X load instead of 4 (N = 49: 2, N tail of 8: 1)
+#if SRT_TAILMERGE
+    const int xoff = col < (int)min((int64_t)NT, a.N - n0) ? li * (C * S) : 0;
+#else
+    const int xoff = li * (C * S);
+#endif
     for (int j = 0; j < nloc; ++j) {
       mbar_wait(full0 + 8 * slot, ph);
       const uint8_t* st = smem + slot * a.stage_bytes;
       if (TM) tm_fill(st, q);
-      const uint8_t* xs = st + li * (C * S);
+      const uint8_t* xs = st + xoff;
       const uint32_t* shdr = (const uint32_t*)(st + a.x_stage_bytes);
       const uint4* ents = (const uint4*)(st + a.x_stage_bytes + a.hdr_bytes);
       uint32_t h[R];

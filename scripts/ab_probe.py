@@ -27,7 +27,10 @@ out = []
 for (M, K, N), dt, kw in cases:
     tdt = torch.float16 if dt == "f16" else torch.float32
     w = gen.pruned_weights(M, K, 90, seed=1)
-    p = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, **kw)
+    try:
+        p = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, **kw)
+    except Exception as e:
+        out.append(dict(us=float("nan"), tflops=str(e)[:40])); continue
     X = torch.rand(K, N, device="cuda", dtype=tdt); Y = torch.empty(M, N, device="cuda", dtype=tdt)
     g = torch.cuda.CUDAGraph(); s = torch.cuda.Stream(); reps = 20
     with torch.cuda.stream(s):
@@ -44,6 +47,9 @@ for (M, K, N), dt, kw in cases:
     out.append(dict(shape=[M, K, N], dt=dt, cfg=kw, us=round(us, 2), tflops=round(2 * w.nnz * N / us / 1e6, 2)))
 print(json.dumps(out))
 '''
+# optional first argument: a JSON file of cases [[[M, K, N], "f32", {opts}], ...]
+if sys.argv[1].endswith(".json"):
+    CASES = [(tuple(c[0]), c[1], c[2]) for c in json.load(open(sys.argv.pop(1)))]
 res = {}
 for lib in sys.argv[1:]:
     env = dict(os.environ, SPARSERT_LIB=os.path.abspath(lib))
