@@ -102,10 +102,13 @@ typedef struct {
                             with warp-uniform tcgen05.ld, which has ~2x the shared-memory
                             bandwidth.  Needs split_k = 1, k_split = 1,
                             x_multicast = 1, k_chunk <= 56 (default 56).  Result-neutral. */
-  int32_t conv_kernel;   /* conv: 0 = auto (the vectorised kernel - three dx-shifted copies of the
-                            staged input, 128-bit loads of C consecutive positions - when a padded
-                            row of W + 2 positions fits twice in 32 * C positions, else the
-                            position-strided kernel); 1 = position-strided kernel */
+  int32_t conv_kernel;   /* conv: 0 = auto (the TMA-fed vectorised kernel - three dx-shifted copies
+                            of the staged input, 128-bit loads of C consecutive positions - when a
+                            padded row of W + 2 positions fits twice in 32 * C positions, else the
+                            position-strided kernel); 1 = position-strided kernel; 2 = TMA-fed
+                            vectorised kernel: the shifted copies are written once to a stream-
+                            ordered scratch by a pre-pass, then each is one 5-D TMA box per chunk;
+                            3 = register-staged vectorised kernel.  All result-identical. */
   int32_t row_order;     /* 0 = load-balanced panels (rows sorted by nnz, LPT-binned, P:163-165;
                             default); 1 = natural contiguous row ranges (the "no load balancing"
                             ablation of P:385).  Result-neutral for split_k = k_split = 1. */
@@ -201,7 +204,7 @@ typedef struct {
   uint64_t digest;      /* FNV-1a of the packed plan: equal digests <=> identical replicas */
   int32_t x_multicast;  /* CTAs per cluster sharing X tiles (TMA multicast) */
   int32_t x_source;     /* 0 shared memory, 1 tensor memory */
-  int32_t conv_kernel;  /* conv: 0 vectorised, 1 position-strided */
+  int32_t conv_kernel;  /* conv: 1 position-strided, 2 TMA-fed vectorised, 3 register-staged vectorised */
   int32_t row_order;    /* 0 LPT panels, 1 natural order */
   int32_t tc_min_density; /* effective threshold (%), 0 = no tensor-core sub-blocks */
   int32_t tc_row_blocks;  /* 16-row blocks with >= 1 dense tile */

@@ -420,6 +420,23 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
         p.conv_cs = ccv * p.conv_sci;  // elements per shifted copy
         p.conv_stage_elems = 3 * p.conv_cs + NTv + 16;  // + zero block
         p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
+        if (o.conv_vec == 2) {
+          // TMA-fed variant (conv3x3_tma_kernel): each shifted copy is one 4-D TMA box
+          // {wp, rb + 2, 1 image, cc channels} of the width-padded input (no guard), at a
+          // 128-byte aligned offset; no register staging, so up to 64 channels per chunk
+          p.conv_vec = 2;
+          p.conv_guard = 0;
+          p.conv_sci = (p.conv_rb + 2) * wpv;
+          const int per_ch3 = 3 * p.conv_sci * S;
+          int cct = o.k_chunk ? o.k_chunk : std::max(1, std::min(o.c_in, (64 * 1024) / per_ch3));
+          cct = std::min(cct, 64);
+          p.cc = cct;
+          p.kc = 9 * cct;
+          p.nchunks = (o.c_in + cct - 1) / cct;
+          p.conv_cs = (int)((int64_t)cct * p.conv_sci * S + 127) / 128 * 128 / S;
+          p.conv_stage_elems = 3 * p.conv_cs + NTv + 16;
+          p.x_stage_bytes = (int)(((int64_t)p.conv_stage_elems * S + 127) & ~int64_t(127));
+        }
       }
     }
   }
@@ -706,6 +723,12 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     p.smem_bytes = std::max(p.stages * stage_bytes, p.red_bytes) + 256;  // + mbarriers etc.
     // tensor memory plans allocate all 512 TMEM columns: one CTA per SM (> half the smem)
     if (p.tm) p.smem_bytes = std::max(p.smem_bytes, 116 * 1024);
+  } else if (p.conv_vec == 2) {
+    // TMA-fed conv: mbarrier ring as deep as ~200 KB allows (persistent CTAs)
+    stage_bytes = (stage_bytes + 127) & ~127;
+    p.stages = o.stages > 0 ? o.stages : std::max(2, std::min(kMaxStages, 200 * 1024 / stage_bytes));
+    p.red_bytes = 0;
+    p.smem_bytes = p.stages * stage_bytes + 256;
   } else {
     p.stages = 2;
     p.red_bytes = 0;

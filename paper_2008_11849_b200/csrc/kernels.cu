@@ -813,6 +813,7 @@ struct ConvArgs {
   int32_t B, H, W, c_in, cc, nchunks, Mp;
   int32_t x_stage_bytes, stage_bytes, hdr_bytes;
   int32_t rb, ipt, wp, simg, sci, guard, stage_elems, T, bands, cs;
+  int32_t npanels, stages;  // TMA-fed kernel
   const uint8_t* bias;  // fused epilogue (plan.h Epilogue)
   float beta;
   int32_t relu;
@@ -1101,6 +1102,151 @@ __global__ void __launch_bounds__(512) conv3x3_vec_kernel(const ConvArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ conv 3x3, TMA-fed
+// The vectorised implicit im2col above with the staging done by the TMA engine instead of
+// registers.  TMA rows must be 16-byte aligned (H8) and so must the innermost box coordinate
+// (a box starting 1 element off raises an illegal-instruction fault on B200:
+// scripts/micro/tma4d.cu), so the shift cannot be done by the TMA engine: a pre-pass
+// (pad_conv_input) writes the three shifted, zero-haloed copies to global memory,
+// xp3[dx][ci][b][r][c] = x[ci][b][r - 1][c + dx - 2] (zero outside), rows of wp elements.  Copy
+// dx of a chunk is then ONE 5-D TMA box {wp, rb + 2, 1, cc, 1} at {0, y0, b, ci0, dx}; rows and
+// channels past the end arrive as zeros, so the zero halo of P:215 costs nothing in the loop.  Persistent CTAs walk the tiles (panel fastest, then image band) through an
+// mbarrier ring refilled by the last releasing warp (as spmm_kernel); the FMA loop is
+// run_rows on the same plan format (offset dx * cs + ci * sci + dy * wp, guard 0).
+template <int R, bool F16>
+__global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                          const ConvArgs a) {
+  constexpr int C = F16 ? 8 : 4;
+  constexpr int S = F16 ? 2 : 4;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int np = a.npanels;
+  const int64_t ntiles = (int64_t)np * a.B * a.bands;
+  const int my_tiles = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+  const int total = my_tiles * a.nchunks;
+  const int64_t plane = (int64_t)a.H * a.W;
+  const uint32_t full0 = smem_u32(smem + (size_t)a.stages * a.stage_bytes);
+  uint32_t* ctr = (uint32_t*)(smem + (size_t)a.stages * a.stage_bytes + 8 * kMaxStages);
+  // zero block after the three copies of every stage (target of neutral padding entries)
+  for (int s = 0; s < a.stages; ++s)
+    for (int i = tid; i < (a.T + 16) * S / 16; i += blockDim.x)
+      *(uint4*)(smem + (size_t)s * a.stage_bytes + (size_t)3 * a.cs * S + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
+  if (tid < kMaxStages) ctr[tid] = 0u;
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) mbar_init(full0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  auto tile_of = [&](int ti, int& panel, int& b, int& band) {
+    const int64_t t = blockIdx.x + (int64_t)ti * gridDim.x;
+    panel = (int)(t % np);
+    const int64_t ib = t / np;
+    b = (int)(ib / a.bands);
+    band = (int)(ib % a.bands);
+  };
+  const uint32_t box_bytes = (uint32_t)(a.cc * a.sci * S);
+  auto refill = [&](int q) {  // lane 0 of one warp
+    const int slot = q % a.stages;
+    const int ti = q / a.nchunks, c = q - ti * a.nchunks;
+    int panel, b, band;
+    tile_of(ti, panel, b, band);
+    const int64_t bi = (int64_t)panel * a.nchunks + c;
+    const int64_t blk0 = a.blk_off[bi];
+    const uint32_t nb = (uint32_t)(a.blk_off[bi + 1] - blk0);
+    uint8_t* st = smem + (size_t)slot * a.stage_bytes;
+    const uint32_t fb = full0 + 8 * slot;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(fb, 3 * box_bytes + nb);
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(st + (size_t)dx * a.cs * S)),
+          "l"((uint64_t)&tmap), "r"(0), "r"(band * a.rb), "r"(b), "r"(c * a.cc), "r"(dx), "r"(fb)
+          : "memory");
+    }
+    if (nb) bulk_load(smem_u32(st + a.x_stage_bytes), a.blob + blk0, nb, fb);
+  };
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (warp == 0 && lane == 0)
+    for (int q = 0; q < min(a.stages, total); ++q) refill(q);
+
+  float acc[R][C];
+  int q = 0, slot = 0;
+  uint32_t ph = 0;
+  for (int ti = 0; ti < my_tiles; ++ti) {
+    int panel, b, band;
+    tile_of(ti, panel, b, band);
+    const int y0 = band * a.rb;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+    // lanes whose C positions all lie below the band's last image row read lane 0's address
+    const bool junk = (lane * C) / a.wp >= min(a.rb, a.H - y0);
+    const int xoff = junk ? 0 : lane * C * S;
+    for (int j = 0; j < a.nchunks; ++j) {
+      mbar_wait(full0 + 8 * slot, ph);
+      const uint8_t* st = smem + (size_t)slot * a.stage_bytes;
+      const uint32_t* shdr = (const uint32_t*)(st + a.x_stage_bytes);
+      const uint4* ents = (const uint4*)(st + a.x_stage_bytes + a.hdr_bytes);
+      uint32_t h[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) h[r] = shdr[warp * R + r];
+      run_rows<F16, R>(acc, h, ents, st + xoff);
+      __syncwarp();
+      uint32_t old = 0;
+      if (lane == 0)
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if ((old + 1u) % (uint32_t)nwarps == 0u && q + a.stages < total && lane == 0) refill(q + a.stages);
+      ++q;
+      if (++slot == a.stages) {
+        slot = 0;
+        ph ^= 1u;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = a.row_id[(int64_t)panel * a.Mp + warp * R + r];
+      if (row < 0) continue;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int p = lane * C + c;
+        const int rr = p / a.wp, x = p - rr * a.wp - 1;
+        const int y = y0 + rr;
+        if (rr >= a.rb || y >= a.H || x < 0 || x >= a.W) continue;
+        const int64_t o = ((int64_t)row * a.B + b) * plane + (int64_t)y * a.W + x;
+        const float v = epilogue_one<F16>(acc[r][c], a.bias, row, a.beta, a.y + o * S, a.relu);
+        if (F16)
+          ((__half*)a.y)[o] = __float2half_rn(v);
+        else
+          ((float*)a.y)[o] = v;
+      }
+    }
+  }
+}
+
+// x[C_in][B][H][W] -> xp3[3][C_in][B][H + 1][wp]: xp3[dx][..][r][c] = x[..][r - 1][c + dx - 2],
+// zero outside the image (the layout conv3x3_tma_kernel reads through TMA).  Pure data movement.
+template <typename T>
+__global__ void pad_conv_input(const T* __restrict__ x, T* __restrict__ xp, int64_t planes, int H, int W, int wp) {
+  const int64_t per = planes * (H + 1) * wp, n = 3 * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int dx = (int)(i / per);
+    const int64_t r = (i - dx * per) / wp;  // padded row over all planes
+    const int c = (int)(i - dx * per - r * wp);
+    const int64_t pl = r / (H + 1);
+    const int y = (int)(r - pl * (H + 1)) - 1, xx = c + dx - 2;
+    xp[i] = (y >= 0 && xx >= 0 && xx < W) ? x[(pl * H + y) * W + xx] : T(0);
+  }
+}
+
 // ------------------------------------------------------------------ tensor-core sub-blocks
 // the dense-enough 16 x 16 tiles of W (plan.h tc_*) as a dense contraction on
 // the tensor cores.  CTA = (row block, 128 columns of N), 4 warps x 32 columns; per tile of
@@ -1358,6 +1504,18 @@ int upload_plan(Plan& p, std::string& err) {
   }
   DeviceGuard dg(p.device);
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
+  {
+    // The executors take stream-ordered scratch (X repack, conv input copies, tensor-core
+    // workspace) with cudaMallocAsync.  With the default release threshold (0) the device pool
+    // hands its memory back to the driver at every synchronisation, so the next call pays a
+    // real allocation; keep it instead (the pool then grows to the largest scratch used).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, p.device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   const size_t nrow = p.row_id.size() * 4, noff = p.blk_off.size() * 8, nblob = p.blob.size();
   const size_t o_off = 0, o_row = (noff + 255) & ~size_t(255),
                o_blob = (o_row + nrow + 255) & ~size_t(255);
@@ -1614,7 +1772,7 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
   const bool f16 = p.dtype == SPARSE_F16;
   ConvFn fn = p.conv_vec ? (f16 ? pick_conv_vec<true>(p.R) : pick_conv_vec<false>(p.R))
                         : (f16 ? pick_conv<true>(p.R, p.C) : pick_conv<false>(p.R, p.C));
-  if (!fn) {
+  if (!fn && p.conv_vec != 2) {
     err = "internal: no conv kernel instance for this tile configuration";
     return SPARSE_EINTERNAL;
   }
@@ -1655,6 +1813,77 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
+  a.npanels = p.npanels;
+  a.stages = p.stages;
+  if (p.conv_vec == 2) {
+    a.stage_bytes = (a.stage_bytes + 127) & ~127;  // TMA destinations 128-byte aligned (inspector)
+    // TMA-fed kernel: width-pad the input into a stream-ordered scratch, then one persistent
+    // wave of CTAs (programmatic dependent launch after the pad kernel)
+    using TmaFn = void (*)(const CUtensorMap, const ConvArgs);
+    TmaFn tf = nullptr;
+    if (p.R == 1) tf = f16 ? conv3x3_tma_kernel<1, true> : conv3x3_tma_kernel<1, false>;
+    if (p.R == 2) tf = f16 ? conv3x3_tma_kernel<2, true> : conv3x3_tma_kernel<2, false>;
+    if (p.R == 4) tf = f16 ? conv3x3_tma_kernel<4, true> : conv3x3_tma_kernel<4, false>;
+    if (p.R == 8) tf = f16 ? conv3x3_tma_kernel<8, true> : conv3x3_tma_kernel<8, false>;
+    auto encode = tensor_map_encoder();
+    if (!tf || !encode) {
+      err = "internal: no TMA conv kernel instance / tensor-map encoder";
+      return SPARSE_EINTERNAL;
+    }
+    if ((e = ensure_smem_attr(tf, p.smem_bytes)) != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
+    const int S = f16 ? 2 : 4;
+    const int64_t planes = (int64_t)p.c_in * batch, rows = planes * (p.h + 1);
+    void* xp = nullptr;
+    e = cudaMallocAsync(&xp, (size_t)(3 * rows * p.conv_wp * S), (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cuda_fail(e, "cudaMallocAsync(conv pad)", err);
+    }
+    const unsigned pg = (unsigned)std::min<int64_t>((3 * rows * p.conv_wp + 255) / 256, 148 * 16);
+    if (f16)
+      pad_conv_input<uint16_t><<<pg, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, planes, p.h,
+                                                                     p.w, p.conv_wp);
+    else
+      pad_conv_input<float><<<pg, 256, 0, (cudaStream_t)stream>>>((const float*)x, (float*)xp, planes, p.h, p.w, p.conv_wp);
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof tmap);
+    cuuint64_t dims[5] = {(cuuint64_t)p.conv_wp, (cuuint64_t)(p.h + 1), (cuuint64_t)batch, (cuuint64_t)p.c_in, 3};
+    cuuint64_t strides[4] = {(cuuint64_t)p.conv_wp * S, (cuuint64_t)p.conv_wp * S * (p.h + 1),
+                             (cuuint64_t)p.conv_wp * S * (p.h + 1) * batch,
+                             (cuuint64_t)p.conv_wp * S * (p.h + 1) * batch * p.c_in};
+    cuuint32_t box[5] = {(cuuint32_t)p.conv_wp, (cuuint32_t)(p.conv_rb + 2), 1u, (cuuint32_t)p.cc, 1u};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode(&tmap, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, xp, dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      cudaFreeAsync(xp, (cudaStream_t)stream);
+      err = "conv: cuTensorMapEncodeTiled failed for the padded input";
+      return SPARSE_EINTERNAL;
+    }
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tf, p.warps * 32, p.smem_bytes) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    cudaGetLastError();
+    const int64_t ntot = (int64_t)p.npanels * batch * a.bands;
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ntot, (int64_t)sms * per_sm)), 1, 1);
+    cfg.blockDim = dim3((unsigned)(p.warps * 32), 1, 1);
+    cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, tf, tmap, a);
+    cudaFreeAsync(xp, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "conv3x3 (TMA) launch", err);
+    return SPARSE_OK;
+  }
   const int64_t groups = (batch + p.conv_ipt - 1) / p.conv_ipt;
   const int64_t ntiles = groups * a.bands;
   if (ntiles > 65535) {

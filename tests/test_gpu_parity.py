@@ -380,16 +380,17 @@ def test_conv_integer_exact_and_delta(f16):
     (16, 24, 3, 14, 14, 2, 16, 5), (256, 64, 2, 14, 14, 8, 16, 16), (8, 40, 2, 7, 7, 4, 8, 3),
     (32, 16, 1, 56, 56, 2, 16, 8), (12, 20, 2, 28, 28, 8, 8, 4), (5, 9, 3, 5, 9, 1, 4, 2)])
 def test_conv_vectorised_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, f16):
-    # the vectorised conv kernel (three dx-shifted input copies, 128-bit position loads):
-    # exact on integer data, bitwise equal to the position-strided kernel (same k order)
+    # the vectorised conv kernels (three dx-shifted input copies, 128-bit position loads;
+    # register-staged (0) and TMA-fed (2)): exact on integer data, bitwise equal to the
+    # position-strided kernel (same k order)
     dev = _dev()
     vmax_w, vmax_x = (2, 4) if f16 else (3, 3)
     w = gen.int_weights(cout, 9 * cin, 90, seed=cin + H, vmax=vmax_w)
     x = gen.int_x(cin * B * H, W, seed=cout, vmax=vmax_x).reshape(cin, B, H, W)
     xt = torch.from_numpy(x).to(dev).to(_tdt(f16))
     ys = []
-    for ck in (0, 1):
-        kw = dict(rows_per_warp=R, warps=warps, k_chunk=cc) if ck == 0 else {}
+    for ck in (3, 1, 2):
+        kw = dict(rows_per_warp=R, warps=warps, k_chunk=cc) if ck != 1 else {}
         plan = srt.Plan.from_csr(w, dtype=_tdt(f16), kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W,
                                  n_hint=B, conv_kernel=ck, **kw)
         assert plan.info["conv_kernel"] == ck
@@ -401,6 +402,7 @@ def test_conv_vectorised_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, f16
         ref = _f16_round(ref)
     assert np.array_equal(ys[0], ref)
     assert np.array_equal(ys[0], ys[1])
+    assert np.array_equal(ys[2], ys[1])
 
 
 @pytest.mark.parametrize("f16", [False, True])
@@ -416,7 +418,8 @@ def test_conv_center_tap_equals_spmm(f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
-def test_conv_c5_full_batch_sampled(f16):
+@pytest.mark.parametrize("ck", [2, 3])
+def test_conv_c5_full_batch_sampled(ck, f16):
     # BASELINE configs[4] at full size (256 ch, 14x14, batch 256, 90%), in the bench's launch
     # configuration; integer data, images {0, 101, 255} checked bitwise against the oracle,
     # and image-slab sharding (the N-sharded multi-GPU split) checked bitwise.
@@ -424,7 +427,8 @@ def test_conv_c5_full_batch_sampled(f16):
     B, H, W = 256, 14, 14
     w = gen.int_weights(cout, 9 * cin, 90, seed=5, vmax=2)
     x = gen.int_x(cin, B * H * W, seed=6, vmax=2).reshape(cin, B, H, W)
-    y, plan = _conv_run(w, cin, x, f16)
+    y, plan = _conv_run(w, cin, x, f16, conv_kernel=ck)
+    assert plan.info["conv_kernel"] == ck
     idx = [0, 101, 255]
     ref = _conv_ref(w, np.ascontiguousarray(x[:, idx]), f16)
     if f16:
@@ -532,7 +536,7 @@ def test_spmm_epilogue_exact(opts, f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
-@pytest.mark.parametrize("ck", [0, 1])
+@pytest.mark.parametrize("ck", [1, 2, 3])
 def test_conv_epilogue_exact(ck, f16):
     dev = _dev()
     cin, cout, B, H, W = 24, 40, 2, 14, 14
