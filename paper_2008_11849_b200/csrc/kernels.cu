@@ -1236,14 +1236,25 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
 // zero outside the image (the layout conv3x3_tma_kernel reads through TMA).  Pure data movement.
 template <typename T>
 __global__ void pad_conv_input(const T* __restrict__ x, T* __restrict__ xp, int64_t planes, int H, int W, int wp) {
-  const int64_t per = planes * (H + 1) * wp, n = 3 * per;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int dx = (int)(i / per);
-    const int64_t r = (i - dx * per) / wp;  // padded row over all planes
-    const int c = (int)(i - dx * per - r * wp);
+  // one thread per padded row (dx, plane, r): index math once per row, 16-byte stores
+  constexpr int V = 16 / sizeof(T);
+  const int64_t rows = planes * (H + 1), n = 3 * rows;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int dx = (int)(t / rows);
+    const int64_t r = t - dx * rows;
     const int64_t pl = r / (H + 1);
-    const int y = (int)(r - pl * (H + 1)) - 1, xx = c + dx - 2;
-    xp[i] = (y >= 0 && xx >= 0 && xx < W) ? x[(pl * H + y) * W + xx] : T(0);
+    const int y = (int)(r - pl * (H + 1)) - 1;
+    const T* src = x + (pl * H + (y < 0 ? 0 : y)) * W;
+    T* dst = xp + t * wp;
+    for (int c0 = 0; c0 < wp; c0 += V) {
+      T v[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) {
+        const int xx = c0 + c + dx - 2;
+        v[c] = (y >= 0 && xx >= 0 && xx < W) ? __ldg(src + xx) : T(0);
+      }
+      *(uint4*)(dst + c0) = *(const uint4*)v;
+    }
   }
 }
 
@@ -1839,7 +1850,7 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
       cudaGetLastError();
       return cuda_fail(e, "cudaMallocAsync(conv pad)", err);
     }
-    const unsigned pg = (unsigned)std::min<int64_t>((3 * rows * p.conv_wp + 255) / 256, 148 * 16);
+    const unsigned pg = (unsigned)std::min<int64_t>((3 * rows + 255) / 256, 148 * 16);
     if (f16)
       pad_conv_input<uint16_t><<<pg, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, planes, p.h,
                                                                      p.w, p.conv_wp);
