@@ -127,7 +127,10 @@ void sparse_plan_opts_init(sparse_plan_opts* opts);
  * values float32[nnz] — host arrays, borrowed for the duration of the call only.
  * On success *out owns the plan and its device memory on opts->device.
  * Errors: EINVAL (null out / arrays, M or K < 1, nnz < 0, bad dtype/kind),
- * EMATRIX (invalid CSR, see above), EUNSUPPORTED, ENOMEM, ECUDA. */
+ * EMATRIX (invalid CSR, see above), EUNSUPPORTED, ENOMEM, ECUDA.
+ * Side effect: the device's default stream-ordered memory pool is set to keep its memory
+ * (cudaMemPoolAttrReleaseThreshold = max): the executors take per-call scratch from it
+ * (unaligned-X repack, conv input copies, tensor-core workspace) with cudaMallocAsync. */
 int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
                        const int32_t* row_ptr, const int32_t* col_idx,
                        const float* values, int32_t dtype,

@@ -4,7 +4,7 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-for wl in ${WLS:-rn50_b8 rn50_b1 mbv1_b32 bert}; do
+for wl in ${WLS:-conv rn50_b8 rn50_b1 mbv1_b32 bert}; do
   for dt in f32 f16; do
     timeout 900 python bench.py --workload $wl --dtype $dt --no-cpu-baseline ${RETUNE:---retune} > gpurun_out/bench_${wl}_${dt}.json 2> gpurun_out/bench_${wl}_${dt}.err
   done
