@@ -420,7 +420,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
         p.conv_cs = ccv * p.conv_sci;  // elements per shifted copy
         p.conv_stage_elems = 3 * p.conv_cs + NTv + 16;  // + zero block
         p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
-        if (o.conv_vec == 2) {
+        if (o.conv_vec == 2 && wpv <= 64) {  // (pad_conv_input holds a padded row in registers)
           // TMA-fed variant (conv3x3_tma_kernel): each shifted copy is one 4-D TMA box
           // {wp, rb + 2, 1 image, cc channels} of the width-padded input (no guard), at a
           // 128-byte aligned offset; no register staging, so up to 64 channels per chunk

@@ -657,7 +657,9 @@ __global__ void __launch_bounds__(512, SRT_MINB) spmm_kernel(const __grid_consta
     // merge into lane 0's wavefront, so a tile with n valid lanes costs ceil(n / 8)
     // shared-memory wavefronts per X load instead of 4 (N = 49: 2, N tail of 8: 1)
 #if SRT_TAILMERGE
-    const int xoff = col < (int)min((int64_t)NT, a.N - n0) ? li * (C * S) : 0;
+    // (decided per quarter-warp: a 128-bit load is served 8 lanes at a time, and a junk lane
+    // of a partly valid quarter reading lane 0's banks would conflict with a valid lane)
+    const int xoff = (li & ~7) * C < (int)min((int64_t)NT, a.N - n0) ? li * (C * S) : 0;
 #else
     const int xoff = li * (C * S);
 #endif
@@ -1051,7 +1053,7 @@ __global__ void __launch_bounds__(512) conv3x3_vec_kernel(const ConvArgs a) {
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
-  const bool junk = (lane * C) / a.wp >= min(a.rb, a.H - y0);
+  const bool junk = ((lane & ~7) * C) / a.wp >= min(a.rb, a.H - y0);  // whole quarter-warp
 
   load(0);
   store(0, 0);
@@ -1187,7 +1189,9 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
     // lanes whose C positions all lie below the band's last image row read lane 0's address
-    const bool junk = (lane * C) / a.wp >= min(a.rb, a.H - y0);
+    // (per quarter-warp: a junk lane of a partly valid quarter keeps its own address, which
+    // shares the quarter's wavefront, instead of conflicting with a valid lane on lane 0's banks)
+    const bool junk = ((lane & ~7) * C) / a.wp >= min(a.rb, a.H - y0);
     const int xoff = junk ? 0 : lane * C * S;
     for (int j = 0; j < a.nchunks; ++j) {
       mbar_wait(full0 + 8 * slot, ph);
@@ -1236,24 +1240,28 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
 // zero outside the image (the layout conv3x3_tma_kernel reads through TMA).  Pure data movement.
 template <typename T>
 __global__ void pad_conv_input(const T* __restrict__ x, T* __restrict__ xp, int64_t planes, int H, int W, int wp) {
-  // one thread per padded row (dx, plane, r): index math once per row, 16-byte stores
-  constexpr int V = 16 / sizeof(T);
-  const int64_t rows = planes * (H + 1), n = 3 * rows;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int dx = (int)(t / rows);
-    const int64_t r = t - dx * rows;
-    const int64_t pl = r / (H + 1);
-    const int y = (int)(r - pl * (H + 1)) - 1;
+  // one thread per padded row (plane, r): the input row is read once into registers, the
+  // three shifted copies are written with 16-byte stores
+  constexpr int V = 16 / sizeof(T), MAXW = 72;  // wp <= 64 (inspector), row index <= wp + 1
+  const int64_t rows = planes * (H + 1);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pl = t / (H + 1);
+    const int y = (int)(t - pl * (H + 1)) - 1;
     const T* src = x + (pl * H + (y < 0 ? 0 : y)) * W;
-    T* dst = xp + t * wp;
-    for (int c0 = 0; c0 < wp; c0 += V) {
-      T v[V];
+    T row[MAXW];  // row[j] = x[y][j - 2], zero outside
 #pragma unroll
-      for (int c = 0; c < V; ++c) {
-        const int xx = c0 + c + dx - 2;
-        v[c] = (y >= 0 && xx >= 0 && xx < W) ? __ldg(src + xx) : T(0);
+    for (int j = 0; j < MAXW; ++j) row[j] = (y >= 0 && j >= 2 && j - 2 < W) ? __ldg(src + j - 2) : T(0);
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      T* dst = xp + (dx * rows + t) * wp;
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += V) {
+        if (c0 >= wp) break;
+        T v[V];
+#pragma unroll
+        for (int c = 0; c < V; ++c) v[c] = row[c0 + c + dx];
+        *(uint4*)(dst + c0) = *(const uint4*)v;
       }
-      *(uint4*)(dst + c0) = *(const uint4*)v;
     }
   }
 }
@@ -1850,7 +1858,7 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
       cudaGetLastError();
       return cuda_fail(e, "cudaMallocAsync(conv pad)", err);
     }
-    const unsigned pg = (unsigned)std::min<int64_t>((3 * rows + 255) / 256, 148 * 16);
+    const unsigned pg = (unsigned)std::min<int64_t>((rows + 255) / 256, 148 * 16);
     if (f16)
       pad_conv_input<uint16_t><<<pg, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, planes, p.h,
                                                                      p.w, p.conv_wp);
