@@ -89,7 +89,12 @@ typedef struct {
                             generator (Sec. 3.5) - per row panel, straight-line PTX with
                             the weights as FFMA immediates, assembled in-process at plan creation
                             (slow to create: seconds for 10^5 nonzeros).  X that is not 16-byte
-                            aligned falls back to the plan-driven kernels (same results, bitwise). */
+                            aligned falls back to the plan-driven kernels (same results, bitwise).
+                            3 = tensor-core condensed panels (fp16 only): per 16-row
+                            panel and 64-row K chunk the union of the panel's nonzero columns runs
+                            as a dense mma.sync m16n8k16 block (fp32 accumulate) with the union's X
+                            rows gathered by ldmatrix; summation order differs from the CUDA-core
+                            kernels (within tolerance; exact on integer data). */
   int32_t jit_rows;      /* JIT: rows per panel (accumulator registers per thread), 0 = auto */
   int32_t jit_warps;     /* JIT: warps per CTA (each owns 32 columns), 0 = auto */
   int32_t x_multicast;   /* SpMM, k_split == 1: CTAs of a thread-block cluster (consecutive row
@@ -198,7 +203,7 @@ typedef struct {
   int32_t conv_rows_per_tile, conv_images_per_tile; /* conv tiling */
   int64_t max_panel_nnz, min_panel_nnz;            /* load-balance metrics */
   double build_ms;      /* host inspector wall time */
-  int32_t executor;     /* 0 plan-driven, 1 JIT */
+  int32_t executor;     /* 0 plan-driven, 1 JIT, 3 tensor-core condensed panels */
   int32_t jit_modules;  /* JIT: compiled modules (launches per call) */
   int32_t jit_rows, jit_warps;
   int64_t jit_cubin_bytes;

@@ -20,6 +20,7 @@
 //  a5  tile-parameter selection (heuristic; the paper's autotuned parameters
 //      M_blocks, N_blocks, Gy).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -222,7 +223,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   std::vector<uint16_t> tc_a;
   int64_t tc_nnz = 0;
   // (not with the JIT executor, which bakes every nonzero into its code)
-  const int tc_pct = (dtype == SPARSE_F16 && o.kind == SPARSE_SPMM && o.executor != 1) ? o.tc_min_pct : 0;
+  const int tc_pct = (dtype == SPARSE_F16 && o.kind == SPARSE_SPMM && o.executor != 1 && o.executor != 3) ? o.tc_min_pct : 0;
   if (tc_pct < 0 || tc_pct > 100) {
     err = "tc_min_density must be in [0, 100] (percent)";
     return SPARSE_EINVAL;
@@ -756,8 +757,141 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     }
     const int rc = jit_generate(p, re, o, err);
     if (rc != SPARSE_OK) return rc;
+  } else if (o.executor == 3) {
+    // ---- condensed-panel tensor-core executor (fp16 SpMM) ----
+    // Panels of 16 consecutive rows; per K chunk of kTcpKc rows the union U of the panel's
+    // nonzero columns is the dense contraction: W[16 x U] (zeros where a row lacks a column)
+    // times the gathered X rows U.  U is laid out in k16 steps of two 8-row halves; rows of a
+    // half have distinct k mod 8 where possible (the staged X chunk is 128-byte swizzled, so
+    // ldmatrix rows with distinct k mod 8 hit distinct banks), padded with zero-weight rows.
+    if (o.kind != SPARSE_SPMM || dtype != SPARSE_F16) {
+      err = "executor = 3 (tensor-core condensed panels) needs an fp16 SpMM plan";
+      return SPARSE_EUNSUPPORTED;
+    }
+    const int KC = kTcpKc;
+    p.tcp_npanels = (M + 15) / 16;
+    p.tcp_nchunks = (K + KC - 1) / KC;
+    const int32_t ngroups = (p.tcp_npanels + kTcpPanels - 1) / kTcpPanels;
+    // steps stored group-major, then chunk, then panel: the steps of one CTA's kTcpPanels
+    // panels for one chunk are contiguous (one bulk copy into the chunk's pipeline stage)
+    p.tcp_step_off.assign((size_t)ngroups * p.tcp_nchunks * (kTcpPanels + 1), 0);
+    p.tcp_steps.clear();
+    p.tcp_max_blk = 0;
+    std::vector<uint16_t> wd((size_t)16 * KC);
+    std::vector<int32_t> cursor_all((size_t)p.tcp_npanels * 16, 0);
+    int64_t nsteps = 0;
+    for (int32_t G = 0; G < ngroups; ++G)
+    for (int32_t c = 0; c < p.tcp_nchunks; ++c) {
+      const int64_t blk0 = nsteps;
+      for (int32_t pi = 0; pi < kTcpPanels; ++pi) {
+        const int32_t q = G * kTcpPanels + pi;
+        p.tcp_step_off[((size_t)G * p.tcp_nchunks + c) * (kTcpPanels + 1) + pi] = (int32_t)nsteps;
+        if (q >= p.tcp_npanels) continue;
+        int32_t* cur = cursor_all.data() + (size_t)q * 16;
+      {
+        const int32_t k0 = c * KC, k1 = std::min(K, k0 + KC);
+        std::fill(wd.begin(), wd.end(), (uint16_t)0);
+        bool used[256] = {false};
+        for (int i = 0; i < 16; ++i) {
+          const int32_t m = 16 * q + i;
+          if (m >= M) continue;
+          int32_t& e = cur[i];
+          while (e < (int32_t)rows[m].size() && rows[m][e].k < k1) {
+            const int kl = rows[m][e].k - k0;
+            wd[(size_t)i * KC + kl] = rows[m][e].wh;
+            used[kl] = true;
+            ++e;
+          }
+        }
+        std::vector<int> bucket[8];
+        int nu = 0;
+        for (int kl = 0; kl < k1 - k0; ++kl)
+          if (used[kl]) {
+            bucket[kl & 7].push_back(kl);
+            ++nu;
+          }
+        // halves of 8 rows: distinct residues first (largest buckets first), then fill
+        std::vector<std::array<int, 8>> halves;
+        int left = nu;
+        while (left > 0) {
+          std::array<int, 8> hf;
+          hf.fill(-1);
+          bool taken[8] = {false};
+          int order[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+          std::sort(order, order + 8, [&](int a, int b) { return bucket[a].size() > bucket[b].size(); });
+          int n = 0;
+          for (int t = 0; t < 8 && left > 0; ++t) {
+            const int r = order[t];
+            if (bucket[r].empty()) continue;
+            hf[n++] = bucket[r].back();
+            bucket[r].pop_back();
+            taken[r] = true;
+            --left;
+          }
+          for (int t = 0; t < 8 && n < 8 && left > 0; ++t) {  // conflicting fill
+            const int r = order[t];
+            while (!bucket[r].empty() && n < 8) {
+              hf[n++] = bucket[r].back();
+              bucket[r].pop_back();
+              --left;
+            }
+          }
+          for (int r = 0; r < 8 && n < 8; ++r)  // zero-weight pads on free residues
+            if (!taken[r] && r < k1 - k0) {
+              hf[n++] = 256 + r;  // 256 + k_local marks a zero-weight pad slot
+              taken[r] = true;
+            }
+          for (; n < 8; ++n) hf[n] = 256;
+          halves.push_back(hf);
+        }
+        if (halves.size() % 2) {
+          std::array<int, 8> pad;
+          for (int r = 0; r < 8; ++r) pad[r] = 256 + (r < k1 - k0 ? r : 0);
+          halves.push_back(pad);
+        }
+        // steps: A fragment (lane l = 4 g + t: W[g][2t, 2t+1], W[g+8][2t, 2t+1],
+        // W[g][2t+8, 2t+9], W[g+8][2t+8, 2t+9] of the step's 16 slots) + 16 slot rows
+        for (size_t hs = 0; hs < halves.size(); hs += 2) {
+          int slot[16];
+          for (int j = 0; j < 8; ++j) {
+            slot[j] = halves[hs][j];
+            slot[8 + j] = halves[hs + 1][j];
+          }
+          // a pad slot reads some staged row (maybe also a real slot elsewhere): weight 0
+          bool real[16];
+          for (int j = 0; j < 16; ++j) {
+            real[j] = slot[j] < 256;
+            slot[j] &= 255;
+          }
+          auto wv = [&](int i, int j) -> uint16_t { return real[j] ? wd[(size_t)i * KC + slot[j]] : (uint16_t)0; };
+          const size_t off = p.tcp_steps.size();
+          p.tcp_steps.resize(off + kTcpStepBytes, 0);
+          uint16_t* a = (uint16_t*)(p.tcp_steps.data() + off);
+          for (int l = 0; l < 32; ++l) {
+            const int g = l / 4, t = l % 4;
+            uint16_t* f = a + l * 8;
+            f[0] = wv(g, 2 * t);
+            f[1] = wv(g, 2 * t + 1);
+            f[2] = wv(g + 8, 2 * t);
+            f[3] = wv(g + 8, 2 * t + 1);
+            f[4] = wv(g, 2 * t + 8);
+            f[5] = wv(g, 2 * t + 9);
+            f[6] = wv(g + 8, 2 * t + 8);
+            f[7] = wv(g + 8, 2 * t + 9);
+          }
+          uint8_t* idx = p.tcp_steps.data() + off + 512;
+          for (int j = 0; j < 16; ++j) idx[j] = (uint8_t)slot[j];
+          ++nsteps;
+        }
+      }
+      }
+      p.tcp_step_off[((size_t)G * p.tcp_nchunks + c) * (kTcpPanels + 1) + kTcpPanels] = (int32_t)nsteps;
+      p.tcp_max_blk = std::max<int32_t>(p.tcp_max_blk, (int32_t)((nsteps - blk0) * kTcpStepBytes));
+    }
+    p.executor = 3;
+    p.plan_bytes += (int64_t)p.tcp_steps.size() + (int64_t)p.tcp_step_off.size() * 4;
   } else if (o.executor != 0) {
-    err = "executor must be 0 (plan-driven), 1 (JIT) or 2 (auto)";
+    err = "executor must be 0 (plan-driven), 1 (JIT), 2 (auto) or 3 (tensor-core condensed panels)";
     return SPARSE_EINVAL;
   }
 
@@ -772,6 +906,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   h = fnv1a(h, p.blob.data(), p.blob.size());
   h = fnv1a(h, p.tc_cb.data(), p.tc_cb.size() * 4);
   h = fnv1a(h, p.tc_a.data(), p.tc_a.size() * 2);
+  h = fnv1a(h, p.tcp_steps.data(), p.tcp_steps.size());
   p.digest = h;
   p.build_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

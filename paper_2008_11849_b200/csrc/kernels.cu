@@ -1542,7 +1542,8 @@ int upload_plan(Plan& p, std::string& err) {
   const size_t o_tca = al(o_blob + nblob), o_tcrb = al(o_tca + p.tc_a.size() * 2),
                o_tctb = al(o_tcrb + p.tc_rb.size() * 4), o_tccb = al(o_tctb + p.tc_tile_begin.size() * 4),
                o_wsr = al(o_tccb + p.tc_cb.size() * 4);
-  const size_t total = o_wsr + p.ws_row.size() * 4;
+  const size_t o_tcpo = al(o_wsr + p.ws_row.size() * 4), o_tcps = al(o_tcpo + p.tcp_step_off.size() * 4);
+  const size_t total = o_tcps + p.tcp_steps.size();
   void* mem = nullptr;
   e = cudaMalloc(&mem, total);
   if (e != cudaSuccess) {
@@ -1564,6 +1565,13 @@ int upload_plan(Plan& p, std::string& err) {
     cudaFree(mem);
     return cuda_fail(e, "cudaMemcpy(plan)", err);
   }
+  if (p.executor == 3 &&
+      ((e = cudaMemcpy(b + o_tcpo, p.tcp_step_off.data(), p.tcp_step_off.size() * 4, cudaMemcpyHostToDevice)) !=
+           cudaSuccess ||
+       (e = cudaMemcpy(b + o_tcps, p.tcp_steps.data(), p.tcp_steps.size(), cudaMemcpyHostToDevice)) != cudaSuccess)) {
+    cudaFree(mem);
+    return cuda_fail(e, "cudaMemcpy(tensor-core panels)", err);
+  }
   // A cudaMemcpy from pageable memory may return before the DMA has landed; it is ordered
   // only with the legacy default stream.  Executors may run on any (non-blocking) stream,
   // so the plan must be complete in device memory when create returns.
@@ -1582,6 +1590,10 @@ int upload_plan(Plan& p, std::string& err) {
     p.d_tc_cb = (const int32_t*)(b + o_tccb);
     p.d_ws_row = (const int32_t*)(b + o_wsr);
   }
+  if (p.executor == 3) {
+    p.d_tcp_step_off = (const int32_t*)(b + o_tcpo);
+    p.d_tcp_steps = b + o_tcps;
+  }
   return SPARSE_OK;
 }
 
@@ -1593,8 +1605,223 @@ void free_plan_device(Plan& p) {
   }
 }
 
+// ------------------------------------------------------------------ condensed-panel tensor cores
+// SURVEY NEXT #1 (executor = 3, fp16 SpMM): per 16-row panel and 64-row K chunk, the union of
+// the panel's nonzero columns is multiplied as a dense block on the tensor cores,
+// mma.sync m16n8k16 (fp16 x fp16, fp32 accumulate): A = W[16 rows x 16 union slots] (packed
+// by the inspector in fragment order), B = the union's X rows, GATHERED by ldmatrix.x4.trans
+// with one row address per lane from the staged chunk.  The chunk is two 128-byte-swizzled
+// TMA boxes (64 K rows x 64 columns each), so the 8 rows of one ldmatrix matrix, chosen
+// with distinct k mod 8 by the inspector, hit distinct banks.  CTA = 16 warps = 16 panels
+// x 128 columns; every warp keeps 16 rows x 128 columns of fp32 accumulators; mbarrier ring
+// over the K chunks refilled by the last releasing warp.
+struct TcpArgs {
+  const int32_t* step_off;
+  const uint8_t* steps;
+  uint8_t* Y;
+  int64_t ldy, N;
+  int32_t M, nchunks, npanels, stages, stage_bytes;
+  const uint8_t* bias;
+  float beta;
+  int32_t relu;
+};
+constexpr int kTcpStage = 2 * kTcpKc * 128;  // X part of a stage: two boxes of 64 rows x 128 bytes
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+               "{%0, %1, %2, %3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(512) spmm_tcp_kernel(const __grid_constant__ CUtensorMap tmap, const TcpArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int q = blockIdx.x * nwarps + warp;  // this warp's panel
+  const int64_t n0 = (int64_t)blockIdx.y * 128;
+  uint8_t* sbase = (uint8_t*)(((uintptr_t)smem + 1023) & ~(uintptr_t)1023);  // 128B swizzle: 1 KB aligned
+  const uint32_t full0 = smem_u32(sbase + (size_t)a.stages * a.stage_bytes);
+  uint32_t* ctr = (uint32_t*)(sbase + (size_t)a.stages * a.stage_bytes + 8 * kMaxStages);
+  const int G = blockIdx.x;
+  const int32_t* offs = a.step_off + (int64_t)G * a.nchunks * (kTcpPanels + 1);
+  if (tid < kMaxStages) ctr[tid] = 0u;
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) mbar_init(full0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  auto refill = [&](int c) {  // lane 0 of one warp: X chunk (2 TMA boxes) + the group's steps
+    const int slot = c % a.stages;
+    uint8_t* st = sbase + (size_t)slot * a.stage_bytes;
+    const uint32_t fb = full0 + 8 * slot;
+    const int o0 = __ldg(offs + c * (kTcpPanels + 1)), o1 = __ldg(offs + c * (kTcpPanels + 1) + kTcpPanels);
+    const uint32_t nb = (uint32_t)(o1 - o0) * (uint32_t)kTcpStepBytes;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(fb, (uint32_t)kTcpStage + nb);
+    tma_load_2d(smem_u32(st), &tmap, (int)n0, c * kTcpKc, fb);
+    tma_load_2d(smem_u32(st + kTcpStage / 2), &tmap, (int)n0 + 64, c * kTcpKc, fb);
+    if (nb) bulk_load(smem_u32(st + kTcpStage), a.steps + (int64_t)o0 * kTcpStepBytes, nb, fb);
+  };
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid == 0)
+    for (int c = 0; c < min(a.stages, a.nchunks); ++c) refill(c);
+
+  float acc[16][4];
+#pragma unroll
+  for (int t = 0; t < 16; ++t)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[t][i] = 0.0f;
+  const bool active = q < a.npanels;
+  // lane's role in ldmatrix.x4.trans: slot (lane & 15) of the step, n8 tile 2 j + (lane >> 4)
+  const int lslot = lane & 15, lhi = lane >> 4;
+  uint32_t ph = 0;
+  for (int c = 0; c < a.nchunks; ++c) {
+    const int slot = c % a.stages;
+    mbar_wait(full0 + 8 * slot, ph);
+    const uint32_t st = smem_u32(sbase + (size_t)slot * a.stage_bytes);
+    if (active) {
+      const int* oc = offs + c * (kTcpPanels + 1);
+      const int o0 = __ldg(oc), s0 = __ldg(oc + warp), s1 = __ldg(oc + warp + 1);
+      const uint8_t* sp = sbase + (size_t)slot * a.stage_bytes + kTcpStage + (size_t)(s0 - o0) * kTcpStepBytes;
+      uint4 av = s0 < s1 ? *(const uint4*)(sp + lane * 16) : make_uint4(0, 0, 0, 0);
+      int kr = s0 < s1 ? (int)sp[512 + lslot] : 0;
+#pragma unroll 1
+      for (int s = s0; s < s1; ++s) {
+        // prefetch the next step's A fragment and slot row (shared memory)
+        uint4 an = av;
+        int kn = kr;
+        if (s + 1 < s1) {
+          an = *(const uint4*)(sp + kTcpStepBytes + lane * 16);
+          kn = (int)sp[kTcpStepBytes + 512 + lslot];
+        }
+        const uint32_t rowa = st + (uint32_t)kr * 128u;
+        const uint32_t sw = (uint32_t)(kr & 7);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int tile = 2 * j + lhi;          // n8 tile 0..15 of the 128 columns
+          const uint32_t box = (uint32_t)(tile >> 3), ch = (uint32_t)(tile & 7);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(rowa + box * (kTcpStage / 2) + ((ch ^ sw) << 4), b0, b1, b2, b3);
+          mma16816(acc[2 * j], av, b0, b1);
+          mma16816(acc[2 * j + 1], av, b2, b3);
+        }
+        av = an;
+        kr = kn;
+        sp += kTcpStepBytes;
+      }
+    }
+    __syncwarp();
+    uint32_t old = 0;
+    if (lane == 0)
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if ((old + 1u) % (uint32_t)nwarps == 0u && c + a.stages < a.nchunks && lane == 0) refill(c + a.stages);
+    if (slot == a.stages - 1) ph ^= 1u;
+  }
+  if (!active) return;
+  // epilogue: c0, c1 -> (row g, columns 2t, 2t + 1 of tile), c2, c3 -> row g + 8
+  const int g = lane >> 2, t = lane & 3;
+  const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int row = 16 * q + g + 8 * h;
+    if (row >= a.M) continue;
+    __half* yr = (__half*)a.Y + (int64_t)row * a.ldy;
+#pragma unroll
+    for (int tile = 0; tile < 16; ++tile) {
+      const int64_t col = n0 + tile * 8 + 2 * t;
+      float v0 = acc[tile][2 * h], v1 = acc[tile][2 * h + 1];
+      if (epi) {
+        if (col < a.N) v0 = epilogue_one<true>(v0, a.bias, row, a.beta, (const uint8_t*)(yr + col), a.relu);
+        if (col + 1 < a.N) v1 = epilogue_one<true>(v1, a.bias, row, a.beta, (const uint8_t*)(yr + col + 1), a.relu);
+      }
+      if (col + 1 < a.N && ((((uintptr_t)(yr + col)) & 3) == 0)) {
+        *(__half2*)(yr + col) = __floats2half2_rn(v0, v1);
+      } else {
+        if (col < a.N) yr[col] = __float2half_rn(v0);
+        if (col + 1 < a.N) yr[col + 1] = __float2half_rn(v1);
+      }
+    }
+  }
+}
+
+static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy, void* stream,
+                      std::string& err, const Epilogue& ep) {
+  auto encode = tensor_map_encoder();
+  if (!encode || ((uintptr_t)X % 16) || ((ldx * 2) % 16)) {
+    err = "tensor-core panels need a TMA-aligned X (16-byte base and row stride)";
+    return SPARSE_EINTERNAL;
+  }
+  DeviceGuard dg(p.device);
+  if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
+  const int warps = kTcpPanels;
+  const int stage_bytes = (kTcpStage + p.tcp_max_blk + 1023) & ~1023;  // X boxes stay 1 KB aligned
+  const int stages = std::min(kMaxStages, (227 * 1024 - 1024 - 256) / stage_bytes);
+  if (stages < 2) {
+    err = "tensor-core panels: a chunk's steps do not fit two pipeline stages";
+    return SPARSE_EUNSUPPORTED;
+  }
+  const int smem = stages * stage_bytes + 1024 + 256;
+  cudaError_t e = ensure_smem_attr(spmm_tcp_kernel, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof tmap);
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)p.K};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldx * 2)};
+  cuuint32_t box[2] = {64u, (cuuint32_t)kTcpKc};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)X, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "tensor-core panels: cuTensorMapEncodeTiled failed";
+    return SPARSE_EINTERNAL;
+  }
+  TcpArgs a;
+  a.step_off = p.d_tcp_step_off;
+  a.steps = p.d_tcp_steps;
+  a.Y = (uint8_t*)Y;
+  a.ldy = ldy;
+  a.N = N;
+  a.M = p.M;
+  a.nchunks = p.tcp_nchunks;
+  a.npanels = p.tcp_npanels;
+  a.stages = stages;
+  a.stage_bytes = stage_bytes;
+  a.bias = (const uint8_t*)ep.bias;
+  a.beta = ep.beta;
+  a.relu = ep.relu;
+  const int64_t ntn = (N + 127) / 128;
+  if (ntn > 65535) {
+    err = "tensor-core panels: N too large for one launch";
+    return SPARSE_EUNSUPPORTED;
+  }
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((unsigned)((p.tcp_npanels + warps - 1) / warps), (unsigned)ntn, 1);  // x = group G
+  cfg.blockDim = dim3((unsigned)(warps * 32), 1, 1);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, spmm_tcp_kernel, tmap, a);
+  if (e != cudaSuccess) return cuda_fail(e, "tensor-core panel launch", err);
+  return SPARSE_OK;
+}
+
 int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
                 void* stream, std::string& err, const Epilogue& ep) {
+  if (p.executor == 3) return launch_tcp(p, N, X, ldx, Y, ldy, stream, err, ep);
   const bool f16 = p.dtype == SPARSE_F16;
   const int S = f16 ? 2 : 4;
   SpmmFn fn = f16 ? pick_spmm<true>(p.R, p.gk, p.tm) : pick_spmm<false>(p.R, p.gk, p.tm);

@@ -104,7 +104,7 @@ struct Plan {
   // P:183-185): per row panel, straight-line PTX that walks the panel's K
   // union in ascending order, loads X[k, lane column] once and issues one FFMA
   // with the weight as an immediate per nonzero of column k (Alg. 3).
-  int32_t executor = 0;      // 0 = plan-driven kernels, 1 = JIT
+  int32_t executor = 0;      // 0 = plan-driven kernels, 1 = JIT, 3 = tensor-core condensed panels
   struct JitModule {
     std::string ptx;
     std::vector<char> cubin;
@@ -148,7 +148,21 @@ struct Plan {
   const int32_t* d_tc_cb = nullptr;
   const uint16_t* d_tc_a = nullptr;
   const int32_t* d_ws_row = nullptr;
+
+  // Condensed-panel tensor-core executor (executor = 3; fp16 SpMM): panel q =
+  // rows 16 q .. 16 q + 15 (group G = q / kTcpPanels, i = q % kTcpPanels); chunk c = K rows
+  // kTcpKc c ..; its steps are [off[(G nch + c)(kTcpPanels + 1) + i], ... + i + 1) of
+  // kTcpStepBytes each = mma A fragment (32 lanes x 8 fp16) of W[16 rows x 16 union slots] +
+  // the 16 slot rows (uint8 k_local, padded to 16 bytes); one group's chunk is contiguous
+  int32_t tcp_npanels = 0, tcp_nchunks = 0, tcp_max_blk = 0;
+  std::vector<int32_t> tcp_step_off;
+  std::vector<uint8_t> tcp_steps;
+  const int32_t* d_tcp_step_off = nullptr;
+  const uint8_t* d_tcp_steps = nullptr;
 };
+constexpr int kTcpKc = 64;          // K rows per staged chunk (one 128-byte swizzled TMA box row)
+constexpr int kTcpPanels = 16;      // panels (warps) per CTA
+constexpr int kTcpStepBytes = 528;  // 512 B A fragment + 16 B slot rows
 
 struct BuildOpts {
   int32_t kind = 0, c_in = 0, h = 0, w = 0;

@@ -122,6 +122,11 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     BuildOpts j = base;
     j.executor = 1;
     cands.push_back(j);
+    if (f16) {  // condensed-panel tensor cores
+      BuildOpts t = base;
+      t.executor = 3;
+      cands.push_back(t);
+    }
   } else {
     // vectorised kernels (16-byte loads of consecutive positions; TMA-fed = 2, register-
     // staged = 1) and the position-strided one (0); cc = channels per chunk (0: inspector)

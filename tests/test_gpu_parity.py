@@ -592,3 +592,54 @@ def test_tensor_core_subblocks_rel_l2():
     assert p_tc.info["tc_tiles"] > 0 and p_cc.info["tc_tiles"] == 0
     ref = _ref(w, X, True)
     assert oracle.rel_l2(y_tc, ref) <= F16_TOL and oracle.rel_l2(y_cc, ref) <= F16_TOL
+
+
+# --------------------------------------------------------------------------- condensed-panel tensor cores
+
+@pytest.mark.parametrize("p", [80, 90, 95, 98])
+@pytest.mark.parametrize("M,K,N", [(64, 64, 128), (300, 200, 517), (1000, 64, 49), (77, 1111, 300),
+                                   (3072, 768, 512)])
+def test_tcp_rel_l2(M, K, N, p):
+    # executor 3: per 16-row panel the union of nonzero columns runs as a dense
+    # mma.sync block (fp16 x fp16, fp32 accumulate), X rows gathered by ldmatrix
+    w = gen.pruned_weights(M, K, p, seed=gen.case_seed(f"tcp{M}x{K}x{N}", p))
+    X = gen.uniform_x(K, N, seed=N + p + 7)
+    y, plan = _run_spmm(w, X, True, executor=3)
+    assert plan.info["executor"] == 3
+    err = oracle.rel_l2(y, _ref(w, X, True))
+    assert err <= F16_TOL, err
+
+
+@pytest.mark.parametrize("case", [(64, 256, 3136), (512, 2048, 49), (2048, 512, 392), (1024, 1024, 1568),
+                                  (3072, 768, 512), (768, 3072, 512), (17, 70, 33)])
+@pytest.mark.parametrize("p", [90, 98])
+def test_tcp_integer_exact(case, p):
+    # integer data: every fp32 partial sum is exact, so the tensor-core path (any summation
+    # order inside the mma) must equal the RN-even fp16 rounding of the exact result
+    M, K, N = case
+    _exact_case(M, K, N, p, True, seed=gen.case_seed("tcp" + str(case), p), executor=3)
+
+
+def test_tcp_closed_forms_and_epilogue():
+    dev = _dev()
+    K, N = 300, 777
+    X = gen.uniform_x(K, N, seed=3)
+    z = gen.stress_pattern("empty", 50, K, seed=1)
+    y, _ = _run_spmm(z, X, True, executor=3)
+    assert np.array_equal(y, np.zeros_like(y))
+    y, _ = _run_spmm(gen.identity_csr(K), X, True, executor=3)
+    assert np.array_equal(y, _x64(X, True))
+    # fused epilogue: relu(W X + bias + 0.5 Y0), integer data -> exact
+    M = 96
+    w = gen.int_weights(M, K, 90, seed=91, vmax=2)
+    Xi = gen.int_x(K, N, seed=92, vmax=4)
+    rng = np.random.default_rng(93)
+    bias = rng.integers(-8, 9, M).astype(np.float32)
+    Y0 = rng.integers(-8, 9, (M, N)).astype(np.float32)
+    plan = srt.Plan.from_csr(w, dtype=torch.float16, n_hint=N, executor=3)
+    Y = torch.from_numpy(Y0).to(dev).half()
+    plan.spmm(torch.from_numpy(Xi).to(dev).half(), Y, bias=torch.from_numpy(bias).to(dev).half(), beta=0.5,
+              relu=True)
+    torch.cuda.synchronize()
+    ref = np.maximum(_ref(w, Xi, True) + bias[:, None] + 0.5 * Y0, 0.0)
+    assert np.array_equal(Y.double().cpu().numpy(), _f16_round(ref))
