@@ -1612,9 +1612,10 @@ void free_plan_device(Plan& p) {
 // by the inspector in fragment order), B = the union's X rows, GATHERED by ldmatrix.x4.trans
 // with one row address per lane from the staged chunk.  The chunk is two 128-byte-swizzled
 // TMA boxes (64 K rows x 64 columns each), so the 8 rows of one ldmatrix matrix, chosen
-// with distinct k mod 8 by the inspector, hit distinct banks.  CTA = 16 warps = 16 panels
-// x 128 columns; every warp keeps 16 rows x 128 columns of fp32 accumulators; mbarrier ring
-// over the K chunks refilled by the last releasing warp.
+// with distinct k mod 8 by the inspector, hit distinct banks.  CTA = kTcpPanels warps (8: two
+// CTAs per SM; measured faster than 16 warps in one CTA) = 8 panels x 128 columns; every warp
+// keeps 16 rows x 128 columns of fp32 accumulators; the chunk's A fragments and slot rows
+// arrive with the X boxes (bulk copy); mbarrier ring refilled by the last releasing warp.
 struct TcpArgs {
   const int32_t* step_off;
   const uint8_t* steps;
@@ -1638,7 +1639,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint4& a, uint32_t
                : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
-__global__ void __launch_bounds__(512) spmm_tcp_kernel(const __grid_constant__ CUtensorMap tmap, const TcpArgs a) {
+__global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spmm_tcp_kernel(const __grid_constant__ CUtensorMap tmap, const TcpArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nwarps = blockDim.x >> 5;
@@ -1763,7 +1764,9 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
   const int warps = kTcpPanels;
   const int stage_bytes = (kTcpStage + p.tcp_max_blk + 1023) & ~1023;  // X boxes stay 1 KB aligned
-  const int stages = std::min(kMaxStages, (227 * 1024 - 1024 - 256) / stage_bytes);
+  // 16 panels per CTA: one CTA per SM (126 registers x 512 threads); 8: two CTAs per SM
+  const int budget = kTcpPanels >= 16 ? 227 * 1024 : 113 * 1024;
+  const int stages = std::min(kMaxStages, (budget - 1024 - 256) / stage_bytes);
   if (stages < 2) {
     err = "tensor-core panels: a chunk's steps do not fit two pipeline stages";
     return SPARSE_EUNSUPPORTED;

@@ -161,7 +161,13 @@ struct Plan {
   const uint8_t* d_tcp_steps = nullptr;
 };
 constexpr int kTcpKc = 64;          // K rows per staged chunk (one 128-byte swizzled TMA box row)
-constexpr int kTcpPanels = 16;      // panels (warps) per CTA
+#ifndef SRT_TCP_PANELS
+#define SRT_TCP_PANELS 8
+#endif
+#ifndef SRT_TCP_STRICT
+#define SRT_TCP_STRICT 1
+#endif
+constexpr int kTcpPanels = SRT_TCP_PANELS;  // panels (warps) per CTA
 constexpr int kTcpStepBytes = 528;  // 512 B A fragment + 16 B slot rows
 
 struct BuildOpts {
