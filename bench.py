@@ -142,8 +142,8 @@ def load_peaks():
     if os.path.exists(p):
         d = json.load(open(p))
         return dict(hbm_gbs=float(d["hbm_gbs"]), sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)),
-                    source="measured")
-    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback")
+                    bf16_tflops=float(d.get("bf16_tflops", 2250.0)), source="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, bf16_tflops=2250.0, source="fallback")
 
 
 def alu_peak_gflops(sm_mhz: float) -> float:
@@ -467,7 +467,16 @@ def main():
     if os.path.exists(tpath):
         t = json.load(open(tpath)).get(d["name"])
         traffic = t and t.get("traffic_bytes_per_launch")
-    if d["bound"] == "hbm":
+    pinfo = plans[dom][0].info
+    if pinfo.get("executor") == 3:
+        # condensed-panel tensor cores (DESIGN.md kernel 5b): a dense fp16 contraction of the
+        # panels' column unions; executed flops = 2 * 16 * 16 * N per k16 step, against the
+        # measured dense bf16 peak (fp16 runs at the same tensor rate)
+        tc_flops = 2 * 16 * 16 * d["N"] * pinfo["tc_panel_steps"]
+        roof = {"bound": "tensor", "achieved": tc_flops / sec / 1e12, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "useful_tflops": 2 * d["nnz"] * d["N"] / sec / 1e12,
+                "executed_flops_per_launch": tc_flops}
+    elif d["bound"] == "hbm":
         roof = {"bound": "hbm", "achieved": d["alg_bytes"] / sec / 1e9, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s"}
     else:
@@ -477,7 +486,9 @@ def main():
     roof["traffic"] = traffic
     roof["kernel"] = d["name"]
     roof["peak_source"] = peaks["source"] if roof["bound"] == "hbm" else \
-        "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"
+        ("MEASURED_PEAKS.json bf16_tflops (dense tcgen05 cuBLAS; this kernel issues mma.sync)"
+         if roof["bound"] == "tensor" else
+         "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)")
     roof["alg_bytes_per_launch"] = d["alg_bytes"]
     roof["flops_per_launch"] = 2 * d["nnz"] * d["N"]
     # Design ceilings of the CUDA-core executor, context for `frac`: one shared-

@@ -218,6 +218,8 @@ typedef struct {
   int32_t tc_row_blocks;  /* 16-row blocks with >= 1 dense tile */
   int64_t tc_tiles;       /* dense 16 x 16 tiles on the tensor cores */
   int64_t tc_nnz;         /* nonzeros inside them (counted in nnz) */
+  int64_t tc_panel_steps; /* executor 3: k16 steps over all (panel, chunk) pairs; the tensor cores
+                             execute 2 * 16 * 16 * N flops per step (useful: 2 * nnz * N) */
 } sparse_plan_info_t;
 
 int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out);

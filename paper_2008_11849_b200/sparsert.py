@@ -76,7 +76,7 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
                 ("row_order", ctypes.c_int32), ("tc_min_density", ctypes.c_int32),
                 ("tc_row_blocks", ctypes.c_int32), ("tc_tiles", ctypes.c_int64),
-                ("tc_nnz", ctypes.c_int64)]
+                ("tc_nnz", ctypes.c_int64), ("tc_panel_steps", ctypes.c_int64)]
 
 
 def _load() -> ctypes.CDLL:
