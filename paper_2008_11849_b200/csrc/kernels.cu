@@ -1626,7 +1626,6 @@ struct TcpArgs {
   float beta;
   int32_t relu;
 };
-constexpr int kTcpStage = 2 * kTcpKc * 128;  // X part of a stage: two boxes of 64 rows x 128 bytes
 
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
@@ -1639,12 +1638,19 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint4& a, uint32_t
                : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
+// NB = 64-column boxes per CTA (N tile = 64 NB): 2 for large N (A fragments reused over 16
+// n8 tiles), 1 below (twice the CTAs; measured 1.4x faster at N = 1568 / 392).  Loading the
+// next step's B fragments ahead of this step's mma.sync (software pipelining) was measured
+// 1.2-1.6x slower (register pressure at 2 CTAs per SM).
+template <int NB>
 __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spmm_tcp_kernel(const __grid_constant__ CUtensorMap tmap, const TcpArgs a) {
+  constexpr int NTT = 8 * NB;       // n8 tiles per warp
+  constexpr int XST = NB * kTcpKc * 128;  // X part of a stage
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nwarps = blockDim.x >> 5;
   const int q = blockIdx.x * nwarps + warp;  // this warp's panel
-  const int64_t n0 = (int64_t)blockIdx.y * 128;
+  const int64_t n0 = (int64_t)blockIdx.y * (64 * NB);
   uint8_t* sbase = (uint8_t*)(((uintptr_t)smem + 1023) & ~(uintptr_t)1023);  // 128B swizzle: 1 KB aligned
   const uint32_t full0 = smem_u32(sbase + (size_t)a.stages * a.stage_bytes);
   uint32_t* ctr = (uint32_t*)(sbase + (size_t)a.stages * a.stage_bytes + 8 * kMaxStages);
@@ -1657,31 +1663,42 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  auto refill = [&](int c) {  // lane 0 of one warp: X chunk (2 TMA boxes) + the group's steps
+  auto refill = [&](int c) {  // lane 0 of one warp: X chunk (NB TMA boxes) + the group's steps
     const int slot = c % a.stages;
     uint8_t* st = sbase + (size_t)slot * a.stage_bytes;
     const uint32_t fb = full0 + 8 * slot;
     const int o0 = __ldg(offs + c * (kTcpPanels + 1)), o1 = __ldg(offs + c * (kTcpPanels + 1) + kTcpPanels);
     const uint32_t nb = (uint32_t)(o1 - o0) * (uint32_t)kTcpStepBytes;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive_expect_tx(fb, (uint32_t)kTcpStage + nb);
-    tma_load_2d(smem_u32(st), &tmap, (int)n0, c * kTcpKc, fb);
-    tma_load_2d(smem_u32(st + kTcpStage / 2), &tmap, (int)n0 + 64, c * kTcpKc, fb);
-    if (nb) bulk_load(smem_u32(st + kTcpStage), a.steps + (int64_t)o0 * kTcpStepBytes, nb, fb);
+    mbar_arrive_expect_tx(fb, (uint32_t)XST + nb);
+#pragma unroll
+    for (int bx = 0; bx < NB; ++bx)
+      tma_load_2d(smem_u32(st + bx * (kTcpKc * 128)), &tmap, (int)n0 + 64 * bx, c * kTcpKc, fb);
+    if (nb) bulk_load(smem_u32(st + XST), a.steps + (int64_t)o0 * kTcpStepBytes, nb, fb);
   };
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (tid == 0)
     for (int c = 0; c < min(a.stages, a.nchunks); ++c) refill(c);
 
-  float acc[16][4];
+  float acc[NTT][4];
 #pragma unroll
-  for (int t = 0; t < 16; ++t)
+  for (int t = 0; t < NTT; ++t)
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[t][i] = 0.0f;
   const bool active = q < a.npanels;
   // lane's role in ldmatrix.x4.trans: slot (lane & 15) of the step, n8 tile 2 j + (lane >> 4)
   const int lslot = lane & 15, lhi = lane >> 4;
+  auto load_b = [&](uint32_t st, int kr, uint32_t (&bf)[NTT / 2][4]) {
+    const uint32_t rowa = st + (uint32_t)kr * 128u;
+    const uint32_t sw = (uint32_t)(kr & 7);
+#pragma unroll
+    for (int j = 0; j < NTT / 2; ++j) {
+      const int tile = 2 * j + lhi;
+      const uint32_t box = (uint32_t)(tile >> 3), ch = (uint32_t)(tile & 7);
+      ldsm_x4_t(rowa + box * (kTcpKc * 128) + ((ch ^ sw) << 4), bf[j][0], bf[j][1], bf[j][2], bf[j][3]);
+    }
+  };
   uint32_t ph = 0;
   for (int c = 0; c < a.nchunks; ++c) {
     const int slot = c % a.stages;
@@ -1690,7 +1707,7 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
     if (active) {
       const int* oc = offs + c * (kTcpPanels + 1);
       const int o0 = __ldg(oc), s0 = __ldg(oc + warp), s1 = __ldg(oc + warp + 1);
-      const uint8_t* sp = sbase + (size_t)slot * a.stage_bytes + kTcpStage + (size_t)(s0 - o0) * kTcpStepBytes;
+      const uint8_t* sp = sbase + (size_t)slot * a.stage_bytes + XST + (size_t)(s0 - o0) * kTcpStepBytes;
       uint4 av = s0 < s1 ? *(const uint4*)(sp + lane * 16) : make_uint4(0, 0, 0, 0);
       int kr = s0 < s1 ? (int)sp[512 + lslot] : 0;
 #pragma unroll 1
@@ -1702,16 +1719,12 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
           an = *(const uint4*)(sp + kTcpStepBytes + lane * 16);
           kn = (int)sp[kTcpStepBytes + 512 + lslot];
         }
-        const uint32_t rowa = st + (uint32_t)kr * 128u;
-        const uint32_t sw = (uint32_t)(kr & 7);
+        uint32_t bcur[NTT / 2][4];
+        load_b(st, kr, bcur);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int tile = 2 * j + lhi;          // n8 tile 0..15 of the 128 columns
-          const uint32_t box = (uint32_t)(tile >> 3), ch = (uint32_t)(tile & 7);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(rowa + box * (kTcpStage / 2) + ((ch ^ sw) << 4), b0, b1, b2, b3);
-          mma16816(acc[2 * j], av, b0, b1);
-          mma16816(acc[2 * j + 1], av, b2, b3);
+        for (int j = 0; j < NTT / 2; ++j) {
+          mma16816(acc[2 * j], av, bcur[j][0], bcur[j][1]);
+          mma16816(acc[2 * j + 1], av, bcur[j][2], bcur[j][3]);
         }
         av = an;
         kr = kn;
@@ -1736,7 +1749,7 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
     if (row >= a.M) continue;
     __half* yr = (__half*)a.Y + (int64_t)row * a.ldy;
 #pragma unroll
-    for (int tile = 0; tile < 16; ++tile) {
+    for (int tile = 0; tile < NTT; ++tile) {
       const int64_t col = n0 + tile * 8 + 2 * t;
       float v0 = acc[tile][2 * h], v1 = acc[tile][2 * h + 1];
       if (epi) {
@@ -1763,7 +1776,9 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   DeviceGuard dg(p.device);
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
   const int warps = kTcpPanels;
-  const int stage_bytes = (kTcpStage + p.tcp_max_blk + 1023) & ~1023;  // X boxes stay 1 KB aligned
+  const int NB = N >= 4096 ? 2 : 1;
+  auto kfn = NB == 2 ? spmm_tcp_kernel<2> : spmm_tcp_kernel<1>;
+  const int stage_bytes = (NB * kTcpKc * 128 + p.tcp_max_blk + 1023) & ~1023;  // X boxes stay 1 KB aligned
   // 16 panels per CTA: one CTA per SM (126 registers x 512 threads); 8: two CTAs per SM
   const int budget = kTcpPanels >= 16 ? 227 * 1024 : 113 * 1024;
   const int stages = std::min(kMaxStages, (budget - 1024 - 256) / stage_bytes);
@@ -1772,7 +1787,7 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
     return SPARSE_EUNSUPPORTED;
   }
   const int smem = stages * stage_bytes + 1024 + 256;
-  cudaError_t e = ensure_smem_attr(spmm_tcp_kernel, smem);
+  cudaError_t e = ensure_smem_attr(kfn, smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
@@ -1801,7 +1816,7 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
-  const int64_t ntn = (N + 127) / 128;
+  const int64_t ntn = (N + 64 * NB - 1) / (64 * NB);
   if (ntn > 65535) {
     err = "tensor-core panels: N too large for one launch";
     return SPARSE_EUNSUPPORTED;
@@ -1817,7 +1832,7 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, spmm_tcp_kernel, tmap, a);
+  e = cudaLaunchKernelEx(&cfg, kfn, tmap, a);
   if (e != cudaSuccess) return cuda_fail(e, "tensor-core panel launch", err);
   return SPARSE_OK;
 }
