@@ -1622,6 +1622,7 @@ struct TcpArgs {
   uint8_t* Y;
   int64_t ldy, N;
   int32_t M, nchunks, npanels, stages, stage_bytes;
+  int32_t cy;  // CTAs per cluster along N sharing (multicasting) the panels' A steps
   const uint8_t* bias;
   float beta;
   int32_t relu;
@@ -1642,6 +1643,9 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint4& a, uint32_t
 // n8 tiles), 1 below (twice the CTAs; measured 1.4x faster at N = 1568 / 392).  Loading the
 // next step's B fragments ahead of this step's mma.sync (software pipelining) was measured
 // 1.2-1.6x slower (register pressure at 2 CTAs per SM).
+#ifndef SRT_TCP_CY
+#define SRT_TCP_CY 1
+#endif
 template <int NB>
 __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spmm_tcp_kernel(const __grid_constant__ CUtensorMap tmap, const TcpArgs a) {
   constexpr int NTT = 8 * NB;       // n8 tiles per warp
@@ -1656,30 +1660,60 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
   uint32_t* ctr = (uint32_t*)(sbase + (size_t)a.stages * a.stage_bytes + 8 * kMaxStages);
   const int G = blockIdx.x;
   const int32_t* offs = a.step_off + (int64_t)G * a.nchunks * (kTcpPanels + 1);
+  // cy > 1 (-DSRT_TCP_CY=2/4, exact-tested): the cy CTAs of a cluster (consecutive N tiles,
+  // same panel group) receive every chunk's A steps through ONE multicast bulk copy issued by
+  // rank 0, which refills a slot once all cy CTAs released it (cluster-empty barrier in rank 0,
+  // one remote arrive per CTA).  Cuts the A-step L2 traffic by cy but measured 1.4-1.7x slower
+  // (the cluster-wide release lockstep), as the X multicast of spmm_kernel; off by default.
+  constexpr int cy = SRT_TCP_CY;  // compile-time: the multicast code vanishes for cy == 1
+  const uint32_t crank = cy > 1 ? cluster_rank() : 0u;
+  const uint32_t cempty0 = full0 + 8 * kMaxStages + 64;  // after ctr[8]
   if (tid < kMaxStages) ctr[tid] = 0u;
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) mbar_init(full0 + 8 * s, 1);
+    for (int s = 0; cy > 1 && s < a.stages; ++s) mbar_init(cempty0 + 8 * s, (uint32_t)cy);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  auto refill = [&](int c) {  // lane 0 of one warp: X chunk (NB TMA boxes) + the group's steps
+  if (cy > 1) cluster_sync_all();  // every CTA's barriers exist before multicasts arrive
+  auto nbytes = [&](int c) -> uint32_t {
+    const int o0 = __ldg(offs + c * (kTcpPanels + 1)), o1 = __ldg(offs + c * (kTcpPanels + 1) + kTcpPanels);
+    return (uint32_t)(o1 - o0) * (uint32_t)kTcpStepBytes;
+  };
+  auto load_a = [&](int c) {  // the group's steps of chunk c -> slot (multicast when cy > 1)
+    const int slot = c % a.stages;
+    const uint32_t nb = nbytes(c);
+    if (!nb) return;
+    const int o0 = __ldg(offs + c * (kTcpPanels + 1));
+    const uint32_t dst = smem_u32(sbase + (size_t)slot * a.stage_bytes + XST), fb = full0 + 8 * slot;
+    const uint8_t* src = a.steps + (int64_t)o0 * kTcpStepBytes;
+    if (cy > 1)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+          " [%0], [%1], %2, [%3], %4;" ::"r"(dst), "l"(src), "r"(nb), "r"(fb), "h"((uint16_t)((1u << cy) - 1u))
+          : "memory");
+    else
+      bulk_load(dst, src, nb, fb);
+  };
+  auto refill = [&](int c) {  // lane 0 of one warp: X chunk (NB TMA boxes) (+ A steps if cy == 1)
     const int slot = c % a.stages;
     uint8_t* st = sbase + (size_t)slot * a.stage_bytes;
     const uint32_t fb = full0 + 8 * slot;
-    const int o0 = __ldg(offs + c * (kTcpPanels + 1)), o1 = __ldg(offs + c * (kTcpPanels + 1) + kTcpPanels);
-    const uint32_t nb = (uint32_t)(o1 - o0) * (uint32_t)kTcpStepBytes;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive_expect_tx(fb, (uint32_t)XST + nb);
+    mbar_arrive_expect_tx(fb, (uint32_t)XST + nbytes(c));
 #pragma unroll
     for (int bx = 0; bx < NB; ++bx)
       tma_load_2d(smem_u32(st + bx * (kTcpKc * 128)), &tmap, (int)n0 + 64 * bx, c * kTcpKc, fb);
-    if (nb) bulk_load(smem_u32(st + XST), a.steps + (int64_t)o0 * kTcpStepBytes, nb, fb);
+    if (cy == 1) load_a(c);
   };
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (tid == 0)
+  if (tid == 0) {
     for (int c = 0; c < min(a.stages, a.nchunks); ++c) refill(c);
+    if (cy > 1 && crank == 0)
+      for (int c = 0; c < min(a.stages, a.nchunks); ++c) load_a(c);
+  }
 
   float acc[NTT][4];
 #pragma unroll
@@ -1736,9 +1770,22 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
     if (lane == 0)
       asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
     old = __shfl_sync(0xffffffffu, old, 0);
-    if ((old + 1u) % (uint32_t)nwarps == 0u && c + a.stages < a.nchunks && lane == 0) refill(c + a.stages);
+    if ((old + 1u) % (uint32_t)nwarps == 0u && c + a.stages < a.nchunks && lane == 0) {
+      refill(c + a.stages);
+      if (cy > 1) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(map_rank(cempty0 + 8 * slot, 0u))
+                     : "memory");
+        if (crank == 0) {
+          mbar_wait(cempty0 + 8 * slot, (uint32_t)((c / a.stages) & 1));
+          asm volatile("fence.acq_rel.cluster;" ::: "memory");
+          load_a(c + a.stages);
+        }
+      }
+    }
     if (slot == a.stages - 1) ph ^= 1u;
   }
+  if (cy > 1) cluster_sync_all();  // no CTA leaves while multicasts / remote arrives may target it
   if (!active) return;
   // epilogue: c0, c1 -> (row g, columns 2t, 2t + 1 of tile), c2, c3 -> row g + 8
   const int g = lane >> 2, t = lane & 3;
@@ -1787,6 +1834,7 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
     return SPARSE_EUNSUPPORTED;
   }
   const int smem = stages * stage_bytes + 1024 + 256;
+  const int cy = SRT_TCP_CY;
   cudaError_t e = ensure_smem_attr(kfn, smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
   CUtensorMap tmap;
@@ -1813,10 +1861,11 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   a.npanels = p.tcp_npanels;
   a.stages = stages;
   a.stage_bytes = stage_bytes;
+  a.cy = cy;
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
-  const int64_t ntn = (N + 64 * NB - 1) / (64 * NB);
+  const int64_t ntn = ((N + 64 * NB - 1) / (64 * NB) + cy - 1) / cy * cy;  // whole clusters
   if (ntn > 65535) {
     err = "tensor-core panels: N too large for one launch";
     return SPARSE_EUNSUPPORTED;
@@ -1827,11 +1876,15 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   cfg.blockDim = dim3((unsigned)(warps * 32), 1, 1);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = (unsigned)cy;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   e = cudaLaunchKernelEx(&cfg, kfn, tmap, a);
   if (e != cudaSuccess) return cuda_fail(e, "tensor-core panel launch", err);
   return SPARSE_OK;
