@@ -260,3 +260,28 @@ def test_jit_codegen_compiles_on_host():
     assert pl16.info["jit_cubin_bytes"] > 0
     with pytest.raises(S.SparseRTError):
         _plan(w, kind=srt.SPARSE_CONV3X3, c_in=w.K // 9, h=4, w=4, executor=1)
+
+
+@pytest.mark.parametrize("M,K,p", [(64, 64, 90), (300, 200, 90), (77, 1111, 80), (512, 512, 98), (33, 70, 50)])
+def test_tensor_core_panel_steps(M, K, p):
+    # executor 3 (condensed panels): per 16-row panel and 64-row K chunk the union's rows are
+    # laid out in 8-row halves with pairwise distinct k mod 8, two halves per k16 step, so a
+    # panel-chunk takes ceil(max_r |{k in union : k mod 8 = r}| / 2) steps.  Independent count:
+    import torch
+    w = gen.pruned_weights(M, K, p, seed=M + K)
+    info = _plan(w, torch.float16, n_hint=256, executor=3).info
+    assert info["executor"] == 3
+    rows = np.repeat(np.arange(M), np.diff(w.row_ptr))
+    expect = 0
+    for q in range((M + 15) // 16):
+        for c in range((K + 63) // 64):
+            sel = (rows // 16 == q) & (w.col_idx // 64 == c)
+            union = np.unique(w.col_idx[sel] - 64 * c)
+            if union.size == 0:
+                continue
+            halves = np.bincount(union % 8, minlength=8).max()
+            expect += (halves + 1) // 2
+    assert info["tc_panel_steps"] == expect
+    # fp32 plans and conv plans do not take it
+    with pytest.raises(srt.SparseRTError):
+        _plan(w, torch.float32, n_hint=256, executor=3)
