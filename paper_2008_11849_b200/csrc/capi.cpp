@@ -283,7 +283,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->tc_min_density = p.tc_ntiles > 0 || p.tc_min_pct > 0 ? p.tc_min_pct : 0;
   out->tc_row_blocks = p.tc_nrb;
   out->tc_tiles = p.tc_ntiles;
-  out->tc_panel_steps = (int64_t)(p.tcp_steps.size() / srt::kTcpStepBytes);
+  out->tc_panel_steps = p.tcp_nsteps;
   out->tc_nnz = p.tc_nnz;
   return ok();
 }

@@ -783,10 +783,10 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     int64_t nsteps = 0;
     for (int32_t G = 0; G < ngroups; ++G)
     for (int32_t c = 0; c < p.tcp_nchunks; ++c) {
-      const int64_t blk0 = nsteps;
+      const int64_t blk0 = (int64_t)p.tcp_steps.size();
       for (int32_t pi = 0; pi < kTcpPanels; ++pi) {
         const int32_t q = G * kTcpPanels + pi;
-        p.tcp_step_off[((size_t)G * p.tcp_nchunks + c) * (kTcpPanels + 1) + pi] = (int32_t)nsteps;
+        p.tcp_step_off[((size_t)G * p.tcp_nchunks + c) * (kTcpPanels + 1) + pi] = (int32_t)p.tcp_steps.size();
         if (q >= p.tcp_npanels) continue;
         int32_t* cur = cursor_all.data() + (size_t)q * 16;
       {
@@ -865,12 +865,10 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
             slot[j] &= 255;
           }
           auto wv = [&](int i, int j) -> uint16_t { return real[j] ? wd[(size_t)i * KC + slot[j]] : (uint16_t)0; };
-          const size_t off = p.tcp_steps.size();
-          p.tcp_steps.resize(off + kTcpStepBytes, 0);
-          uint16_t* a = (uint16_t*)(p.tcp_steps.data() + off);
+          uint16_t fr[32][8];  // A fragment, lane l = 4 g + t
           for (int l = 0; l < 32; ++l) {
             const int g = l / 4, t = l % 4;
-            uint16_t* f = a + l * 8;
+            uint16_t* f = fr[l];
             f[0] = wv(g, 2 * t);
             f[1] = wv(g, 2 * t + 1);
             f[2] = wv(g + 8, 2 * t);
@@ -880,15 +878,43 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
             f[6] = wv(g + 8, 2 * t + 8);
             f[7] = wv(g + 8, 2 * t + 9);
           }
-          uint8_t* idx = p.tcp_steps.data() + off + 512;
-          for (int j = 0; j < 16; ++j) idx[j] = (uint8_t)slot[j];
+          const size_t off = p.tcp_steps.size();
+          if (SRT_TCP_PACK) {
+            // packed step: [0, 16) slot rows | [16, 48) per-lane mask of nonzero fragment
+            // halves | [48, 80) per-lane count of values before the lane | [80, 82) record
+            // bytes | [96, ...) the nonzero halves, lane-major (~12 % of the 256)
+            std::vector<uint16_t> vals;
+            uint8_t hdr[96] = {0};
+            for (int l = 0; l < 32; ++l) {
+              uint8_t m = 0;
+              hdr[48 + l] = (uint8_t)vals.size();
+              for (int i = 0; i < 8; ++i)
+                if (fr[l][i]) {
+                  m |= (uint8_t)(1u << i);
+                  vals.push_back(fr[l][i]);
+                }
+              hdr[16 + l] = m;
+            }
+            for (int j = 0; j < 16; ++j) hdr[j] = (uint8_t)slot[j];
+            const uint16_t rec = (uint16_t)(96 + ((vals.size() * 2 + 15) & ~(size_t)15));
+            std::memcpy(hdr + 80, &rec, 2);
+            p.tcp_steps.resize(off + rec, 0);
+            std::memcpy(p.tcp_steps.data() + off, hdr, 96);
+            if (!vals.empty()) std::memcpy(p.tcp_steps.data() + off + 96, vals.data(), vals.size() * 2);
+          } else {
+            p.tcp_steps.resize(off + kTcpStepBytes, 0);
+            std::memcpy(p.tcp_steps.data() + off, fr, 512);
+            uint8_t* idx = p.tcp_steps.data() + off + 512;
+            for (int j = 0; j < 16; ++j) idx[j] = (uint8_t)slot[j];
+          }
           ++nsteps;
         }
       }
       }
-      p.tcp_step_off[((size_t)G * p.tcp_nchunks + c) * (kTcpPanels + 1) + kTcpPanels] = (int32_t)nsteps;
-      p.tcp_max_blk = std::max<int32_t>(p.tcp_max_blk, (int32_t)((nsteps - blk0) * kTcpStepBytes));
+      p.tcp_step_off[((size_t)G * p.tcp_nchunks + c) * (kTcpPanels + 1) + kTcpPanels] = (int32_t)p.tcp_steps.size();
+      p.tcp_max_blk = std::max<int32_t>(p.tcp_max_blk, (int32_t)(p.tcp_steps.size() - blk0));
     }
+    p.tcp_nsteps = nsteps;
     p.executor = 3;
     p.plan_bytes += (int64_t)p.tcp_steps.size() + (int64_t)p.tcp_step_off.size() * 4;
   } else if (o.executor != 0) {

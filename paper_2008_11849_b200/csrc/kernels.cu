@@ -1679,7 +1679,7 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
   if (cy > 1) cluster_sync_all();  // every CTA's barriers exist before multicasts arrive
   auto nbytes = [&](int c) -> uint32_t {
     const int o0 = __ldg(offs + c * (kTcpPanels + 1)), o1 = __ldg(offs + c * (kTcpPanels + 1) + kTcpPanels);
-    return (uint32_t)(o1 - o0) * (uint32_t)kTcpStepBytes;
+    return (uint32_t)(o1 - o0);  // byte offsets
   };
   auto load_a = [&](int c) {  // the group's steps of chunk c -> slot (multicast when cy > 1)
     const int slot = c % a.stages;
@@ -1687,7 +1687,7 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
     if (!nb) return;
     const int o0 = __ldg(offs + c * (kTcpPanels + 1));
     const uint32_t dst = smem_u32(sbase + (size_t)slot * a.stage_bytes + XST), fb = full0 + 8 * slot;
-    const uint8_t* src = a.steps + (int64_t)o0 * kTcpStepBytes;
+    const uint8_t* src = a.steps + o0;
     if (cy > 1)
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
@@ -1741,15 +1741,47 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
     if (active) {
       const int* oc = offs + c * (kTcpPanels + 1);
       const int o0 = __ldg(oc), s0 = __ldg(oc + warp), s1 = __ldg(oc + warp + 1);
-      const uint8_t* sp = sbase + (size_t)slot * a.stage_bytes + XST + (size_t)(s0 - o0) * kTcpStepBytes;
-      uint4 av = s0 < s1 ? *(const uint4*)(sp + lane * 16) : make_uint4(0, 0, 0, 0);
-      int kr = s0 < s1 ? (int)sp[512 + lslot] : 0;
+      const uint8_t* sp = sbase + (size_t)slot * a.stage_bytes + XST + (s0 - o0);
+      const uint8_t* se = sp + (s1 - s0);
+#if SRT_TCP_PACK
+      // packed steps (-DSRT_TCP_PACK=1, exact-tested): each lane rebuilds its 8 fragment halves
+      // from its mask and the lane-major nonzero values (~31 of 256 per step): 3.3x fewer plan
+      // bytes to stream from L2, but the decode chain (header -> values -> mma) measured
+      // 1.4-1.6x slower than the dense fragment; off by default
 #pragma unroll 1
-      for (int s = s0; s < s1; ++s) {
+      while (sp < se) {
+        const int kr = (int)sp[lslot];
+        const uint32_t m = sp[16 + lane];
+        const uint16_t* vals = (const uint16_t*)(sp + 96) + sp[48 + lane];
+        const uint32_t rec = *(const uint16_t*)(sp + 80);
+        uint32_t bcur[NTT / 2][4];
+        load_b(st, kr, bcur);
+        uint32_t hv[8];
+        int k = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const bool on = (m >> i) & 1u;
+          hv[i] = on ? (uint32_t)vals[k] : 0u;
+          k += on ? 1 : 0;
+        }
+        const uint4 av = make_uint4(hv[0] | (hv[1] << 16), hv[2] | (hv[3] << 16), hv[4] | (hv[5] << 16),
+                                    hv[6] | (hv[7] << 16));
+#pragma unroll
+        for (int j = 0; j < NTT / 2; ++j) {
+          mma16816(acc[2 * j], av, bcur[j][0], bcur[j][1]);
+          mma16816(acc[2 * j + 1], av, bcur[j][2], bcur[j][3]);
+        }
+        sp += rec;
+      }
+#else
+      uint4 av = sp < se ? *(const uint4*)(sp + lane * 16) : make_uint4(0, 0, 0, 0);
+      int kr = sp < se ? (int)sp[512 + lslot] : 0;
+#pragma unroll 1
+      for (; sp < se; sp += kTcpStepBytes) {
         // prefetch the next step's A fragment and slot row (shared memory)
         uint4 an = av;
         int kn = kr;
-        if (s + 1 < s1) {
+        if (sp + kTcpStepBytes < se) {
           an = *(const uint4*)(sp + kTcpStepBytes + lane * 16);
           kn = (int)sp[kTcpStepBytes + 512 + lslot];
         }
@@ -1762,8 +1794,8 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
         }
         av = an;
         kr = kn;
-        sp += kTcpStepBytes;
       }
+#endif
     }
     __syncwarp();
     uint32_t old = 0;

@@ -151,10 +151,12 @@ struct Plan {
 
   // Condensed-panel tensor-core executor (executor = 3; fp16 SpMM): panel q =
   // rows 16 q .. 16 q + 15 (group G = q / kTcpPanels, i = q % kTcpPanels); chunk c = K rows
-  // kTcpKc c ..; its steps are [off[(G nch + c)(kTcpPanels + 1) + i], ... + i + 1) of
-  // kTcpStepBytes each = mma A fragment (32 lanes x 8 fp16) of W[16 rows x 16 union slots] +
-  // the 16 slot rows (uint8 k_local, padded to 16 bytes); one group's chunk is contiguous
+  // kTcpKc c ..; its steps are the bytes [off[(G nch + c)(kTcpPanels + 1) + i], ... + i + 1)
+  // of tcp_steps; one step = the mma A fragment (32 lanes x 8 fp16) of W[16 rows x 16 union
+  // slots] + the 16 slot rows (uint8 k_local): packed (SRT_TCP_PACK, inspector.cpp: per-lane
+  // masks + the nonzero halves) or dense (kTcpStepBytes); one group's chunk is contiguous
   int32_t tcp_npanels = 0, tcp_nchunks = 0, tcp_max_blk = 0;
+  int64_t tcp_nsteps = 0;
   std::vector<int32_t> tcp_step_off;
   std::vector<uint8_t> tcp_steps;
   const int32_t* d_tcp_step_off = nullptr;
@@ -168,7 +170,10 @@ constexpr int kTcpKc = 64;          // K rows per staged chunk (one 128-byte swi
 #define SRT_TCP_STRICT 1
 #endif
 constexpr int kTcpPanels = SRT_TCP_PANELS;  // panels (warps) per CTA
-constexpr int kTcpStepBytes = 528;  // 512 B A fragment + 16 B slot rows
+constexpr int kTcpStepBytes = 528;  // dense step: 512 B A fragment + 16 B slot rows
+#ifndef SRT_TCP_PACK
+#define SRT_TCP_PACK 0
+#endif
 
 struct BuildOpts {
   int32_t kind = 0, c_in = 0, h = 0, w = 0;
