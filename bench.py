@@ -439,7 +439,18 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max = float(t.item())
     value = flops_step * world * args.steps / (total_ms_max * 1e-3) / 1e9
-    launches = args.steps * nl
+    # kernels per layer call: the executor, + the device repack of an X whose row stride is
+    # not 16-byte aligned (N = 49 ...), + the tensor-core sub-block kernel when the plan has
+    # dense tiles; TMA-fed conv: the input pre-pass + the conv kernel
+    def kernels_per_call(i):
+        info = plans[i][0].info
+        if layers[i]["kind"] != "spmm":
+            return 2 if info["conv_kernel"] == 2 else 1
+        X = xs[i]
+        unaligned = (X.data_ptr() % 16) != 0 or (X.stride(0) * X.element_size()) % 16 != 0
+        return 1 + int(unaligned) + int(info["tc_tiles"] > 0)
+
+    launches = args.steps * sum(kernels_per_call(i) for i in range(nl))
 
     # ---------------- roofline of the dominant kernel (longest layer)
     peaks = load_peaks()
