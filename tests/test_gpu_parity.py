@@ -611,8 +611,9 @@ def test_tcp_rel_l2(M, K, N, p):
 
 
 @pytest.mark.parametrize("case", [(64, 256, 3136), (512, 2048, 49), (2048, 512, 392), (1024, 1024, 1568),
-                                  (3072, 768, 512), (768, 3072, 512), (17, 70, 33)])
-@pytest.mark.parametrize("p", [90, 98])
+                                  (3072, 768, 512), (768, 3072, 512), (17, 70, 33), (40, 300, 1),
+                                  (48, 128, 8), (16, 64, 4099)])
+@pytest.mark.parametrize("p", [0, 50, 90, 98])
 def test_tcp_integer_exact(case, p):
     # integer data: every fp32 partial sum is exact, so the tensor-core path (any summation
     # order inside the mma) must equal the RN-even fp16 rounding of the exact result
