@@ -179,6 +179,16 @@ int sparse_spmm_ex(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, vo
 int sparse_conv3x3_ex(sparse_plan_t plan, int64_t batch, const void* x, void* y,
                       const sparse_epilogue* ep, sparse_stream_t stream);
 
+/* Token-major layout (NEXT #4; the PyTorch nn.Linear convention, e.g. BERT activations):
+ *   Y[N x M] = X[N x K] * W^T        X, Y row-major (features contiguous), ldx >= K, ldy >= M
+ * i.e. the same product as sparse_spmm on the transposed operands.  Implemented as a tiled
+ * device transpose of X into a stream-ordered scratch (K x N), sparse_spmm, and a tiled
+ * transpose of the result into Y - two extra passes over X and Y in HBM, never a host copy.
+ * Results are bitwise those of sparse_spmm on X^T.  N == 0 is a no-op.  Errors as sparse_spmm
+ * (+ ENOMEM when the scratch cannot be allocated). */
+int sparse_linear(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                  sparse_stream_t stream);
+
 /* Free the plan and its device memory (north-star name).  Must not race with
  * work still enqueued that uses the plan.  NULL is a no-op. */
 int plan_destroy(sparse_plan_t plan);

@@ -9,4 +9,5 @@ from .sparsert import (  # noqa: F401
     SPARSE_CONV3X3, SPARSE_DEVICE_HOST_ONLY, SPARSE_F16, SPARSE_F32, SPARSE_SPMM, Plan,
     SparseRTError, lib, plan_destroy, sparse_conv3x3, sparse_plan_create, sparse_plan_dump,
     sparse_plan_info, sparse_spmm, version, sparse_spmm_ex, sparse_conv3x3_ex, sparse_epilogue,
+    sparse_linear,
 )

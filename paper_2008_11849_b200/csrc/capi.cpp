@@ -201,6 +201,43 @@ int sparse_spmm_ex(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, vo
   return spmm_impl(plan, N, X, ldx, Y, ldy, ep, stream);
 }
 
+int sparse_linear(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                  sparse_stream_t stream) {
+  if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
+  if (plan->p.kind != SPARSE_SPMM) return fail(SPARSE_EINVAL, "sparse_linear on a conv plan");
+  if (plan->host_only) return fail(SPARSE_EINVAL, "host-only plan cannot compute");
+  if (N < 0) return fail(SPARSE_EINVAL, "N < 0");
+  if (N == 0) return ok();
+  if (!X || !Y) return fail(SPARSE_EINVAL, "X or Y is NULL");
+  const srt::Plan& p = plan->p;
+  if (ldx < p.K || ldy < p.M) return fail(SPARSE_EINVAL, "ldx must be >= K and ldy >= M");
+  const int S = p.dtype == SPARSE_F16 ? 2 : 4;
+  const int64_t ldt = (N + 15) / 16 * 16;  // 16-byte aligned rows for the TMA paths (S <= 4)
+  void* Xt = nullptr;
+  void* Yt = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMallocAsync(&Xt, (size_t)(p.K * ldt * S), st) != cudaSuccess ||
+      cudaMallocAsync(&Yt, (size_t)(p.M * ldt * S), st) != cudaSuccess) {
+    cudaGetLastError();
+    if (Xt) cudaFreeAsync(Xt, st);
+    return fail(SPARSE_ENOMEM, "sparse_linear: cannot allocate the transposed scratch");
+  }
+  std::string err;
+  int rc = srt::launch_transpose(p.device, S, X, ldx, Xt, ldt, N, p.K, stream, err);  // Xt = X^T (K x N)
+  if (rc == SPARSE_OK) {
+    const int r2 = sparse_spmm(plan, N, Xt, ldt, Yt, ldt, stream);
+    if (r2 != SPARSE_OK) {
+      cudaFreeAsync(Xt, st);
+      cudaFreeAsync(Yt, st);
+      return r2;  // sparse_spmm set the error detail
+    }
+    rc = srt::launch_transpose(p.device, S, Yt, ldt, Y, ldy, p.M, N, stream, err);  // Y = Yt^T (N x M)
+  }
+  cudaFreeAsync(Xt, st);
+  cudaFreeAsync(Yt, st);
+  return rc == SPARSE_OK ? ok() : fail(rc, err);
+}
+
 static int conv_impl(sparse_plan_t plan, int64_t batch, const void* x, void* y,
                      const sparse_epilogue* e, sparse_stream_t stream) {
   if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");

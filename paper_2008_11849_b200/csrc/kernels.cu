@@ -1501,6 +1501,44 @@ int launch_repack(int device, int64_t K, int64_t N, int S, const void* X, int64_
   return SPARSE_OK;
 }
 
+// Tiled transpose out[c][r] = in[r][c] (rows x cols, leading dims in elements), 32 x 32 tiles
+// through shared memory (padded: conflict-free), element size 2 or 4 bytes.  Pure data movement
+// for the token-major entry point sparse_linear.
+template <typename T>
+__global__ void transpose_2d(const T* __restrict__ in, int64_t ldi, T* __restrict__ out, int64_t ldo,
+                             int64_t rows, int64_t cols) {
+  __shared__ T tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * ldi + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * ldo + r] = tile[threadIdx.x][i];
+  }
+}
+
+int launch_transpose(int device, int S, const void* in, int64_t ldi, void* out, int64_t ldo, int64_t rows,
+                     int64_t cols, void* stream, std::string& err) {
+  DeviceGuard dg(device);
+  if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
+  for (int64_t rb = 0; rb < rows; rb += 32 * 65535) {  // grid.y limit
+    const int64_t rr = std::min<int64_t>(rows - rb, 32 * 65535);
+    const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rr + 31) / 32)), block(32, 8);
+    if (S == 2)
+      transpose_2d<uint16_t><<<grid, block, 0, (cudaStream_t)stream>>>((const uint16_t*)in + rb * ldi, ldi,
+                                                                       (uint16_t*)out + rb, ldo, rr, cols);
+    else
+      transpose_2d<float><<<grid, block, 0, (cudaStream_t)stream>>>((const float*)in + rb * ldi, ldi,
+                                                                    (float*)out + rb, ldo, rr, cols);
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "transpose launch", err);
+  return SPARSE_OK;
+}
+
 void free_repack(int device, void* Xp, void* stream) {
   DeviceGuard dg(device);
   cudaFreeAsync(Xp, (cudaStream_t)stream);

@@ -28,7 +28,7 @@ STATUS_NAMES = {0: "SPARSE_OK", 1: "SPARSE_EINVAL", 2: "SPARSE_EMATRIX", 3: "SPA
 
 # every symbol include/sparsert.h declares (checked by tests/test_capi_host.py)
 EXPORTED = ["sparse_plan_opts_init", "sparse_plan_create", "sparse_spmm", "sparse_conv3x3",
-            "sparse_spmm_ex", "sparse_conv3x3_ex",
+            "sparse_spmm_ex", "sparse_conv3x3_ex", "sparse_linear",
             "plan_destroy", "sparse_plan_destroy", "sparse_plan_info", "sparse_plan_dump",
             "sparse_last_error", "sparse_version"]
 
@@ -93,6 +93,7 @@ def _load() -> ctypes.CDLL:
     lib.sparse_spmm.argtypes = [P, i64, P, i64, P, i64, P]
     lib.sparse_spmm.restype = ctypes.c_int
     lib.sparse_conv3x3.argtypes = [P, i64, P, P, P]
+    lib.sparse_linear.argtypes = [P, i64, P, i64, P, i64, P]
     lib.sparse_conv3x3.restype = ctypes.c_int
     lib.sparse_spmm_ex.argtypes = [P, i64, P, i64, P, i64, ctypes.POINTER(sparse_epilogue), P]
     lib.sparse_spmm_ex.restype = ctypes.c_int
@@ -148,6 +149,10 @@ def sparse_plan_create(M, K, row_ptr, col_idx, values, dtype=SPARSE_F32, **opts)
 
 def sparse_spmm(plan, N, X_ptr, ldx, Y_ptr, ldy, stream=0):
     _check(lib.sparse_spmm(plan, int(N), X_ptr, int(ldx), Y_ptr, int(ldy), stream))
+
+
+def sparse_linear(plan, N, X_ptr, ldx, Y_ptr, ldy, stream=0):
+    _check(lib.sparse_linear(plan, int(N), X_ptr, int(ldx), Y_ptr, int(ldy), stream))
 
 
 def sparse_conv3x3(plan, batch, x_ptr, y_ptr, stream=0):
@@ -317,6 +322,25 @@ class Plan:
         else:
             sparse_spmm_ex(self._h, N, ctypes.c_void_p(X.data_ptr()), max(ldx, N),
                            ctypes.c_void_p(Y.data_ptr()), max(ldy, N), ep, ctypes.c_void_p(s))
+        return Y
+
+    def linear(self, X, Y=None, stream=None):
+        """Token-major layout (nn.Linear): Y (N, M) = X (N, K) @ W^T, rows contiguous."""
+        import torch
+        if self.kind != SPARSE_SPMM:
+            raise ValueError("linear on a conv plan")
+        self._check_tensor(X, "X")
+        if X.dim() != 2 or X.shape[1] != self.K or (self.K > 1 and X.stride(1) != 1):
+            raise ValueError("X must be (N, K) with unit column stride")
+        N = X.shape[0]
+        if Y is None:
+            Y = torch.empty((N, self.M), dtype=self.dtype, device=X.device)
+        self._check_tensor(Y, "Y")
+        if Y.dim() != 2 or Y.shape != (N, self.M) or (self.M > 1 and Y.stride(1) != 1):
+            raise ValueError("Y must be (N, M) with unit column stride")
+        s = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        sparse_linear(self._h, N, ctypes.c_void_p(X.data_ptr()), max(X.stride(0), self.K),
+                      ctypes.c_void_p(Y.data_ptr()), max(Y.stride(0), self.M), ctypes.c_void_p(s))
         return Y
 
     def conv3x3(self, x, y=None, stream=None, bias=None, beta=0.0, relu=False):

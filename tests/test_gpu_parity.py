@@ -644,3 +644,30 @@ def test_tcp_closed_forms_and_epilogue():
     torch.cuda.synchronize()
     ref = np.maximum(_ref(w, Xi, True) + bias[:, None] + 0.5 * Y0, 0.0)
     assert np.array_equal(Y.double().cpu().numpy(), _f16_round(ref))
+
+
+# --------------------------------------------------------------------------- token-major layout
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("M,K,N,ex", [(3072, 768, 512, 0), (768, 3072, 333, 0), (77, 1111, 49, 0),
+                                      (300, 200, 1, 0), (3072, 768, 512, 3)])
+def test_linear_token_major(M, K, N, ex, f16):
+    # sparse_linear (nn.Linear layout): Y (N, M) = X (N, K) @ W^T, bitwise equal to sparse_spmm on
+    # X^T (the transposes are pure data movement), and exact on integer data
+    if ex == 3 and not f16:
+        pytest.skip("tensor-core panels are fp16 only")
+    dev = _dev()
+    vmax_w, vmax_x = (2, 4) if f16 else (3, 3)
+    w = gen.int_weights(M, K, 90, seed=M + N, vmax=vmax_w)
+    Xkn = gen.int_x(K, N, seed=K, vmax=vmax_x)
+    plan = srt.Plan.from_csr(w, dtype=_tdt(f16), n_hint=N, executor=ex)
+    Xt = torch.from_numpy(np.ascontiguousarray(Xkn.T)).to(dev).to(_tdt(f16))
+    Y = plan.linear(Xt)
+    Yref = plan.spmm(Xt.t().contiguous())
+    torch.cuda.synchronize()
+    assert Y.shape == (N, M)
+    assert torch.equal(Y, Yref.t())
+    ref = _ref(w, Xkn, f16)
+    if f16:
+        ref = _f16_round(ref)
+    assert np.array_equal(Y.double().cpu().numpy(), ref.T)
