@@ -240,7 +240,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="rn50_b8",
                     choices=["rn50_b8", "rn50_b1", "mbv1_b32", "bert", "conv", "tiny"])
-    ap.add_argument("--dtype", default="f32", choices=["f32", "f16"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f16", "bf16"])
     ap.add_argument("--sparsity", type=int, default=90)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
@@ -272,8 +272,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    tdt = torch.float16 if args.dtype == "f16" else torch.float32
-    S = 2 if args.dtype == "f16" else 4
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16}.get(args.dtype, torch.float32)
+    S = 2 if args.dtype in ("f16", "bf16") else 4
 
     layers, scaling, desc = workload_layers(args.workload, args.sparsity, world)
     plans, xs, ys, host = [], [], [], []
@@ -508,10 +508,10 @@ def main():
     pi = plans[dom][0].info
     Ld = layers[dom]
     xb = S * (Ld["K"] if Ld["kind"] == "spmm" else Ld["c_in"]) * d["N"]
-    t_smem = 2 * d["nnz"] * d["N"] / (alu * 1e9 * (0.5 if args.dtype == "f16" else 0.25))
+    t_smem = 2 * d["nnz"] * d["N"] / (alu * 1e9 * (0.5 if S == 2 else 0.25))
     t_l2 = pi["panels"] * xb / 4.7e12
     t_ceil = max(t_smem, t_l2, max(d["alg_bytes"] / (peaks["hbm_gbs"] * 1e9), 0.0))
-    roof["design_ceiling"] = {"smem_fma_frac_max": 0.5 if args.dtype == "f16" else 0.25,
+    roof["design_ceiling"] = {"smem_fma_frac_max": 0.5 if S == 2 else 0.25,
                               "t_smem_us": t_smem * 1e6, "t_l2_reread_us": t_l2 * 1e6,
                               "frac_of_design_ceiling": t_ceil / (d["ms"] * 1e-3)}
 
@@ -603,7 +603,10 @@ def main():
         torch.backends.cudnn.benchmark = True
         # fp32 dense context = true fp32 (SGEMM / fp32 cuDNN conv, TF32 off), the paper's
         # cuBLAS / cuDNN fp32 baselines; fp16 = tensor cores
-        for label, ddt, tf32 in [("fp32_sgemm", torch.float32, False), ("fp16_tc", torch.float16, False)]:
+        ctx = [("fp32_sgemm", torch.float32, False), ("fp16_tc", torch.float16, False)]
+        if args.dtype == "bf16":
+            ctx.append(("bf16_tc", torch.bfloat16, False))
+        for label, ddt, tf32 in ctx:
             torch.backends.cuda.matmul.allow_tf32 = tf32
             torch.backends.cudnn.allow_tf32 = tf32
             tot = 0.0

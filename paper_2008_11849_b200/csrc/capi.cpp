@@ -170,7 +170,7 @@ static int spmm_impl(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, 
   }
   std::string err;
   const srt::Plan& p = plan->p;
-  const int S = p.dtype == SPARSE_F16 ? 2 : 4;
+  const int S = p.dtype != SPARSE_F32 ? 2 : 4;
   const void* Xa = X;
   int64_t lda = ldx;
   void* scratch = nullptr;
@@ -211,7 +211,7 @@ int sparse_linear(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, voi
   if (!X || !Y) return fail(SPARSE_EINVAL, "X or Y is NULL");
   const srt::Plan& p = plan->p;
   if (ldx < p.K || ldy < p.M) return fail(SPARSE_EINVAL, "ldx must be >= K and ldy >= M");
-  const int S = p.dtype == SPARSE_F16 ? 2 : 4;
+  const int S = p.dtype != SPARSE_F32 ? 2 : 4;
   const int64_t ldt = (N + 15) / 16 * 16;  // 16-byte aligned rows for the TMA paths (S <= 4)
   void* Xt = nullptr;
   void* Yt = nullptr;
@@ -330,7 +330,8 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
   if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
   const srt::Plan& p = plan->p;
   if (cap < p.nnz) return fail(SPARSE_EINVAL, "cap < nnz");
-  const bool f16 = p.dtype == SPARSE_F16;
+  const bool f16 = p.dtype != SPARSE_F32;  // 16-bit entries (fp16 or bf16 values)
+  const bool bf = p.dtype == SPARSE_BF16;
   const int A = p.entry_align;
   int64_t out = 0;
   auto emit = [&](int32_t m, int32_t k, float w, int32_t q, int32_t c, int32_t s, int32_t g) {
@@ -366,7 +367,12 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
                 std::memcpy(&a, rec, 2);
                 std::memcpy(&wh, rec + 2, 2);
                 xoff = (int64_t)a * 16;
-                w = srt::f16_to_f32(wh);
+                if (bf) {
+                  const uint32_t b = (uint32_t)wh << 16;
+                  std::memcpy(&w, &b, 4);
+                } else {
+                  w = srt::f16_to_f32(wh);
+                }
               } else {
                 uint32_t a;
                 std::memcpy(&a, rec, 4);

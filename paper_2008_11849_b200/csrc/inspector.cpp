@@ -114,9 +114,14 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     err = "M and K must be >= 1 and nnz >= 0";
     return SPARSE_EINVAL;
   }
-  if (dtype != SPARSE_F32 && dtype != SPARSE_F16) {
-    err = "dtype must be SPARSE_F32 or SPARSE_F16";
+  if (dtype != SPARSE_F32 && dtype != SPARSE_F16 && dtype != SPARSE_BF16) {
+    err = "dtype must be SPARSE_F32, SPARSE_F16 or SPARSE_BF16";
     return SPARSE_EINVAL;
+  }
+  if (dtype == SPARSE_BF16 && (o.kind != SPARSE_SPMM || o.executor == 1 || o.executor == 3 || o.tm)) {
+    err = "bf16 plans: SpMM on the plan-driven CUDA-core kernels only (no conv / JIT / tensor-core "
+          "panels / TMEM X source)";
+    return SPARSE_EUNSUPPORTED;
   }
   if (o.kind != SPARSE_SPMM && o.kind != SPARSE_CONV3X3) {
     err = "kind must be SPARSE_SPMM or SPARSE_CONV3X3";
@@ -201,6 +206,19 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
           return SPARSE_EMATRIX;
         }
         wv = f16_to_f32(wh);
+      } else if (dtype == SPARSE_BF16) {
+        uint32_t u;
+        std::memcpy(&u, &v, 4);
+        u += 0x7fffu + ((u >> 16) & 1u);  // round to nearest even (v finite)
+        wh = (uint16_t)(u >> 16);
+        if ((wh & 0x7f80u) == 0x7f80u) {
+          snprintf(buf, sizeof buf, "row %d: value %g overflows bf16 at %d", m, (double)v,
+                   e - row_ptr[m]);
+          err = buf;
+          return SPARSE_EMATRIX;
+        }
+        const uint32_t b = (uint32_t)wh << 16;
+        std::memcpy(&wv, &b, 4);
       }
       if (wv == 0.0f) {
         if (o.drop_zeros) continue;
@@ -296,7 +314,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     p.ws_row.swap(ws_row);
   }
   p.n_hint = o.n_hint;
-  const bool f16 = dtype == SPARSE_F16;
+  const bool f16 = dtype != SPARSE_F32;  // 16-bit storage (fp16 or bf16)
   const int S = f16 ? 2 : 4;
   p.entry_bytes = f16 ? 4 : 8;
 

@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -151,11 +152,18 @@ __device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* 
 __device__ __forceinline__ void fma_h(float& acc, uint16_t w, uint16_t x) {
   asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(w), "h"(x));
 }
+template <bool BF = false>
 __device__ __forceinline__ void fma_h2(float& a0, float& a1, uint16_t w, uint32_t x2) {
-  asm("{\n\t.reg .b16 xl, xh;\n\tmov.b32 {xl, xh}, %3;\n\t"
-      "fma.rn.f32.f16 %0, %2, xl, %0;\n\tfma.rn.f32.f16 %1, %2, xh, %1;\n\t}"
-      : "+f"(a0), "+f"(a1)
-      : "h"(w), "r"(x2));
+  if (BF)  // bfloat16 inputs (SASS FHFMA.BF16), fp32 accumulate
+    asm("{\n\t.reg .b16 xl, xh;\n\tmov.b32 {xl, xh}, %3;\n\t"
+        "fma.rn.f32.bf16 %0, %2, xl, %0;\n\tfma.rn.f32.bf16 %1, %2, xh, %1;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "h"(w), "r"(x2));
+  else
+    asm("{\n\t.reg .b16 xl, xh;\n\tmov.b32 {xl, xh}, %3;\n\t"
+        "fma.rn.f32.f16 %0, %2, xl, %0;\n\tfma.rn.f32.f16 %1, %2, xh, %1;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "h"(w), "r"(x2));
 }
 
 // Inner loop of Alg. 3 for one thread group, one row and one staged chunk: `cnt`
@@ -170,19 +178,31 @@ __device__ __forceinline__ void fma4(float (&acc)[4], uint32_t wbits, const floa
   acc[2] = fmaf(w, x.z, acc[2]);
   acc[3] = fmaf(w, x.w, acc[3]);
 }
+template <bool BF = false>
 __device__ __forceinline__ void fma8h(float (&acc)[8], uint32_t en, const uint4 xv) {
   const uint16_t w = (uint16_t)(en >> 16);
-  fma_h2(acc[0], acc[1], w, xv.x);
-  fma_h2(acc[2], acc[3], w, xv.y);
-  fma_h2(acc[4], acc[5], w, xv.z);
-  fma_h2(acc[6], acc[7], w, xv.w);
+  fma_h2<BF>(acc[0], acc[1], w, xv.x);
+  fma_h2<BF>(acc[2], acc[3], w, xv.y);
+  fma_h2<BF>(acc[4], acc[5], w, xv.z);
+  fma_h2<BF>(acc[6], acc[7], w, xv.w);
+}
+// fp32 -> 16-bit output bits, round to nearest even (fp16 or bf16)
+template <bool BF>
+__device__ __forceinline__ uint16_t to16(float v) {
+  if (BF) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  return __half_as_ushort(__float2half_rn(v));
+}
+template <bool BF>
+__device__ __forceinline__ float from16(const void* p) {
+  if (BF) return __bfloat162float(*(const __nv_bfloat16*)p);
+  return __half2float(*(const __half*)p);
 }
 
-template <bool F16>
+template <bool F16, bool BF = false>
 struct EntryOps;
 
 template <>
-struct EntryOps<false> {  // unit = 2 x {uint32 xoff (bytes), float w}
+struct EntryOps<false, false> {  // unit = 2 x {uint32 xoff (bytes), float w}
   static constexpr int C = 4;
   __device__ __forceinline__ static void unit(float (&acc)[4], const uint4 p, const uint8_t* xs) {
     const float4 x0 = *(const float4*)(xs + p.x);
@@ -192,8 +212,8 @@ struct EntryOps<false> {  // unit = 2 x {uint32 xoff (bytes), float w}
   }
 };
 
-template <>
-struct EntryOps<true> {  // unit = 4 x {uint16 xoff (16-byte units), half w}
+template <bool BF>
+struct EntryOps<true, BF> {  // unit = 4 x {uint16 xoff (16-byte units), half / bf16 w}
   static constexpr int C = 8;
   __device__ __forceinline__ static const uint8_t* xrow(const uint8_t* xs, uint32_t en) {
     return xs + ((en & 0xffffu) << 4);
@@ -203,10 +223,10 @@ struct EntryOps<true> {  // unit = 4 x {uint16 xoff (16-byte units), half w}
     const uint4 x1 = *(const uint4*)xrow(xs, q.y);
     const uint4 x2 = *(const uint4*)xrow(xs, q.z);
     const uint4 x3 = *(const uint4*)xrow(xs, q.w);
-    fma8h(acc, q.x, x0);
-    fma8h(acc, q.y, x1);
-    fma8h(acc, q.z, x2);
-    fma8h(acc, q.w, x3);
+    fma8h<BF>(acc, q.x, x0);
+    fma8h<BF>(acc, q.y, x1);
+    fma8h<BF>(acc, q.z, x2);
+    fma8h<BF>(acc, q.w, x3);
   }
 };
 
@@ -224,10 +244,10 @@ struct EntryOps<true> {  // unit = 4 x {uint16 xoff (16-byte units), half w}
 #ifndef SRT_TAILMERGE
 #define SRT_TAILMERGE 1
 #endif
-template <bool F16>
+template <bool F16, bool BF = false>
 __device__ __forceinline__ void run_one_row(float (&acc)[F16 ? 8 : 4], const uint4* up, int u, int cnt,
                                             const uint8_t* xs) {
-  using E = EntryOps<F16>;
+  using E = EntryOps<F16, BF>;
 #pragma unroll 1
   for (; u + 2 <= cnt; u += 2) {
     const uint4 q0 = up[u], q1 = up[u + 1];
@@ -237,13 +257,13 @@ __device__ __forceinline__ void run_one_row(float (&acc)[F16 ? 8 : 4], const uin
   if (u < cnt) E::unit(acc, up[u], xs);
 }
 
-template <bool F16, int R>
+template <bool F16, int R, bool BF = false>
 __device__ __forceinline__ void run_rows(float (&acc)[R][F16 ? 8 : 4], const uint32_t (&h)[R],
                                          const uint4* ents, const uint8_t* xs) {
-  using E = EntryOps<F16>;
+  using E = EntryOps<F16, BF>;
 #if SRT_JOINT == 0
 #pragma unroll
-  for (int r = 0; r < R; ++r) run_one_row<F16>(acc[r], ents + (h[r] & 0xffffu), 0, (int)(h[r] >> 16), xs);
+  for (int r = 0; r < R; ++r) run_one_row<F16, BF>(acc[r], ents + (h[r] & 0xffffu), 0, (int)(h[r] >> 16), xs);
 #else
   constexpr int P = (SRT_JOINT == 2 && R > 2) ? 2 : R;  // rows walked jointly
 #pragma unroll
@@ -276,7 +296,7 @@ __device__ __forceinline__ void run_rows(float (&acc)[R][F16 ? 8 : 4], const uin
     }
 #pragma unroll
     for (int r = 0; r < P; ++r)
-      run_one_row<F16>(acc[r0 + r], ents + (h[r0 + r] & 0xffffu), mn, (int)(h[r0 + r] >> 16), xs);
+      run_one_row<F16, BF>(acc[r0 + r], ents + (h[r0 + r] & 0xffffu), mn, (int)(h[r0 + r] >> 16), xs);
   }
 #endif
 }
@@ -380,11 +400,11 @@ __device__ __forceinline__ void run_rows_tm(float (&acc)[R][F16 ? 8 : 4], const 
 }
 
 // Fused epilogue on one output value: act(acc + bias[row] + beta * y_old), fp32.
-template <bool F16>
+template <bool F16, bool BF = false>
 __device__ __forceinline__ float epilogue_one(float v, const uint8_t* bias, int row, float beta,
                                               const uint8_t* yold, int relu) {
-  if (bias) v += F16 ? __half2float(((const __half*)bias)[row]) : ((const float*)bias)[row];
-  if (beta != 0.0f) v = fmaf(beta, F16 ? __half2float(*(const __half*)yold) : *(const float*)yold, v);
+  if (bias) v += F16 ? from16<BF>((const uint16_t*)bias + row) : ((const float*)bias)[row];
+  if (beta != 0.0f) v = fmaf(beta, F16 ? from16<BF>(yold) : *(const float*)yold, v);
   if (relu) v = v < 0.0f ? 0.0f : v;
   return v;
 }
@@ -408,7 +428,7 @@ struct SpmmArgs {
   int64_t ldws;
 };
 
-template <int R, int GK, bool F16, bool TM>
+template <int R, int GK, bool F16, bool TM, bool BF = false>
 __global__ void __launch_bounds__(512, SRT_MINB) spmm_kernel(const __grid_constant__ CUtensorMap tmap,
                                                    const SpmmArgs a) {
   constexpr int C = F16 ? 8 : 4;  // columns per lane (16 bytes of X)
@@ -612,18 +632,18 @@ __global__ void __launch_bounds__(512, SRT_MINB) spmm_kernel(const __grid_consta
 #pragma unroll
         for (int c = 0; c < C; ++c)
           if (col + c < ncol)
-            acc[r][c] = epilogue_one<F16>(acc[r][c], a.bias, row, a.beta, yp + c * S, a.relu);
+            acc[r][c] = epilogue_one<F16, BF>(acc[r][c], a.bias, row, a.beta, yp + c * S, a.relu);
       }
       if (F16) {
-        __half h[C];
+        alignas(16) uint16_t h[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) h[c] = __float2half_rn(acc[r][c]);
+        for (int c = 0; c < C; ++c) h[c] = to16<BF>(acc[r][c]);
         if (a.vec_y && col + C <= ncol) {
           *(uint4*)yp = *(const uint4*)h;
         } else {
 #pragma unroll
           for (int c = 0; c < C; ++c)
-            if (col + c < ncol) ((__half*)yp)[c] = h[c];
+            if (col + c < ncol) ((uint16_t*)yp)[c] = h[c];
         }
       } else {
         if (a.vec_y && col + C <= ncol) {
@@ -677,7 +697,7 @@ __global__ void __launch_bounds__(512, SRT_MINB) spmm_kernel(const __grid_consta
         run_rows_tm<F16, R>(acc, h, ents, tq_base + 256u * (uint32_t)(q & 1));
         tm_fence_before();
       } else {
-        run_rows<F16, R>(acc, h, ents, xs);
+        run_rows<F16, R, BF>(acc, h, ents, xs);
       }
       __syncwarp();
       uint32_t old = 0;
@@ -775,22 +795,22 @@ __global__ void __launch_bounds__(512, SRT_MINB) spmm_kernel(const __grid_consta
       if (c4 + 3 < ncol) v.w += wp[3];
     }
     if (a.bias != nullptr || a.beta != 0.0f || a.relu) {
-      if (c4 + 0 < ncol) v.x = epilogue_one<F16>(v.x, a.bias, row, a.beta, yp + 0 * S, a.relu);
-      if (c4 + 1 < ncol) v.y = epilogue_one<F16>(v.y, a.bias, row, a.beta, yp + 1 * S, a.relu);
-      if (c4 + 2 < ncol) v.z = epilogue_one<F16>(v.z, a.bias, row, a.beta, yp + 2 * S, a.relu);
-      if (c4 + 3 < ncol) v.w = epilogue_one<F16>(v.w, a.bias, row, a.beta, yp + 3 * S, a.relu);
+      if (c4 + 0 < ncol) v.x = epilogue_one<F16, BF>(v.x, a.bias, row, a.beta, yp + 0 * S, a.relu);
+      if (c4 + 1 < ncol) v.y = epilogue_one<F16, BF>(v.y, a.bias, row, a.beta, yp + 1 * S, a.relu);
+      if (c4 + 2 < ncol) v.z = epilogue_one<F16, BF>(v.z, a.bias, row, a.beta, yp + 2 * S, a.relu);
+      if (c4 + 3 < ncol) v.w = epilogue_one<F16, BF>(v.w, a.bias, row, a.beta, yp + 3 * S, a.relu);
     }
     const float vv[4] = {v.x, v.y, v.z, v.w};
     if (F16) {
-      __half h[4];
+      alignas(8) uint16_t h[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) h[c] = __float2half_rn(vv[c]);
+      for (int c = 0; c < 4; ++c) h[c] = to16<BF>(vv[c]);
       if (a.vec_y && c4 + 4 <= ncol) {
         *(uint2*)yp = *(const uint2*)h;
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          if (c4 + c < ncol) ((__half*)yp)[c] = h[c];
+          if (c4 + c < ncol) ((uint16_t*)yp)[c] = h[c];
       }
     } else {
       if (a.vec_y && c4 + 4 <= ncol) {
@@ -1368,8 +1388,18 @@ __global__ void __launch_bounds__(128) spmm_tc_kernel(const TcArgs a) {
 using SpmmFn = void (*)(const __grid_constant__ CUtensorMap, const SpmmArgs);
 using ConvFn = void (*)(const ConvArgs);
 
-template <bool F16>
+template <bool F16, bool BF = false>
 static SpmmFn pick_spmm(int R, int GK, bool tm) {
+  if (BF) {  // bf16: CUDA-core kernel, shared-memory X source only
+    if (tm) return nullptr;
+#define SRT_B(RR, GG) \
+  if (R == RR && GK == GG) return spmm_kernel<RR, GG, true, false, true>;
+#define SRT_BR(RR) SRT_B(RR, 1) SRT_B(RR, 2) SRT_B(RR, 4) SRT_B(RR, 8)
+    SRT_BR(1) SRT_BR(2) SRT_BR(4) SRT_BR(8)
+#undef SRT_BR
+#undef SRT_B
+    return nullptr;
+  }
   if (tm) {  // TMEM X source: split_k = 1 only
     if (GK != 1) return nullptr;
     if (R == 1) return spmm_kernel<1, 1, F16, true>;
@@ -1963,9 +1993,10 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
 int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
                 void* stream, std::string& err, const Epilogue& ep) {
   if (p.executor == 3) return launch_tcp(p, N, X, ldx, Y, ldy, stream, err, ep);
-  const bool f16 = p.dtype == SPARSE_F16;
+  const bool f16 = p.dtype != SPARSE_F32;  // 16-bit X / Y (fp16 or bf16: TMA copies the bits)
   const int S = f16 ? 2 : 4;
-  SpmmFn fn = f16 ? pick_spmm<true>(p.R, p.gk, p.tm) : pick_spmm<false>(p.R, p.gk, p.tm);
+  SpmmFn fn = p.dtype == SPARSE_BF16 ? pick_spmm<true, true>(p.R, p.gk, p.tm)
+            : f16 ? pick_spmm<true>(p.R, p.gk, p.tm) : pick_spmm<false>(p.R, p.gk, p.tm);
   if (!fn) {
     err = "internal: no kernel instance for this tile configuration";
     return SPARSE_EINTERNAL;

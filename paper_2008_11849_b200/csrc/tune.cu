@@ -72,7 +72,7 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     return SPARSE_EINVAL;
   }
   const bool f16 = dtype == SPARSE_F16;
-  const int S = f16 ? 2 : 4;
+  const int S = dtype != SPARSE_F32 ? 2 : 4;
   // candidate grid (hand-picked): warps per CTA, rows per warp, pipeline depth,
   // cluster K-split, split-K groups (small N); plus the JIT executor
   std::vector<BuildOpts> cands;
@@ -80,7 +80,7 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     // consumer warps x rows per warp (panel height), K chunk, pipeline depth (stages < 0:
     // the inspector fills a shared-memory budget, -1 = one CTA per SM, -2 = two), cluster
     // K-split (N <= 4096), split-K groups (N <= 512)
-    const int C = f16 ? 8 : 4;
+    const int C = S == 2 ? 8 : 4;
     const int64_t N = base.n_hint;
     const bool small = N <= 512, medium = N <= 4096;
     for (int w : {8, 16})
@@ -173,7 +173,7 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   cudaEventCreate(&ev[0]);
   cudaEventCreate(&ev[1]);
-  fill_uniform<<<1024, 256, 0, st>>>(X, xe, f16 ? 1 : 0, 12345u);
+  fill_uniform<<<1024, 256, 0, st>>>(X, xe, S == 2 ? 1 : 0, 12345u);
   void* flush = nullptr;
   if (cudaMalloc(&flush, 2 * kFlushBytes) != cudaSuccess) {
     cudaGetLastError();

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("SPARSERT_LIB") or os.path.join(_PKG, "libsparsert.so"
 
 SPARSE_OK, SPARSE_EINVAL, SPARSE_EMATRIX, SPARSE_EUNSUPPORTED = 0, 1, 2, 3
 SPARSE_ENOMEM, SPARSE_ECUDA, SPARSE_EINTERNAL = 4, 5, 6
-SPARSE_F32, SPARSE_F16 = 0, 1
+SPARSE_F32, SPARSE_F16, SPARSE_BF16 = 0, 1, 2
 SPARSE_SPMM, SPARSE_CONV3X3 = 0, 1
 SPARSE_DEVICE_HOST_ONLY = -2
 
@@ -215,6 +215,8 @@ def _dtype_code(t) -> int:
         return SPARSE_F32
     if t == torch.float16:
         return SPARSE_F16
+    if t == torch.bfloat16:
+        return SPARSE_BF16
     raise TypeError(f"unsupported dtype {t}")
 
 

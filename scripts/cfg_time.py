@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2008_11849_b200 as srt
 from synth import gen
 M, K, N = map(int, sys.argv[1:4])
-tdt = torch.float16 if sys.argv[4] == "f16" else torch.float32
+tdt = {"f16": torch.float16, "bf16": torch.bfloat16}.get(sys.argv[4], torch.float32)
 w = gen.pruned_weights(M, K, 90, seed=1)
 X = torch.rand(K, N, device="cuda", dtype=tdt); Y = torch.empty(M, N, device="cuda", dtype=tdt)
 for cs in sys.argv[5].split(";"):

@@ -671,3 +671,55 @@ def test_linear_token_major(M, K, N, ex, f16):
     if f16:
         ref = _f16_round(ref)
     assert np.array_equal(Y.double().cpu().numpy(), ref.T)
+
+
+# --------------------------------------------------------------------------- bf16 (NEXT #4)
+
+def _bf16_f64(a):
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).double().numpy()
+
+
+@pytest.mark.parametrize("opts", [dict(), dict(k_split=2, rows_per_warp=4), dict(split_k=2, warps=8),
+                                  dict(rows_per_warp=8, k_chunk=64)])
+@pytest.mark.parametrize("M,K,N,p", [(64, 64, 128, 90), (300, 200, 517, 80), (1000, 64, 49, 95),
+                                     (3072, 768, 512, 90), (77, 1111, 300, 98)])
+def test_bf16_rel_l2_and_exact(M, K, N, p, opts):
+    # bfloat16 X / W / Y with fp32 accumulation (FHFMA.BF16): rel-L2 <= 1e-2 against the oracle
+    # on bf16-rounded inputs, and exact (= RN-even bf16 of the exact sum) on integer data
+    dev = _dev()
+    w = gen.pruned_weights(M, K, p, seed=gen.case_seed(f"bf{M}x{K}", p))
+    X = gen.uniform_x(K, N, seed=N + 3)
+    plan = srt.Plan.from_csr(w, dtype=torch.bfloat16, n_hint=N, **opts)
+    Y = plan.spmm(torch.from_numpy(X).to(dev).to(torch.bfloat16))
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, _bf16_f64(w.values), _bf16_f64(X))
+    err = oracle.rel_l2(Y.double().cpu().numpy(), ref)
+    assert err <= F16_TOL, err
+    wi = gen.int_weights(M, K, p, seed=M + 1, vmax=2)
+    Xi = gen.int_x(K, N, seed=K + 1, vmax=4)
+    plan = srt.Plan.from_csr(wi, dtype=torch.bfloat16, n_hint=N, **opts)
+    Y = plan.spmm(torch.from_numpy(Xi).to(dev).to(torch.bfloat16))
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), Xi.astype(np.float64))
+    assert np.array_equal(Y.double().cpu().numpy(), _bf16_f64(ref))
+
+
+def test_bf16_epilogue_and_unsupported():
+    dev = _dev()
+    M, K, N = 96, 300, 777
+    w = gen.int_weights(M, K, 90, seed=5, vmax=2)
+    Xi = gen.int_x(K, N, seed=6, vmax=4)
+    rng = np.random.default_rng(7)
+    bias = rng.integers(-8, 9, M).astype(np.float32)
+    Y0 = rng.integers(-8, 9, (M, N)).astype(np.float32)
+    plan = srt.Plan.from_csr(w, dtype=torch.bfloat16, n_hint=N)
+    Y = torch.from_numpy(Y0).to(dev).to(torch.bfloat16)
+    plan.spmm(torch.from_numpy(Xi).to(dev).to(torch.bfloat16), Y,
+              bias=torch.from_numpy(bias).to(dev).to(torch.bfloat16), beta=0.5, relu=True)
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), Xi.astype(np.float64))
+    ref = np.maximum(ref + bias[:, None] + 0.5 * Y0, 0.0)
+    assert np.array_equal(Y.double().cpu().numpy(), _bf16_f64(ref))
+    for kw in [dict(executor=3), dict(executor=1), dict(x_source=1)]:
+        with pytest.raises(srt.SparseRTError):
+            srt.Plan.from_csr(w, dtype=torch.bfloat16, n_hint=N, **kw)
