@@ -118,9 +118,9 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     err = "dtype must be SPARSE_F32, SPARSE_F16 or SPARSE_BF16";
     return SPARSE_EINVAL;
   }
-  if (dtype == SPARSE_BF16 && (o.kind != SPARSE_SPMM || o.executor == 1 || o.executor == 3 || o.tm)) {
-    err = "bf16 plans: SpMM on the plan-driven CUDA-core kernels only (no conv / JIT / tensor-core "
-          "panels / TMEM X source)";
+  if (dtype == SPARSE_BF16 && (o.kind != SPARSE_SPMM || o.executor == 1 || o.tm)) {
+    err = "bf16 plans: SpMM on the plan-driven CUDA-core kernels or the tensor-core panels only (no "
+          "conv / JIT / TMEM X source)";
     return SPARSE_EUNSUPPORTED;
   }
   if (o.kind != SPARSE_SPMM && o.kind != SPARSE_CONV3X3) {
@@ -783,8 +783,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // half have distinct k mod 8 (the staged X chunk is 128-byte swizzled, so ldmatrix rows
     // with distinct k mod 8 hit distinct banks), padded with zero-weight rows (SRT_TCP_STRICT;
     // measured faster than filling halves with conflicting rows: BERT fp16 303 -> 279 us).
-    if (o.kind != SPARSE_SPMM || dtype != SPARSE_F16) {
-      err = "executor = 3 (tensor-core condensed panels) needs an fp16 SpMM plan";
+    if (o.kind != SPARSE_SPMM || dtype == SPARSE_F32) {
+      err = "executor = 3 (tensor-core condensed panels) needs an fp16 or bf16 SpMM plan";
       return SPARSE_EUNSUPPORTED;
     }
     const int KC = kTcpKc;

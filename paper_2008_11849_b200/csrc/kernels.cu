@@ -1700,11 +1700,18 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
 }
+template <bool BF = false>
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint4& a, uint32_t b0, uint32_t b1) {
-  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-               "{%0, %1, %2, %3};"
-               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-               : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+  if (BF)
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                 "{%8, %9}, {%0, %1, %2, %3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+  else
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+                 "{%0, %1, %2, %3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
 // NB = 64-column boxes per CTA (N tile = 64 NB): 2 for large N (A fragments reused over 16
@@ -1714,7 +1721,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint4& a, uint32_t
 #ifndef SRT_TCP_CY
 #define SRT_TCP_CY 1
 #endif
-template <int NB>
+template <int NB, bool BF = false>
 __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spmm_tcp_kernel(const __grid_constant__ CUtensorMap tmap, const TcpArgs a) {
   constexpr int NTT = 8 * NB;       // n8 tiles per warp
   constexpr int XST = NB * kTcpKc * 128;  // X part of a stage
@@ -1836,8 +1843,8 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
                                     hv[6] | (hv[7] << 16));
 #pragma unroll
         for (int j = 0; j < NTT / 2; ++j) {
-          mma16816(acc[2 * j], av, bcur[j][0], bcur[j][1]);
-          mma16816(acc[2 * j + 1], av, bcur[j][2], bcur[j][3]);
+          mma16816<BF>(acc[2 * j], av, bcur[j][0], bcur[j][1]);
+          mma16816<BF>(acc[2 * j + 1], av, bcur[j][2], bcur[j][3]);
         }
         sp += rec;
       }
@@ -1857,8 +1864,8 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
         load_b(st, kr, bcur);
 #pragma unroll
         for (int j = 0; j < NTT / 2; ++j) {
-          mma16816(acc[2 * j], av, bcur[j][0], bcur[j][1]);
-          mma16816(acc[2 * j + 1], av, bcur[j][2], bcur[j][3]);
+          mma16816<BF>(acc[2 * j], av, bcur[j][0], bcur[j][1]);
+          mma16816<BF>(acc[2 * j + 1], av, bcur[j][2], bcur[j][3]);
         }
         av = an;
         kr = kn;
@@ -1894,20 +1901,20 @@ __global__ void __launch_bounds__(32 * kTcpPanels, kTcpPanels >= 16 ? 1 : 2) spm
   for (int h = 0; h < 2; ++h) {
     const int row = 16 * q + g + 8 * h;
     if (row >= a.M) continue;
-    __half* yr = (__half*)a.Y + (int64_t)row * a.ldy;
+    uint16_t* yr = (uint16_t*)a.Y + (int64_t)row * a.ldy;
 #pragma unroll
     for (int tile = 0; tile < NTT; ++tile) {
       const int64_t col = n0 + tile * 8 + 2 * t;
       float v0 = acc[tile][2 * h], v1 = acc[tile][2 * h + 1];
       if (epi) {
-        if (col < a.N) v0 = epilogue_one<true>(v0, a.bias, row, a.beta, (const uint8_t*)(yr + col), a.relu);
-        if (col + 1 < a.N) v1 = epilogue_one<true>(v1, a.bias, row, a.beta, (const uint8_t*)(yr + col + 1), a.relu);
+        if (col < a.N) v0 = epilogue_one<true, BF>(v0, a.bias, row, a.beta, (const uint8_t*)(yr + col), a.relu);
+        if (col + 1 < a.N) v1 = epilogue_one<true, BF>(v1, a.bias, row, a.beta, (const uint8_t*)(yr + col + 1), a.relu);
       }
       if (col + 1 < a.N && ((((uintptr_t)(yr + col)) & 3) == 0)) {
-        *(__half2*)(yr + col) = __floats2half2_rn(v0, v1);
+        *(uint32_t*)(yr + col) = (uint32_t)to16<BF>(v0) | ((uint32_t)to16<BF>(v1) << 16);
       } else {
-        if (col < a.N) yr[col] = __float2half_rn(v0);
-        if (col + 1 < a.N) yr[col + 1] = __float2half_rn(v1);
+        if (col < a.N) yr[col] = to16<BF>(v0);
+        if (col + 1 < a.N) yr[col + 1] = to16<BF>(v1);
       }
     }
   }
@@ -1924,7 +1931,9 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
   const int warps = kTcpPanels;
   const int NB = N >= 4096 ? 2 : 1;
-  auto kfn = NB == 2 ? spmm_tcp_kernel<2> : spmm_tcp_kernel<1>;
+  const bool bf = p.dtype == SPARSE_BF16;
+  auto kfn = NB == 2 ? (bf ? spmm_tcp_kernel<2, true> : spmm_tcp_kernel<2, false>)
+                     : (bf ? spmm_tcp_kernel<1, true> : spmm_tcp_kernel<1, false>);
   const int stage_bytes = (NB * kTcpKc * 128 + p.tcp_max_blk + 1023) & ~1023;  // X boxes stay 1 KB aligned
   // 16 panels per CTA: one CTA per SM (126 registers x 512 threads); 8: two CTAs per SM
   const int budget = kTcpPanels >= 16 ? 227 * 1024 : 113 * 1024;

@@ -122,7 +122,7 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     BuildOpts j = base;
     j.executor = 1;
     cands.push_back(j);
-    if (f16) {  // condensed-panel tensor cores
+    if (S == 2) {  // condensed-panel tensor cores (fp16 and bf16)
       BuildOpts t = base;
       t.executor = 3;
       cands.push_back(t);

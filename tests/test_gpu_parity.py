@@ -720,6 +720,21 @@ def test_bf16_epilogue_and_unsupported():
     ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), Xi.astype(np.float64))
     ref = np.maximum(ref + bias[:, None] + 0.5 * Y0, 0.0)
     assert np.array_equal(Y.double().cpu().numpy(), _bf16_f64(ref))
-    for kw in [dict(executor=3), dict(executor=1), dict(x_source=1)]:
+    for kw in [dict(executor=1), dict(x_source=1)]:
         with pytest.raises(srt.SparseRTError):
             srt.Plan.from_csr(w, dtype=torch.bfloat16, n_hint=N, **kw)
+
+
+@pytest.mark.parametrize("case", [(64, 256, 3136), (512, 2048, 49), (3072, 768, 512), (17, 70, 33), (16, 64, 4099)])
+def test_bf16_tcp_exact(case):
+    # the tensor-core panels with bf16 operands (mma.sync ... .bf16): exact on integer data
+    dev = _dev()
+    M, K, N = case
+    w = gen.int_weights(M, K, 90, seed=M + K, vmax=2)
+    Xi = gen.int_x(K, N, seed=N, vmax=4)
+    plan = srt.Plan.from_csr(w, dtype=torch.bfloat16, n_hint=N, executor=3)
+    assert plan.info["executor"] == 3
+    Y = plan.spmm(torch.from_numpy(Xi).to(dev).to(torch.bfloat16))
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), Xi.astype(np.float64))
+    assert np.array_equal(Y.double().cpu().numpy(), _bf16_f64(ref))
