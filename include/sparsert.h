@@ -52,9 +52,9 @@ enum sparse_status {
 /* X, Y and the plan's values share the dtype; accumulation is always fp32.
  * SPARSE_F16: W is rounded to fp16 (RN-even) at plan time; each product
  * f16 x f16 is exact in fp32; Y is rounded RN-even to fp16 once.
- * SPARSE_BF16 (NEXT #4): the same with bfloat16 (FHFMA.BF16); SpMM plans on the CUDA-core
- * kernels or the tensor-core panels (executor 3) only (conv, JIT, dense-tile tensor cores and
- * the TMEM X source: EUNSUPPORTED). */
+ * SPARSE_BF16 (NEXT #4): the same with bfloat16 (FHFMA.BF16 / mma .bf16): SpMM on the CUDA-core
+ * kernels or the tensor-core panels (executor 3), conv on the TMA-fed kernel (JIT, dense-tile
+ * tensor cores, the TMEM X source and the other conv kernels: EUNSUPPORTED). */
 enum sparse_dtype { SPARSE_F32 = 0, SPARSE_F16 = 1, SPARSE_BF16 = 2 };
 enum sparse_kind { SPARSE_SPMM = 0, SPARSE_CONV3X3 = 1 };
 

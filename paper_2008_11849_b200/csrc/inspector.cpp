@@ -118,9 +118,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     err = "dtype must be SPARSE_F32, SPARSE_F16 or SPARSE_BF16";
     return SPARSE_EINVAL;
   }
-  if (dtype == SPARSE_BF16 && (o.kind != SPARSE_SPMM || o.executor == 1 || o.tm)) {
-    err = "bf16 plans: SpMM on the plan-driven CUDA-core kernels or the tensor-core panels only (no "
-          "conv / JIT / TMEM X source)";
+  if (dtype == SPARSE_BF16 && (o.executor == 1 || o.tm)) {
+    err = "bf16 plans: no JIT executor / TMEM X source";
     return SPARSE_EUNSUPPORTED;
   }
   if (o.kind != SPARSE_SPMM && o.kind != SPARSE_CONV3X3) {
@@ -458,6 +457,10 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
         }
       }
     }
+  }
+  if (dtype == SPARSE_BF16 && o.kind == SPARSE_CONV3X3 && p.conv_vec != 2) {
+    err = "bf16 conv plans need the TMA-fed conv kernel (conv_kernel 0 or 2, W + 2 <= 64)";
+    return SPARSE_EUNSUPPORTED;
   }
   p.warps = o.warps ? o.warps : (o.kind == SPARSE_SPMM || p.conv_vec ? 16 : 8);
   if (p.warps < 1 || p.warps > kMaxWarps) {

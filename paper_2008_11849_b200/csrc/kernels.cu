@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(512) conv3x3_vec_kernel(const ConvArgs a) {
 // channels past the end arrive as zeros, so the zero halo of P:215 costs nothing in the loop.  Persistent CTAs walk the tiles (panel fastest, then image band) through an
 // mbarrier ring refilled by the last releasing warp (as spmm_kernel); the FMA loop is
 // run_rows on the same plan format (offset dx * cs + ci * sci + dy * wp, guard 0).
-template <int R, bool F16>
+template <int R, bool F16, bool BF = false>
 __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const ConvArgs a) {
   constexpr int C = F16 ? 8 : 4;
@@ -1221,7 +1221,7 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
       uint32_t h[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) h[r] = shdr[warp * R + r];
-      run_rows<F16, R>(acc, h, ents, st + xoff);
+      run_rows<F16, R, BF>(acc, h, ents, st + xoff);
       __syncwarp();
       uint32_t old = 0;
       if (lane == 0)
@@ -1246,9 +1246,9 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
         const int y = y0 + rr;
         if (rr >= a.rb || y >= a.H || x < 0 || x >= a.W) continue;
         const int64_t o = ((int64_t)row * a.B + b) * plane + (int64_t)y * a.W + x;
-        const float v = epilogue_one<F16>(acc[r][c], a.bias, row, a.beta, a.y + o * S, a.relu);
+        const float v = epilogue_one<F16, BF>(acc[r][c], a.bias, row, a.beta, a.y + o * S, a.relu);
         if (F16)
-          ((__half*)a.y)[o] = __float2half_rn(v);
+          ((uint16_t*)a.y)[o] = to16<BF>(v);
         else
           ((float*)a.y)[o] = v;
       }
@@ -2196,7 +2196,7 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
 
 int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
                    std::string& err, const Epilogue& ep) {
-  const bool f16 = p.dtype == SPARSE_F16;
+  const bool f16 = p.dtype != SPARSE_F32;  // 16-bit data (bf16 plans always take the TMA-fed kernel)
   ConvFn fn = p.conv_vec ? (f16 ? pick_conv_vec<true>(p.R) : pick_conv_vec<false>(p.R))
                         : (f16 ? pick_conv<true>(p.R, p.C) : pick_conv<false>(p.R, p.C));
   if (!fn && p.conv_vec != 2) {
@@ -2248,10 +2248,11 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
     // wave of CTAs (programmatic dependent launch after the pad kernel)
     using TmaFn = void (*)(const CUtensorMap, const ConvArgs);
     TmaFn tf = nullptr;
-    if (p.R == 1) tf = f16 ? conv3x3_tma_kernel<1, true> : conv3x3_tma_kernel<1, false>;
-    if (p.R == 2) tf = f16 ? conv3x3_tma_kernel<2, true> : conv3x3_tma_kernel<2, false>;
-    if (p.R == 4) tf = f16 ? conv3x3_tma_kernel<4, true> : conv3x3_tma_kernel<4, false>;
-    if (p.R == 8) tf = f16 ? conv3x3_tma_kernel<8, true> : conv3x3_tma_kernel<8, false>;
+    const bool bf = p.dtype == SPARSE_BF16;
+#define SRT_T(RR) \
+    if (p.R == RR) tf = bf ? conv3x3_tma_kernel<RR, true, true> : f16 ? conv3x3_tma_kernel<RR, true> : conv3x3_tma_kernel<RR, false>;
+    SRT_T(1) SRT_T(2) SRT_T(4) SRT_T(8)
+#undef SRT_T
     auto encode = tensor_map_encoder();
     if (!tf || !encode) {
       err = "internal: no TMA conv kernel instance / tensor-map encoder";

@@ -738,3 +738,21 @@ def test_bf16_tcp_exact(case):
     torch.cuda.synchronize()
     ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), Xi.astype(np.float64))
     assert np.array_equal(Y.double().cpu().numpy(), _bf16_f64(ref))
+
+
+@pytest.mark.parametrize("cin,cout,B,H,W", [(32, 48, 3, 14, 14), (256, 64, 2, 14, 14), (16, 24, 2, 28, 28)])
+def test_bf16_conv_exact(cin, cout, B, H, W):
+    # bf16 implicit-im2col conv on the TMA-fed kernel: exact on integer data (RN-even bf16 of the
+    # exact sum), fused epilogue included; the other conv kernels refuse bf16
+    dev = _dev()
+    w = gen.int_weights(cout, 9 * cin, 90, seed=cin + W, vmax=2)
+    x = gen.int_x(cin * B * H, W, seed=cout, vmax=4).reshape(cin, B, H, W)
+    plan = srt.Plan.from_csr(w, dtype=torch.bfloat16, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B)
+    assert plan.info["conv_kernel"] == 2
+    y = plan.conv3x3(torch.from_numpy(x).to(dev).to(torch.bfloat16))
+    torch.cuda.synchronize()
+    ref = oracle.conv3x3(cout, w.row_ptr, w.col_idx, w.values.astype(np.float64), x.astype(np.float64))
+    assert np.array_equal(y.double().cpu().numpy(), _bf16_f64(ref))
+    with pytest.raises(srt.SparseRTError):
+        srt.Plan.from_csr(w, dtype=torch.bfloat16, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B,
+                          conv_kernel=3)
