@@ -162,7 +162,10 @@ struct Plan {
   const int32_t* d_tcp_step_off = nullptr;
   const uint8_t* d_tcp_steps = nullptr;
 };
-constexpr int kTcpKc = 64;          // K rows per staged chunk (one 128-byte swizzled TMA box row)
+#ifndef SRT_TCP_KC
+#define SRT_TCP_KC 64
+#endif
+constexpr int kTcpKc = SRT_TCP_KC;  // K rows per staged chunk (TMA box rows, 128-byte swizzled)
 #ifndef SRT_TCP_PANELS
 #define SRT_TCP_PANELS 8
 #endif
