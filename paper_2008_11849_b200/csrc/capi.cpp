@@ -90,13 +90,15 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
       delete h;
       return fail(SPARSE_EINVAL, "tune = 1 needs a device");
     }
-    int dev = o.device;
-    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+    int dev = o.device, prev_dev = -1;
+    if (cudaGetDevice(&prev_dev) != cudaSuccess) {
       delete h;
       return fail(SPARSE_ECUDA, "no CUDA device");
     }
+    if (dev < 0) dev = prev_dev;
     try {
       rc = srt::tune_plan(h->p, M, K, nnz, row_ptr, col_idx, values, dtype, bo, dev, err);
+      cudaSetDevice(prev_dev);  // the tuner selects `dev`; the caller's current device is kept
     } catch (const std::bad_alloc&) {
       rc = SPARSE_ENOMEM;
       err = "host allocation failed in tuner";
@@ -109,11 +111,14 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
     return ok();
   }
   const bool auto_exec = bo.executor == 2;
-  if (auto_exec) bo.executor = 1;
+  // auto: try the JIT executor first, except where it cannot apply (bf16 values, the TMEM X
+  // source, conv plans), which go straight to the plan-driven kernel
+  if (auto_exec) bo.executor = (dtype == SPARSE_BF16 || bo.tm || bo.kind != SPARSE_SPMM) ? 0 : 1;
   try {
     rc = srt::build_plan(h->p, M, K, nnz, row_ptr, col_idx, values, dtype, bo, err);
-    if (rc == SPARSE_OK && auto_exec && h->p.executor == 1 &&
-        srt::jit_panel_code_bytes(h->p) > 24 * 1024) {
+    if (auto_exec && bo.executor == 1 &&
+        (rc == SPARSE_EUNSUPPORTED ||
+         (rc == SPARSE_OK && h->p.executor == 1 && srt::jit_panel_code_bytes(h->p) > 24 * 1024))) {
       // auto: the JIT executor only where each panel's code fits the instruction cache
       bo.executor = 0;
       rc = srt::build_plan(h->p, M, K, nnz, row_ptr, col_idx, values, dtype, bo, err);
@@ -216,6 +221,14 @@ int sparse_linear(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, voi
   void* Xt = nullptr;
   void* Yt = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
+  int prev_dev = -1;
+  if (cudaGetDevice(&prev_dev) != cudaSuccess) return fail(SPARSE_ECUDA, "cudaGetDevice failed");
+  struct Restore {  // the scratch lives on the plan's device; restore the caller's device
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{prev_dev};
+  if (p.device >= 0 && p.device != prev_dev && cudaSetDevice(p.device) != cudaSuccess)
+    return fail(SPARSE_ECUDA, "cudaSetDevice(plan device) failed");
   if (cudaMallocAsync(&Xt, (size_t)(p.K * ldt * S), st) != cudaSuccess ||
       cudaMallocAsync(&Yt, (size_t)(p.M * ldt * S), st) != cudaSuccess) {
     cudaGetLastError();

@@ -947,7 +947,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   const int32_t cfg[] = {p.M,  p.K,      p.dtype,   p.kind,    p.c_in,   p.h,
                          p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
                          p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm,
-                         p.conv_vec, p.row_order};
+                         p.conv_vec, p.row_order, p.executor, p.jit_mp, p.jit_warps, p.stages,
+                         p.tc_min_pct};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

@@ -1527,7 +1527,11 @@ int launch_repack(int device, int64_t K, int64_t N, int S, const void* X, int64_
         (const uint8_t*)X + k0 * ldx * S, ldx * S, (uint8_t*)*Xp + k0 * *ldp * S, *ldp * S, N, S);
   }
   e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "repack launch", err);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(*Xp, (cudaStream_t)stream);
+    *Xp = nullptr;
+    return cuda_fail(e, "repack launch", err);
+  }
   return SPARSE_OK;
 }
 
