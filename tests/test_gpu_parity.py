@@ -756,3 +756,30 @@ def test_bf16_conv_exact(cin, cout, B, H, W):
     with pytest.raises(srt.SparseRTError):
         srt.Plan.from_csr(w, dtype=torch.bfloat16, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B,
                           conv_kernel=3)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16, torch.float32])
+def test_auto_executor_all_dtypes(dt):
+    # executor = 2 (auto) builds for every dtype: the JIT where it applies (fp32 / fp16 SpMM with
+    # small panels), the plan-driven kernel otherwise (bf16 always); exact on integer data
+    dev = _dev()
+    M, K, N = 256, 64, 3136
+    vw, vx = (3, 3) if dt == torch.float32 else (2, 4)
+    w = gen.int_weights(M, K, 90, seed=11, vmax=vw)
+    Xi = gen.int_x(K, N, seed=12, vmax=vx)
+    plan = srt.Plan.from_csr(w, dtype=dt, n_hint=N, executor=2)
+    if dt == torch.bfloat16:
+        assert plan.info["executor"] == 0
+    Y = plan.spmm(torch.from_numpy(Xi).to(dev).to(dt))
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), Xi.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(dt).double().numpy()
+    assert np.array_equal(Y.double().cpu().numpy(), ref)
+
+
+def test_tune_keeps_current_device():
+    _dev()
+    torch.cuda.set_device(0)
+    w = gen.pruned_weights(128, 128, 90, seed=3)
+    plan = srt.Plan.from_csr(w, n_hint=1024, tune=1, device=0)
+    assert torch.cuda.current_device() == 0 and plan.info["tuned_us"] > 0
