@@ -65,10 +65,11 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   bo.jit_warps = o.jit_warps;
   bo.cm = o.x_multicast;
   bo.tm = o.x_source;
-  if (o.conv_kernel < 0 || o.conv_kernel > 3)
+  if (o.conv_kernel < 0 || o.conv_kernel > 4)
     return fail(SPARSE_EINVAL,
-                "conv_kernel must be 0 (auto), 1 (position-strided), 2 (TMA-fed) or 3 (register-staged)");
-  bo.conv_vec = o.conv_kernel == 1 ? 0 : o.conv_kernel == 3 ? 1 : 2;
+                "conv_kernel must be 0 (auto), 1 (position-strided), 2 (TMA-fed), 3 (register-staged) "
+                "or 4 (packed)");
+  bo.conv_vec = o.conv_kernel == 1 ? 0 : o.conv_kernel == 3 ? 1 : o.conv_kernel == 4 ? 4 : 2;
   if (o.row_order != 0 && o.row_order != 1)
     return fail(SPARSE_EINVAL, "row_order must be 0 (load balanced) or 1 (natural)");
   bo.row_order = o.row_order;
@@ -328,7 +329,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->tuned_us = p.tuned_us;
   out->x_multicast = p.cm;
   out->x_source = p.tm;
-  out->conv_kernel = p.kind != SPARSE_CONV3X3 ? 0 : !p.conv_vec ? 1 : p.conv_vec == 2 ? 2 : 3;
+  out->conv_kernel = p.kind != SPARSE_CONV3X3 ? 0 : !p.conv_vec ? 1 : p.conv_vec == 2 ? 2 : p.conv_vec == 4 ? 4 : 3;
   out->row_order = p.row_order;
   out->tc_min_density = p.tc_ntiles > 0 || p.tc_min_pct > 0 ? p.tc_min_pct : 0;
   out->tc_row_blocks = p.tc_nrb;
@@ -396,6 +397,21 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
               if (p.kind == SPARSE_SPMM) {
                 if (xoff % rowb) return fail(SPARSE_EINTERNAL, "plan entry offset not a row multiple");
                 kl = xoff / rowb;
+              } else if (p.conv_vec == 4) {  // packed conv: el = k cs + ci lc + (dy-1) W - a + bias
+                const int64_t el = (f16 ? xoff / 16 : xoff / 4) - p.pk_bias;
+                const int ncop = 3 * p.pk_ncls;
+                if (el == (int64_t)ncop * p.conv_cs) {
+                  kl = p.kc;
+                } else {
+                  const int64_t v = el + p.w + 1;  // >= 0: (dy - 1) W - a >= -W - 1
+                  const int64_t k = v / p.conv_cs, rem = v % p.conv_cs;
+                  const int64_t ci = rem / p.pk_lc, e2 = rem % p.pk_lc - (p.w + 1);
+                  const int64_t dx = k / p.pk_ncls, a = k % p.pk_ncls;
+                  const int64_t d = e2 + a;
+                  if (k >= ncop || d % p.w || d / p.w < -1 || d / p.w > 1 || ((d % p.C) + p.C) % p.C != a)
+                    return fail(SPARSE_EINTERNAL, "packed conv plan entry offset does not decode");
+                  kl = ci * 9 + (d / p.w + 1) * 3 + dx;
+                }
               } else {  // vectorised conv: elems = dx * cs + ci * sci + dy * wp, or the zero block
                 const int64_t el = xoff / (f16 ? 2 : 4);
                 if (el == 3 * (int64_t)p.conv_cs) {

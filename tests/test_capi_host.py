@@ -8,6 +8,7 @@ import re
 import subprocess
 
 import numpy as np
+import torch
 import pytest
 
 from synth import gen
@@ -186,6 +187,25 @@ def test_conv_plan_decode():
         ref_rows = np.repeat(np.arange(cout), np.diff(w.row_ptr))
         assert np.array_equal(np.sort(d.row.astype(np.int64) * 9 * cin + d.col),
                               np.sort(ref_rows.astype(np.int64) * 9 * cin + w.col_idx))
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float16, torch.bfloat16])
+def test_packed_conv_plan_decode(dt):
+    # packed conv plans (conv_kernel 4): every nonzero decodes back to its (row, ci, dy, dx)
+    # with its value, for even and odd image widths (one / two alignment classes of copies)
+    cin, cout = 16, 24
+    w = gen.pruned_weights(cout, 9 * cin, 80, seed=4)
+    for (h, wd, nb, cc) in [(14, 14, 8, 5), (28, 28, 2, 3), (56, 56, 1, 16), (6, 9, 3, 4), (4, 4, 5, 7)]:
+        pl = _plan(w, dtype=dt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=h, w=wd, n_hint=nb, k_chunk=cc,
+                   conv_kernel=4)
+        assert pl.info["conv_kernel"] == 4
+        d = pl.dump()
+        dense = np.zeros((cout, 9 * cin))
+        dense[d.row, d.col] = d.value
+        ref = torch.from_numpy(gen.to_dense(w, np.float32)).to(dt).double().numpy()
+        assert np.array_equal(dense, ref)
+    with pytest.raises(S.SparseRTError):  # odd H * W
+        _plan(w, kind=srt.SPARSE_CONV3X3, c_in=cin, h=7, w=7, n_hint=2, conv_kernel=4)
 
 
 def _rc(fn):

@@ -405,6 +405,63 @@ def test_conv_vectorised_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, f16
     assert np.array_equal(ys[2], ys[1])
 
 
+@pytest.mark.parametrize("dt", ["f32", "f16", "bf16"])
+@pytest.mark.parametrize("cin,cout,B,H,W,R,warps,cc", [
+    (16, 24, 3, 14, 14, 8, 16, 5), (256, 64, 2, 14, 14, 8, 16, 16), (256, 256, 5, 14, 14, 8, 16, 0),
+    (32, 16, 1, 56, 56, 4, 16, 8), (12, 20, 2, 28, 28, 8, 8, 4), (5, 9, 3, 6, 9, 2, 16, 2),
+    (8, 8, 5, 4, 4, 8, 16, 3), (64, 128, 4, 14, 14, 16, 16, 8), (40, 33, 7, 10, 6, 2, 8, 7)])
+def test_conv_packed_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, dt):
+    # the packed implicit-im2col kernel (conv_kernel 4: positions n = (b H + y) W + x, no junk
+    # positions, raw input staged by TMA and the zero-haloed shifted copies built in shared
+    # memory): exact on integer data and bitwise equal to the register-staged vectorised kernel
+    # (same k order); odd B x H x W in 16-bit takes the device repack of the input
+    dev = _dev()
+    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[dt]
+    vmax_w, vmax_x = (3, 3) if dt == "f32" else (2, 4)
+    w = gen.int_weights(cout, 9 * cin, 90, seed=cin + H + W, vmax=vmax_w)
+    x = gen.int_x(cin * B * H, W, seed=cout + B, vmax=vmax_x).reshape(cin, B, H, W)
+    xt = torch.from_numpy(x).to(dev).to(tdt)
+    kw = dict(rows_per_warp=R, warps=warps)
+    if cc:
+        kw["k_chunk"] = cc
+    plan = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B,
+                             conv_kernel=4, **kw)
+    assert plan.info["conv_kernel"] == 4
+    y = torch.full((cout, B, H, W), float("nan"), dtype=tdt, device=dev)
+    plan.conv3x3(xt, y)
+    torch.cuda.synchronize()
+    got = y.double().cpu().numpy()
+    ref = oracle.conv3x3(cout, w.row_ptr, w.col_idx, w.values.astype(np.float64), x.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(got, ref)
+    if dt != "bf16":
+        other = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B,
+                                  conv_kernel=3)
+        y3 = other.conv3x3(xt)
+        torch.cuda.synchronize()
+        assert np.array_equal(y3.double().cpu().numpy(), got)
+    # the plan decodes back to W exactly (every nonzero once, at its (ci, dy, dx))
+    d = plan.dump()
+    dense = np.zeros((cout, 9 * cin))
+    dense[d.row, d.col] = d.value
+    assert np.array_equal(dense, gen.to_dense(w))
+
+
+def test_conv_packed_real_valued_and_unsupported():
+    dev = _dev()
+    cin, cout, B, H, W = 128, 128, 6, 28, 28
+    w = gen.pruned_weights(cout, 9 * cin, 95, seed=77)
+    x = gen.relu_normal_x((cin, B, H, W), seed=78)
+    for f16 in (False, True):
+        y, plan = _conv_run(w, cin, x, f16, conv_kernel=4)
+        assert plan.info["conv_kernel"] == 4
+        err = oracle.rel_l2(y, _conv_ref(w, x, f16))
+        assert err <= (F16_TOL if f16 else F32_TOL), err
+    w7 = gen.pruned_weights(16, 9 * 8, 90, seed=79)
+    with pytest.raises(srt.SparseRTError):  # H * W odd: no packed layout
+        srt.Plan.from_csr(w7, kind=srt.SPARSE_CONV3X3, c_in=8, h=7, w=7, n_hint=2, conv_kernel=4)
+
+
 @pytest.mark.parametrize("f16", [False, True])
 def test_conv_center_tap_equals_spmm(f16):
     # a W using only the center tap (dy = dx = 1) is a 1x1 conv: conv3x3 == spmm bitwise
@@ -418,7 +475,7 @@ def test_conv_center_tap_equals_spmm(f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
-@pytest.mark.parametrize("ck", [2, 3])
+@pytest.mark.parametrize("ck", [2, 3, 4])
 def test_conv_c5_full_batch_sampled(ck, f16):
     # BASELINE configs[4] at full size (256 ch, 14x14, batch 256, 90%), in the bench's launch
     # configuration; integer data, images {0, 101, 255} checked bitwise against the oracle,
@@ -536,7 +593,7 @@ def test_spmm_epilogue_exact(opts, f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
-@pytest.mark.parametrize("ck", [1, 2, 3])
+@pytest.mark.parametrize("ck", [1, 2, 3, 4])
 def test_conv_epilogue_exact(ck, f16):
     dev = _dev()
     cin, cout, B, H, W = 24, 40, 2, 14, 14
