@@ -397,21 +397,10 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
               if (p.kind == SPARSE_SPMM) {
                 if (xoff % rowb) return fail(SPARSE_EINTERNAL, "plan entry offset not a row multiple");
                 kl = xoff / rowb;
-              } else if (p.conv_vec == 4) {  // packed conv: el = k cs + ci lc + (dy-1) W - a + bias
-                const int64_t el = (f16 ? xoff / 16 : xoff / 4) - p.pk_bias;
-                const int ncop = 3 * p.pk_ncls;
-                if (el == (int64_t)ncop * p.conv_cs) {
-                  kl = p.kc;
-                } else {
-                  const int64_t v = el + p.w + 1;  // >= 0: (dy - 1) W - a >= -W - 1
-                  const int64_t k = v / p.conv_cs, rem = v % p.conv_cs;
-                  const int64_t ci = rem / p.pk_lc, e2 = rem % p.pk_lc - (p.w + 1);
-                  const int64_t dx = k / p.pk_ncls, a = k % p.pk_ncls;
-                  const int64_t d = e2 + a;
-                  if (k >= ncop || d % p.w || d / p.w < -1 || d / p.w > 1 || ((d % p.C) + p.C) % p.C != a)
-                    return fail(SPARSE_EINTERNAL, "packed conv plan entry offset does not decode");
-                  kl = ci * 9 + (d / p.w + 1) * 3 + dx;
-                }
+              } else if (p.conv_vec == 4) {  // packed conv: im2col row (tap, ci) of the tile
+                if (xoff % rowb) return fail(SPARSE_EINTERNAL, "packed conv entry offset not a row multiple");
+                const int64_t row = xoff / rowb;
+                kl = row == p.kc ? p.kc : (row % p.cc) * 9 + row / p.cc;
               } else {  // vectorised conv: elems = dx * cs + ci * sci + dy * wp, or the zero block
                 const int64_t el = xoff / (f16 ? 2 : 4);
                 if (el == 3 * (int64_t)p.conv_cs) {

@@ -439,58 +439,35 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
         p.conv_stage_elems = 3 * p.conv_cs + NTv + 16;  // + zero block
         p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
         if (o.conv_vec == 4) {
-          // packed kernel (conv3x3_pk_kernel): lane loads 2 consecutive positions, 2 groups,
-          // 128 positions per tile; copies in the halo'd image coordinate (kernels.cu)
-          const int Cp = 2, NTp = 128, HW = o.h * o.w;
-          const int el16 = 16 / S, el128 = 128 / S;
+          // packed kernel (conv3x3_pk_kernel): NT = 32 C packed positions per tile, the chunk's
+          // im2col tile [9 cc rows x NT] (+ a zero row) built in shared memory from a raw span
+          // of RAWN elements per channel staged by TMA (kernels.cu)
+          const int el16 = 16 / S;
           auto rup = [](int v, int m) { return (v + m - 1) / m * m; };
-          if (HW % Cp) {
-            err = "packed conv (conv_kernel 4) needs H * W even";
-            return SPARSE_EUNSUPPORTED;
-          }
           p.conv_vec = 4;
-          p.C = Cp;
-          p.n_tile = NTp;
+          p.C = Cv;
+          p.n_tile = NTv;
           p.conv_rb = 0;
           p.conv_ipt = 0;
           p.conv_wp = o.w;
           p.conv_guard = 0;
-          p.pk_w0 = rup(o.w + Cp - 1, Cp);
-          p.pk_bias = o.w + Cp;
-          p.pk_ncls = (o.w % Cp) ? 2 : 1;
-          const int nbx = (NTp - 1) / HW + 1;  // image boundaries a tile can straddle
-          const int nthr_b = 32 * (o.warps ? o.warps : 16);
-          // image stride in the halo'd coordinate: the jump between images a whole number of
-          // 128-byte rows (lanes past an image boundary stay on the same banks), unless the
-          // copies then need more than 4 build pairs per thread (small images)
-          for (int jump : {rup(2 * o.w, el128), rup(2 * o.w, Cp)}) {
-            p.conv_simg = HW + jump;
-            const int maxspan = NTp - 1 + nbx * jump;
-            p.pk_lc = rup(p.pk_w0 + maxspan + o.w + Cp + 1, el16);
-            if (3 * p.pk_ncls * p.pk_lc <= 4 * nthr_b) break;
-          }
           p.pk_p0 = rup(o.w + 1, el16);
-          p.pk_rawn = rup(p.pk_p0 + NTp + o.w + 1, el16);
-          if (p.pk_rawn > 256) {
-            err = "packed conv: image width too large for one TMA box (W > 56)";
+          p.pk_rawn = rup(p.pk_p0 + NTv + o.w + 1, 2 * el16);  // even number of 16-byte units
+          if (p.pk_rawn > 512) {
+            err = "packed conv: image width too large for the raw TMA boxes";
             return SPARSE_EUNSUPPORTED;
           }
-          const int ncop = 3 * p.pk_ncls;
-          const int per_ch = (p.pk_rawn + ncop * p.pk_lc) * S;
-          int ccp = o.k_chunk ? o.k_chunk : std::max(1, std::min(o.c_in, (40 * 1024) / per_ch));
+          const int per_ch = (p.pk_rawn + 9 * NTv) * S;
+          int ccp = o.k_chunk ? o.k_chunk : std::max(1, std::min(o.c_in, (48 * 1024) / per_ch));
           ccp = std::min(ccp, 64);
           p.cc = ccp;
           p.kc = 9 * ccp;
           p.nchunks = (o.c_in + ccp - 1) / ccp;
-          p.conv_cs = ccp * p.pk_lc;
-          p.conv_sci = p.pk_lc;
-          p.conv_stage_elems = ncop * p.conv_cs + p.pk_lc;
+          p.conv_cs = 0;
+          p.conv_sci = NTv;
+          p.conv_stage_elems = (9 * ccp + 1) * NTv;  // im2col rows + the zero row
           p.x_stage_bytes = (int)(((int64_t)p.conv_stage_elems * S + 127) & ~int64_t(127));
           p.pk_raw_bytes = ccp * p.pk_rawn * S;
-          if ((int64_t)ncop * p.conv_cs + p.pk_bias + p.pk_lc > 65535) {
-            err = "packed conv: k_chunk too large for 16-bit entry offsets";
-            return SPARSE_EUNSUPPORTED;
-          }
         } else if (o.conv_vec == 2 && wpv <= 64) {  // (pad_conv_input holds a padded row in registers)
           // TMA-fed variant (conv3x3_tma_kernel): each shifted copy is one 4-D TMA box
           // {wp, rb + 2, 1 image, cc channels} of the width-padded input (no guard), at a
@@ -562,8 +539,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     err = "rows_per_warp must be 1, 2, 4, 8 or 16";
     return SPARSE_EUNSUPPORTED;
   }
-  if (p.conv_vec && p.R > (p.conv_vec == 4 ? 16 : 8)) {
-    err = "rows_per_warp must be <= 8 for the vectorised conv kernel (16 for the packed one)";
+  if (p.conv_vec && p.R > 8) {
+    err = "rows_per_warp must be <= 8 for the vectorised conv kernels";
     return SPARSE_EUNSUPPORTED;
   }
   if (p.R * p.C > 128) {
@@ -669,13 +646,10 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   // (ci, dy, dx) = shifted copy dx, channel plane ci, row dy; kl == kc: the zero row/block)
   auto elem_off = [&](int32_t kl) -> int64_t {
     if (o.kind == SPARSE_SPMM) return (int64_t)kl * p.n_tile;
-    if (p.conv_vec == 4) {  // packed: copy (dx, a), channel row ci, tap shift (dy - 1) W - a
-      if (kl == p.kc) return 3 * (int64_t)p.pk_ncls * p.conv_cs + p.pk_bias;
-      const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
-      const int d = (dy - 1) * p.w;
-      const int a = ((d % p.C) + p.C) % p.C;
-      const int k = dx * p.pk_ncls + (p.pk_ncls == 2 ? a : 0);
-      return (int64_t)k * p.conv_cs + (int64_t)ci * p.pk_lc + d - a + p.pk_bias;
+    if (p.conv_vec == 4) {  // packed: im2col row (tap, ci) of the staged tile, row 9 cc = zero
+      if (kl == p.kc) return (int64_t)p.kc * p.n_tile;
+      const int ci = kl / 9, tap = kl % 9;
+      return ((int64_t)tap * p.cc + ci) * p.n_tile;
     }
     if (kl == p.kc) return 3 * (int64_t)p.conv_cs;
     const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
@@ -684,7 +658,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   auto put_spmm = [&](int32_t kl, float w, uint16_t wh) {
     uint8_t rec[8];
     if (f16) {
-      const uint16_t o16 = (uint16_t)(p.conv_vec == 4 ? elem_off(kl) : elem_off(kl) * 2 / 16);
+      const uint16_t o16 = (uint16_t)(elem_off(kl) * 2 / 16);
       std::memcpy(rec, &o16, 2);
       std::memcpy(rec + 2, &wh, 2);
     } else {
@@ -808,18 +782,13 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // tensor memory plans allocate all 512 TMEM columns: one CTA per SM (> half the smem)
     if (p.tm) p.smem_bytes = std::max(p.smem_bytes, 116 * 1024);
   } else if (p.conv_vec == 4) {
-    // packed conv: stage = raw box | plan block | copies (+ zero block), 128-byte aligned parts
+    // packed conv: stage = raw span | plan block | im2col tile, 128-byte aligned parts
     p.pk_blk_at = (p.pk_raw_bytes + 127) & ~127;
     p.pk_cp_at = (p.pk_blk_at + p.max_blk_bytes + 127) & ~127;
     stage_bytes = p.pk_cp_at + p.x_stage_bytes;
-    p.stages = o.stages > 0 ? o.stages : std::max(2, std::min(kMaxStages, 200 * 1024 / stage_bytes));
+    p.stages = o.stages > 0 ? o.stages : std::max(2, std::min(kMaxStages, 210 * 1024 / stage_bytes));
     p.red_bytes = 0;
     p.smem_bytes = p.stages * stage_bytes + 256;
-    const int nthr = 32 * p.warps;
-    if (3 * p.pk_ncls * p.pk_lc > 4 * nthr) {
-      err = "packed conv: too few threads for the copy build (raise warps)";
-      return SPARSE_EUNSUPPORTED;
-    }
   } else if (p.conv_vec == 2) {
     // TMA-fed conv: mbarrier ring as deep as ~200 KB allows (persistent CTAs)
     stage_bytes = (stage_bytes + 127) & ~127;

@@ -257,7 +257,7 @@ __device__ __forceinline__ void run_one_row(float (&acc)[F16 ? 8 : 4], const uin
   if (u < cnt) E::unit(acc, up[u], xs);
 }
 
-template <bool F16, int R, bool BF = false>
+template <bool F16, int R, bool BF = false, int JP = R>
 __device__ __forceinline__ void run_rows(float (&acc)[R][F16 ? 8 : 4], const uint32_t (&h)[R],
                                          const uint4* ents, const uint8_t* xs) {
   using E = EntryOps<F16, BF>;
@@ -265,7 +265,8 @@ __device__ __forceinline__ void run_rows(float (&acc)[R][F16 ? 8 : 4], const uin
 #pragma unroll
   for (int r = 0; r < R; ++r) run_one_row<F16, BF>(acc[r], ents + (h[r] & 0xffffu), 0, (int)(h[r] >> 16), xs);
 #else
-  constexpr int P = (SRT_JOINT == 2 && R > 2) ? 2 : R;  // rows walked jointly
+  // rows walked jointly (JP < R: in groups of JP rows, fewer live plan registers)
+  constexpr int P = (SRT_JOINT == 2 && R > 2) ? 2 : JP;
 #pragma unroll
   for (int r0 = 0; r0 < R; r0 += P) {
     int mn = (int)(h[r0] >> 16);
@@ -1259,120 +1260,50 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
 // ------------------------------------------------------------------ conv 3x3, packed
 // Implicit im2col (Sec. 3.6) with the output positions PACKED: position
 // n = (b * H + y) * W + x of the CNHW output (no padded / junk positions), so the conv is the
-// SpMM Y[C_out x N] = W[C_out x 9 C_in] * X~[9 C_in x N] over a virtual X~ that is never
-// materialised in HBM.  Lane l owns G groups of C = 2 consecutive positions (8-byte fp32 /
-// 4-byte 16-bit loads), n = n0 + g * 64 + 2 l; a tile is NT = 32 * C * G positions of one row
-// panel.  Per chunk of cc input channels the TMA engine stages the RAW input span
-// x[ci][n0 - P0 .. n0 - P0 + RAWN) (one 2-D box over the CNHW input viewed as C_in x N,
-// zero-filled outside), and the CTA's warps build, in shared memory, `ncopies` zero-haloed
-// copies of it in a "halo'd image" coordinate h(n) = b * Simg + W + (n - b * H W) (a zero row
-// above and below every image, Simg >= (H + 2) W): copy (dx, a)[j] = x~[b][r - 1][x + dx - 1]
-// for (b, r, x) = decode(hb + j + a), zero outside the image, hb = h(n0) - W0.  Tap
-// (ci, dy, dx) of the lane's positions is then ONE aligned load at u + (dy - 1) W - a of copy
-// (dx, a) (u = h(n) - hb, a = ((dy - 1) W) mod C): the zero halo resolves the padding
-// statically, every FMA is on a real output position, and the input is read from
-// HBM once.  The build of chunk q + 1 (all warps, each a fixed share of the (copy, j) pairs)
-// overlaps the FMAs of chunk q: ring slot = {raw box, plan block, copies}; full[s] (TMA
-// complete_tx) -> build -> built[s] (one arrive per warp) -> Alg. 3 FMAs (run over the
-// plan's unit entries, k ascending) -> release counter, the last warp refills the slot.
-// Summation order per output: k = (ci * 3 + dy) * 3 + dx ascending, chunks ascending -- the
-// same as every other conv kernel, so results are bitwise equal to them.
+// SpMM Y[C_out x N] = W[C_out x 9 C_in] * X~[9 C_in x N] over a virtual im2col matrix X~
+// that never exists in HBM.  Per chunk of cc input channels the TMA engine stages the RAW
+// input span x[ci][n0 - P0 .. n0 - P0 + RAWN) of the tile's NT positions (2-D boxes over the
+// CNHW input viewed as C_in x N, zero-filled outside), and dedicated BUILDER warps
+// (kPkBuilders warps, warp-specialised like a TMA producer) expands it in shared memory into the
+// chunk's im2col tile: row (tap, ci) = x~[ci][b][y + dy - 1][x + dx - 1] for the NT
+// positions, zero where the tap falls outside the image (the zero padding of P:215 is
+// resolved while building, never in the FMA loop).  The FMA warps then run exactly the SpMM
+// inner loop (run_rows: one 128-bit shared load of the lane's C positions per plan entry) on
+// that tile.  Ring slot = {raw box, plan block, im2col tile}: full[s] (TMA complete_tx) ->
+// builders -> built[s] (one arrive per builder warp) -> FMA warps -> release counter, the last
+// FMA warp refills the slot.  Summation order per output: k = (ci * 3 + dy) * 3 + dx
+// ascending, chunks ascending -- bitwise equal to the other conv kernels.
+constexpr int kPkBuilders = 2;  // builder warps (16 FMA warps + 2 = 576 threads: 112 registers)
 struct PkArgs {
   const uint8_t* blob;
   const int64_t* blk_off;
   const int32_t* row_id;
   uint8_t* y;
   int64_t N;  // B * H * W output positions
-  int32_t H, W, HW, Simg, Bt;
-  int32_t cc, nchunks, Mp, npanels, stages, stage_bytes;
-  int32_t raw_bytes, blk_at, cp_at;  // stage layout (bytes): raw | plan block | copies
-  int32_t rawn, p0, w0, lc, cs, ncls, ncopies, bias_el;
-  int32_t hdr_bytes, bar_off;
+  int32_t H, W, HW;
+  int32_t cc, nchunks, Mp, npanels, stages, stage_bytes, fwarps;
+  int32_t raw_bytes, blk_at, cp_at;  // stage layout (bytes): raw | plan block | im2col tile
+  int32_t rawn, p0, hdr_bytes, bar_off, vec_y;
   const uint8_t* bias;
   float beta;
   int32_t relu;
 };
 
-template <bool F16, bool BF>
-struct PkOps;
-template <bool BF>
-struct PkOps<false, BF> {  // unit = 2 x {uint32 xoff (bytes), float w}; lane loads 2 fp32 per group
-  template <int G>
-  __device__ __forceinline__ static void unit(float (&acc)[2 * G], const uint4 p, const uint8_t* const (&lp)[G]) {
-    const float w0 = __uint_as_float(p.y), w1 = __uint_as_float(p.w);
-    float2 x0[G], x1[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      x0[g] = *(const float2*)(lp[g] + p.x);
-      x1[g] = *(const float2*)(lp[g] + p.z);
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      acc[2 * g] = fmaf(w0, x0[g].x, acc[2 * g]);
-      acc[2 * g + 1] = fmaf(w0, x0[g].y, acc[2 * g + 1]);
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      acc[2 * g] = fmaf(w1, x1[g].x, acc[2 * g]);
-      acc[2 * g + 1] = fmaf(w1, x1[g].y, acc[2 * g + 1]);
-    }
-  }
-};
-template <bool BF>
-struct PkOps<true, BF> {  // unit = 4 x {uint16 xoff (elements), half / bf16 w}; 2 x 16-bit per group
-  template <int G>
-  __device__ __forceinline__ static void unit(float (&acc)[2 * G], const uint4 q, const uint8_t* const (&lp)[G]) {
-    const uint32_t en[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      uint32_t x[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) x[g] = *(const uint32_t*)(lp[g] + ((en[e] & 0xffffu) << 1));
-#pragma unroll
-      for (int g = 0; g < G; ++g) fma_h2<BF>(acc[2 * g], acc[2 * g + 1], (uint16_t)(en[e] >> 16), x[g]);
-    }
-  }
-};
-
-// R rows of one warp over one chunk: rows walked jointly for their common unit count, then
-// each row's remaining units (every row applies its entries in storage = k order).
-template <bool F16, bool BF, int R, int G>
-__device__ __forceinline__ void run_rows_pk(float (&acc)[R][2 * G], const uint32_t (&h)[R], const uint4* ents,
-                                            const uint8_t* const (&lp)[G]) {
-  using E = PkOps<F16, BF>;
-  int mn = (int)(h[0] >> 16);
-#pragma unroll
-  for (int r = 1; r < R; ++r) mn = min(mn, (int)(h[r] >> 16));
-  const uint4* pr[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) pr[r] = ents + (h[r] & 0xffffu);
-#pragma unroll 1
-  for (int u = 0; u < mn; ++u) {
-    uint4 q[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) q[r] = pr[r][u];
-#pragma unroll
-    for (int r = 0; r < R; ++r) E::template unit<G>(acc[r], q[r], lp);
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int cnt = (int)(h[r] >> 16);
-#pragma unroll 1
-    for (int u = mn; u < cnt; ++u) E::template unit<G>(acc[r], pr[r][u], lp);
-  }
-}
-
 template <int R, bool F16, bool BF = false>
-__global__ void __launch_bounds__(512) conv3x3_pk_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                         const PkArgs a) {
-  constexpr int C = 2, G = 2, NT = 32 * C * G;  // positions: per lane-load, groups, per tile
+__global__ void __launch_bounds__(576, 1) conv3x3_pk_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                            const PkArgs a) {
+  constexpr int C = F16 ? 8 : 4;  // positions per lane (16 bytes)
   constexpr int S = F16 ? 2 : 4;
-  constexpr int MAXP = 4;  // (copy, j) build pairs per thread (inspector bound)
+  constexpr int NT = 32 * C;      // positions per tile
+  constexpr int ROWB = NT * S;    // bytes per im2col row
+  constexpr int NB = 32 * kPkBuilders;  // builder threads
+  constexpr int NPAIR = 9 * (NT / C);  // (tap, lane quad) build items per channel
+  constexpr int MAXP = (NPAIR + NB - 1) / NB;
   using T = typename std::conditional<F16, uint16_t, float>::type;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int nwarps = nthr >> 5;
+  const int fw = a.fwarps;  // FMA warps; warps fw .. fw + kPkBuilders - 1 build
   const int np = a.npanels;
   const int64_t ntn = (a.N + NT - 1) / NT;
   const int64_t ntiles = (int64_t)np * ntn;
@@ -1381,16 +1312,16 @@ __global__ void __launch_bounds__(512) conv3x3_pk_kernel(const __grid_constant__
   const uint32_t full0 = smem_u32(smem + a.bar_off);
   const uint32_t built0 = full0 + 8 * kMaxStages;
   uint32_t* ctr = (uint32_t*)(smem + a.bar_off + 16 * kMaxStages);
-  // the zero block after the copies of every stage (target of neutral padding entries)
+  // the zero row after the 9 cc im2col rows of every stage (target of neutral padding entries)
   for (int s = 0; s < a.stages; ++s)
-    for (int i = tid; i < a.lc * S / 16; i += nthr)
-      *(uint4*)(smem + (size_t)s * a.stage_bytes + a.cp_at + (size_t)a.ncopies * a.cs * S + 16 * i) =
+    for (int i = tid; i < ROWB / 16; i += blockDim.x)
+      *(uint4*)(smem + (size_t)s * a.stage_bytes + a.cp_at + (size_t)9 * a.cc * ROWB + 16 * i) =
           make_uint4(0u, 0u, 0u, 0u);
   if (tid < kMaxStages) ctr[tid] = 0u;
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(built0 + 8 * s, (uint32_t)nwarps);
+      mbar_init(built0 + 8 * s, kPkBuilders);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1401,12 +1332,7 @@ __global__ void __launch_bounds__(512) conv3x3_pk_kernel(const __grid_constant__
     panel = (int)(t % np);
     n0 = (t / np) * NT;
   };
-  // halo'd coordinate of position n (n inside image b = n / HW)
-  auto hcoord = [&](int64_t n) -> int64_t {
-    const int64_t b = n / a.HW;
-    return b * a.Simg + a.W + (n - b * a.HW);
-  };
-  auto refill = [&](int q) {  // lane 0 of one warp
+  auto refill = [&](int q) {  // lane 0 of one FMA warp
     const int slot = q % a.stages;
     const int ti = q / a.nchunks, c = q - ti * a.nchunks;
     int panel;
@@ -1419,75 +1345,80 @@ __global__ void __launch_bounds__(512) conv3x3_pk_kernel(const __grid_constant__
     const uint32_t fb = full0 + 8 * slot;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_expect_tx(fb, (uint32_t)a.raw_bytes + nb);
-    tma_load_2d(smem_u32(st), &tmap, (int)(n0 - a.p0), c * a.cc, fb);
+    // the raw span in boxes of at most 256 elements (two halves when RAWN > 256)
+    const int nbox = a.rawn > 256 ? 2 : 1, bw = a.rawn / nbox;
+    for (int i = 0; i < nbox; ++i)  // box i = cc rows of bw elements, at i * cc * bw
+      tma_load_2d(smem_u32(st + (size_t)i * a.cc * bw * S), &tmap, (int)(n0 - a.p0) + i * bw, c * a.cc, fb);
     if (nb) bulk_load(smem_u32(st + a.blk_at), a.blob + blk0, nb, fb);
-  };
-  // build pairs of this thread: pair p = tid + i * nthr -> copy k = p / lc, j = p % lc;
-  // src[i] = raw element of (k, j) for the current tile, or -1 (zero)
-  const int npairs = a.ncopies * a.lc;
-  int src[MAXP];
-  int64_t src_n0 = -1;
-  auto make_src = [&](int64_t n0) {
-    const int64_t hb = hcoord(n0) - a.w0;
-    const int64_t r0 = n0 - a.p0;
-#pragma unroll
-    for (int i = 0; i < MAXP; ++i) {
-      src[i] = -1;
-      const int p = tid + i * nthr;
-      if (p >= npairs) continue;
-      const int k = p / a.lc, j = p - k * a.lc;
-      const int dx = k / a.ncls, cls = k - dx * a.ncls;
-      const int64_t hh = hb + j + cls;  // class copy (dx, a = cls) reads copy dx at j + a
-      if (hh < 0) continue;
-      const int64_t b = hh / a.Simg;
-      const int rem = (int)(hh - b * a.Simg);
-      const int r = rem / a.W, x = rem - r * a.W;
-      const int xs = x + dx - 1;
-      if (b >= a.Bt || r < 1 || r > a.H || xs < 0 || xs >= a.W) continue;
-      const int64_t n = b * a.HW + (int64_t)(r - 1) * a.W + xs - r0;
-      // elements outside the staged span are never read by a tap of the tile (inspector)
-      src[i] = (n >= 0 && n < a.rawn) ? (int)n : -1;
-    }
-  };
-  auto build = [&](int q) {
-    const int slot = q % a.stages;
-    const int ti = q / a.nchunks;
-    int panel;
-    int64_t n0;
-    tile_of(ti, panel, n0);
-    if (n0 != src_n0) {
-      make_src(n0);
-      src_n0 = n0;
-    }
-    uint8_t* st = smem + (size_t)slot * a.stage_bytes;
-    const T* raw = (const T*)st;
-    T* cp = (T*)(st + a.cp_at);
-    mbar_wait(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
-#pragma unroll
-    for (int i = 0; i < MAXP; ++i) {
-      const int p = tid + i * nthr;
-      if (p >= npairs) break;
-      const int k = p / a.lc, j = p - k * a.lc;
-      T* d = cp + (size_t)k * a.cs + j;
-      const int sidx = src[i];
-      if (sidx < 0) {
-        for (int ci = 0; ci < a.cc; ++ci) d[(size_t)ci * a.lc] = T(0);
-      } else {
-        const T* sp = raw + sidx;
-        for (int ci = 0; ci < a.cc; ++ci) d[(size_t)ci * a.lc] = sp[(size_t)ci * a.rawn];
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(built0 + 8 * slot);
   };
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp >= fw) {
+    // ---------------- builder warpgroup: raw span -> im2col rows (tap, ci) of the tile
+    const int bt = tid - fw * 32;
+    const int bw = a.rawn > 256 ? a.rawn / 2 : a.rawn;  // raw box width (refill)
+    int src[MAXP][C];  // raw element of (pair, position) for the current tile, or -1 (zero)
+    int64_t cur_n0 = -1;
+    for (int q = 0; q < total; ++q) {
+      const int slot = q % a.stages;
+      int panel;
+      int64_t n0;
+      tile_of(q / a.nchunks, panel, n0);
+      if (n0 != cur_n0) {  // per tile: decode the positions of this thread's (tap, quad) pairs
+        cur_n0 = n0;
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i) {
+          const int pr = bt + i * NB;
+          const int tap = pr / (NT / C), quad = pr % (NT / C);
+          const int dy = tap / 3, dx = tap % 3;
+          int64_t n = n0 + quad * C;
+          int b = (int)(n / a.HW);
+          int rem = (int)(n - (int64_t)b * a.HW);
+          int y = rem / a.W, x = rem - y * a.W;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const int yy = y + dy - 1, xx = x + dx - 1;
+            const int e = (int)(n - n0) + (dy - 1) * a.W + (dx - 1) + a.p0;  // raw span element
+            src[i][c] = (pr < NPAIR && n < a.N && yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
+                            ? (e < bw ? e : a.cc * bw + e - bw)  // (channel 0 of its box)
+                            : -1;
+            ++n;
+            if (++x == a.W) {
+              x = 0;
+              if (++y == a.H) y = 0;
+            }
+          }
+        }
+      }
+      mbar_wait(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
+      uint8_t* st = smem + (size_t)slot * a.stage_bytes;
+      const T* raw = (const T*)st;
+      uint8_t* cp = st + a.cp_at;
+#pragma unroll
+      for (int i = 0; i < MAXP; ++i) {
+        const int pr = bt + i * NB;
+        if (pr >= NPAIR) break;
+        const int tap = pr / (NT / C), quad = pr % (NT / C);
+        uint8_t* d = cp + (size_t)tap * a.cc * ROWB + quad * 16;
+        for (int ci = 0; ci < a.cc; ++ci) {
+          const T* rp = raw + (size_t)ci * bw;
+          alignas(16) T v[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) v[c] = src[i][c] >= 0 ? rp[src[i][c]] : T(0);
+          *(uint4*)(d + (size_t)ci * ROWB) = *(const uint4*)v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(built0 + 8 * slot);
+    }
+    return;
+  }
+
+  // ---------------- FMA warps (the SpMM executor on the built im2col tile)
   if (warp == 0 && lane == 0)
     for (int q = 0; q < min(a.stages, total); ++q) refill(q);
-  if (total > 0) build(0);
-
-  float acc[R][2 * G];
-  const uint8_t* lp[G];
+  float acc[R][C];
   int q = 0, slot = 0;
   uint32_t ph = 0;
   for (int ti = 0; ti < my_tiles; ++ti) {
@@ -1497,63 +1428,65 @@ __global__ void __launch_bounds__(512) conv3x3_pk_kernel(const __grid_constant__
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int c = 0; c < 2 * G; ++c) acc[r][c] = 0.0f;
-    const int64_t hb = hcoord(n0) - a.w0;
-    int64_t nl[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      nl[g] = n0 + g * (NT / G) + C * lane;
-      // lanes past the end of N read the tile's first position (never stored); per
-      // quarter-warp, so a partly valid quarter keeps its own (in-range) addresses
-      const int64_t nq = n0 + g * (NT / G) + C * (lane & ~7);
-      const int64_t u = (nq < a.N ? hcoord(nl[g]) : hcoord(n0)) - hb;
-      lp[g] = (const uint8_t*)(uintptr_t)((u - a.bias_el) * S);  // + copies base per chunk
-    }
+      for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+    // lanes past the end of N read lane 0's positions (never stored), per quarter-warp
+    const int xoff = n0 + (lane & ~7) * C < a.N ? lane * (C * S) : 0;
     for (int j = 0; j < a.nchunks; ++j) {
-      if (q + 1 < total) build(q + 1);
       mbar_wait(built0 + 8 * slot, ph);
       const uint8_t* st = smem + (size_t)slot * a.stage_bytes;
       const uint32_t* shdr = (const uint32_t*)(st + a.blk_at);
       const uint4* ents = (const uint4*)(st + a.blk_at + a.hdr_bytes);
-      const uint8_t* cpb = st + a.cp_at;
-      const uint8_t* lpc[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) lpc[g] = cpb + (intptr_t)lp[g];
       uint32_t h[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) h[r] = shdr[warp * R + r];
-      run_rows_pk<F16, BF, R, G>(acc, h, ents, lpc);
+      run_rows<F16, R, BF, (R > 2 ? 2 : R)>(acc, h, ents, st + a.cp_at + xoff);
       __syncwarp();
       uint32_t old = 0;
       if (lane == 0)
         asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                      : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
       old = __shfl_sync(0xffffffffu, old, 0);
-      if ((old + 1u) % (uint32_t)nwarps == 0u && q + a.stages < total && lane == 0) refill(q + a.stages);
+      if ((old + 1u) % (uint32_t)fw == 0u && q + a.stages < total && lane == 0) refill(q + a.stages);
       ++q;
       if (++slot == a.stages) {
         slot = 0;
         ph ^= 1u;
       }
     }
-    // epilogue: Y[row][n], CNHW = the flat M x N layout; 2 consecutive positions per store
+    // epilogue: Y[row][n] (CNHW = the flat M x N layout), C consecutive positions per lane
+    const int64_t nl = n0 + lane * C;
+    const int ncol = (int)min((int64_t)C, a.N - nl);
+    if (ncol <= 0) continue;
+    const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int row = a.row_id[(int64_t)panel * a.Mp + warp * R + r];
       if (row < 0) continue;
+      uint8_t* yp = a.y + ((int64_t)row * a.N + nl) * S;
+      if (epi) {
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (nl[g] >= a.N) continue;
-        uint8_t* yp = a.y + ((int64_t)row * a.N + nl[g]) * S;
-        float v0 = acc[r][2 * g], v1 = acc[r][2 * g + 1];
-        if (a.bias != nullptr || a.beta != 0.0f || a.relu) {
-          v0 = epilogue_one<F16, BF>(v0, a.bias, row, a.beta, yp, a.relu);
-          v1 = epilogue_one<F16, BF>(v1, a.bias, row, a.beta, yp + S, a.relu);
+        for (int c = 0; c < C; ++c)
+          if (c < ncol) acc[r][c] = epilogue_one<F16, BF>(acc[r][c], a.bias, row, a.beta, yp + c * S, a.relu);
+      }
+      if (F16) {
+        alignas(16) uint16_t hv[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) hv[c] = to16<BF>(acc[r][c]);
+        if (a.vec_y && ncol == C) {
+          *(uint4*)yp = *(const uint4*)hv;
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (c < ncol) ((uint16_t*)yp)[c] = hv[c];
         }
-        if (F16)
-          *(uint32_t*)yp = (uint32_t)to16<BF>(v0) | ((uint32_t)to16<BF>(v1) << 16);
-        else
-          *(float2*)yp = make_float2(v0, v1);
+      } else {
+        if (a.vec_y && ncol == C) {
+          *(float4*)yp = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (c < ncol) ((float*)yp)[c] = acc[r][c];
+        }
       }
     }
   }
@@ -2512,7 +2445,7 @@ static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, 
   PkFn fn = nullptr;
 #define SRT_P(RR) \
   if (p.R == RR) fn = bf ? conv3x3_pk_kernel<RR, true, true> : f16 ? conv3x3_pk_kernel<RR, true> : conv3x3_pk_kernel<RR, false>;
-  SRT_P(2) SRT_P(4) SRT_P(8) SRT_P(16)
+  SRT_P(1) SRT_P(2) SRT_P(4) SRT_P(8)
 #undef SRT_P
   auto encode = tensor_map_encoder();
   if (!fn || !encode) {
@@ -2548,7 +2481,7 @@ static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, 
   std::memset(&tmap, 0, sizeof tmap);
   cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)p.c_in};
   cuuint64_t strides[1] = {(cuuint64_t)(ldx * S)};
-  cuuint32_t box[2] = {(cuuint32_t)p.pk_rawn, (cuuint32_t)p.cc};
+  cuuint32_t box[2] = {(cuuint32_t)(p.pk_rawn > 256 ? p.pk_rawn / 2 : p.pk_rawn), (cuuint32_t)p.cc};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(&tmap, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                       const_cast<void*>(xa), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -2566,33 +2499,28 @@ static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, 
   a.H = p.h;
   a.W = p.w;
   a.HW = p.h * p.w;
-  a.Simg = p.conv_simg;
-  a.Bt = (int32_t)batch;
   a.cc = p.cc;
   a.nchunks = p.nchunks;
   a.Mp = p.Mp;
   a.npanels = p.npanels;
   a.stages = p.stages;
+  a.fwarps = p.warps;
   a.raw_bytes = p.pk_raw_bytes;
   a.blk_at = p.pk_blk_at;
   a.cp_at = p.pk_cp_at;
   a.stage_bytes = p.pk_cp_at + p.x_stage_bytes;
   a.rawn = p.pk_rawn;
   a.p0 = p.pk_p0;
-  a.w0 = p.pk_w0;
-  a.lc = p.pk_lc;
-  a.cs = p.conv_cs;
-  a.ncls = p.pk_ncls;
-  a.ncopies = 3 * p.pk_ncls;
-  a.bias_el = p.pk_bias;
   a.hdr_bytes = p.hdr_bytes;
   a.bar_off = p.smem_bytes - 256;
+  a.vec_y = ((uintptr_t)y % 16 == 0) && ((N * S) % 16 == 0);
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
+  const int threads = (p.warps + kPkBuilders) * 32;  // FMA warps + the builder warps
   int sms = 148, per_sm = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p.warps * 32, p.smem_bytes) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, p.smem_bytes) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
   cudaGetLastError();
@@ -2600,7 +2528,7 @@ static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, 
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ntot, (int64_t)sms * per_sm)), 1, 1);
-  cfg.blockDim = dim3((unsigned)(p.warps * 32), 1, 1);
+  cfg.blockDim = dim3((unsigned)threads, 1, 1);
   cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
