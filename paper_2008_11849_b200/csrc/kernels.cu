@@ -91,6 +91,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// the same wait with a suspend-time hint: the warp sleeps until the phase completes (or the
+// hint elapses) instead of re-polling, so waiting warps do not steal issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(0x100000u)
+        : "memory");
+  } while (!done);
+}
 // TMA: 2-D tile of X (coordinates {n, k}) -> smem, completion on an mbarrier
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint32_t bar) {
@@ -1273,7 +1287,7 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
 // builders -> built[s] (one arrive per builder warp) -> FMA warps -> release counter, the last
 // FMA warp refills the slot.  Summation order per output: k = (ci * 3 + dy) * 3 + dx
 // ascending, chunks ascending -- bitwise equal to the other conv kernels.
-constexpr int kPkBuilders = 2;  // builder warps (16 FMA warps + 2 = 576 threads: 112 registers)
+constexpr int kPkBuilders = 4;  // builder warps (one warpgroup)
 struct PkArgs {
   const uint8_t* blob;
   const int64_t* blk_off;
@@ -1290,15 +1304,12 @@ struct PkArgs {
 };
 
 template <int R, bool F16, bool BF = false>
-__global__ void __launch_bounds__(576, 1) conv3x3_pk_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constant__ CUtensorMap tmap,
                                                             const PkArgs a) {
   constexpr int C = F16 ? 8 : 4;  // positions per lane (16 bytes)
   constexpr int S = F16 ? 2 : 4;
   constexpr int NT = 32 * C;      // positions per tile
   constexpr int ROWB = NT * S;    // bytes per im2col row
-  constexpr int NB = 32 * kPkBuilders;  // builder threads
-  constexpr int NPAIR = 9 * (NT / C);  // (tap, lane quad) build items per channel
-  constexpr int MAXP = (NPAIR + NB - 1) / NB;
   using T = typename std::conditional<F16, uint16_t, float>::type;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
@@ -1355,58 +1366,49 @@ __global__ void __launch_bounds__(576, 1) conv3x3_pk_kernel(const __grid_constan
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp >= fw) {
-    // ---------------- builder warpgroup: raw span -> im2col rows (tap, ci) of the tile
-    const int bt = tid - fw * 32;
+    // ---------------- builder warps: raw span -> im2col rows (tap, ci) of the tile.  Builder
+    // warp w takes rows tap * cc + ci = w, w + nbw, ...; lane l writes positions l + 32 k
+    // (k < C) of a row: conflict-free scalar loads of the raw span (shifted by the tap) and
+    // stores; mask bit (tap, k) = position l + 32 k has tap (dy, dx) inside its image.
+    const int bw_id = warp - fw;
     const int bw = a.rawn > 256 ? a.rawn / 2 : a.rawn;  // raw box width (refill)
-    int src[MAXP][C];  // raw element of (pair, position) for the current tile, or -1 (zero)
+    const int rows = 9 * a.cc;
+    uint32_t mask[C];  // bit tap of mask[k]: position l + 32 k has tap (dy, dx) inside its image
     int64_t cur_n0 = -1;
     for (int q = 0; q < total; ++q) {
       const int slot = q % a.stages;
       int panel;
       int64_t n0;
       tile_of(q / a.nchunks, panel, n0);
-      if (n0 != cur_n0) {  // per tile: decode the positions of this thread's (tap, quad) pairs
+      if (n0 != cur_n0) {
         cur_n0 = n0;
 #pragma unroll
-        for (int i = 0; i < MAXP; ++i) {
-          const int pr = bt + i * NB;
-          const int tap = pr / (NT / C), quad = pr % (NT / C);
-          const int dy = tap / 3, dx = tap % 3;
-          int64_t n = n0 + quad * C;
-          int b = (int)(n / a.HW);
-          int rem = (int)(n - (int64_t)b * a.HW);
-          int y = rem / a.W, x = rem - y * a.W;
+        for (int k = 0; k < C; ++k) {
+          const int64_t n = n0 + lane + 32 * k;
+          const int b = (int)(n / a.HW);
+          const int rem = (int)(n - (int64_t)b * a.HW);
+          const int y = rem / a.W, x = rem - y * a.W;
+          mask[k] = 0;
 #pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const int yy = y + dy - 1, xx = x + dx - 1;
-            const int e = (int)(n - n0) + (dy - 1) * a.W + (dx - 1) + a.p0;  // raw span element
-            src[i][c] = (pr < NPAIR && n < a.N && yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
-                            ? (e < bw ? e : a.cc * bw + e - bw)  // (channel 0 of its box)
-                            : -1;
-            ++n;
-            if (++x == a.W) {
-              x = 0;
-              if (++y == a.H) y = 0;
-            }
+          for (int tap = 0; tap < 9; ++tap) {
+            const int yy = y + tap / 3 - 1, xx = x + tap % 3 - 1;
+            if (n < a.N && yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) mask[k] |= 1u << tap;
           }
         }
       }
-      mbar_wait(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
+      mbar_wait_sleep(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
       uint8_t* st = smem + (size_t)slot * a.stage_bytes;
       const T* raw = (const T*)st;
-      uint8_t* cp = st + a.cp_at;
+      T* cp = (T*)(st + a.cp_at);
+      for (int rw = bw_id; rw < rows; rw += kPkBuilders) {
+        const int tap = rw / a.cc, ci = rw - tap * a.cc;
+        const int sh = (tap / 3 - 1) * a.W + (tap % 3 - 1) + a.p0;  // raw element of position 0
+        T* d = cp + (size_t)rw * NT + lane;
 #pragma unroll
-      for (int i = 0; i < MAXP; ++i) {
-        const int pr = bt + i * NB;
-        if (pr >= NPAIR) break;
-        const int tap = pr / (NT / C), quad = pr % (NT / C);
-        uint8_t* d = cp + (size_t)tap * a.cc * ROWB + quad * 16;
-        for (int ci = 0; ci < a.cc; ++ci) {
-          const T* rp = raw + (size_t)ci * bw;
-          alignas(16) T v[C];
-#pragma unroll
-          for (int c = 0; c < C; ++c) v[c] = src[i][c] >= 0 ? rp[src[i][c]] : T(0);
-          *(uint4*)(d + (size_t)ci * ROWB) = *(const uint4*)v;
+        for (int k = 0; k < C; ++k) {
+          const int e = lane + 32 * k + sh;
+          const int idx = e < bw ? ci * bw + e : a.cc * bw + ci * bw + e - bw;  // box 0 / box 1
+          d[32 * k] = ((mask[k] >> tap) & 1u) ? raw[idx] : T(0);
         }
       }
       __syncwarp();
@@ -1432,7 +1434,7 @@ __global__ void __launch_bounds__(576, 1) conv3x3_pk_kernel(const __grid_constan
     // lanes past the end of N read lane 0's positions (never stored), per quarter-warp
     const int xoff = n0 + (lane & ~7) * C < a.N ? lane * (C * S) : 0;
     for (int j = 0; j < a.nchunks; ++j) {
-      mbar_wait(built0 + 8 * slot, ph);
+      mbar_wait_sleep(built0 + 8 * slot, ph);
       const uint8_t* st = smem + (size_t)slot * a.stage_bytes;
       const uint32_t* shdr = (const uint32_t*)(st + a.blk_at);
       const uint4* ents = (const uint4*)(st + a.blk_at + a.hdr_bytes);
