@@ -467,7 +467,9 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
           p.conv_sci = NTv;
           p.conv_stage_elems = (9 * ccp + 1) * NTv;  // im2col rows + the zero row
           p.x_stage_bytes = (int)(((int64_t)p.conv_stage_elems * S + 127) & ~int64_t(127));
-          p.pk_raw_bytes = ccp * p.pk_rawn * S;
+          // raw span: one TMA box, or two when RAWN > 256 (the second at a 128-byte boundary)
+          p.pk_raw_bytes = p.pk_rawn > 256 ? ((ccp * (p.pk_rawn / 2) * S + 127) / 128 * 128) * 2
+                                           : ccp * p.pk_rawn * S;
         } else if (o.conv_vec == 2 && wpv <= 64) {  // (pad_conv_input holds a padded row in registers)
           // TMA-fed variant (conv3x3_tma_kernel): each shifted copy is one 4-D TMA box
           // {wp, rb + 2, 1 image, cc channels} of the width-padded input (no guard), at a

@@ -1297,7 +1297,7 @@ struct PkArgs {
   int32_t H, W, HW;
   int32_t cc, nchunks, Mp, npanels, stages, stage_bytes, fwarps;
   int32_t raw_bytes, blk_at, cp_at;  // stage layout (bytes): raw | plan block | im2col tile
-  int32_t rawn, p0, hdr_bytes, bar_off, vec_y;
+  int32_t rawn, p0, hdr_bytes, bar_off, vec_y, box1_at;
   const uint8_t* bias;
   float beta;
   int32_t relu;
@@ -1355,11 +1355,11 @@ __global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constan
     uint8_t* st = smem + (size_t)slot * a.stage_bytes;
     const uint32_t fb = full0 + 8 * slot;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive_expect_tx(fb, (uint32_t)a.raw_bytes + nb);
+    mbar_arrive_expect_tx(fb, (uint32_t)(a.cc * a.rawn * S) + nb);  // TMA bytes (no padding)
     // the raw span in boxes of at most 256 elements (two halves when RAWN > 256)
     const int nbox = a.rawn > 256 ? 2 : 1, bw = a.rawn / nbox;
-    for (int i = 0; i < nbox; ++i)  // box i = cc rows of bw elements, at i * cc * bw
-      tma_load_2d(smem_u32(st + (size_t)i * a.cc * bw * S), &tmap, (int)(n0 - a.p0) + i * bw, c * a.cc, fb);
+    for (int i = 0; i < nbox; ++i)  // box i = cc rows of bw elements, at i * box1_at (128-B aligned)
+      tma_load_2d(smem_u32(st + (size_t)i * a.box1_at), &tmap, (int)(n0 - a.p0) + i * bw, c * a.cc, fb);
     if (nb) bulk_load(smem_u32(st + a.blk_at), a.blob + blk0, nb, fb);
   };
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1398,17 +1398,30 @@ __global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constan
       }
       mbar_wait_sleep(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
       uint8_t* st = smem + (size_t)slot * a.stage_bytes;
-      const T* raw = (const T*)st;
-      T* cp = (T*)(st + a.cp_at);
-      for (int rw = bw_id; rw < rows; rw += kPkBuilders) {
-        const int tap = rw / a.cc, ci = rw - tap * a.cc;
+      uint8_t* cp = st + a.cp_at;
+      // rows (tap, ci) with ci = bw_id (mod kPkBuilders); per tap the lane's C raw elements
+      // (position l + 32 k shifted by the tap; box 1 for the upper half of a 2-box span)
+#pragma unroll 1
+      for (int tap = 0; tap < 9; ++tap) {
         const int sh = (tap / 3 - 1) * a.W + (tap % 3 - 1) + a.p0;  // raw element of position 0
-        T* d = cp + (size_t)rw * NT + lane;
+        const uint8_t* rp[C];
+        bool ok[C];
 #pragma unroll
         for (int k = 0; k < C; ++k) {
           const int e = lane + 32 * k + sh;
-          const int idx = e < bw ? ci * bw + e : a.cc * bw + ci * bw + e - bw;  // box 0 / box 1
-          d[32 * k] = ((mask[k] >> tap) & 1u) ? raw[idx] : T(0);
+          rp[k] = st + (e < bw ? (size_t)e * S : (size_t)a.box1_at + (size_t)(e - bw) * S) + (size_t)bw_id * bw * S;
+          ok[k] = (mask[k] >> tap) & 1u;
+        }
+        uint8_t* d = cp + ((size_t)tap * a.cc + bw_id) * ROWB + lane * S;
+#pragma unroll 1
+        for (int ci = bw_id; ci < a.cc; ci += kPkBuilders) {
+#pragma unroll
+          for (int k = 0; k < C; ++k) {
+            const T v = ok[k] ? *(const T*)rp[k] : T(0);
+            *(T*)(d + k * 32 * S) = v;
+            rp[k] += (size_t)kPkBuilders * bw * S;
+          }
+          d += (size_t)kPkBuilders * ROWB;
         }
       }
       __syncwarp();
@@ -2516,6 +2529,7 @@ static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, 
   a.hdr_bytes = p.hdr_bytes;
   a.bar_off = p.smem_bytes - 256;
   a.vec_y = ((uintptr_t)y % 16 == 0) && ((N * S) % 16 == 0);
+  a.box1_at = p.pk_rawn > 256 ? (p.cc * (p.pk_rawn / 2) * S + 127) / 128 * 128 : 0;
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
