@@ -1396,7 +1396,7 @@ __global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constan
           }
         }
       }
-      mbar_wait_sleep(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
+      mbar_wait(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
       uint8_t* st = smem + (size_t)slot * a.stage_bytes;
       uint8_t* cp = st + a.cp_at;
       // rows (tap, ci) with ci = bw_id (mod kPkBuilders); per tap the lane's C raw elements
@@ -1447,7 +1447,7 @@ __global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constan
     // lanes past the end of N read lane 0's positions (never stored), per quarter-warp
     const int xoff = n0 + (lane & ~7) * C < a.N ? lane * (C * S) : 0;
     for (int j = 0; j < a.nchunks; ++j) {
-      mbar_wait_sleep(built0 + 8 * slot, ph);
+      mbar_wait(built0 + 8 * slot, ph);
       const uint8_t* st = smem + (size_t)slot * a.stage_bytes;
       const uint32_t* shdr = (const uint32_t*)(st + a.blk_at);
       const uint4* ents = (const uint4*)(st + a.blk_at + a.hdr_bytes);
