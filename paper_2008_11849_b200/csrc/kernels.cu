@@ -1277,17 +1277,17 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
 // SpMM Y[C_out x N] = W[C_out x 9 C_in] * X~[9 C_in x N] over a virtual im2col matrix X~
 // that never exists in HBM.  Per chunk of cc input channels the TMA engine stages the RAW
 // input span x[ci][n0 - P0 .. n0 - P0 + RAWN) of the tile's NT positions (2-D boxes over the
-// CNHW input viewed as C_in x N, zero-filled outside), and the CTA's warps expand it in
-// shared memory into the chunk's im2col tile: row (tap, ci) = x~[ci][b][y + dy - 1][x + dx - 1]
-// for the NT positions, zero where the tap falls outside the image (the zero padding of P:215
-// is resolved while building, never in the FMA loop).  The warps then run exactly the SpMM
+// CNHW input viewed as C_in x N, zero-filled outside), and dedicated BUILDER warps
+// (kPkBuilders warps, warp-specialised like a TMA producer) expands it in shared memory into the
+// chunk's im2col tile: row (tap, ci) = x~[ci][b][y + dy - 1][x + dx - 1] for the NT
+// positions, zero where the tap falls outside the image (the zero padding of P:215 is
+// resolved while building, never in the FMA loop).  The FMA warps then run exactly the SpMM
 // inner loop (run_rows: one 128-bit shared load of the lane's C positions per plan entry) on
 // that tile.  Ring slot = {raw box, plan block, im2col tile}: full[s] (TMA complete_tx) ->
-// every warp builds its share of the tile D chunks ahead -> built[s] (one arrive per warp) ->
-// FMAs -> release counter, the last warp refills the slot.  (Dedicated builder warps were
-// measured slower: a fifth warp per SMSP caps ptxas at 96 registers and four warps could not
-// keep up with the build.)  Summation order per output: k = (ci * 3 + dy) * 3 + dx ascending,
-// chunks ascending -- bitwise equal to the other conv kernels.
+// builders -> built[s] (one arrive per builder warp) -> FMA warps -> release counter, the last
+// FMA warp refills the slot.  Summation order per output: k = (ci * 3 + dy) * 3 + dx
+// ascending, chunks ascending -- bitwise equal to the other conv kernels.
+constexpr int kPkBuilders = 4;  // builder warps (one warpgroup)
 struct PkArgs {
   const uint8_t* blob;
   const int64_t* blk_off;
@@ -1295,7 +1295,7 @@ struct PkArgs {
   uint8_t* y;
   int64_t N;  // B * H * W output positions
   int32_t H, W, HW;
-  int32_t cc, nchunks, Mp, npanels, stages, stage_bytes;
+  int32_t cc, nchunks, Mp, npanels, stages, stage_bytes, fwarps;
   int32_t raw_bytes, blk_at, cp_at;  // stage layout (bytes): raw | plan block | im2col tile
   int32_t rawn, p0, hdr_bytes, bar_off, vec_y, box1_at;
   const uint8_t* bias;
@@ -1304,7 +1304,7 @@ struct PkArgs {
 };
 
 template <int R, bool F16, bool BF = false>
-__global__ void __launch_bounds__(512, 1) conv3x3_pk_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constant__ CUtensorMap tmap,
                                                             const PkArgs a) {
   constexpr int C = F16 ? 8 : 4;  // positions per lane (16 bytes)
   constexpr int S = F16 ? 2 : 4;
@@ -1314,7 +1314,7 @@ __global__ void __launch_bounds__(512, 1) conv3x3_pk_kernel(const __grid_constan
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int nw = blockDim.x >> 5;
+  const int fw = a.fwarps;  // FMA warps; warps fw .. fw + kPkBuilders - 1 build
   const int np = a.npanels;
   const int64_t ntn = (a.N + NT - 1) / NT;
   const int64_t ntiles = (int64_t)np * ntn;
@@ -1332,7 +1332,7 @@ __global__ void __launch_bounds__(512, 1) conv3x3_pk_kernel(const __grid_constan
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(built0 + 8 * s, (uint32_t)nw);
+      mbar_init(built0 + 8 * s, kPkBuilders);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1343,8 +1343,7 @@ __global__ void __launch_bounds__(512, 1) conv3x3_pk_kernel(const __grid_constan
     panel = (int)(t % np);
     n0 = (t / np) * NT;
   };
-  const int bw = a.rawn > 256 ? a.rawn / 2 : a.rawn;  // raw box width
-  auto refill = [&](int q) {  // lane 0 of one warp
+  auto refill = [&](int q) {  // lane 0 of one FMA warp
     const int slot = q % a.stages;
     const int ti = q / a.nchunks, c = q - ti * a.nchunks;
     int panel;
@@ -1357,77 +1356,83 @@ __global__ void __launch_bounds__(512, 1) conv3x3_pk_kernel(const __grid_constan
     const uint32_t fb = full0 + 8 * slot;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_expect_tx(fb, (uint32_t)(a.cc * a.rawn * S) + nb);  // TMA bytes (no padding)
-    const int nbox = a.rawn > 256 ? 2 : 1;
+    // the raw span in boxes of at most 256 elements (two halves when RAWN > 256)
+    const int nbox = a.rawn > 256 ? 2 : 1, bw = a.rawn / nbox;
     for (int i = 0; i < nbox; ++i)  // box i = cc rows of bw elements, at i * box1_at (128-B aligned)
       tma_load_2d(smem_u32(st + (size_t)i * a.box1_at), &tmap, (int)(n0 - a.p0) + i * bw, c * a.cc, fb);
     if (nb) bulk_load(smem_u32(st + a.blk_at), a.blob + blk0, nb, fb);
   };
-  // ---- im2col build of chunk qb: warp w writes rows (tap, ci) = w, w + nw, ... of the tile;
-  // lane l writes positions l + 32 k (k < C): conflict-free scalar loads of the raw span
-  // shifted by the tap and scalar stores; mask[k] bit tap = position l + 32 k has tap
-  // (dy, dx) inside its image (zero otherwise: the padding of P:215 resolved here)
-  uint32_t mask[C];
-  int64_t mask_n0 = -1;
-  auto build = [&](int qb) {
-    const int slot = qb % a.stages;
-    int panel;
-    int64_t n0;
-    tile_of(qb / a.nchunks, panel, n0);
-    if (n0 != mask_n0) {
-      mask_n0 = n0;
-#pragma unroll
-      for (int k = 0; k < C; ++k) {
-        const int64_t n = n0 + lane + 32 * k;
-        const int b = (int)(n / a.HW);
-        const int rem = (int)(n - (int64_t)b * a.HW);
-        const int y = rem / a.W, x = rem - y * a.W;
-        uint32_t m = 0;
-#pragma unroll
-        for (int tap = 0; tap < 9; ++tap) {
-          const int yy = y + tap / 3 - 1, xx = x + tap % 3 - 1;
-          if (n < a.N && yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) m |= 1u << tap;
-        }
-        mask[k] = m;
-      }
-    }
-    mbar_wait(full0 + 8 * slot, (uint32_t)((qb / a.stages) & 1));
-    uint8_t* st = smem + (size_t)slot * a.stage_bytes;
-    uint8_t* cp = st + a.cp_at + lane * S;
-    const int rows = 9 * a.cc;
-#pragma unroll 1
-    for (int rw = warp; rw < rows; rw += nw) {
-      const int tap = rw / a.cc, ci = rw - tap * a.cc;
-      const int sh = (tap / 3 - 1) * a.W + (tap % 3 - 1) + a.p0 + lane;  // raw element of position l
-      uint8_t* d = cp + (size_t)rw * ROWB;
-      T v[C];
-      if (a.rawn <= 256) {
-        const T* rp = (const T*)st + (size_t)ci * bw + sh;
-#pragma unroll
-        for (int k = 0; k < C; ++k) v[k] = ((mask[k] >> tap) & 1u) ? rp[32 * k] : T(0);
-      } else {
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-          const int e = sh + 32 * k;
-          const T* rp = (const T*)(st + (e < bw ? (size_t)0 : (size_t)a.box1_at)) + (size_t)ci * bw + (e < bw ? e : e - bw);
-          v[k] = ((mask[k] >> tap) & 1u) ? *rp : T(0);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < C; ++k) *(T*)(d + k * 32 * S) = v[k];
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(built0 + 8 * slot);
-  };
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp >= fw) {
+    // ---------------- builder warps: raw span -> im2col rows (tap, ci) of the tile.  Builder
+    // warp w takes rows tap * cc + ci = w, w + nbw, ...; lane l writes positions l + 32 k
+    // (k < C) of a row: conflict-free scalar loads of the raw span (shifted by the tap) and
+    // stores; mask bit (tap, k) = position l + 32 k has tap (dy, dx) inside its image.
+    const int bw_id = warp - fw;
+    const int bw = a.rawn > 256 ? a.rawn / 2 : a.rawn;  // raw box width (refill)
+    const int rows = 9 * a.cc;
+    uint32_t mask[C];  // bit tap of mask[k]: position l + 32 k has tap (dy, dx) inside its image
+    int64_t cur_n0 = -1;
+    for (int q = 0; q < total; ++q) {
+      const int slot = q % a.stages;
+      int panel;
+      int64_t n0;
+      tile_of(q / a.nchunks, panel, n0);
+      if (n0 != cur_n0) {
+        cur_n0 = n0;
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          const int64_t n = n0 + lane + 32 * k;
+          const int b = (int)(n / a.HW);
+          const int rem = (int)(n - (int64_t)b * a.HW);
+          const int y = rem / a.W, x = rem - y * a.W;
+          mask[k] = 0;
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int yy = y + tap / 3 - 1, xx = x + tap % 3 - 1;
+            if (n < a.N && yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) mask[k] |= 1u << tap;
+          }
+        }
+      }
+      mbar_wait(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
+      uint8_t* st = smem + (size_t)slot * a.stage_bytes;
+      uint8_t* cp = st + a.cp_at;
+      // rows (tap, ci) with ci = bw_id (mod kPkBuilders); per tap the lane's C raw elements
+      // (position l + 32 k shifted by the tap; box 1 for the upper half of a 2-box span)
+#pragma unroll 1
+      for (int tap = 0; tap < 9; ++tap) {
+        const int sh = (tap / 3 - 1) * a.W + (tap % 3 - 1) + a.p0;  // raw element of position 0
+        const uint8_t* rp[C];
+        bool ok[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          const int e = lane + 32 * k + sh;
+          rp[k] = st + (e < bw ? (size_t)e * S : (size_t)a.box1_at + (size_t)(e - bw) * S) + (size_t)bw_id * bw * S;
+          ok[k] = (mask[k] >> tap) & 1u;
+        }
+        uint8_t* d = cp + ((size_t)tap * a.cc + bw_id) * ROWB + lane * S;
+#pragma unroll 1
+        for (int ci = bw_id; ci < a.cc; ci += kPkBuilders) {
+#pragma unroll
+          for (int k = 0; k < C; ++k) {
+            const T v = ok[k] ? *(const T*)rp[k] : T(0);
+            *(T*)(d + k * 32 * S) = v;
+            rp[k] += (size_t)kPkBuilders * bw * S;
+          }
+          d += (size_t)kPkBuilders * ROWB;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(built0 + 8 * slot);
+    }
+    return;
+  }
+
+  // ---------------- FMA warps (the SpMM executor on the built im2col tile)
   if (warp == 0 && lane == 0)
     for (int q = 0; q < min(a.stages, total); ++q) refill(q);
-  // tiles are built D chunks ahead of the FMAs: a warp waits on built[q] only for the warps
-  // that have not yet reached iteration q - D (bounded drift); D <= S - 2 keeps the refills
-  // of the ring one chunk ahead of the builds
-  const int D = max(1, min(a.stages - 2, 2));
-  for (int qq = 0; qq < min(D, total); ++qq) build(qq);
-
   float acc[R][C];
   int q = 0, slot = 0;
   uint32_t ph = 0;
@@ -1442,7 +1447,6 @@ __global__ void __launch_bounds__(512, 1) conv3x3_pk_kernel(const __grid_constan
     // lanes past the end of N read lane 0's positions (never stored), per quarter-warp
     const int xoff = n0 + (lane & ~7) * C < a.N ? lane * (C * S) : 0;
     for (int j = 0; j < a.nchunks; ++j) {
-      if (q + D < total) build(q + D);
       mbar_wait(built0 + 8 * slot, ph);
       const uint8_t* st = smem + (size_t)slot * a.stage_bytes;
       const uint32_t* shdr = (const uint32_t*)(st + a.blk_at);
@@ -1450,14 +1454,14 @@ __global__ void __launch_bounds__(512, 1) conv3x3_pk_kernel(const __grid_constan
       uint32_t h[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) h[r] = shdr[warp * R + r];
-      run_rows<F16, R, BF>(acc, h, ents, st + a.cp_at + xoff);
+      run_rows<F16, R, BF, (R > 2 ? 2 : R)>(acc, h, ents, st + a.cp_at + xoff);
       __syncwarp();
       uint32_t old = 0;
       if (lane == 0)
         asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                      : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
       old = __shfl_sync(0xffffffffu, old, 0);
-      if ((old + 1u) % (uint32_t)nw == 0u && q + a.stages < total && lane == 0) refill(q + a.stages);
+      if ((old + 1u) % (uint32_t)fw == 0u && q + a.stages < total && lane == 0) refill(q + a.stages);
       ++q;
       if (++slot == a.stages) {
         slot = 0;
@@ -2515,6 +2519,7 @@ static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, 
   a.Mp = p.Mp;
   a.npanels = p.npanels;
   a.stages = p.stages;
+  a.fwarps = p.warps;
   a.raw_bytes = p.pk_raw_bytes;
   a.blk_at = p.pk_blk_at;
   a.cp_at = p.pk_cp_at;
@@ -2528,7 +2533,7 @@ static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, 
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
-  const int threads = p.warps * 32;
+  const int threads = (p.warps + kPkBuilders) * 32;  // FMA warps + the builder warps
   int sms = 148, per_sm = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, p.smem_bytes) != cudaSuccess ||

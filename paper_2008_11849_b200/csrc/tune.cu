@@ -130,12 +130,12 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
   } else {
     // vectorised kernels (16-byte loads of consecutive positions; TMA-fed = 2, register-
     // staged = 1) and the position-strided one (0); cc = channels per chunk (0: inspector)
-    for (int vec : {2, 1, 0})
+    for (int vec : {2, 4, 1, 0})
       for (int R : {2, 4, 8})
         for (int w : {8, 16})
           for (int cc : {0, 8, 16, 24, 32}) {
             if (!vec && w == 16) continue;  // the position-strided kernel runs <= 8 warps
-            if (vec == 2 ? cc == 8 : (cc == 0 || cc == 24)) continue;
+            if (vec == 4 ? (R != 8 || w != 16 || cc == 0 || cc > 16) : vec == 2 ? cc == 8 : (cc == 0 || cc == 24)) continue;
             BuildOpts o = base;
             o.rows_per_warp = R;
             o.warps = w;

@@ -841,3 +841,94 @@ def test_tune_keeps_current_device():
     w = gen.pruned_weights(128, 128, 90, seed=3)
     plan = srt.Plan.from_csr(w, n_hint=1024, tune=1, device=0)
     assert torch.cuda.current_device() == 0 and plan.info["tuned_us"] > 0
+
+
+# --------------------------------------------------------------------------- the timed configurations
+
+import glob as _glob
+import json as _json
+import os as _os
+
+_ROOT = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+
+
+def _tuned_cases():
+    import bench
+    cases = []
+    for path in sorted(_glob.glob(_os.path.join(_ROOT, "profiles", "tuned_*.json"))):
+        m = _os.path.basename(path)[len("tuned_"):-len(".json")].split("_")
+        # tuned_<workload>_<dtype>_s<sparsity>_x<executor>.json
+        wl, dt, sp = "_".join(m[:-3]), m[-3], int(m[-2][1:])
+        layers, _, _ = bench.workload_layers(wl, 1, 0)
+        opts = _json.load(open(path))
+        for L in layers:
+            if L["name"] in opts:
+                cases.append(pytest.param(L, dt, sp, opts[L["name"]], id=f"{wl}-{dt}-s{sp}-{L['name']}"))
+    return cases
+
+
+@pytest.mark.parametrize("L,dt,sp,opts", _tuned_cases())
+def test_tuned_configuration_exact_at_full_size(L, dt, sp, opts):
+    # every configuration bench.py times (profiles/tuned_*.json), built with exactly those options
+    # at the workload's full size, on integer data: sampled outputs bitwise equal to the oracle
+    import bench
+    dev = _dev()
+    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[dt]
+    w, x = bench.make_inputs(L, sp, 0, integer=True, f16=dt != "f32")
+    if L["kind"] == "spmm":
+        plan = srt.Plan.from_csr(w, dtype=tdt, n_hint=L["N"], **opts)
+        Y = plan.spmm(torch.from_numpy(x).to(dev).to(tdt))
+        ids = np.unique(np.r_[0, L["N"] - 1, np.random.default_rng(1).integers(0, L["N"], 48)])
+        ref = oracle.spmm(w.M, w.K, w.row_ptr, w.col_idx, w.values.astype(np.float64), x[:, ids].astype(np.float64))
+    else:
+        plan = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=L["c_in"], h=L["H"], w=L["W"],
+                                 n_hint=L["B"], **opts)
+        Y = plan.conv3x3(torch.from_numpy(x).to(dev).to(tdt))
+        ids = np.array([0, 37, 128, 255])
+        ref = oracle.conv3x3(w.M, w.row_ptr, w.col_idx, w.values.astype(np.float64), x[:, ids].astype(np.float64))
+    torch.cuda.synchronize()
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    got = Y[:, torch.from_numpy(ids).to(dev)].double().cpu().numpy()
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f16"])
+def test_bert_full_size_real_valued(dt):
+    # BASELINE configs[3] at full size (N = 32 x 512) with the real-valued synthetic inputs and the
+    # tuned options bench.py times: rel-L2 over 256 sampled columns within the north-star gate
+    import bench
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    path = _os.path.join(_ROOT, "profiles", f"tuned_bert_{dt}_s90_x2.json")
+    tuned = _json.load(open(path)) if _os.path.exists(path) else {}
+    layers, _, _ = bench.workload_layers("bert", 1, 0)
+    for L in layers:
+        w, x = bench.make_inputs(L, 90, 0)
+        plan = srt.Plan.from_csr(w, dtype=tdt, n_hint=L["N"], **tuned.get(L["name"], {}))
+        Y = plan.spmm(torch.from_numpy(x).to(dev).to(tdt))
+        ids = np.unique(np.random.default_rng(2).integers(0, L["N"], 256))
+        ref = oracle.spmm(w.M, w.K, w.row_ptr, w.col_idx, _w64(w, dt == "f16"), _x64(x[:, ids], dt == "f16"))
+        torch.cuda.synchronize()
+        err = oracle.rel_l2(Y[:, torch.from_numpy(ids).to(dev)].double().cpu().numpy(), ref)
+        assert err <= (F16_TOL if dt == "f16" else F32_TOL), (L["name"], err)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f16"])
+def test_conv_full_batch_real_valued(dt):
+    # BASELINE configs[4] at full size (batch 256) with the real-valued inputs and the tuned
+    # options: rel-L2 over 32 sampled images within the north-star gate
+    import bench
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    path = _os.path.join(_ROOT, "profiles", f"tuned_conv_{dt}_s90_x2.json")
+    tuned = _json.load(open(path)) if _os.path.exists(path) else {}
+    L = bench.workload_layers("conv", 1, 0)[0][0]
+    w, x = bench.make_inputs(L, 90, 0)
+    plan = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=256, h=14, w=14, n_hint=256,
+                             **tuned.get(L["name"], {}))
+    y = plan.conv3x3(torch.from_numpy(x).to(dev).to(tdt))
+    ids = np.sort(np.random.default_rng(3).choice(256, 32, replace=False))
+    ref = oracle.conv3x3(256, w.row_ptr, w.col_idx, _w64(w, dt == "f16"), _x64(x[:, ids], dt == "f16"))
+    torch.cuda.synchronize()
+    err = oracle.rel_l2(y[:, torch.from_numpy(ids).to(dev)].double().cpu().numpy(), ref)
+    assert err <= (F16_TOL if dt == "f16" else F32_TOL), err
