@@ -192,6 +192,25 @@ int sparse_conv3x3_ex(sparse_plan_t plan, int64_t batch, const void* x, void* y,
 int sparse_linear(sparse_plan_t plan, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
                   sparse_stream_t stream);
 
+/* Strided 1x1 convolution (NEXT #4: the stride-2 projection shortcuts of ResNet-50, SURVEY
+ * Appendix D) on a SPARSE_SPMM plan of W [C_out x C_in]:
+ *   y[co][b][oy][ox] = sum_ci W[co][ci] * x[ci][b][oy*stride][ox*stride]
+ * x: DEVICE [C_in][batch][h][w] (CNHW), y: DEVICE [C_out][batch][ho][wo], ho = ceil(h/stride),
+ * wo = ceil(w/stride), contiguous.  stride 1 is sparse_spmm on x viewed as C_in x (batch h w).
+ * stride > 1: a device gather of the sampled pixels into a stream-ordered scratch
+ * [C_in][batch ho wo], then sparse_spmm (bitwise that product).  Errors as sparse_spmm
+ * (+ EINVAL for stride < 1 or h, w < 1; ENOMEM for the scratch). */
+int sparse_conv1x1(sparse_plan_t plan, int64_t batch, int32_t h, int32_t w, int32_t stride,
+                   const void* x, void* y, sparse_stream_t stream);
+
+/* NHWC (channels-last) 3x3 convolution on a SPARSE_CONV3X3 plan: x DEVICE [batch][H][W][C_in],
+ * y DEVICE [batch][H][W][C_out], contiguous; the same sum as sparse_conv3x3.  Implemented as a
+ * tiled device transpose of x into a CNHW scratch, sparse_conv3x3, and a transpose of the result
+ * (results bitwise those of sparse_conv3x3 on the CNHW tensors).  Errors as sparse_conv3x3
+ * (+ ENOMEM for the scratch). */
+int sparse_conv3x3_nhwc(sparse_plan_t plan, int64_t batch, const void* x, void* y,
+                        sparse_stream_t stream);
+
 /* Free the plan and its device memory (north-star name).  Must not race with
  * work still enqueued that uses the plan.  NULL is a no-op. */
 int plan_destroy(sparse_plan_t plan);

@@ -282,6 +282,70 @@ int sparse_conv3x3_ex(sparse_plan_t plan, int64_t batch, const void* x, void* y,
   return conv_impl(plan, batch, x, y, ep, stream);
 }
 
+namespace {
+// stream-ordered device scratch on the plan's device (caller's device restored on return)
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  int prev = -1;
+  bool ok = false;
+  Scratch(int dev, size_t bytes, sparse_stream_t stream) : st((cudaStream_t)stream) {
+    if (cudaGetDevice(&prev) != cudaSuccess) return;
+    if (dev >= 0 && dev != prev && cudaSetDevice(dev) != cudaSuccess) return;
+    ok = cudaMallocAsync(&p, bytes ? bytes : 16, st) == cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, st);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+int sparse_conv1x1(sparse_plan_t plan, int64_t batch, int32_t h, int32_t w, int32_t stride, const void* x,
+                   void* y, sparse_stream_t stream) {
+  if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
+  if (plan->p.kind != SPARSE_SPMM) return fail(SPARSE_EINVAL, "sparse_conv1x1 needs an SpMM plan (W = C_out x C_in)");
+  if (plan->host_only) return fail(SPARSE_EINVAL, "host-only plan cannot compute");
+  if (batch < 0 || h < 1 || w < 1 || stride < 1) return fail(SPARSE_EINVAL, "batch >= 0, h, w, stride >= 1 required");
+  if (batch == 0) return ok();
+  if (!x || !y) return fail(SPARSE_EINVAL, "x or y is NULL");
+  const srt::Plan& p = plan->p;
+  const int S = p.dtype != SPARSE_F32 ? 2 : 4;
+  const int64_t ho = (h + stride - 1) / stride, wo = (w + stride - 1) / stride, N = batch * ho * wo;
+  if (stride == 1) return sparse_spmm(plan, N, x, N, y, N, stream);
+  Scratch xs(p.device, (size_t)(p.K * N * S), stream);
+  if (!xs.ok) return fail(SPARSE_ENOMEM, "sparse_conv1x1: cannot allocate the gather scratch");
+  std::string err;
+  const int rc = srt::launch_stride_gather(p.device, S, x, p.K, batch, h, w, stride, xs.p, stream, err);
+  if (rc != SPARSE_OK) return fail(rc, err);
+  return sparse_spmm(plan, N, xs.p, N, y, N, stream);  // sets the error detail itself
+}
+
+int sparse_conv3x3_nhwc(sparse_plan_t plan, int64_t batch, const void* x, void* y, sparse_stream_t stream) {
+  if (!plan) return fail(SPARSE_EINVAL, "plan is NULL");
+  if (plan->p.kind != SPARSE_CONV3X3) return fail(SPARSE_EINVAL, "sparse_conv3x3_nhwc on an SpMM plan");
+  if (plan->host_only) return fail(SPARSE_EINVAL, "host-only plan cannot compute");
+  if (batch < 0) return fail(SPARSE_EINVAL, "batch < 0");
+  if (batch == 0) return ok();
+  if (!x || !y) return fail(SPARSE_EINVAL, "x or y is NULL");
+  const srt::Plan& p = plan->p;
+  const int S = p.dtype != SPARSE_F32 ? 2 : 4;
+  const int64_t N = batch * (int64_t)p.h * p.w;
+  Scratch xt(p.device, (size_t)(p.c_in * N * S), stream), yt(p.device, (size_t)(p.M * N * S), stream);
+  if (!xt.ok || !yt.ok) return fail(SPARSE_ENOMEM, "sparse_conv3x3_nhwc: cannot allocate the CNHW scratch");
+  std::string err;
+  int rc = srt::launch_transpose(p.device, S, x, p.c_in, xt.p, N, N, p.c_in, stream, err);  // [N][C] -> [C][N]
+  if (rc != SPARSE_OK) return fail(rc, err);
+  const int r2 = sparse_conv3x3(plan, batch, xt.p, yt.p, stream);
+  if (r2 != SPARSE_OK) return r2;
+  rc = srt::launch_transpose(p.device, S, yt.p, N, y, p.M, p.M, N, stream, err);  // [M][N] -> [N][M]
+  return rc == SPARSE_OK ? ok() : fail(rc, err);
+}
+
 int plan_destroy(sparse_plan_t plan) {
   if (!plan) return ok();
   srt::jit_unload(plan->p);

@@ -1824,6 +1824,36 @@ int launch_transpose(int device, int S, const void* in, int64_t ldi, void* out, 
   return SPARSE_OK;
 }
 
+// Sampled pixels of a strided 1x1 convolution: xs[k][(b ho + oy) wo + ox] = x[k][b][oy s][ox s].
+// Pure data movement (one thread per output element, consecutive threads -> consecutive ox).
+template <typename T>
+__global__ void stride_gather(const T* __restrict__ x, T* __restrict__ xs, int64_t planes, int h, int w, int s,
+                              int ho, int wo) {
+  const int64_t per = (int64_t)ho * wo, tot = planes * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pl = i / per;
+    const int r = (int)(i - pl * per), oy = r / wo, ox = r - oy * wo;
+    xs[i] = __ldg(x + (pl * h + (int64_t)oy * s) * w + (int64_t)ox * s);
+  }
+}
+
+int launch_stride_gather(int device, int S, const void* x, int64_t K, int64_t B, int h, int w, int s, void* xs,
+                         void* stream, std::string& err) {
+  DeviceGuard dg(device);
+  if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
+  const int ho = (h + s - 1) / s, wo = (w + s - 1) / s;
+  const int64_t tot = K * B * ho * wo;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 32));
+  if (S == 2)
+    stride_gather<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xs, K * B, h, w,
+                                                                    s, ho, wo);
+  else
+    stride_gather<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)x, (float*)xs, K * B, h, w, s, ho, wo);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "stride gather launch", err);
+  return SPARSE_OK;
+}
+
 void free_repack(int device, void* Xp, void* stream) {
   DeviceGuard dg(device);
   cudaFreeAsync(Xp, (cudaStream_t)stream);

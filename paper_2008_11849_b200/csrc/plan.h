@@ -253,6 +253,9 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
 int launch_repack(int device, int64_t K, int64_t N, int S, const void* X, int64_t ldx, void** Xp,
                   int64_t* ldp, void* stream, std::string& err);
 void free_repack(int device, void* Xp, void* stream);
+// xs[k][(b ho + oy) wo + ox] = x[k][b][oy s][ox s] (x CNHW [K][B][h][w]), stream ordered
+int launch_stride_gather(int device, int S, const void* x, int64_t K, int64_t B, int h, int w, int s, void* xs,
+                         void* stream, std::string& err);
 // out[c][r] = in[r][c] for a rows x cols matrix (element size S), stream ordered
 int launch_transpose(int device, int S, const void* in, int64_t ldi, void* out, int64_t ldo, int64_t rows,
                      int64_t cols, void* stream, std::string& err);

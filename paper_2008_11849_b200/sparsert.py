@@ -28,7 +28,7 @@ STATUS_NAMES = {0: "SPARSE_OK", 1: "SPARSE_EINVAL", 2: "SPARSE_EMATRIX", 3: "SPA
 
 # every symbol include/sparsert.h declares (checked by tests/test_capi_host.py)
 EXPORTED = ["sparse_plan_opts_init", "sparse_plan_create", "sparse_spmm", "sparse_conv3x3",
-            "sparse_spmm_ex", "sparse_conv3x3_ex", "sparse_linear",
+            "sparse_spmm_ex", "sparse_conv3x3_ex", "sparse_linear", "sparse_conv1x1", "sparse_conv3x3_nhwc",
             "plan_destroy", "sparse_plan_destroy", "sparse_plan_info", "sparse_plan_dump",
             "sparse_last_error", "sparse_version"]
 
@@ -99,6 +99,10 @@ def _load() -> ctypes.CDLL:
     lib.sparse_spmm_ex.restype = ctypes.c_int
     lib.sparse_conv3x3_ex.argtypes = [P, i64, P, P, ctypes.POINTER(sparse_epilogue), P]
     lib.sparse_conv3x3_ex.restype = ctypes.c_int
+    lib.sparse_conv1x1.argtypes = [P, i64, i32, i32, i32, P, P, P]
+    lib.sparse_conv1x1.restype = ctypes.c_int
+    lib.sparse_conv3x3_nhwc.argtypes = [P, i64, P, P, P]
+    lib.sparse_conv3x3_nhwc.restype = ctypes.c_int
     lib.plan_destroy.argtypes = [P]
     lib.plan_destroy.restype = ctypes.c_int
     lib.sparse_plan_destroy.argtypes = [P]
@@ -167,6 +171,14 @@ def sparse_spmm_ex(plan, N, X_ptr, ldx, Y_ptr, ldy, epilogue=None, stream=0):
 def sparse_conv3x3_ex(plan, batch, x_ptr, y_ptr, epilogue=None, stream=0):
     ep = ctypes.byref(epilogue) if epilogue is not None else None
     _check(lib.sparse_conv3x3_ex(plan, int(batch), x_ptr, y_ptr, ep, stream))
+
+
+def sparse_conv1x1(plan, batch, h, w, stride, x_ptr, y_ptr, stream=0):
+    _check(lib.sparse_conv1x1(plan, int(batch), int(h), int(w), int(stride), x_ptr, y_ptr, stream))
+
+
+def sparse_conv3x3_nhwc(plan, batch, x_ptr, y_ptr, stream=0):
+    _check(lib.sparse_conv3x3_nhwc(plan, int(batch), x_ptr, y_ptr, stream))
 
 
 def plan_destroy(plan):
@@ -371,4 +383,45 @@ class Plan:
         else:
             sparse_conv3x3_ex(self._h, B, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
                               ep, ctypes.c_void_p(s))
+        return y
+
+    def conv1x1(self, x, stride=1, y=None, stream=None):
+        """Strided 1x1 convolution on an SpMM plan of W (C_out x C_in): x (C_in, B, h, w) CNHW ->
+        y (C_out, B, ceil(h/stride), ceil(w/stride)), y[co, b, oy, ox] = sum W[co, ci] x[ci, b, oy s, ox s]."""
+        import torch
+        if self.kind != SPARSE_SPMM:
+            raise ValueError("conv1x1 needs an SpMM plan")
+        self._check_tensor(x, "x")
+        if x.dim() != 4 or x.shape[0] != self.K or not x.is_contiguous():
+            raise ValueError(f"x must be contiguous (C_in={self.K}, B, h, w)")
+        _, B, h, w = x.shape
+        ho, wo = (h + stride - 1) // stride, (w + stride - 1) // stride
+        if y is None:
+            y = torch.empty((self.M, B, ho, wo), dtype=self.dtype, device=x.device)
+        self._check_tensor(y, "y")
+        if tuple(y.shape) != (self.M, B, ho, wo) or not y.is_contiguous():
+            raise ValueError("y must be contiguous (C_out, B, ho, wo)")
+        s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
+        sparse_conv1x1(self._h, B, h, w, stride, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                       ctypes.c_void_p(s))
+        return y
+
+    def conv3x3_nhwc(self, x, y=None, stream=None):
+        """Channels-last 3x3 conv: x (B, H, W, C_in) -> y (B, H, W, C_out), contiguous."""
+        import torch
+        if self.kind != SPARSE_CONV3X3:
+            raise ValueError("conv3x3_nhwc on an SpMM plan")
+        self._check_tensor(x, "x")
+        c_in, h, w = self.conv_geom
+        if x.dim() != 4 or tuple(x.shape[1:]) != (h, w, c_in) or not x.is_contiguous():
+            raise ValueError(f"x must be contiguous (B, H={h}, W={w}, C_in={c_in})")
+        B = x.shape[0]
+        if y is None:
+            y = torch.empty((B, h, w, self.M), dtype=self.dtype, device=x.device)
+        self._check_tensor(y, "y")
+        if tuple(y.shape) != (B, h, w, self.M) or not y.is_contiguous():
+            raise ValueError("y must be contiguous (B, H, W, C_out)")
+        s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
+        sparse_conv3x3_nhwc(self._h, B, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                            ctypes.c_void_p(s))
         return y

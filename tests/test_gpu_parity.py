@@ -932,3 +932,49 @@ def test_conv_full_batch_real_valued(dt):
     torch.cuda.synchronize()
     err = oracle.rel_l2(y[:, torch.from_numpy(ids).to(dev)].double().cpu().numpy(), ref)
     assert err <= (F16_TOL if dt == "f16" else F32_TOL), err
+
+
+# --------------------------------------------------------------------------- strided 1x1 / NHWC conv (NEXT #4)
+
+@pytest.mark.parametrize("dt", ["f32", "f16"])
+@pytest.mark.parametrize("cin,cout,B,h,w,s", [(256, 512, 2, 56, 56, 2), (512, 1024, 3, 28, 28, 2),
+                                               (1024, 2048, 2, 14, 14, 2), (64, 96, 3, 15, 9, 2),
+                                               (32, 48, 2, 14, 14, 1), (40, 24, 1, 10, 7, 3)])
+def test_conv1x1_strided_exact(cin, cout, B, h, w, s, dt):
+    # the ResNet-50 stride-2 projection shapes and ragged cases: exact on
+    # integer data against the oracle product on the sampled pixels (sampling = input plumbing)
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    vw, vx = (3, 3) if dt == "f32" else (2, 4)
+    wi = gen.int_weights(cout, cin, 90, seed=cin + h, vmax=vw)
+    x = gen.int_x(cin * B * h, w, seed=cout + s, vmax=vx).reshape(cin, B, h, w)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, n_hint=B * ((h + s - 1) // s) * ((w + s - 1) // s))
+    y = plan.conv1x1(torch.from_numpy(x).to(dev).to(tdt), stride=s)
+    torch.cuda.synchronize()
+    xs = np.ascontiguousarray(x[:, :, ::s, ::s])
+    ho, wo = xs.shape[2], xs.shape[3]
+    ref = oracle.spmm(cout, cin, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64),
+                      xs.reshape(cin, -1).astype(np.float64)).reshape(cout, B, ho, wo)
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert y.shape == (cout, B, ho, wo)
+    assert np.array_equal(y.double().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f16"])
+@pytest.mark.parametrize("cin,cout,B,H,W", [(64, 64, 2, 56, 56), (256, 256, 3, 14, 14), (12, 20, 2, 7, 9)])
+def test_conv3x3_nhwc_exact(cin, cout, B, H, W, dt):
+    # channels-last activations: exact on integer data, and bitwise the CNHW call
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    vw, vx = (3, 3) if dt == "f32" else (2, 4)
+    wi = gen.int_weights(cout, 9 * cin, 90, seed=cin + W, vmax=vw)
+    x = gen.int_x(cin * B * H, W, seed=cout, vmax=vx).reshape(cin, B, H, W)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B)
+    xt = torch.from_numpy(x).to(dev).to(tdt)
+    y_nhwc = plan.conv3x3_nhwc(xt.permute(1, 2, 3, 0).contiguous())
+    y_cnhw = plan.conv3x3(xt)
+    torch.cuda.synchronize()
+    assert torch.equal(y_nhwc, y_cnhw.permute(1, 2, 3, 0))
+    ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), x.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(y_cnhw.double().cpu().numpy(), ref)
