@@ -1508,32 +1508,42 @@ __global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constan
 }
 
 // x[C_in][B][H][W] -> xp3[3][C_in][B][H + 1][wp]: xp3[dx][..][r][c] = x[..][r - 1][c + dx - 2],
-// zero outside the image (the layout conv3x3_tma_kernel reads through TMA).  Pure data movement.
+// zero outside the image (the layout conv3x3_tma_kernel reads through TMA).  Pure data movement:
+// a CTA stages kPadPlanes whole input planes in shared memory with coalesced loads (consecutive
+// threads, consecutive elements of the contiguous planes), then writes each plane's three
+// shifted, zero-haloed copies ((H + 1) x wp elements, contiguous per plane and copy) with
+// 16-byte stores.  (Round 1 used one thread per padded row with a 72-element register row:
+// scalar loads strided by a row per thread, ~50 % of HBM bandwidth.)
 template <typename T>
-__global__ void pad_conv_input(const T* __restrict__ x, T* __restrict__ xp, int64_t planes, int H, int W, int wp) {
-  // one thread per padded row (plane, r): the input row is read once into registers, the
-  // three shifted copies are written with 16-byte stores
-  constexpr int V = 16 / sizeof(T), MAXW = 72;  // wp <= 64 (inspector), row index <= wp + 1
+__global__ void __launch_bounds__(256) pad_conv_input(const T* __restrict__ x, T* __restrict__ xp, int64_t planes,
+                                                      int H, int W, int wp, int kPadPlanes) {
+  constexpr int V = 16 / sizeof(T);
+  extern __shared__ __align__(16) uint8_t pad_smem[];
+  T* sp = (T*)pad_smem;  // [kPadPlanes][H][W] (kPadPlanes: planes per CTA round, host-chosen)
+  const int HW = H * W, per = (H + 1) * wp;  // output elements per plane and copy (wp % V == 0)
   const int64_t rows = planes * (H + 1);
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t pl = t / (H + 1);
-    const int y = (int)(t - pl * (H + 1)) - 1;
-    const T* src = x + (pl * H + (y < 0 ? 0 : y)) * W;
-    T row[MAXW];  // row[j] = x[y][j - 2], zero outside
-#pragma unroll
-    for (int j = 0; j < MAXW; ++j) row[j] = (y >= 0 && j >= 2 && j - 2 < W) ? __ldg(src + j - 2) : T(0);
-#pragma unroll
+  for (int64_t p0 = (int64_t)blockIdx.x * kPadPlanes; p0 < planes; p0 += (int64_t)gridDim.x * kPadPlanes) {
+    const int np = (int)min((int64_t)kPadPlanes, planes - p0);
+    const T* src = x + p0 * HW;
+    for (int i = threadIdx.x; i < np * HW; i += blockDim.x) sp[i] = __ldg(src + i);
+    __syncthreads();
+    const int nv = np * (per / V);  // 16-byte vectors per copy
     for (int dx = 0; dx < 3; ++dx) {
-      T* dst = xp + (dx * rows + t) * wp;
+      T* dst = xp + ((int64_t)dx * rows + p0 * (H + 1)) * wp;  // planes p0.. of copy dx: contiguous
+      for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        const int e0 = i * V, pl = e0 / per, rem = e0 - pl * per;
+        const int r = rem / wp, c0 = rem - r * wp;
+        const int y = r - 1;
+        alignas(16) T v[V];
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += V) {
-        if (c0 >= wp) break;
-        T v[V];
-#pragma unroll
-        for (int c = 0; c < V; ++c) v[c] = row[c0 + c + dx];
-        *(uint4*)(dst + c0) = *(const uint4*)v;
+        for (int c = 0; c < V; ++c) {
+          const int xx = c0 + c + dx - 2;
+          v[c] = (y >= 0 && xx >= 0 && xx < W) ? sp[pl * HW + y * W + xx] : T(0);
+        }
+        *(uint4*)(dst + e0) = *(const uint4*)v;
       }
     }
+    __syncthreads();
   }
 }
 
@@ -2661,12 +2671,20 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
       cudaGetLastError();
       return cuda_fail(e, "cudaMallocAsync(conv pad)", err);
     }
-    const unsigned pg = (unsigned)std::min<int64_t>((rows + 255) / 256, 148 * 16);
-    if (f16)
-      pad_conv_input<uint16_t><<<pg, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, planes, p.h,
-                                                                     p.w, p.conv_wp);
-    else
-      pad_conv_input<float><<<pg, 256, 0, (cudaStream_t)stream>>>((const float*)x, (float*)xp, planes, p.h, p.w, p.conv_wp);
+    const int kPadPlanes = (int)std::max<int64_t>(1, std::min<int64_t>(8, (160 * 1024) / ((int64_t)p.h * p.w * S)));
+    const unsigned pg = (unsigned)std::min<int64_t>((planes + kPadPlanes - 1) / kPadPlanes, 148 * 8);
+    const size_t psm = (size_t)kPadPlanes * p.h * p.w * S;
+    if (f16) {
+      if ((e = ensure_smem_attr(pad_conv_input<uint16_t>, (int)psm)) != cudaSuccess)
+        return cuda_fail(e, "cudaFuncSetAttribute(pad)", err);
+      pad_conv_input<uint16_t><<<pg, 256, psm, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, planes,
+                                                                       p.h, p.w, p.conv_wp, kPadPlanes);
+    } else {
+      if ((e = ensure_smem_attr(pad_conv_input<float>, (int)psm)) != cudaSuccess)
+        return cuda_fail(e, "cudaFuncSetAttribute(pad)", err);
+      pad_conv_input<float><<<pg, 256, psm, (cudaStream_t)stream>>>((const float*)x, (float*)xp, planes, p.h, p.w,
+                                                                    p.conv_wp, kPadPlanes);
+    }
     CUtensorMap tmap;
     std::memset(&tmap, 0, sizeof tmap);
     cuuint64_t dims[5] = {(cuuint64_t)p.conv_wp, (cuuint64_t)(p.h + 1), (cuuint64_t)batch, (cuuint64_t)p.c_in, 3};
