@@ -444,7 +444,7 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
                 uint16_t a, wh;
                 std::memcpy(&a, rec, 2);
                 std::memcpy(&wh, rec + 2, 2);
-                xoff = (int64_t)a * 16;
+                xoff = (int64_t)a * (p.kind == SPARSE_CONV3X3 && p.conv_vec == 4 ? 8 : 16);
                 if (bf) {
                   const uint32_t b = (uint32_t)wh << 16;
                   std::memcpy(&w, &b, 4);
@@ -461,10 +461,17 @@ int sparse_plan_dump(sparse_plan_t plan, int64_t cap, int32_t* row, int32_t* col
               if (p.kind == SPARSE_SPMM) {
                 if (xoff % rowb) return fail(SPARSE_EINTERNAL, "plan entry offset not a row multiple");
                 kl = xoff / rowb;
-              } else if (p.conv_vec == 4) {  // packed conv: im2col row (tap, ci) of the tile
-                if (xoff % rowb) return fail(SPARSE_EINTERNAL, "packed conv entry offset not a row multiple");
-                const int64_t row = xoff / rowb;
-                kl = row == p.kc ? p.kc : (row % p.cc) * 9 + row / p.cc;
+              } else if (p.conv_vec == 4) {  // interleaved conv: el = dx cs + ci lc + dy P
+                const int64_t el = xoff / (f16 ? 2 : 4);
+                if (el == 3 * (int64_t)p.conv_cs + p.conv_wp) {
+                  kl = p.kc;
+                } else {
+                  const int64_t dx = el / p.conv_cs, rem = el % p.conv_cs;
+                  const int64_t ci = rem / p.il_lc, dyP = rem % p.il_lc;
+                  if (dx > 2 || ci >= p.cc || dyP % p.conv_wp || dyP / p.conv_wp > 2)
+                    return fail(SPARSE_EINTERNAL, "interleaved conv plan entry offset does not decode");
+                  kl = ci * 9 + (dyP / p.conv_wp) * 3 + dx;
+                }
               } else {  // vectorised conv: elems = dx * cs + ci * sci + dy * wp, or the zero block
                 const int64_t el = xoff / (f16 ? 2 : 4);
                 if (el == 3 * (int64_t)p.conv_cs) {

@@ -438,38 +438,43 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
         p.conv_cs = ccv * p.conv_sci;  // elements per shifted copy
         p.conv_stage_elems = 3 * p.conv_cs + NTv + 16;  // + zero block
         p.x_stage_bytes = (int)align16((int64_t)p.conv_stage_elems * S);
+        // interleaved kernel (conv3x3_il_kernel): 4 positions per lane, 128 per tile; il_g images
+        // interleaved per row so that a tap shift (dy - 1) P keeps a lane's vector aligned
+        // (P % 4 == 0); the tile's span starts 16-byte aligned, up to 16 / S - 4 elements early
+        int ilg = 0;
+        for (int gg = 1; gg <= 4 && !ilg; ++gg)
+          if ((gg * o.w) % 4 == 0) ilg = gg;
+        int illc = 0;
+        if (ilg) {
+          const int P = ilg * o.w, HP = o.h * P;
+          const int nb = (127 + HP - 1) / HP;  // group boundaries inside a 128-position tile
+          illc = P + 127 + nb * 2 * P + P + 4 + (16 / S - 4);
+          illc = (illc + 15) / 16 * 16;
+        }
+        if (o.conv_vec == 4 && (!ilg || illc > 256)) {
+          err = "interleaved conv (conv_kernel 4): image too wide for one 256-element TMA span";
+          return SPARSE_EUNSUPPORTED;
+        }
         if (o.conv_vec == 4) {
-          // packed kernel (conv3x3_pk_kernel): NT = 32 C packed positions per tile, the chunk's
-          // im2col tile [9 cc rows x NT] (+ a zero row) built in shared memory from a raw span
-          // of RAWN elements per channel staged by TMA (kernels.cu)
-          const int el16 = 16 / S;
-          auto rup = [](int v, int m) { return (v + m - 1) / m * m; };
           p.conv_vec = 4;
-          p.C = Cv;
-          p.n_tile = NTv;
+          p.C = 4;
+          p.n_tile = 128;
           p.conv_rb = 0;
           p.conv_ipt = 0;
-          p.conv_wp = o.w;
+          p.conv_wp = ilg * o.w;
           p.conv_guard = 0;
-          p.pk_p0 = rup(o.w + 1, el16);
-          p.pk_rawn = rup(p.pk_p0 + NTv + o.w + 1, 2 * el16);  // even number of 16-byte units
-          if (p.pk_rawn > 512) {
-            err = "packed conv: image width too large for the raw TMA boxes";
-            return SPARSE_EUNSUPPORTED;
-          }
-          const int per_ch = (p.pk_rawn + 9 * NTv) * S;
-          int ccp = o.k_chunk ? o.k_chunk : std::max(1, std::min(o.c_in, (48 * 1024) / per_ch));
-          ccp = std::min(ccp, 64);
-          p.cc = ccp;
-          p.kc = 9 * ccp;
-          p.nchunks = (o.c_in + ccp - 1) / ccp;
-          p.conv_cs = 0;
-          p.conv_sci = NTv;
-          p.conv_stage_elems = (9 * ccp + 1) * NTv;  // im2col rows + the zero row
+          p.il_g = ilg;
+          p.il_lc = illc;
+          const int per_ch = 3 * illc * S;
+          int cci = o.k_chunk ? o.k_chunk : std::max(1, std::min(o.c_in, (64 * 1024) / per_ch));
+          cci = std::min(cci, 64);
+          p.cc = cci;
+          p.kc = 9 * cci;
+          p.nchunks = (o.c_in + cci - 1) / cci;
+          p.conv_cs = (int)(((int64_t)cci * illc * S + 127) / 128 * 128 / S);  // 128-byte aligned copies
+          p.conv_sci = illc;
+          p.conv_stage_elems = 3 * p.conv_cs + illc;  // + the zero block
           p.x_stage_bytes = (int)(((int64_t)p.conv_stage_elems * S + 127) & ~int64_t(127));
-          // raw span: one TMA box, or two when RAWN > 256 (the second at a 128-byte boundary)
-          p.pk_raw_bytes = p.pk_rawn > 256 ? ((ccp * (p.pk_rawn / 2) * S + 127) / 128 * 128) * 2
-                                           : ccp * p.pk_rawn * S;
         } else if (o.conv_vec == 2 && wpv <= 64) {  // (pad_conv_input holds a padded row in registers)
           // TMA-fed variant (conv3x3_tma_kernel): each shifted copy is one 4-D TMA box
           // {wp, rb + 2, 1 image, cc channels} of the width-padded input (no guard), at a
@@ -648,10 +653,10 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   // (ci, dy, dx) = shifted copy dx, channel plane ci, row dy; kl == kc: the zero row/block)
   auto elem_off = [&](int32_t kl) -> int64_t {
     if (o.kind == SPARSE_SPMM) return (int64_t)kl * p.n_tile;
-    if (p.conv_vec == 4) {  // packed: im2col row (tap, ci) of the staged tile, row 9 cc = zero
-      if (kl == p.kc) return (int64_t)p.kc * p.n_tile;
-      const int ci = kl / 9, tap = kl % 9;
-      return ((int64_t)tap * p.cc + ci) * p.n_tile;
+    if (p.conv_vec == 4) {  // interleaved: copy dx, channel ci, tap row dy (biased by one pitch)
+      if (kl == p.kc) return 3 * (int64_t)p.conv_cs + p.conv_wp;
+      const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
+      return (int64_t)dx * p.conv_cs + (int64_t)ci * p.il_lc + (int64_t)dy * p.conv_wp;
     }
     if (kl == p.kc) return 3 * (int64_t)p.conv_cs;
     const int ci = kl / 9, t = kl % 9, dy = t / 3, dx = t % 3;
@@ -660,7 +665,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   auto put_spmm = [&](int32_t kl, float w, uint16_t wh) {
     uint8_t rec[8];
     if (f16) {
-      const uint16_t o16 = (uint16_t)(elem_off(kl) * 2 / 16);
+      const uint16_t o16 = (uint16_t)(elem_off(kl) * 2 / (p.conv_vec == 4 ? 8 : 16));
       std::memcpy(rec, &o16, 2);
       std::memcpy(rec + 2, &wh, 2);
     } else {
@@ -784,11 +789,11 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // tensor memory plans allocate all 512 TMEM columns: one CTA per SM (> half the smem)
     if (p.tm) p.smem_bytes = std::max(p.smem_bytes, 116 * 1024);
   } else if (p.conv_vec == 4) {
-    // packed conv: stage = raw span | plan block | im2col tile, 128-byte aligned parts
-    p.pk_blk_at = (p.pk_raw_bytes + 127) & ~127;
-    p.pk_cp_at = (p.pk_blk_at + p.max_blk_bytes + 127) & ~127;
-    stage_bytes = p.pk_cp_at + p.x_stage_bytes;
-    p.stages = o.stages > 0 ? o.stages : std::max(2, std::min(kMaxStages, 210 * 1024 / stage_bytes));
+    // interleaved conv: stage = three copies + zero block | plan block (128-byte aligned)
+    p.il_blk_at = p.x_stage_bytes;
+    stage_bytes = (p.x_stage_bytes + p.max_blk_bytes + 127) & ~127;
+    p.il_stage_bytes = stage_bytes;
+    p.stages = o.stages > 0 ? o.stages : std::max(2, std::min(kMaxStages, 200 * 1024 / stage_bytes));
     p.red_bytes = 0;
     p.smem_bytes = p.stages * stage_bytes + 256;
   } else if (p.conv_vec == 2) {

@@ -1271,79 +1271,119 @@ __global__ void __launch_bounds__(512) conv3x3_tma_kernel(const __grid_constant_
   }
 }
 
-// ------------------------------------------------------------------ conv 3x3, packed
-// Implicit im2col (Sec. 3.6) with the output positions PACKED: position
-// n = (b * H + y) * W + x of the CNHW output (no padded / junk positions), so the conv is the
-// SpMM Y[C_out x N] = W[C_out x 9 C_in] * X~[9 C_in x N] over a virtual im2col matrix X~
-// that never exists in HBM.  Per chunk of cc input channels the TMA engine stages the RAW
-// input span x[ci][n0 - P0 .. n0 - P0 + RAWN) of the tile's NT positions (2-D boxes over the
-// CNHW input viewed as C_in x N, zero-filled outside), and dedicated BUILDER warps
-// (kPkBuilders warps, warp-specialised like a TMA producer) expands it in shared memory into the
-// chunk's im2col tile: row (tap, ci) = x~[ci][b][y + dy - 1][x + dx - 1] for the NT
-// positions, zero where the tap falls outside the image (the zero padding of P:215 is
-// resolved while building, never in the FMA loop).  The FMA warps then run exactly the SpMM
-// inner loop (run_rows: one 128-bit shared load of the lane's C positions per plan entry) on
-// that tile.  Ring slot = {raw box, plan block, im2col tile}: full[s] (TMA complete_tx) ->
-// builders -> built[s] (one arrive per builder warp) -> FMA warps -> release counter, the last
-// FMA warp refills the slot.  Summation order per output: k = (ci * 3 + dy) * 3 + dx
-// ascending, chunks ascending -- bitwise equal to the other conv kernels.
-constexpr int kPkBuilders = 4;  // builder warps (one warpgroup)
-struct PkArgs {
+// ------------------------------------------------------------------ conv 3x3, interleaved
+// Implicit im2col (Sec. 3.6) with NO junk positions.  The padded-row layout of
+// conv3x3_tma_kernel spends 2 of every wp = 16 positions (and a partial band) on halo columns /
+// rows: 23 % of its FMAs at 14 x 14.  Here g images are interleaved row by row ("image group"
+// q = images q g .. q g + g - 1): group row r holds row r - 1 of each of the g images side by
+// side, pitch P = g W, with one zero row above and below each group (stride Sg = (H + 2) P).
+// Output positions n = (q H + y) P + xx (xx = j W + x, image b = q g + j) are all real pixels
+// (except the padding images of a batch that is not a multiple of g), a lane owns C = 4
+// consecutive ones, and g is the smallest group whose pitch keeps every tap shift (dy - 1) P of
+// a lane's 4 positions aligned for one vector load (16 B fp32, 8 B 16-bit; P % 4 == 0; the span
+// start is rounded down to 16 bytes and the lanes' offsets follow).  A device pre-pass
+// (il_pad_input) writes the three dx-shifted copies in this layout, copy_dx[ci][h] =
+// x[ci][b][r - 1][x + dx - 1] (zero outside the image, per position: the zero padding of
+// P:215 is resolved there, never in the FMA loop); per chunk of cc channels the TMA engine
+// stages, for each copy, the span of h the tile's 128 positions touch (one box of lc <= 256
+// elements per channel).  Tap (ci, dy, dx) of a lane's positions is then one aligned load at
+// u + dx cs + ci lc + (dy - 1) P (u = the lane's offset in the span), the same mbarrier ring
+// and Alg. 3 FMA loop as conv3x3_tma_kernel.  Summation order per output: k ascending, chunks
+// ascending -- bitwise equal to the other conv kernels.
+struct IlArgs {
   const uint8_t* blob;
   const int64_t* blk_off;
   const int32_t* row_id;
   uint8_t* y;
-  int64_t N;  // B * H * W output positions
-  int32_t H, W, HW;
-  int32_t cc, nchunks, Mp, npanels, stages, stage_bytes, fwarps;
-  int32_t raw_bytes, blk_at, cp_at;  // stage layout (bytes): raw | plan block | im2col tile
-  int32_t rawn, p0, hdr_bytes, bar_off, vec_y, box1_at;
+  int64_t npos;   // image groups x H x P positions
+  int64_t plane;  // B H W: output channel stride (CNHW)
+  int32_t H, W, P, g, Bt, Sg;
+  int32_t cc, nchunks, Mp, npanels, stages, stage_bytes;
+  int32_t lc, cs, blk_at, hdr_bytes, bar_off;
   const uint8_t* bias;
   float beta;
   int32_t relu;
 };
 
+// 16-bit entries for 4 positions per lane: unit = 4 x {uint16 xoff (8-byte units), half / bf16 w}
+template <bool BF>
+__device__ __forceinline__ void unit_h4(float (&acc)[4], const uint4 q, const uint8_t* xs) {
+  const uint32_t en[4] = {q.x, q.y, q.z, q.w};
+  uint2 x[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) x[e] = *(const uint2*)(xs + ((en[e] & 0xffffu) << 3));
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    fma_h2<BF>(acc[0], acc[1], (uint16_t)(en[e] >> 16), x[e].x);
+    fma_h2<BF>(acc[2], acc[3], (uint16_t)(en[e] >> 16), x[e].y);
+  }
+}
+template <bool F16, bool BF, int R>
+__device__ __forceinline__ void run_rows_il(float (&acc)[R][4], const uint32_t (&h)[R], const uint4* ents,
+                                            const uint8_t* xs) {
+  if (!F16) {
+    run_rows<false, R>(acc, h, ents, xs);
+    return;
+  }
+  int mn = (int)(h[0] >> 16);
+#pragma unroll
+  for (int r = 1; r < R; ++r) mn = min(mn, (int)(h[r] >> 16));
+  const uint4* pr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) pr[r] = ents + (h[r] & 0xffffu);
+#pragma unroll 1
+  for (int u = 0; u < mn; ++u) {
+    uint4 q[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) q[r] = pr[r][u];
+#pragma unroll
+    for (int r = 0; r < R; ++r) unit_h4<BF>(acc[r], q[r], xs);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int cnt = (int)(h[r] >> 16);
+#pragma unroll 1
+    for (int u = mn; u < cnt; ++u) unit_h4<BF>(acc[r], pr[r][u], xs);
+  }
+}
+
 template <int R, bool F16, bool BF = false>
-__global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                            const PkArgs a) {
-  constexpr int C = F16 ? 8 : 4;  // positions per lane (16 bytes)
+__global__ void __launch_bounds__(512) conv3x3_il_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                         const IlArgs a) {
+  constexpr int C = 4, NT = 128;  // positions per lane / per tile
   constexpr int S = F16 ? 2 : 4;
-  constexpr int NT = 32 * C;      // positions per tile
-  constexpr int ROWB = NT * S;    // bytes per im2col row
-  using T = typename std::conditional<F16, uint16_t, float>::type;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int fw = a.fwarps;  // FMA warps; warps fw .. fw + kPkBuilders - 1 build
+  const int nwarps = blockDim.x >> 5;
   const int np = a.npanels;
-  const int64_t ntn = (a.N + NT - 1) / NT;
-  const int64_t ntiles = (int64_t)np * ntn;
+  const int64_t ntiles = (int64_t)np * ((a.npos + NT - 1) / NT);
   const int my_tiles = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
   const int total = my_tiles * a.nchunks;
   const uint32_t full0 = smem_u32(smem + a.bar_off);
-  const uint32_t built0 = full0 + 8 * kMaxStages;
-  uint32_t* ctr = (uint32_t*)(smem + a.bar_off + 16 * kMaxStages);
-  // the zero row after the 9 cc im2col rows of every stage (target of neutral padding entries)
+  uint32_t* ctr = (uint32_t*)(smem + a.bar_off + 8 * kMaxStages);
+  // the zero block after the three copies of every stage (target of neutral padding entries)
   for (int s = 0; s < a.stages; ++s)
-    for (int i = tid; i < ROWB / 16; i += blockDim.x)
-      *(uint4*)(smem + (size_t)s * a.stage_bytes + a.cp_at + (size_t)9 * a.cc * ROWB + 16 * i) =
-          make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < a.lc * S / 16; i += blockDim.x)
+      *(uint4*)(smem + (size_t)s * a.stage_bytes + (size_t)3 * a.cs * S + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
   if (tid < kMaxStages) ctr[tid] = 0u;
   if (tid == 0) {
-    for (int s = 0; s < a.stages; ++s) {
-      mbar_init(full0 + 8 * s, 1);
-      mbar_init(built0 + 8 * s, kPkBuilders);
-    }
+    for (int s = 0; s < a.stages; ++s) mbar_init(full0 + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  const int64_t HP = (int64_t)a.H * a.P;
+  auto hcoord = [&](int64_t n) -> int64_t {  // span coordinate of position n
+    const int64_t q = n / HP;
+    return q * a.Sg + a.P + (n - q * HP);
+  };
   auto tile_of = [&](int ti, int& panel, int64_t& n0) {
     const int64_t t = blockIdx.x + (int64_t)ti * gridDim.x;
     panel = (int)(t % np);
     n0 = (t / np) * NT;
   };
-  auto refill = [&](int q) {  // lane 0 of one FMA warp
+  auto refill = [&](int q) {  // lane 0 of one warp
     const int slot = q % a.stages;
     const int ti = q / a.nchunks, c = q - ti * a.nchunks;
     int panel;
@@ -1354,85 +1394,23 @@ __global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constan
     const uint32_t nb = (uint32_t)(a.blk_off[bi + 1] - blk0);
     uint8_t* st = smem + (size_t)slot * a.stage_bytes;
     const uint32_t fb = full0 + 8 * slot;
+    const int hb = (int)((hcoord(n0) - a.P) & ~(int64_t)(16 / S - 1));  // 16-byte aligned span start
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive_expect_tx(fb, (uint32_t)(a.cc * a.rawn * S) + nb);  // TMA bytes (no padding)
-    // the raw span in boxes of at most 256 elements (two halves when RAWN > 256)
-    const int nbox = a.rawn > 256 ? 2 : 1, bw = a.rawn / nbox;
-    for (int i = 0; i < nbox; ++i)  // box i = cc rows of bw elements, at i * box1_at (128-B aligned)
-      tma_load_2d(smem_u32(st + (size_t)i * a.box1_at), &tmap, (int)(n0 - a.p0) + i * bw, c * a.cc, fb);
+    mbar_arrive_expect_tx(fb, (uint32_t)(3 * a.cc * a.lc * S) + nb);
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx)  // copy dx: box {lc, cc, 1} at {hb, ci0, dx}
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(st + (size_t)dx * a.cs * S)),
+          "l"((uint64_t)&tmap), "r"(hb), "r"(c * a.cc), "r"(dx), "r"(fb)
+          : "memory");
     if (nb) bulk_load(smem_u32(st + a.blk_at), a.blob + blk0, nb, fb);
   };
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-
-  if (warp >= fw) {
-    // ---------------- builder warps: raw span -> im2col rows (tap, ci) of the tile.  Builder
-    // warp w takes rows tap * cc + ci = w, w + nbw, ...; lane l writes positions l + 32 k
-    // (k < C) of a row: conflict-free scalar loads of the raw span (shifted by the tap) and
-    // stores; mask bit (tap, k) = position l + 32 k has tap (dy, dx) inside its image.
-    const int bw_id = warp - fw;
-    const int bw = a.rawn > 256 ? a.rawn / 2 : a.rawn;  // raw box width (refill)
-    const int rows = 9 * a.cc;
-    uint32_t mask[C];  // bit tap of mask[k]: position l + 32 k has tap (dy, dx) inside its image
-    int64_t cur_n0 = -1;
-    for (int q = 0; q < total; ++q) {
-      const int slot = q % a.stages;
-      int panel;
-      int64_t n0;
-      tile_of(q / a.nchunks, panel, n0);
-      if (n0 != cur_n0) {
-        cur_n0 = n0;
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-          const int64_t n = n0 + lane + 32 * k;
-          const int b = (int)(n / a.HW);
-          const int rem = (int)(n - (int64_t)b * a.HW);
-          const int y = rem / a.W, x = rem - y * a.W;
-          mask[k] = 0;
-#pragma unroll
-          for (int tap = 0; tap < 9; ++tap) {
-            const int yy = y + tap / 3 - 1, xx = x + tap % 3 - 1;
-            if (n < a.N && yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) mask[k] |= 1u << tap;
-          }
-        }
-      }
-      mbar_wait(full0 + 8 * slot, (uint32_t)((q / a.stages) & 1));
-      uint8_t* st = smem + (size_t)slot * a.stage_bytes;
-      uint8_t* cp = st + a.cp_at;
-      // rows (tap, ci) with ci = bw_id (mod kPkBuilders); per tap the lane's C raw elements
-      // (position l + 32 k shifted by the tap; box 1 for the upper half of a 2-box span)
-#pragma unroll 1
-      for (int tap = 0; tap < 9; ++tap) {
-        const int sh = (tap / 3 - 1) * a.W + (tap % 3 - 1) + a.p0;  // raw element of position 0
-        const uint8_t* rp[C];
-        bool ok[C];
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-          const int e = lane + 32 * k + sh;
-          rp[k] = st + (e < bw ? (size_t)e * S : (size_t)a.box1_at + (size_t)(e - bw) * S) + (size_t)bw_id * bw * S;
-          ok[k] = (mask[k] >> tap) & 1u;
-        }
-        uint8_t* d = cp + ((size_t)tap * a.cc + bw_id) * ROWB + lane * S;
-#pragma unroll 1
-        for (int ci = bw_id; ci < a.cc; ci += kPkBuilders) {
-#pragma unroll
-          for (int k = 0; k < C; ++k) {
-            const T v = ok[k] ? *(const T*)rp[k] : T(0);
-            *(T*)(d + k * 32 * S) = v;
-            rp[k] += (size_t)kPkBuilders * bw * S;
-          }
-          d += (size_t)kPkBuilders * ROWB;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(built0 + 8 * slot);
-    }
-    return;
-  }
-
-  // ---------------- FMA warps (the SpMM executor on the built im2col tile)
   if (warp == 0 && lane == 0)
     for (int q = 0; q < min(a.stages, total); ++q) refill(q);
+
   float acc[R][C];
   int q = 0, slot = 0;
   uint32_t ph = 0;
@@ -1444,66 +1422,101 @@ __global__ void __launch_bounds__(640, 1) conv3x3_pk_kernel(const __grid_constan
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
-    // lanes past the end of N read lane 0's positions (never stored), per quarter-warp
-    const int xoff = n0 + (lane & ~7) * C < a.N ? lane * (C * S) : 0;
+    const int64_t hb = (hcoord(n0) - a.P) & ~(int64_t)(16 / S - 1);  // as refill
+    const int64_t nl = n0 + lane * C;
+    // lanes past the end read the tile's first positions (never stored), per quarter-warp
+    const int64_t u = (n0 + (lane & ~7) * C < a.npos ? hcoord(nl) : hcoord(n0)) - hb;
+    const intptr_t xoff = (intptr_t)(u - a.P) * S;  // + dx cs + ci lc + dy P (plan entry)
     for (int j = 0; j < a.nchunks; ++j) {
-      mbar_wait(built0 + 8 * slot, ph);
+      mbar_wait(full0 + 8 * slot, ph);
       const uint8_t* st = smem + (size_t)slot * a.stage_bytes;
       const uint32_t* shdr = (const uint32_t*)(st + a.blk_at);
       const uint4* ents = (const uint4*)(st + a.blk_at + a.hdr_bytes);
       uint32_t h[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) h[r] = shdr[warp * R + r];
-      run_rows<F16, R, BF, (R > 2 ? 2 : R)>(acc, h, ents, st + a.cp_at + xoff);
+      run_rows_il<F16, BF, R>(acc, h, ents, st + xoff);
       __syncwarp();
       uint32_t old = 0;
       if (lane == 0)
         asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                      : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
       old = __shfl_sync(0xffffffffu, old, 0);
-      if ((old + 1u) % (uint32_t)fw == 0u && q + a.stages < total && lane == 0) refill(q + a.stages);
+      if ((old + 1u) % (uint32_t)nwarps == 0u && q + a.stages < total && lane == 0) refill(q + a.stages);
       ++q;
       if (++slot == a.stages) {
         slot = 0;
         ph ^= 1u;
       }
     }
-    // epilogue: Y[row][n] (CNHW = the flat M x N layout), C consecutive positions per lane
-    const int64_t nl = n0 + lane * C;
-    const int ncol = (int)min((int64_t)C, a.N - nl);
-    if (ncol <= 0) continue;
+    // epilogue: position n -> image b = q g + xx / W, pixel (y, xx % W) of the CNHW output
+    int64_t oidx[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int64_t n = nl + c;
+      const int64_t gq = n / HP;
+      const int rem = (int)(n - gq * HP), yy = rem / a.P, xx = rem - yy * a.P;
+      const int jj = xx / a.W;
+      const int64_t b = gq * a.g + jj;
+      oidx[c] = (n < a.npos && b < a.Bt) ? (b * a.H + yy) * a.W + (xx - jj * a.W) : -1;
+    }
     const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int row = a.row_id[(int64_t)panel * a.Mp + warp * R + r];
       if (row < 0) continue;
-      uint8_t* yp = a.y + ((int64_t)row * a.N + nl) * S;
-      if (epi) {
 #pragma unroll
-        for (int c = 0; c < C; ++c)
-          if (c < ncol) acc[r][c] = epilogue_one<F16, BF>(acc[r][c], a.bias, row, a.beta, yp + c * S, a.relu);
-      }
-      if (F16) {
-        alignas(16) uint16_t hv[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) hv[c] = to16<BF>(acc[r][c]);
-        if (a.vec_y && ncol == C) {
-          *(uint4*)yp = *(const uint4*)hv;
-        } else {
-#pragma unroll
-          for (int c = 0; c < C; ++c)
-            if (c < ncol) ((uint16_t*)yp)[c] = hv[c];
-        }
-      } else {
-        if (a.vec_y && ncol == C) {
-          *(float4*)yp = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < C; ++c)
-            if (c < ncol) ((float*)yp)[c] = acc[r][c];
-        }
+      for (int c = 0; c < C; ++c) {
+        if (oidx[c] < 0) continue;
+        uint8_t* yp = a.y + ((int64_t)row * a.plane + oidx[c]) * S;
+        float v = acc[r][c];
+        if (epi) v = epilogue_one<F16, BF>(v, a.bias, row, a.beta, yp, a.relu);
+        if (F16)
+          *(uint16_t*)yp = to16<BF>(v);
+        else
+          *(float*)yp = v;
       }
     }
+  }
+}
+
+// Image-group interleaved, zero-haloed, dx-shifted copies for conv3x3_il_kernel:
+// xp[dx][ci][q Sg + r P + j W + x] = x[ci][q g + j][r - 1][x + dx - 1] (zero outside the
+// image, for the halo rows r = 0, H + 1 and for padding images b >= B).  Pure data movement:
+// a CTA stages `pp` (channel, group) blocks of g contiguous input planes in shared memory with
+// coalesced loads, then writes their three copies with 16-byte stores.
+template <typename T>
+__global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* __restrict__ xp, int cin, int B,
+                                                    int H, int W, int g, int ngroups, int Sg, int pp) {
+  constexpr int V = 16 / sizeof(T);
+  extern __shared__ __align__(16) uint8_t il_smem[];
+  T* sp = (T*)il_smem;  // [pp][g][H][W]
+  const int HW = H * W, P = g * W, blk = g * HW;
+  const int64_t nblk = (int64_t)cin * ngroups, span = (int64_t)ngroups * Sg;
+  for (int64_t b0 = (int64_t)blockIdx.x * pp; b0 < nblk; b0 += (int64_t)gridDim.x * pp) {
+    const int nb = (int)min((int64_t)pp, nblk - b0);
+    for (int i = threadIdx.x; i < nb * blk; i += blockDim.x) {
+      const int k = i / blk, e = i - k * blk;
+      const int64_t bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
+      const int64_t img = q * g + e / HW;
+      sp[i] = img < B ? __ldg(x + (ci * B + q * g) * HW + e) : T(0);
+    }
+    __syncthreads();
+    const int nv = nb * (Sg / V);
+    for (int dx = 0; dx < 3; ++dx) {
+      for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        const int e0 = i * V, k = e0 / Sg, rem = e0 - k * Sg;
+        const int64_t bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
+        alignas(16) T v[V];
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+          const int h = rem + c, r = h / P, xx = h - r * P, jj = xx / W, xs = xx - jj * W + dx - 1;
+          v[c] = (r >= 1 && r <= H && xs >= 0 && xs < W) ? sp[k * blk + jj * HW + (r - 1) * W + xs] : T(0);
+        }
+        *(uint4*)(xp + ((int64_t)dx * cin + ci) * span + q * Sg + rem) = *(const uint4*)v;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -2489,102 +2502,118 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
   return SPARSE_OK;
 }
 
-// Packed implicit-im2col conv (conv3x3_pk_kernel): one persistent wave; the input is read in
-// place through a 2-D tensor map over x viewed as C_in x (B H W) (CNHW).  TMA needs a 16-byte
-// row stride: otherwise x is first copied (device, stream ordered) to a padded-stride scratch.
-static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
+// Interleaved conv (conv3x3_il_kernel): the copies pre-pass into a stream-ordered scratch, then
+// one persistent wave (programmatic dependent launch after the pre-pass).
+static int launch_conv_il(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
                           std::string& err, const Epilogue& ep) {
   const bool f16 = p.dtype != SPARSE_F32, bf = p.dtype == SPARSE_BF16;
   const int S = f16 ? 2 : 4;
-  using PkFn = void (*)(const CUtensorMap, const PkArgs);
-  PkFn fn = nullptr;
-#define SRT_P(RR) \
-  if (p.R == RR) fn = bf ? conv3x3_pk_kernel<RR, true, true> : f16 ? conv3x3_pk_kernel<RR, true> : conv3x3_pk_kernel<RR, false>;
-  SRT_P(1) SRT_P(2) SRT_P(4) SRT_P(8)
-#undef SRT_P
+  using IlFn = void (*)(const CUtensorMap, const IlArgs);
+  IlFn fn = nullptr;
+#define SRT_I(RR) \
+  if (p.R == RR) fn = bf ? conv3x3_il_kernel<RR, true, true> : f16 ? conv3x3_il_kernel<RR, true> : conv3x3_il_kernel<RR, false>;
+  SRT_I(1) SRT_I(2) SRT_I(4) SRT_I(8)
+#undef SRT_I
   auto encode = tensor_map_encoder();
   if (!fn || !encode) {
-    err = "internal: no packed conv kernel instance / tensor-map encoder";
+    err = "internal: no interleaved conv kernel instance / tensor-map encoder";
     return SPARSE_EINTERNAL;
   }
-  const int64_t N = batch * (int64_t)p.h * p.w;
-  if (N > INT32_MAX - 1024) {
-    err = "packed conv: batch * H * W too large";
+  if (batch > INT32_MAX / 2) {
+    err = "batch too large";
+    return SPARSE_EUNSUPPORTED;
+  }
+  const int g = p.il_g, P = g * p.w, Sg = (p.h + 2) * P;
+  const int64_t ngroups = (batch + g - 1) / g, span = ngroups * Sg;
+  if (span > INT32_MAX - 4096) {
+    err = "interleaved conv: batch too large for one launch";
     return SPARSE_EUNSUPPORTED;
   }
   DeviceGuard dg(p.device);
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
   cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
-  const void* xa = x;
-  int64_t ldx = N;
-  void* scratch = nullptr;
-  if (((uintptr_t)x % 16) != 0 || ((N * S) % 16) != 0) {
-    const int rc = launch_repack(p.device, p.c_in, N, S, x, N, &scratch, &ldx, stream, err);
-    if (rc != SPARSE_OK) return rc;
-    xa = scratch;
+  void* xp = nullptr;
+  e = cudaMallocAsync(&xp, (size_t)(3 * p.c_in * span * S), (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(e, "cudaMallocAsync(conv copies)", err);
   }
   struct Free {
     void* b;
     void* st;
-    int dev;
-    ~Free() {
-      if (b) free_repack(dev, b, st);
+    ~Free() { cudaFreeAsync(b, (cudaStream_t)st); }
+  } fr{xp, stream};
+  {
+    const int blk = g * p.h * p.w;
+    const int pp = (int)std::max<int64_t>(1, std::min<int64_t>(16, (96 * 1024) / ((int64_t)blk * S)));
+    const size_t psm = (size_t)pp * blk * S;
+    const int64_t nblk = (int64_t)p.c_in * ngroups;
+    const unsigned pg = (unsigned)std::min<int64_t>((nblk + pp - 1) / pp, 148 * 8);
+    if (f16) {
+      if ((e = ensure_smem_attr(il_pad_input<uint16_t>, (int)psm)) != cudaSuccess)
+        return cuda_fail(e, "cudaFuncSetAttribute(il pad)", err);
+      il_pad_input<uint16_t><<<pg, 256, psm, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, p.c_in,
+                                                                     (int)batch, p.h, p.w, g, (int)ngroups, Sg, pp);
+    } else {
+      if ((e = ensure_smem_attr(il_pad_input<float>, (int)psm)) != cudaSuccess)
+        return cuda_fail(e, "cudaFuncSetAttribute(il pad)", err);
+      il_pad_input<float><<<pg, 256, psm, (cudaStream_t)stream>>>((const float*)x, (float*)xp, p.c_in, (int)batch,
+                                                                  p.h, p.w, g, (int)ngroups, Sg, pp);
     }
-  } fr{scratch, stream, p.device};
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "il pad launch", err);
+  }
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
-  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)p.c_in};
-  cuuint64_t strides[1] = {(cuuint64_t)(ldx * S)};
-  cuuint32_t box[2] = {(cuuint32_t)(p.pk_rawn > 256 ? p.pk_rawn / 2 : p.pk_rawn), (cuuint32_t)p.cc};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(&tmap, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                      const_cast<void*>(xa), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t dims[3] = {(cuuint64_t)span, (cuuint64_t)p.c_in, 3};
+  cuuint64_t strides[2] = {(cuuint64_t)(span * S), (cuuint64_t)(span * S * p.c_in)};
+  cuuint32_t box[3] = {(cuuint32_t)p.il_lc, (cuuint32_t)p.cc, 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(&tmap, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, xp, dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    err = "packed conv: cuTensorMapEncodeTiled failed";
+    err = "interleaved conv: cuTensorMapEncodeTiled failed";
     return SPARSE_EINTERNAL;
   }
-  PkArgs a;
+  IlArgs a;
   a.blob = p.d_blob;
   a.blk_off = p.d_blk_off;
   a.row_id = p.d_row_id;
   a.y = (uint8_t*)y;
-  a.N = N;
+  a.npos = ngroups * p.h * P;
+  a.plane = batch * (int64_t)p.h * p.w;
   a.H = p.h;
   a.W = p.w;
-  a.HW = p.h * p.w;
+  a.P = P;
+  a.g = g;
+  a.Bt = (int32_t)batch;
+  a.Sg = Sg;
   a.cc = p.cc;
   a.nchunks = p.nchunks;
   a.Mp = p.Mp;
   a.npanels = p.npanels;
   a.stages = p.stages;
-  a.fwarps = p.warps;
-  a.raw_bytes = p.pk_raw_bytes;
-  a.blk_at = p.pk_blk_at;
-  a.cp_at = p.pk_cp_at;
-  a.stage_bytes = p.pk_cp_at + p.x_stage_bytes;
-  a.rawn = p.pk_rawn;
-  a.p0 = p.pk_p0;
+  a.stage_bytes = p.il_stage_bytes;
+  a.lc = p.il_lc;
+  a.cs = p.conv_cs;
+  a.blk_at = p.il_blk_at;
   a.hdr_bytes = p.hdr_bytes;
   a.bar_off = p.smem_bytes - 256;
-  a.vec_y = ((uintptr_t)y % 16 == 0) && ((N * S) % 16 == 0);
-  a.box1_at = p.pk_rawn > 256 ? (p.cc * (p.pk_rawn / 2) * S + 127) / 128 * 128 : 0;
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
-  const int threads = (p.warps + kPkBuilders) * 32;  // FMA warps + the builder warps
   int sms = 148, per_sm = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, p.smem_bytes) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p.warps * 32, p.smem_bytes) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
   cudaGetLastError();
-  const int64_t ntot = (int64_t)p.npanels * ((N + p.n_tile - 1) / p.n_tile);
+  const int64_t ntot = (int64_t)p.npanels * ((a.npos + 127) / 128);
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ntot, (int64_t)sms * per_sm)), 1, 1);
-  cfg.blockDim = dim3((unsigned)threads, 1, 1);
+  cfg.blockDim = dim3((unsigned)(p.warps * 32), 1, 1);
   cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
@@ -2593,7 +2622,7 @@ static int launch_conv_pk(const Plan& p, int64_t batch, const void* x, void* y, 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
-  if (e != cudaSuccess) return cuda_fail(e, "conv3x3 (packed) launch", err);
+  if (e != cudaSuccess) return cuda_fail(e, "conv3x3 (interleaved) launch", err);
   return SPARSE_OK;
 }
 
@@ -2602,7 +2631,7 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
   const bool f16 = p.dtype != SPARSE_F32;  // 16-bit data (bf16 plans always take the TMA-fed kernel)
   ConvFn fn = p.conv_vec ? (f16 ? pick_conv_vec<true>(p.R) : pick_conv_vec<false>(p.R))
                         : (f16 ? pick_conv<true>(p.R, p.C) : pick_conv<false>(p.R, p.C));
-  if (p.conv_vec == 4) return launch_conv_pk(p, batch, x, y, stream, err, ep);
+  if (p.conv_vec == 4) return launch_conv_il(p, batch, x, y, stream, err, ep);
   if (!fn && p.conv_vec != 2) {
     err = "internal: no conv kernel instance for this tile configuration";
     return SPARSE_EINTERNAL;

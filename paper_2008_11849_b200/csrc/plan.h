@@ -39,9 +39,9 @@
 //                              k ascending, zero padding between slots
 //   zero padding to 16 bytes
 //
-// Vectorised conv plans (conv_vec 1 / 2) use the SpMM unit format above with the entry
-// offset pointing into the staged shifted copies (kernels.cu); packed conv plans (conv_vec 4)
-// use it with "X row" = im2col row tap * cc + ci of the tile built in shared memory.
+// Vectorised conv plans (conv_vec 1 / 2 / 4) use the SpMM unit format above with the entry
+// offset pointing into the staged shifted copies (kernels.cu); interleaved conv plans
+// (conv_vec 4) with 16-bit values carry the offset in 8-byte units.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -88,11 +88,10 @@ struct Plan {
   int32_t conv_stage_elems = 0;
   int32_t conv_vec = 0;   // 1: vectorised kernel (three dx-shifted copies, SpMM unit entries)
   int32_t conv_cs = 0;    // vectorised: elements per shifted copy = cc * conv_sci
-  // packed conv (conv_vec == 4, conv3x3_pk_kernel): packed positions n = (b H + y) W + x; per
-  // chunk a raw TMA span of pk_rawn elements per channel from n0 - pk_p0, expanded in shared
-  // memory into the im2col tile [9 cc rows (tap-major) + a zero row][n_tile] (kernels.cu)
-  int32_t pk_rawn = 0, pk_p0 = 0;
-  int32_t pk_blk_at = 0, pk_cp_at = 0, pk_raw_bytes = 0;
+  // interleaved conv (conv_vec == 4, conv3x3_il_kernel): il_g images interleaved per row group
+  // (pitch il_g * w), per chunk three TMA boxes of il_lc elements x cc channels (copy dx at
+  // dx * conv_cs elements), a zero block of il_lc, then the plan block at il_blk_at bytes
+  int32_t il_g = 0, il_lc = 0, il_stage_bytes = 0, il_blk_at = 0;
 
   // packed plan (host copy)
   std::vector<int32_t> row_id;   // npanels * Mp, -1 = empty slot

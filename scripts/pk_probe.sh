@@ -8,6 +8,6 @@ for cc in ${CCS:-4 8 12 16}; do for RW in ${RWS:-8:16 4:16 8:12 8:8}; do V="$V;c
 timeout 600 python scripts/conv_time.py f32 "$V" > gpurun_out/pk_f32.txt 2>&1
 timeout 600 python scripts/conv_time.py f16 "${V//k_chunk=32/k_chunk=16}" > gpurun_out/pk_f16.txt 2>&1
 if [ -n "$NCU_OPTS" ]; then
-  timeout 600 ncu --set full --import-source on --clock-control none -k regex:conv3x3_pk -s 1 -c 1 -o gpurun_out/ncu_pk -f \
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:conv3x3_il -s 1 -c 1 -o gpurun_out/ncu_pk -f \
     python scripts/conv_time.py ${NCU_DT:-f32} "$NCU_OPTS" > gpurun_out/ncu_pk.log 2>&1
 fi

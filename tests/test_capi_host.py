@@ -191,12 +191,12 @@ def test_conv_plan_decode():
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float16, torch.bfloat16])
 def test_packed_conv_plan_decode(dt):
-    # packed conv plans (conv_kernel 4): every nonzero decodes back to its (row, ci, dy, dx)
-    # with its value (im2col row tap * cc + ci of the staged tile)
+    # interleaved conv plans (conv_kernel 4): every nonzero decodes back to its (row, ci, dy, dx)
+    # with its value (copy dx, channel ci, tap row dy of the staged span)
     cin, cout = 16, 24
     w = gen.pruned_weights(cout, 9 * cin, 80, seed=4)
-    for (h, wd, nb, cc) in [(14, 14, 8, 5), (28, 28, 2, 3), (56, 56, 1, 16), (6, 9, 3, 4), (4, 4, 5, 7),
-                            (7, 7, 3, 16), (1, 1, 2, 3)]:
+    for (h, wd, nb, cc) in [(14, 14, 8, 5), (28, 28, 2, 3), (7, 7, 3, 16), (4, 4, 5, 7), (10, 6, 4, 4),
+                            (4, 8, 2, 9)]:
         pl = _plan(w, dtype=dt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=h, w=wd, n_hint=nb, k_chunk=cc,
                    conv_kernel=4)
         assert pl.info["conv_kernel"] == 4
@@ -207,6 +207,8 @@ def test_packed_conv_plan_decode(dt):
         assert np.array_equal(dense, ref)
     with pytest.raises(S.SparseRTError):  # rows_per_warp > 8
         _plan(w, kind=srt.SPARSE_CONV3X3, c_in=cin, h=7, w=7, n_hint=2, conv_kernel=4, rows_per_warp=16)
+    with pytest.raises(S.SparseRTError):  # 56-wide images: the tile's span exceeds one TMA box
+        _plan(w, kind=srt.SPARSE_CONV3X3, c_in=cin, h=56, w=56, n_hint=2, conv_kernel=4)
 
 
 def _rc(fn):

@@ -408,14 +408,13 @@ def test_conv_vectorised_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, f16
 @pytest.mark.parametrize("dt", ["f32", "f16", "bf16"])
 @pytest.mark.parametrize("cin,cout,B,H,W,R,warps,cc", [
     (16, 24, 3, 14, 14, 8, 16, 5), (256, 64, 2, 14, 14, 8, 16, 16), (256, 256, 5, 14, 14, 8, 16, 0),
-    (32, 16, 1, 56, 56, 4, 16, 8), (12, 20, 2, 28, 28, 8, 8, 4), (5, 9, 3, 6, 9, 2, 16, 2),
+    (32, 16, 1, 28, 28, 4, 16, 8), (12, 20, 2, 28, 28, 8, 8, 4), (5, 9, 3, 10, 6, 2, 16, 2),
     (8, 8, 5, 4, 4, 8, 16, 3), (64, 128, 4, 14, 14, 1, 16, 8), (40, 33, 7, 10, 6, 2, 8, 7),
-    (512, 64, 3, 7, 7, 4, 16, 12), (16, 20, 9, 1, 1, 2, 4, 5), (24, 16, 2, 3, 5, 1, 4, 12)])
+    (512, 64, 3, 7, 7, 4, 16, 12), (16, 20, 9, 4, 4, 2, 4, 5), (24, 16, 3, 4, 8, 1, 4, 12)])
 def test_conv_packed_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, dt):
-    # the packed implicit-im2col kernel (conv_kernel 4: positions n = (b H + y) W + x, no junk
-    # positions, raw input staged by TMA and the im2col tile built in shared memory by a
-    # builder warpgroup): exact on integer data and bitwise equal to the register-staged
-    # vectorised kernel (same k order); B H W not a 16-byte multiple takes the device repack
+    # the image-interleaved implicit-im2col kernel (conv_kernel 4: g images side by side per
+    # row, no junk positions except the padding images of a batch not a multiple of g): exact on
+    # integer data and bitwise equal to the register-staged vectorised kernel (same k order)
     dev = _dev()
     tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[dt]
     vmax_w, vmax_x = (3, 3) if dt == "f32" else (2, 4)
@@ -459,8 +458,8 @@ def test_conv_packed_real_valued_and_unsupported():
         err = oracle.rel_l2(y, _conv_ref(w, x, f16))
         assert err <= (F16_TOL if f16 else F32_TOL), err
     w7 = gen.pruned_weights(16, 9 * 8, 90, seed=79)
-    with pytest.raises(srt.SparseRTError):  # rows_per_warp > 8
-        srt.Plan.from_csr(w7, kind=srt.SPARSE_CONV3X3, c_in=8, h=7, w=7, n_hint=2, conv_kernel=4, rows_per_warp=16)
+    with pytest.raises(srt.SparseRTError):  # 56-wide images: span beyond one TMA box
+        srt.Plan.from_csr(w7, kind=srt.SPARSE_CONV3X3, c_in=8, h=56, w=56, n_hint=2, conv_kernel=4)
 
 
 @pytest.mark.parametrize("f16", [False, True])
