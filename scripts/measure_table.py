@@ -119,7 +119,7 @@ def run_case(c, sp, dt, timer, peaks, args):
         x = torch.from_numpy(gen.uniform_x(K, N, seed + 1)).to(dev).to(tdt)
         y = torch.empty((M, N), dtype=tdt, device=dev)
         base = dict(n_hint=N, executor=2)
-        mk = lambda ww, **kw: srt.Plan.from_csr(ww, dtype=tdt, device=0, **base, **kw)  # noqa: E731
+        mk = lambda ww, **kw: srt.Plan.from_csr(ww, dtype=tdt, device=0, **{**base, **kw})  # noqa: E731
         call = lambda p: p.spmm(x, y)  # noqa: E731
         Nn, Kx = N, K
     else:
@@ -129,7 +129,7 @@ def run_case(c, sp, dt, timer, peaks, args):
         x = torch.from_numpy(gen.relu_normal_x((C, B, H, H), seed + 1)).to(dev).to(tdt)
         y = torch.empty((M, B, H, H), dtype=tdt, device=dev)
         base = dict(kind=srt.SPARSE_CONV3X3, c_in=C, h=H, w=H, n_hint=B)
-        mk = lambda ww, **kw: srt.Plan.from_csr(ww, dtype=tdt, device=0, **base, **kw)  # noqa: E731
+        mk = lambda ww, **kw: srt.Plan.from_csr(ww, dtype=tdt, device=0, **{**base, **kw})  # noqa: E731
         call = lambda p: p.conv3x3(x, y)  # noqa: E731
         Nn, Kx = B * H * H, C
     t0 = time.perf_counter()

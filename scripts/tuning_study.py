@@ -68,10 +68,10 @@ def main():
                     opts_i.append(o)
                     if i == 0:
                         shape_opts = o
-                    p = srt.Plan.from_csr(w, dtype=tdt, **base, **o)
+                    p = srt.Plan.from_csr(w, dtype=tdt, **{**base, **o})
                     res["per_instance"].append(timer.cold(lambda: run(p)))
                     p.close()
-                    p = srt.Plan.from_csr(w, dtype=tdt, **base, **shape_opts)
+                    p = srt.Plan.from_csr(w, dtype=tdt, **{**base, **shape_opts})
                     res["per_shape"].append(timer.cold(lambda: run(p)))
                     p.close()
                 row = dict(name=name, dtype=dt, sparsity=args.sparsity, M=M, K=K, N=N, instances=args.instances,
