@@ -442,8 +442,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
         // interleaved per row so that a tap shift (dy - 1) P keeps a lane's vector aligned
         // (P % 4 == 0); the tile's span starts 16-byte aligned, up to 16 / S - 4 elements early
         int ilg = 0;
-        for (int gg = 1; gg <= 4 && !ilg; ++gg)
-          if ((gg * o.w) % 4 == 0) ilg = gg;
+        for (int gg = 1; gg <= 8 && !ilg; ++gg)  // (and whole 16-byte group blocks in the copies)
+          if ((gg * o.w) % 4 == 0 && ((int64_t)(o.h + 2) * gg * o.w * S) % 16 == 0) ilg = gg;
         int illc = 0;
         if (ilg) {
           const int P = ilg * o.w, HP = o.h * P;

@@ -410,7 +410,7 @@ def test_conv_vectorised_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, f16
     (16, 24, 3, 14, 14, 8, 16, 5), (256, 64, 2, 14, 14, 8, 16, 16), (256, 256, 5, 14, 14, 8, 16, 0),
     (32, 16, 1, 28, 28, 4, 16, 8), (12, 20, 2, 28, 28, 8, 8, 4), (5, 9, 3, 10, 6, 2, 16, 2),
     (8, 8, 5, 4, 4, 8, 16, 3), (64, 128, 4, 14, 14, 1, 16, 8), (40, 33, 7, 10, 6, 2, 8, 7),
-    (512, 64, 3, 7, 7, 4, 16, 12), (16, 20, 9, 4, 4, 2, 4, 5), (24, 16, 3, 4, 8, 1, 4, 12)])
+    (512, 64, 3, 7, 8, 4, 16, 12), (16, 20, 9, 4, 4, 2, 4, 5), (24, 16, 3, 4, 8, 1, 4, 12)])
 def test_conv_packed_exact_and_bitwise(cin, cout, B, H, W, R, warps, cc, dt):
     # the image-interleaved implicit-im2col kernel (conv_kernel 4: g images side by side per
     # row, no junk positions except the padding images of a batch not a multiple of g): exact on
