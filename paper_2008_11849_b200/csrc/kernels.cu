@@ -1484,36 +1484,46 @@ __global__ void __launch_bounds__(512) conv3x3_il_kernel(const __grid_constant__
 // xp[dx][ci][q Sg + r P + j W + x] = x[ci][q g + j][r - 1][x + dx - 1] (zero outside the
 // image, for the halo rows r = 0, H + 1 and for padding images b >= B).  Pure data movement:
 // a CTA stages `pp` (channel, group) blocks of g contiguous input planes in shared memory with
-// coalesced loads, then writes their three copies with 16-byte stores.
+// coalesced loads, then every warp writes whole output rows (lane = column of the row: the
+// column -> (image, x) decode is per lane, the row -> (block, copy, r) decode per row), so
+// the stores of a row are contiguous and the index math is amortised.
 template <typename T>
 __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* __restrict__ xp, int cin, int B,
                                                     int H, int W, int g, int ngroups, int Sg, int pp) {
-  constexpr int V = 16 / sizeof(T);
   extern __shared__ __align__(16) uint8_t il_smem[];
   T* sp = (T*)il_smem;  // [pp][g][H][W]
   const int HW = H * W, P = g * W, blk = g * HW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t nblk = (int64_t)cin * ngroups, span = (int64_t)ngroups * Sg;
+  constexpr int MAXC = 8;  // row columns per lane: P <= 256
+  int jx[MAXC];            // per column xx = lane + 32 m: j * W + x packed as j << 16 | x
+#pragma unroll
+  for (int m = 0; m < MAXC; ++m) {
+    const int xx = lane + 32 * m;
+    jx[m] = xx < P ? ((xx / W) << 16) | (xx % W) : -1;
+  }
   for (int64_t b0 = (int64_t)blockIdx.x * pp; b0 < nblk; b0 += (int64_t)gridDim.x * pp) {
     const int nb = (int)min((int64_t)pp, nblk - b0);
-    for (int i = threadIdx.x; i < nb * blk; i += blockDim.x) {
-      const int k = i / blk, e = i - k * blk;
+    for (int k = 0; k < nb; ++k) {  // block k = (ci, q): g contiguous planes (zero past the batch)
       const int64_t bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
-      const int64_t img = q * g + e / HW;
-      sp[i] = img < B ? __ldg(x + (ci * B + q * g) * HW + e) : T(0);
+      const int nimg = (int)min((int64_t)g, (int64_t)B - q * g);
+      const T* src = x + (ci * B + q * g) * HW;
+      T* dst = sp + (size_t)k * blk;
+      for (int i = threadIdx.x; i < blk; i += blockDim.x) dst[i] = i < nimg * HW ? __ldg(src + i) : T(0);
     }
     __syncthreads();
-    const int nv = nb * (Sg / V);
-    for (int dx = 0; dx < 3; ++dx) {
-      for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-        const int e0 = i * V, k = e0 / Sg, rem = e0 - k * Sg;
-        const int64_t bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
-        alignas(16) T v[V];
+    const int rows = nb * 3 * (H + 2);
+    for (int rw = warp; rw < rows; rw += nw) {  // output row (block k, copy dx, group row r)
+      const int k = rw / (3 * (H + 2)), rem = rw - k * 3 * (H + 2), dx = rem / (H + 2), r = rem - dx * (H + 2);
+      const int64_t bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
+      T* drow = xp + ((int64_t)dx * cin + ci) * span + q * Sg + (int64_t)r * P;
+      const T* srow = sp + (size_t)k * blk + (size_t)(r - 1) * W;
+      const bool inrow = r >= 1 && r <= H;
 #pragma unroll
-        for (int c = 0; c < V; ++c) {
-          const int h = rem + c, r = h / P, xx = h - r * P, jj = xx / W, xs = xx - jj * W + dx - 1;
-          v[c] = (r >= 1 && r <= H && xs >= 0 && xs < W) ? sp[k * blk + jj * HW + (r - 1) * W + xs] : T(0);
-        }
-        *(uint4*)(xp + ((int64_t)dx * cin + ci) * span + q * Sg + rem) = *(const uint4*)v;
+      for (int m = 0; m < MAXC; ++m) {
+        if (jx[m] < 0) break;
+        const int j = jx[m] >> 16, xs = (jx[m] & 0xffff) + dx - 1;
+        drow[lane + 32 * m] = (inrow && xs >= 0 && xs < W) ? srow[(size_t)j * HW + xs] : T(0);
       }
     }
     __syncthreads();

@@ -195,7 +195,7 @@ def test_packed_conv_plan_decode(dt):
     # with its value (copy dx, channel ci, tap row dy of the staged span)
     cin, cout = 16, 24
     w = gen.pruned_weights(cout, 9 * cin, 80, seed=4)
-    for (h, wd, nb, cc) in [(14, 14, 8, 5), (28, 28, 2, 3), (7, 7, 3, 16), (4, 4, 5, 7), (10, 6, 4, 4),
+    for (h, wd, nb, cc) in [(14, 14, 8, 5), (28, 28, 2, 3), (7, 8, 3, 16), (4, 4, 5, 7), (10, 6, 4, 4),
                             (4, 8, 2, 9)]:
         pl = _plan(w, dtype=dt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=h, w=wd, n_hint=nb, k_chunk=cc,
                    conv_kernel=4)
