@@ -1484,46 +1484,47 @@ __global__ void __launch_bounds__(512) conv3x3_il_kernel(const __grid_constant__
 // xp[dx][ci][q Sg + r P + j W + x] = x[ci][q g + j][r - 1][x + dx - 1] (zero outside the
 // image, for the halo rows r = 0, H + 1 and for padding images b >= B).  Pure data movement:
 // a CTA stages `pp` (channel, group) blocks of g contiguous input planes in shared memory with
-// coalesced loads, then every warp writes whole output rows (lane = column of the row: the
-// column -> (image, x) decode is per lane, the row -> (block, copy, r) decode per row), so
-// the stores of a row are contiguous and the index math is amortised.
+// coalesced loads; then each warp writes whole (block, copy) outputs of Sg contiguous elements,
+// lane l at elements l, l + 32, ... with the (r, j, x) coordinates advanced incrementally (no
+// per-element division), so every store instruction writes 32 consecutive elements.
 template <typename T>
 __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* __restrict__ xp, int cin, int B,
                                                     int H, int W, int g, int ngroups, int Sg, int pp) {
   extern __shared__ __align__(16) uint8_t il_smem[];
   T* sp = (T*)il_smem;  // [pp][g][H][W]
-  const int HW = H * W, P = g * W, blk = g * HW;
+  const int HW = H * W, blk = g * HW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t nblk = (int64_t)cin * ngroups, span = (int64_t)ngroups * Sg;
-  constexpr int MAXC = 8;  // row columns per lane: P <= 256
-  int jx[MAXC];            // per column xx = lane + 32 m: j * W + x packed as j << 16 | x
-#pragma unroll
-  for (int m = 0; m < MAXC; ++m) {
-    const int xx = lane + 32 * m;
-    jx[m] = xx < P ? ((xx / W) << 16) | (xx % W) : -1;
-  }
-  for (int64_t b0 = (int64_t)blockIdx.x * pp; b0 < nblk; b0 += (int64_t)gridDim.x * pp) {
-    const int nb = (int)min((int64_t)pp, nblk - b0);
+  const int nblk = cin * ngroups;
+  const int64_t span = (int64_t)ngroups * Sg;
+  for (int b0 = blockIdx.x * pp; b0 < nblk; b0 += gridDim.x * pp) {
+    const int nb = min(pp, nblk - b0);
     for (int k = 0; k < nb; ++k) {  // block k = (ci, q): g contiguous planes (zero past the batch)
-      const int64_t bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
-      const int nimg = (int)min((int64_t)g, (int64_t)B - q * g);
-      const T* src = x + (ci * B + q * g) * HW;
+      const int bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
+      const int nimg = min(g, B - q * g);
+      const T* src = x + ((int64_t)ci * B + (int64_t)q * g) * HW;
       T* dst = sp + (size_t)k * blk;
       for (int i = threadIdx.x; i < blk; i += blockDim.x) dst[i] = i < nimg * HW ? __ldg(src + i) : T(0);
     }
     __syncthreads();
-    const int rows = nb * 3 * (H + 2);
-    for (int rw = warp; rw < rows; rw += nw) {  // output row (block k, copy dx, group row r)
-      const int k = rw / (3 * (H + 2)), rem = rw - k * 3 * (H + 2), dx = rem / (H + 2), r = rem - dx * (H + 2);
-      const int64_t bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
-      T* drow = xp + ((int64_t)dx * cin + ci) * span + q * Sg + (int64_t)r * P;
-      const T* srow = sp + (size_t)k * blk + (size_t)(r - 1) * W;
-      const bool inrow = r >= 1 && r <= H;
-#pragma unroll
-      for (int m = 0; m < MAXC; ++m) {
-        if (jx[m] < 0) break;
-        const int j = jx[m] >> 16, xs = (jx[m] & 0xffff) + dx - 1;
-        drow[lane + 32 * m] = (inrow && xs >= 0 && xs < W) ? srow[(size_t)j * HW + xs] : T(0);
+    for (int t = warp; t < 3 * nb; t += nw) {  // output (block k, copy dx): Sg contiguous elements
+      const int k = t / 3, dx = t - 3 * k;
+      const int bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
+      T* dst = xp + ((int64_t)dx * cin + ci) * span + (int64_t)q * Sg;
+      const T* sb = sp + (size_t)k * blk;
+      // element e = lane: r = e / P, j = (e % P) / W, xw = e % W
+      int r = 0, j = 0, xw = lane;
+      while (xw >= W) {
+        xw -= W;
+        if (++j == g) j = 0, ++r;
+      }
+      for (int e = lane; e < Sg; e += 32) {
+        const int xs = xw + dx - 1;
+        dst[e] = (r >= 1 && r <= H && xs >= 0 && xs < W) ? sb[j * HW + (r - 1) * W + xs] : T(0);
+        xw += 32;
+        while (xw >= W) {
+          xw -= W;
+          if (++j == g) j = 0, ++r;
+        }
       }
     }
     __syncthreads();
@@ -1532,38 +1533,34 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
 
 // x[C_in][B][H][W] -> xp3[3][C_in][B][H + 1][wp]: xp3[dx][..][r][c] = x[..][r - 1][c + dx - 2],
 // zero outside the image (the layout conv3x3_tma_kernel reads through TMA).  Pure data movement:
-// a CTA stages kPadPlanes whole input planes in shared memory with coalesced loads (consecutive
-// threads, consecutive elements of the contiguous planes), then writes each plane's three
-// shifted, zero-haloed copies ((H + 1) x wp elements, contiguous per plane and copy) with
-// 16-byte stores.  (Round 1 used one thread per padded row with a 72-element register row:
-// scalar loads strided by a row per thread, ~50 % of HBM bandwidth.)
+// a CTA stages `kPadPlanes` whole input planes in shared memory with coalesced loads, then each
+// warp writes whole (plane, copy) outputs of (H + 1) wp contiguous elements, lane l at elements
+// l, l + 32, ... with (r, c) advanced incrementally.  (Round 1 used one thread per padded row
+// with a 72-element register row: scalar loads strided by a row per thread.)
 template <typename T>
 __global__ void __launch_bounds__(256) pad_conv_input(const T* __restrict__ x, T* __restrict__ xp, int64_t planes,
                                                       int H, int W, int wp, int kPadPlanes) {
-  constexpr int V = 16 / sizeof(T);
   extern __shared__ __align__(16) uint8_t pad_smem[];
-  T* sp = (T*)pad_smem;  // [kPadPlanes][H][W] (kPadPlanes: planes per CTA round, host-chosen)
-  const int HW = H * W, per = (H + 1) * wp;  // output elements per plane and copy (wp % V == 0)
+  T* sp = (T*)pad_smem;  // [kPadPlanes][H][W]
+  const int HW = H * W, per = (H + 1) * wp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t rows = planes * (H + 1);
   for (int64_t p0 = (int64_t)blockIdx.x * kPadPlanes; p0 < planes; p0 += (int64_t)gridDim.x * kPadPlanes) {
     const int np = (int)min((int64_t)kPadPlanes, planes - p0);
     const T* src = x + p0 * HW;
     for (int i = threadIdx.x; i < np * HW; i += blockDim.x) sp[i] = __ldg(src + i);
     __syncthreads();
-    const int nv = np * (per / V);  // 16-byte vectors per copy
-    for (int dx = 0; dx < 3; ++dx) {
-      T* dst = xp + ((int64_t)dx * rows + p0 * (H + 1)) * wp;  // planes p0.. of copy dx: contiguous
-      for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-        const int e0 = i * V, pl = e0 / per, rem = e0 - pl * per;
-        const int r = rem / wp, c0 = rem - r * wp;
-        const int y = r - 1;
-        alignas(16) T v[V];
-#pragma unroll
-        for (int c = 0; c < V; ++c) {
-          const int xx = c0 + c + dx - 2;
-          v[c] = (y >= 0 && xx >= 0 && xx < W) ? sp[pl * HW + y * W + xx] : T(0);
-        }
-        *(uint4*)(dst + e0) = *(const uint4*)v;
+    for (int t = warp; t < 3 * np; t += nw) {  // output (plane k, copy dx)
+      const int k = t / 3, dx = t - 3 * k;
+      T* dst = xp + ((int64_t)dx * rows + (p0 + k) * (H + 1)) * wp;
+      const T* sb = sp + (size_t)k * HW;
+      int r = 0, c = lane;
+      while (c >= wp) c -= wp, ++r;
+      for (int e = lane; e < per; e += 32) {
+        const int y = r - 1, xx = c + dx - 2;
+        dst[e] = (y >= 0 && xx >= 0 && xx < W) ? sb[y * W + xx] : T(0);
+        c += 32;
+        while (c >= wp) c -= wp, ++r;
       }
     }
     __syncthreads();
