@@ -1480,52 +1480,74 @@ __global__ void __launch_bounds__(512) conv3x3_il_kernel(const __grid_constant__
   }
 }
 
+// Shared-memory staging of `count` contiguous elements (16-byte vectors when the source and the
+// count allow it, 4 in flight per thread), zero-filled past `valid`.
+template <typename T>
+__device__ __forceinline__ void stage_contig(T* dst, const T* __restrict__ src, int count, int valid) {
+  constexpr int V = 16 / sizeof(T);
+  if (((uintptr_t)src % 16) == 0 && (count % V) == 0 && (valid % V) == 0) {
+    const int nv = count / V, vv = valid / V;
+    for (int i = threadIdx.x; i < nv; i += 4 * blockDim.x) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int iv = i + u * blockDim.x;
+        v[u] = iv < vv ? __ldg((const uint4*)src + iv) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u * blockDim.x < nv) ((uint4*)dst)[i + u * blockDim.x] = v[u];
+    }
+  } else {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = i < valid ? __ldg(src + i) : T(0);
+  }
+}
+
 // Image-group interleaved, zero-haloed, dx-shifted copies for conv3x3_il_kernel:
 // xp[dx][ci][q Sg + r P + j W + x] = x[ci][q g + j][r - 1][x + dx - 1] (zero outside the
 // image, for the halo rows r = 0, H + 1 and for padding images b >= B).  Pure data movement:
-// a CTA stages `pp` (channel, group) blocks of g contiguous input planes in shared memory with
-// coalesced loads; then each warp writes whole (block, copy) outputs of Sg contiguous elements,
-// lane l at elements l, l + 32, ... with the (r, j, x) coordinates advanced incrementally (no
-// per-element division), so every store instruction writes 32 consecutive elements.
+// a CTA stages `pp` (channel, group) blocks of g contiguous input planes in shared memory
+// (16-byte loads), then writes every (block, copy) output of Sg contiguous elements with
+// 16-byte stores, thread t at elements 4 t .. 4 t + 3 (P % 4 == 0: a vector never leaves its row).
 template <typename T>
 __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* __restrict__ xp, int cin, int B,
                                                     int H, int W, int g, int ngroups, int Sg, int pp) {
   extern __shared__ __align__(16) uint8_t il_smem[];
   T* sp = (T*)il_smem;  // [pp][g][H][W]
-  const int HW = H * W, blk = g * HW;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int HW = H * W, P = g * W, blk = g * HW;
   const int nblk = cin * ngroups;
   const int64_t span = (int64_t)ngroups * Sg;
+  const int nv = Sg / 4;  // 4-element vectors per (block, copy)
   for (int b0 = blockIdx.x * pp; b0 < nblk; b0 += gridDim.x * pp) {
     const int nb = min(pp, nblk - b0);
-    for (int k = 0; k < nb; ++k) {  // block k = (ci, q): g contiguous planes (zero past the batch)
+    // blocks b0 .. b0 + nb - 1 of one channel are contiguous in x unless they cross a channel
+    for (int k = 0; k < nb;) {
       const int bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
-      const int nimg = min(g, B - q * g);
-      const T* src = x + ((int64_t)ci * B + (int64_t)q * g) * HW;
-      T* dst = sp + (size_t)k * blk;
-      for (int i = threadIdx.x; i < blk; i += blockDim.x) dst[i] = i < nimg * HW ? __ldg(src + i) : T(0);
+      const int run = min(nb - k, ngroups - q);  // blocks left in this channel
+      const int valid = max(0, min(run * g, B - q * g)) * HW;
+      stage_contig<T>(sp + (size_t)k * blk, x + ((int64_t)ci * B + (int64_t)q * g) * HW, run * blk, valid);
+      k += run;
     }
     __syncthreads();
-    for (int t = warp; t < 3 * nb; t += nw) {  // output (block k, copy dx): Sg contiguous elements
+    for (int i = threadIdx.x; i < 3 * nb * nv; i += blockDim.x) {
+      const int t = i / nv, e0 = (i - t * nv) * 4;
       const int k = t / 3, dx = t - 3 * k;
       const int bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
-      T* dst = xp + ((int64_t)dx * cin + ci) * span + (int64_t)q * Sg;
-      const T* sb = sp + (size_t)k * blk;
-      // element e = lane: r = e / P, j = (e % P) / W, xw = e % W
-      int r = 0, j = 0, xw = lane;
-      while (xw >= W) {
-        xw -= W;
-        if (++j == g) j = 0, ++r;
-      }
-      for (int e = lane; e < Sg; e += 32) {
+      const int r = e0 / P, xx = e0 - r * P;
+      int j = xx / W, xw = xx - j * W;
+      const T* sb = sp + (size_t)k * blk + (size_t)(r - 1) * W;
+      alignas(16) T v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
         const int xs = xw + dx - 1;
-        dst[e] = (r >= 1 && r <= H && xs >= 0 && xs < W) ? sb[j * HW + (r - 1) * W + xs] : T(0);
-        xw += 32;
-        while (xw >= W) {
-          xw -= W;
-          if (++j == g) j = 0, ++r;
-        }
+        v[c] = (r >= 1 && r <= H && xs >= 0 && xs < W) ? sb[j * HW + xs] : T(0);
+        if (++xw == W) xw = 0, ++j;
       }
+      T* dst = xp + ((int64_t)dx * cin + ci) * span + (int64_t)q * Sg + e0;
+      if (sizeof(T) == 4)
+        *(uint4*)dst = *(const uint4*)v;
+      else
+        *(uint2*)dst = *(const uint2*)v;
     }
     __syncthreads();
   }
@@ -1533,35 +1555,34 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
 
 // x[C_in][B][H][W] -> xp3[3][C_in][B][H + 1][wp]: xp3[dx][..][r][c] = x[..][r - 1][c + dx - 2],
 // zero outside the image (the layout conv3x3_tma_kernel reads through TMA).  Pure data movement:
-// a CTA stages `kPadPlanes` whole input planes in shared memory with coalesced loads, then each
-// warp writes whole (plane, copy) outputs of (H + 1) wp contiguous elements, lane l at elements
-// l, l + 32, ... with (r, c) advanced incrementally.  (Round 1 used one thread per padded row
-// with a 72-element register row: scalar loads strided by a row per thread.)
+// a CTA stages `kPadPlanes` whole input planes in shared memory (16-byte loads when aligned),
+// then writes every (plane, copy) output of (H + 1) wp contiguous elements with 16-byte stores
+// (wp % V == 0: a vector never leaves its row).  (Round 1 used one thread per padded row with a
+// 72-element register row: scalar loads strided by a row per thread.)
 template <typename T>
 __global__ void __launch_bounds__(256) pad_conv_input(const T* __restrict__ x, T* __restrict__ xp, int64_t planes,
                                                       int H, int W, int wp, int kPadPlanes) {
+  constexpr int V = 16 / sizeof(T);
   extern __shared__ __align__(16) uint8_t pad_smem[];
   T* sp = (T*)pad_smem;  // [kPadPlanes][H][W]
-  const int HW = H * W, per = (H + 1) * wp;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int HW = H * W, nv = (H + 1) * wp / V;
   const int64_t rows = planes * (H + 1);
   for (int64_t p0 = (int64_t)blockIdx.x * kPadPlanes; p0 < planes; p0 += (int64_t)gridDim.x * kPadPlanes) {
     const int np = (int)min((int64_t)kPadPlanes, planes - p0);
-    const T* src = x + p0 * HW;
-    for (int i = threadIdx.x; i < np * HW; i += blockDim.x) sp[i] = __ldg(src + i);
+    stage_contig<T>(sp, x + p0 * HW, np * HW, np * HW);
     __syncthreads();
-    for (int t = warp; t < 3 * np; t += nw) {  // output (plane k, copy dx)
+    for (int i = threadIdx.x; i < 3 * np * nv; i += blockDim.x) {
+      const int t = i / nv, e0 = (i - t * nv) * V;
       const int k = t / 3, dx = t - 3 * k;
-      T* dst = xp + ((int64_t)dx * rows + (p0 + k) * (H + 1)) * wp;
-      const T* sb = sp + (size_t)k * HW;
-      int r = 0, c = lane;
-      while (c >= wp) c -= wp, ++r;
-      for (int e = lane; e < per; e += 32) {
-        const int y = r - 1, xx = c + dx - 2;
-        dst[e] = (y >= 0 && xx >= 0 && xx < W) ? sb[y * W + xx] : T(0);
-        c += 32;
-        while (c >= wp) c -= wp, ++r;
+      const int r = e0 / wp, c0 = e0 - r * wp, y = r - 1;
+      const T* sb = sp + (size_t)k * HW + (size_t)y * W;
+      alignas(16) T v[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) {
+        const int xx = c0 + c + dx - 2;
+        v[c] = (y >= 0 && xx >= 0 && xx < W) ? sb[xx] : T(0);
       }
+      *(uint4*)(xp + ((int64_t)dx * rows + (p0 + k) * (H + 1)) * wp + e0) = *(const uint4*)v;
     }
     __syncthreads();
   }
