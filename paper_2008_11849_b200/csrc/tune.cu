@@ -135,7 +135,7 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
         for (int w : {8, 16})
           for (int cc : {0, 8, 16, 24, 32}) {
             if (!vec && w == 16) continue;  // the position-strided kernel runs <= 8 warps
-            if (vec == 4 ? (R != 8 || w != 16 || cc == 0 || cc > 16) : vec == 2 ? cc == 8 : (cc == 0 || cc == 24)) continue;
+            if (vec == 4 ? (R == 2 || w != 16 || cc < 16) : vec == 2 ? cc == 8 : (cc == 0 || cc == 24)) continue;
             BuildOpts o = base;
             o.rows_per_warp = R;
             o.warps = w;
