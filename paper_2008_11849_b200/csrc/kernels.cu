@@ -1480,6 +1480,15 @@ __global__ void __launch_bounds__(512) conv3x3_il_kernel(const __grid_constant__
   }
 }
 
+// a / b for 0 <= a < 2^22 and a runtime divisor b with its reciprocal: one float multiply and
+// a +-1 correction instead of an integer division (pre-pass index math is instruction bound)
+__device__ __forceinline__ int div_rcp(int a, int b, float rb) {
+  int q = (int)((float)a * rb);
+  if (q * b > a) --q;
+  else if ((q + 1) * b <= a) ++q;
+  return q;
+}
+
 // Shared-memory staging of `count` contiguous elements (16-byte vectors when the source and the
 // count allow it, 4 in flight per thread), zero-filled past `valid`.
 template <typename T>
@@ -1529,12 +1538,13 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
       k += run;
     }
     __syncthreads();
+    const float rnv = 1.0f / nv, rng = 1.0f / ngroups, rP = 1.0f / P, rW = 1.0f / W;
     for (int i = threadIdx.x; i < 3 * nb * nv; i += blockDim.x) {
-      const int t = i / nv, e0 = (i - t * nv) * 4;
-      const int k = t / 3, dx = t - 3 * k;
-      const int bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
-      const int r = e0 / P, xx = e0 - r * P;
-      int j = xx / W, xw = xx - j * W;
+      const int t = div_rcp(i, nv, rnv), e0 = (i - t * nv) * 4;
+      const int k = div_rcp(t, 3, 1.0f / 3.0f), dx = t - 3 * k;
+      const int bb = b0 + k, ci = div_rcp(bb, ngroups, rng), q = bb - ci * ngroups;
+      const int r = div_rcp(e0, P, rP), xx = e0 - r * P;
+      int j = div_rcp(xx, W, rW), xw = xx - j * W;
       const T* sb = sp + (size_t)k * blk + (size_t)(r - 1) * W;
       alignas(16) T v[4];
 #pragma unroll
@@ -1571,10 +1581,11 @@ __global__ void __launch_bounds__(256) pad_conv_input(const T* __restrict__ x, T
     const int np = (int)min((int64_t)kPadPlanes, planes - p0);
     stage_contig<T>(sp, x + p0 * HW, np * HW, np * HW);
     __syncthreads();
+    const float rnv = 1.0f / nv, rwp = 1.0f / wp;
     for (int i = threadIdx.x; i < 3 * np * nv; i += blockDim.x) {
-      const int t = i / nv, e0 = (i - t * nv) * V;
-      const int k = t / 3, dx = t - 3 * k;
-      const int r = e0 / wp, c0 = e0 - r * wp, y = r - 1;
+      const int t = div_rcp(i, nv, rnv), e0 = (i - t * nv) * V;
+      const int k = div_rcp(t, 3, 1.0f / 3.0f), dx = t - 3 * k;
+      const int r = div_rcp(e0, wp, rwp), c0 = e0 - r * wp, y = r - 1;
       const T* sb = sp + (size_t)k * HW + (size_t)y * W;
       alignas(16) T v[V];
 #pragma unroll
