@@ -116,7 +116,10 @@ typedef struct {
                             position-strided kernel); 1 = position-strided kernel; 2 = TMA-fed
                             vectorised kernel: the shifted copies are written once to a stream-
                             ordered scratch by a pre-pass, then each is one 5-D TMA box per chunk;
-                            3 = register-staged vectorised kernel.  All result-identical. */
+                            3 = register-staged vectorised kernel; 4 = image-interleaved kernel:
+                            g images side by side per row so that no output position is padding
+                            (copies from a pre-pass, one TMA span box per copy and chunk; images
+                            up to ~28 wide).  All result-identical. */
   int32_t row_order;     /* 0 = load-balanced panels (rows sorted by nnz, LPT-binned, P:163-165;
                             default); 1 = natural contiguous row ranges (the "no load balancing"
                             ablation of P:385).  Result-neutral for split_k = k_split = 1. */
@@ -126,6 +129,12 @@ typedef struct {
                             result before its single rounding.  0 = default
                             (50 %), -1 = off, 1..100 = threshold.  Changes the summation order
                             of the rows concerned (within tolerance; exact on integer data). */
+  int32_t plan_source;   /* SpMM plan-driven executor: 0 = the plan's (panel, chunk) blocks are
+                            staged into shared memory with each X chunk (default); 1 = the whole
+                            plan (<= 30 KB) is passed as a kernel parameter and read through the
+                            constant cache; the paper keeps A's values in the constant cache,
+                            P:185.  Needs split_k = k_split = x_multicast = 1, x_source = 0,
+                            no tensor-core sub-blocks.  Result-neutral (bitwise). */
 } sparse_plan_opts;
 
 /* Fill *opts with defaults (kind SPMM, device -1, everything else 0). */
@@ -252,6 +261,7 @@ typedef struct {
   int64_t tc_nnz;         /* nonzeros inside them (counted in nnz) */
   int64_t tc_panel_steps; /* executor 3: k16 steps over all (panel, chunk) pairs; the tensor cores
                              execute 2 * 16 * 16 * N flops per step (useful: 2 * nnz * N) */
+  int32_t plan_source;  /* 0 staged with X, 1 kernel parameters */
 } sparse_plan_info_t;
 
 int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out);

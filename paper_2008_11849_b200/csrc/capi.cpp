@@ -76,6 +76,7 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   if (o.tc_min_density < -1 || o.tc_min_density > 100)
     return fail(SPARSE_EINVAL, "tc_min_density must be -1 (off), 0 (default) or 1..100");
   bo.tc_min_pct = o.tc_min_density == 0 ? 50 : (o.tc_min_density < 0 ? 0 : o.tc_min_density);
+  bo.ps = o.plan_source;
   if (o.stages < 0 || o.stages > srt::kMaxStages)
     return fail(SPARSE_EUNSUPPORTED, "stages must be in [0, 8]");
   sparse_plan_s* h = nullptr;
@@ -114,7 +115,7 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   const bool auto_exec = bo.executor == 2;
   // auto: try the JIT executor first, except where it cannot apply (bf16 values, the TMEM X
   // source, conv plans), which go straight to the plan-driven kernel
-  if (auto_exec) bo.executor = (dtype == SPARSE_BF16 || bo.tm || bo.kind != SPARSE_SPMM) ? 0 : 1;
+  if (auto_exec) bo.executor = (dtype == SPARSE_BF16 || bo.tm || bo.ps || bo.kind != SPARSE_SPMM) ? 0 : 1;
   try {
     rc = srt::build_plan(h->p, M, K, nnz, row_ptr, col_idx, values, dtype, bo, err);
     if (auto_exec && bo.executor == 1 &&
@@ -400,6 +401,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->tc_tiles = p.tc_ntiles;
   out->tc_panel_steps = p.tcp_nsteps;
   out->tc_nnz = p.tc_nnz;
+  out->plan_source = p.ps;
   return ok();
 }
 

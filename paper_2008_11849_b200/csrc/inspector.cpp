@@ -240,7 +240,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
   std::vector<uint16_t> tc_a;
   int64_t tc_nnz = 0;
   // (not with the JIT executor, which bakes every nonzero into its code)
-  const int tc_pct = (dtype == SPARSE_F16 && o.kind == SPARSE_SPMM && o.executor != 1 && o.executor != 3) ? o.tc_min_pct : 0;
+  const int tc_pct = (dtype == SPARSE_F16 && o.kind == SPARSE_SPMM && o.executor != 1 && o.executor != 3 && !o.ps) ? o.tc_min_pct : 0;
   if (tc_pct < 0 || tc_pct > 100) {
     err = "tc_min_density must be in [0, 100] (percent)";
     return SPARSE_EINVAL;
@@ -817,6 +817,27 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
                  (int64_t)p.blk_off.size() * 8 + (int64_t)p.tc_a.size() * 2 +
                  (int64_t)(p.tc_cb.size() + p.tc_rb.size() + p.tc_tile_begin.size() + p.ws_row.size()) * 4;
 
+  p.ps = o.ps;
+  if (o.ps != 0 && o.ps != 1) {
+    err = "plan_source must be 0 (staged with X) or 1 (kernel parameters)";
+    return SPARSE_EINVAL;
+  }
+  if (o.ps == 1) {
+    // plan in kernel parameters (spmm_param_kernel): the plain persistent plan-driven SpMM only
+    if (o.kind != SPARSE_SPMM || (o.executor != 0 && o.executor != 2) || p.ks != 1 || p.cm != 1 || p.tm ||
+        p.gk != 1 || p.tc_ntiles > 0 || p.R > 8) {
+      err = "plan_source = 1 needs a plan-driven SpMM plan with split_k = k_split = x_multicast = 1, "
+            "x_source = 0, no tensor-core sub-blocks and rows_per_warp <= 8";
+      return SPARSE_EUNSUPPORTED;
+    }
+    if ((int64_t)p.blob.size() > 30 * 1024) {
+      snprintf(buf, sizeof buf, "plan_source = 1: plan blob of %lld bytes exceeds the 30 KB parameter space",
+               (long long)p.blob.size());
+      err = buf;
+      return SPARSE_EUNSUPPORTED;
+    }
+  }
+
   if (o.executor == 1) {
     if (o.kind != SPARSE_SPMM) {
       err = "executor = JIT is only supported for SpMM plans";
@@ -999,7 +1020,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
                          p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
                          p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm,
                          p.conv_vec, p.row_order, p.executor, p.jit_mp, p.jit_warps, p.stages,
-                         p.tc_min_pct};
+                         p.tc_min_pct, p.ps};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

@@ -840,6 +840,145 @@ __global__ void __launch_bounds__(512, SRT_MINB) spmm_kernel(const __grid_consta
   cluster.sync();  // keep every CTA's smem alive until all remote reads are done
 }
 
+// ------------------------------------------------------------------ SpMM, plan in kernel parameters
+// The paper keeps the sparse values in the constant cache (baked into the code, P:185, P:379:
+// "the value of the sparse matrix A is broadcast across the thread group, it is an ideal use case
+// for the constant cache").  plan_source = 1 is that idea for the plan-driven executor: a plan of
+// at most kParamPlanBytes travels as a __grid_constant__ kernel parameter (constant bank 0), so
+// every warp-uniform plan read is an LDC from the constant cache instead of a shared-memory
+// broadcast load, and the ring stages carry X only (no per-chunk bulk copy of plan blocks).
+// Same tiles, ring, FMA order and epilogue as spmm_kernel (k_split = 1, no multicast / TMEM):
+// results are bitwise equal.
+constexpr int kParamPlanBytes = 30 * 1024;
+struct ParamPlan {
+  uint4 d[kParamPlanBytes / 16];
+};
+
+template <int R, bool F16, bool BF = false>
+__global__ void __launch_bounds__(512, SRT_MINB) spmm_param_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                   const SpmmArgs a,
+                                                                   const __grid_constant__ ParamPlan pp) {
+  constexpr int C = F16 ? 8 : 4;
+  constexpr int S = F16 ? 2 : 4;
+  constexpr int NT = 32 * C;
+  constexpr int ROWB = NT * S;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int np = a.npanels;
+  const int ntiles = np * (int)((a.N + NT - 1) / NT);
+  const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = my_tiles * a.nchunks;
+  const uint32_t full0 = smem_u32(smem + a.bar_off);
+  uint32_t* ctr = (uint32_t*)(smem + a.bar_off + 16 * kMaxStages);
+  for (int s = 0; s < a.stages; ++s)  // the zero row after the kc X rows of every stage
+    for (int i = tid; i < ROWB / 16; i += blockDim.x)
+      *(uint4*)(smem + s * a.stage_bytes + a.kc * ROWB + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
+  if (tid < kMaxStages) ctr[tid] = 0u;
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) mbar_init(full0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  auto tile_of = [&](int ti, int& panel, int64_t& n0) {
+    const int t = (int)blockIdx.x + ti * (int)gridDim.x;
+    panel = t % np;
+    n0 = (int64_t)(t / np) * NT;
+  };
+  auto refill = [&](int q) {  // lane 0 of one warp: the X box of chunk q only
+    const int slot = q % a.stages;
+    const int ti = q / a.nchunks, c = q - ti * a.nchunks;
+    int panel;
+    int64_t n0;
+    tile_of(ti, panel, n0);
+    const uint32_t fb = full0 + 8 * slot;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(fb, (uint32_t)(a.kc * ROWB));
+    tma_load_2d(smem_u32(smem + slot * a.stage_bytes), &tmap, (int)n0, c * a.kc, fb);
+  };
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (warp == 0 && lane == 0)
+    for (int q = 0; q < min(a.stages, total); ++q) refill(q);
+  float acc[R][C];
+  int q = 0, slot = 0;
+  uint32_t ph = 0;
+  for (int ti = 0; ti < my_tiles; ++ti) {
+    int panel;
+    int64_t n0;
+    tile_of(ti, panel, n0);
+    int rows[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rows[r] = __ldg(a.row_id + (int64_t)panel * a.Mp + warp * R + r);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+    const int xoff = ((lane & ~7) * C < (int)min((int64_t)NT, a.N - n0)) ? lane * (C * S) : 0;
+    for (int j = 0; j < a.nchunks; ++j) {
+      mbar_wait(full0 + 8 * slot, ph);
+      const uint8_t* xs = smem + slot * a.stage_bytes + xoff;
+      // plan block of (panel, chunk j): fixed stride a.blk_bytes in the parameter blob
+      const int b16 = (panel * a.nchunks + j) * (a.blk_bytes / 16);
+      const uint32_t* shdr = (const uint32_t*)&pp.d[b16];
+      const uint4* ents = &pp.d[b16 + a.hdr_bytes / 16];
+      uint32_t h[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) h[r] = shdr[warp * R + r];
+      run_rows<F16, R, BF>(acc, h, ents, xs);
+      __syncwarp();
+      uint32_t old = 0;
+      if (lane == 0)
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old) : "r"(smem_u32(ctr + slot)) : "memory");
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if ((old + 1u) % (uint32_t)nwarps == 0u && q + a.stages < total && lane == 0) refill(q + a.stages);
+      ++q;
+      if (++slot == a.stages) {
+        slot = 0;
+        ph ^= 1u;
+      }
+    }
+    const int ncol = (int)min((int64_t)NT, a.N - n0);
+    const int col = lane * C;
+    if (col >= ncol) continue;
+    const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = rows[r];
+      if (row < 0) continue;
+      uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + col) * S;
+      if (epi) {
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          if (col + c < ncol) acc[r][c] = epilogue_one<F16, BF>(acc[r][c], a.bias, row, a.beta, yp + c * S, a.relu);
+      }
+      if (F16) {
+        alignas(16) uint16_t hv[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) hv[c] = to16<BF>(acc[r][c]);
+        if (a.vec_y && col + C <= ncol) {
+          *(uint4*)yp = *(const uint4*)hv;
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (col + c < ncol) ((uint16_t*)yp)[c] = hv[c];
+        }
+      } else {
+        if (a.vec_y && col + C <= ncol) {
+          *(float4*)yp = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (col + c < ncol) ((float*)yp)[c] = acc[r][c];
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ conv 3x3
 struct ConvArgs {
   const uint8_t* blob;
@@ -2459,6 +2598,53 @@ int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, i
       if (w) cudaFreeAsync(w, (cudaStream_t)st);
     }
   } ws_free{tcws, stream};
+  if (p.ps == 1) {
+    // plan in kernel parameters (constant bank): X through TMA only
+    a.X = (const uint8_t*)X;
+    a.Y = (uint8_t*)Y;
+    a.N = N;
+    a.cm = 1;
+    CUtensorMap tmap;
+    make_map(tmap);
+    if (!a.use_tma) {
+      err = "plan_source = 1 needs the TMA path (16-byte aligned X)";
+      return SPARSE_EINTERNAL;
+    }
+    using PFn = void (*)(const CUtensorMap, const SpmmArgs, const ParamPlan);
+    PFn pf = nullptr;
+    const bool bf = p.dtype == SPARSE_BF16;
+#define SRT_PP(RR) \
+    if (p.R == RR) pf = bf ? spmm_param_kernel<RR, true, true> : f16 ? spmm_param_kernel<RR, true> : spmm_param_kernel<RR, false>;
+    SRT_PP(1) SRT_PP(2) SRT_PP(4) SRT_PP(8)
+#undef SRT_PP
+    if (!pf || p.blob.size() > sizeof(ParamPlan)) {
+      err = "internal: no parameter-plan kernel instance / plan too large";
+      return SPARSE_EINTERNAL;
+    }
+    if ((e = ensure_smem_attr(pf, smem)) != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
+    static thread_local ParamPlan pp;  // 30 KB: not on the host stack
+    std::memcpy(&pp, p.blob.data(), p.blob.size());
+    const int64_t ntiles = (int64_t)p.npanels * ntn;
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pf, threads, smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    cudaGetLastError();
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm)), 1, 1);
+    cfg.blockDim = dim3((unsigned)threads, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, pf, tmap, a, pp);
+    if (e != cudaSuccess) return cuda_fail(e, "spmm (parameter plan) launch", err);
+    return SPARSE_OK;
+  }
   if (p.ks == 1) {
     // persistent: one wave of CTAs (clusters of cm CTAs when X is multicast), each walking
     // tiles (panel group, N tile) cluster_id + j * clusters

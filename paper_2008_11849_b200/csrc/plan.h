@@ -77,6 +77,7 @@ struct Plan {
   int32_t cm = 1;           // X multicast cluster: CTAs (consecutive panels) sharing X tiles
   int32_t row_order = 0;    // 0 = LPT load balancing (default), 1 = natural order (ablation)
   int32_t tm = 0;           // X source: 0 = shared memory, 1 = tensor memory (tcgen05.ld)
+  int32_t ps = 0;           // plan source: 0 = staged per chunk with X, 1 = kernel parameters
 
   // conv geometry (kind == CONV3X3)
   int32_t conv_rb = 0;    // output rows per tile
@@ -198,6 +199,7 @@ struct BuildOpts {
   int32_t conv_vec = 1;   // allow the vectorised conv kernel
   int32_t row_order = 0;  // 0 = LPT panels (load balancing), 1 = natural contiguous rows
   int32_t tc_min_pct = 50;  // tensor-core sub-blocks: min % of nonzeros in a 16x16 tile (0 = off)
+  int32_t ps = 0;           // plan source (sparse_plan_opts.plan_source)
 };
 
 // JIT executor (jit.cpp).  Row entries per row (k ascending) as validated by the

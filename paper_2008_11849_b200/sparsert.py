@@ -50,7 +50,8 @@ class sparse_plan_opts(ctypes.Structure):
                 ("executor", ctypes.c_int32), ("jit_rows", ctypes.c_int32),
                 ("jit_warps", ctypes.c_int32), ("x_multicast", ctypes.c_int32),
                 ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
-                ("row_order", ctypes.c_int32), ("tc_min_density", ctypes.c_int32)]
+                ("row_order", ctypes.c_int32), ("tc_min_density", ctypes.c_int32),
+                ("plan_source", ctypes.c_int32)]
 
 
 class sparse_epilogue(ctypes.Structure):
@@ -76,7 +77,8 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
                 ("row_order", ctypes.c_int32), ("tc_min_density", ctypes.c_int32),
                 ("tc_row_blocks", ctypes.c_int32), ("tc_tiles", ctypes.c_int64),
-                ("tc_nnz", ctypes.c_int64), ("tc_panel_steps", ctypes.c_int64)]
+                ("tc_nnz", ctypes.c_int64), ("tc_panel_steps", ctypes.c_int64),
+                ("plan_source", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -283,6 +285,8 @@ class Plan:
                      x_source=i["x_source"], tc_min_density=i["tc_min_density"] or -1)
             if i["executor"] == 1:
                 o.update(jit_rows=i["jit_rows"], jit_warps=i["jit_warps"])
+            if i["plan_source"]:
+                o.update(plan_source=i["plan_source"])
         else:
             o.update(k_chunk=i["k_chunk"], conv_kernel=i["conv_kernel"])
             o.pop("split_k")

@@ -977,3 +977,34 @@ def test_conv3x3_nhwc_exact(cin, cout, B, H, W, dt):
     ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), x.astype(np.float64))
     ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
     assert np.array_equal(y_cnhw.double().cpu().numpy(), ref)
+
+
+# --------------------------------------------------------------------------- plan in kernel parameters (NEXT #2)
+
+@pytest.mark.parametrize("dt", ["f32", "f16", "bf16"])
+@pytest.mark.parametrize("M,K,N,opts", [(64, 64, 128, {}), (64, 256, 25088, dict(rows_per_warp=2)),
+                                         (256, 64, 3136, {}), (64, 32, 12544, dict(warps=8)),
+                                         (128, 64, 1000, dict(rows_per_warp=8, k_chunk=32, stages=4)),
+                                         (96, 100, 77, dict(rows_per_warp=1))])
+def test_param_plan_exact_and_bitwise(M, K, N, opts, dt):
+    # plan_source = 1: the plan as a kernel parameter read through the constant cache:
+    # exact on integer data and bitwise equal to the staged-plan kernel on real-valued data
+    dev = _dev()
+    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[dt]
+    vw, vx = (3, 3) if dt == "f32" else (2, 4)
+    wi = gen.int_weights(M, K, 90, seed=M + K, vmax=vw)
+    xi = gen.int_x(K, N, seed=N, vmax=vx)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, plan_source=1, **opts)
+    assert plan.info["plan_source"] == 1
+    y = plan.spmm(torch.from_numpy(xi).to(dev).to(tdt))
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), xi.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(y.double().cpu().numpy(), ref)
+    w = gen.pruned_weights(M, K, 90, seed=M * 3 + K)
+    x = torch.from_numpy(gen.uniform_x(K, N, seed=5)).to(dev).to(tdt)
+    p1 = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, plan_source=1, **opts)
+    p0 = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, plan_source=0, tc_min_density=-1, **opts)
+    assert torch.equal(p1.spmm(x), p0.spmm(x))
+    with pytest.raises(srt.SparseRTError):  # too large for the parameter space
+        srt.Plan.from_csr(gen.pruned_weights(3072, 768, 90, seed=1), dtype=tdt, n_hint=N, plan_source=1)
