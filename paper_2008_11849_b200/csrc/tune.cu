@@ -107,6 +107,14 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
                 o.split_k = gk;
                 o.executor = 0;
                 cands.push_back(o);
+                // small plans: the same tiles with the plan in kernel parameters (constant
+                // cache, plan_source = 1; build_plan rejects plans over 30 KB)
+                const int64_t est = nnz * (S == 2 ? 4 : 8);
+                if (ks == 1 && gk == 1 && st == -1 && kc > 32 && est < 24 * 1024) {
+                  o.ps = 1;
+                  o.tc_min_pct = 0;
+                  cands.push_back(o);
+                }
               }
     if (f16) {  // tensor-core sub-blocks on / off (when the matrix has dense 16x16 tiles)
       for (int tc : {50, 0}) {
