@@ -325,7 +325,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     int gk = 1;
     if (o.split_k) {
       gk = o.split_k;
-    } else if (o.n_hint > 0) {
+    } else if (o.n_hint > 0 && !o.ps) {  // (the parameter-plan kernel has no split-K groups)
       int L = pow2_ceil((int)((o.n_hint + p.C - 1) / p.C));
       L = std::max(4, std::min(32, L));
       gk = 32 / L;
@@ -540,7 +540,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       while (bestKs * 2 <= max_ks) bestKs *= 2;
     }
     p.R = o.rows_per_warp ? o.rows_per_warp : bestR;
-    p.ks = o.k_split ? o.k_split : (o.rows_per_warp ? 1 : bestKs);
+    p.ks = o.k_split ? o.k_split : (o.rows_per_warp || o.ps ? 1 : bestKs);
   }
   if (p.R != 1 && p.R != 2 && p.R != 4 && p.R != 8 && p.R != 16) {
     err = "rows_per_warp must be 1, 2, 4, 8 or 16";
