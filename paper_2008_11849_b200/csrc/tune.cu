@@ -91,7 +91,9 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
               for (int gk : {1, 2, 4}) {
                 const int nch = (K + kc - 1) / kc;
                 if (ks > nch || (ks > 1 && !medium) || (ks == 8 && !small)) continue;
-                if (gk > 1 && !small) continue;
+                // split-K groups: small N (narrow tiles), and gk = 2 for the HBM-streaming
+                // layers (K <= 256: twice the N tiles -> a finer last wave on 148 SMs)
+                if (gk > 1 && !small && !(gk == 2 && K <= 256 && ks == 1 && st == -1)) continue;
                 if (gk == 2 && N <= 256) continue;  // N <= 256: G_k in {1, 4}
                 if (gk == 4 && N > 256) continue;
                 if (R == 8 && (small || R * C > 64)) continue;

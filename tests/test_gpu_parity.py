@@ -1004,7 +1004,7 @@ def test_param_plan_exact_and_bitwise(M, K, N, opts, dt):
     w = gen.pruned_weights(M, K, 90, seed=M * 3 + K)
     x = torch.from_numpy(gen.uniform_x(K, N, seed=5)).to(dev).to(tdt)
     p1 = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, plan_source=1, **opts)
-    p0 = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, plan_source=0, tc_min_density=-1, **opts)
+    p0 = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, plan_source=0, tc_min_density=-1, split_k=1, k_split=1, **opts)
     assert torch.equal(p1.spmm(x), p0.spmm(x))
     with pytest.raises(srt.SparseRTError):  # too large for the parameter space
         srt.Plan.from_csr(gen.pruned_weights(3072, 768, 90, seed=1), dtype=tdt, n_hint=N, plan_source=1)
