@@ -1442,6 +1442,11 @@ struct IlArgs {
   const uint8_t* bias;
   float beta;
   int32_t relu;
+  // overlap with the pre-pass (programmatic dependent launch): group q's copies are complete
+  // when ready[q] == ready_target (= C_in); nullptr = the pre-pass completed before launch
+  const uint32_t* ready;
+  uint32_t ready_target;
+  int32_t ngroups;
 };
 
 // 16-bit entries for 4 positions per lane: unit = 4 x {uint16 xoff (8-byte units), half / bf16 w}
@@ -1534,6 +1539,22 @@ __global__ void __launch_bounds__(512) conv3x3_il_kernel(const __grid_constant__
     uint8_t* st = smem + (size_t)slot * a.stage_bytes;
     const uint32_t fb = full0 + 8 * slot;
     const int hb = (int)((hcoord(n0) - a.P) & ~(int64_t)(16 / S - 1));  // 16-byte aligned span start
+    if (a.ready) {
+      // the span's image groups must be complete in the copies (written by the concurrently
+      // running pre-pass): acquire their counters, then order the async-proxy (TMA) reads
+      // after them; bounded spin (a missing producer traps instead of hanging the GPU)
+      const int q0 = hb / a.Sg, q1 = min(a.ngroups - 1, (hb + a.lc - 1) / a.Sg);
+      for (int qq = q0; qq <= q1; ++qq) {
+        uint32_t v, spins = 0;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.ready + qq) : "memory");
+          if (v >= a.ready_target) break;
+          __nanosleep(64);
+          if (++spins > (1u << 26)) __trap();
+        } while (true);
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_expect_tx(fb, (uint32_t)(3 * a.cc * a.lc * S) + nb);
 #pragma unroll
@@ -1546,7 +1567,8 @@ __global__ void __launch_bounds__(512) conv3x3_il_kernel(const __grid_constant__
     if (nb) bulk_load(smem_u32(st + a.blk_at), a.blob + blk0, nb, fb);
   };
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // overlapped with the pre-pass: do not wait for its completion (per-group counters instead)
+  if (!a.ready) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 0 && lane == 0)
     for (int q = 0; q < min(a.stages, total); ++q) refill(q);
 
@@ -1659,29 +1681,31 @@ __device__ __forceinline__ void stage_contig(T* dst, const T* __restrict__ src, 
 // 16-byte stores, thread t at elements 4 t .. 4 t + 3 (P % 4 == 0: a vector never leaves its row).
 template <typename T>
 __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* __restrict__ xp, int cin, int B,
-                                                    int H, int W, int g, int ngroups, int Sg, int pp) {
+                                                    int H, int W, int g, int ngroups, int Sg, int pp,
+                                                    uint32_t* ready) {
   extern __shared__ __align__(16) uint8_t il_smem[];
   T* sp = (T*)il_smem;  // [pp][g][H][W]
   const int HW = H * W, P = g * W, blk = g * HW;
   const int nblk = cin * ngroups;
   const int64_t span = (int64_t)ngroups * Sg;
   const int nv = Sg / 4;  // 4-element vectors per (block, copy)
+  // the conv kernel may start now (it waits on the per-group counters, not on this grid)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // blocks in group-major order (bb = q cin + ci): the first image groups complete first, in the
+  // order the conv kernel's tiles consume them
+  const float rnv = 1.0f / nv, rcin = 1.0f / cin, rP = 1.0f / P, rW = 1.0f / W;
   for (int b0 = blockIdx.x * pp; b0 < nblk; b0 += gridDim.x * pp) {
     const int nb = min(pp, nblk - b0);
-    // blocks b0 .. b0 + nb - 1 of one channel are contiguous in x unless they cross a channel
-    for (int k = 0; k < nb;) {
-      const int bb = b0 + k, ci = bb / ngroups, q = bb - ci * ngroups;
-      const int run = min(nb - k, ngroups - q);  // blocks left in this channel
-      const int valid = max(0, min(run * g, B - q * g)) * HW;
-      stage_contig<T>(sp + (size_t)k * blk, x + ((int64_t)ci * B + (int64_t)q * g) * HW, run * blk, valid);
-      k += run;
+    for (int k = 0; k < nb; ++k) {  // block (q, ci): g contiguous planes (zero past the batch)
+      const int bb = b0 + k, q = div_rcp(bb, cin, rcin), ci = bb - q * cin;
+      const int valid = max(0, min(g, B - q * g)) * HW;
+      stage_contig<T>(sp + (size_t)k * blk, x + ((int64_t)ci * B + (int64_t)q * g) * HW, blk, valid);
     }
     __syncthreads();
-    const float rnv = 1.0f / nv, rng = 1.0f / ngroups, rP = 1.0f / P, rW = 1.0f / W;
     for (int i = threadIdx.x; i < 3 * nb * nv; i += blockDim.x) {
       const int t = div_rcp(i, nv, rnv), e0 = (i - t * nv) * 4;
       const int k = div_rcp(t, 3, 1.0f / 3.0f), dx = t - 3 * k;
-      const int bb = b0 + k, ci = div_rcp(bb, ngroups, rng), q = bb - ci * ngroups;
+      const int bb = b0 + k, q = div_rcp(bb, cin, rcin), ci = bb - q * cin;
       const int r = div_rcp(e0, P, rP), xx = e0 - r * P;
       int j = div_rcp(xx, W, rW), xw = xx - j * W;
       const T* sb = sp + (size_t)k * blk + (size_t)(r - 1) * W;
@@ -1698,7 +1722,13 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
       else
         *(uint2*)dst = *(const uint2*)v;
     }
+    if (ready) __threadfence();  // this thread's copies visible at device scope
     __syncthreads();
+    if (ready && threadIdx.x < nb) {  // publish: block (q, ci) of every copy is written
+      const int bb = b0 + threadIdx.x, q = bb / cin;
+      __threadfence();
+      atomicAdd(ready + q, 1u);
+    }
   }
 }
 
@@ -2758,8 +2788,10 @@ static int launch_conv_il(const Plan& p, int64_t batch, const void* x, void* y, 
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
   cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
+  // scratch: the three copies, then one ready counter per image group (overlap mode)
+  const size_t copies_bytes = ((size_t)(3 * p.c_in * span * S) + 255) / 256 * 256;
   void* xp = nullptr;
-  e = cudaMallocAsync(&xp, (size_t)(3 * p.c_in * span * S), (cudaStream_t)stream);
+  e = cudaMallocAsync(&xp, copies_bytes + (size_t)ngroups * 4, (cudaStream_t)stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return cuda_fail(e, "cudaMallocAsync(conv copies)", err);
@@ -2769,22 +2801,39 @@ static int launch_conv_il(const Plan& p, int64_t batch, const void* x, void* y, 
     void* st;
     ~Free() { cudaFreeAsync(b, (cudaStream_t)st); }
   } fr{xp, stream};
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+  uint32_t* ready = nullptr;
   {
+    // Overlap (default): the pre-pass runs as one persistent CTA per SM next to the conv
+    // kernel's CTA (programmatic dependent launch; per-group ready counters), when both fit in
+    // one SM's shared memory; otherwise the pre-pass runs alone at full width first.
+    // SPARSERT_CONV_OVERLAP=0 forces the sequential form (A/B).
     const int blk = g * p.h * p.w;
-    const int pp = (int)std::max<int64_t>(1, std::min<int64_t>(16, (96 * 1024) / ((int64_t)blk * S)));
+    const char* ov = getenv("SPARSERT_CONV_OVERLAP");
+    const int64_t budget = 227 * 1024 - (int64_t)p.smem_bytes - 2048;
+    int pp = (int)std::min<int64_t>(16, budget / ((int64_t)blk * S));
+    const bool overlap = (!ov || ov[0] != '0') && pp >= 1;
+    if (!overlap) pp = (int)std::max<int64_t>(1, std::min<int64_t>(16, (96 * 1024) / ((int64_t)blk * S)));
     const size_t psm = (size_t)pp * blk * S;
     const int64_t nblk = (int64_t)p.c_in * ngroups;
-    const unsigned pg = (unsigned)std::min<int64_t>((nblk + pp - 1) / pp, 148 * 8);
+    const unsigned pg = (unsigned)std::min<int64_t>((nblk + pp - 1) / pp, overlap ? (int64_t)sms : (int64_t)sms * 8);
+    if (overlap) {
+      ready = (uint32_t*)((uint8_t*)xp + copies_bytes);
+      if ((e = cudaMemsetAsync(ready, 0, (size_t)ngroups * 4, (cudaStream_t)stream)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemsetAsync(ready)", err);
+    }
     if (f16) {
       if ((e = ensure_smem_attr(il_pad_input<uint16_t>, (int)psm)) != cudaSuccess)
         return cuda_fail(e, "cudaFuncSetAttribute(il pad)", err);
       il_pad_input<uint16_t><<<pg, 256, psm, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, p.c_in,
-                                                                     (int)batch, p.h, p.w, g, (int)ngroups, Sg, pp);
+                                                                     (int)batch, p.h, p.w, g, (int)ngroups, Sg, pp,
+                                                                     ready);
     } else {
       if ((e = ensure_smem_attr(il_pad_input<float>, (int)psm)) != cudaSuccess)
         return cuda_fail(e, "cudaFuncSetAttribute(il pad)", err);
       il_pad_input<float><<<pg, 256, psm, (cudaStream_t)stream>>>((const float*)x, (float*)xp, p.c_in, (int)batch,
-                                                                  p.h, p.w, g, (int)ngroups, Sg, pp);
+                                                                  p.h, p.w, g, (int)ngroups, Sg, pp, ready);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "il pad launch", err);
   }
@@ -2828,8 +2877,10 @@ static int launch_conv_il(const Plan& p, int64_t batch, const void* x, void* y, 
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
-  int sms = 148, per_sm = 1;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+  a.ready = ready;
+  a.ready_target = (uint32_t)p.c_in;
+  a.ngroups = (int32_t)ngroups;
+  int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p.warps * 32, p.smem_bytes) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
