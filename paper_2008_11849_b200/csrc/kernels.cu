@@ -2805,15 +2805,16 @@ static int launch_conv_il(const Plan& p, int64_t batch, const void* x, void* y, 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
   uint32_t* ready = nullptr;
   {
-    // Overlap (default): the pre-pass runs as one persistent CTA per SM next to the conv
-    // kernel's CTA (programmatic dependent launch; per-group ready counters), when both fit in
-    // one SM's shared memory; otherwise the pre-pass runs alone at full width first.
-    // SPARSERT_CONV_OVERLAP=0 forces the sequential form (A/B).
+    // Overlap (opt-in, SPARSERT_CONV_OVERLAP=1): the pre-pass runs as one persistent CTA per SM
+    // next to the conv kernel's CTA (programmatic dependent launch; per-group ready counters)
+    // when both fit in one SM's shared memory.  Measured slower on C5 (one
+    // pre-pass CTA per SM needs ~250 us and competes with the conv kernel), so the default is
+    // the sequential form: the pre-pass alone at full width, then the conv kernel.
     const int blk = g * p.h * p.w;
     const char* ov = getenv("SPARSERT_CONV_OVERLAP");
     const int64_t budget = 227 * 1024 - (int64_t)p.smem_bytes - 2048;
     int pp = (int)std::min<int64_t>(16, budget / ((int64_t)blk * S));
-    const bool overlap = (!ov || ov[0] != '0') && pp >= 1;
+    const bool overlap = ov && ov[0] == '1' && pp >= 1;
     if (!overlap) pp = (int)std::max<int64_t>(1, std::min<int64_t>(16, (96 * 1024) / ((int64_t)blk * S)));
     const size_t psm = (size_t)pp * blk * S;
     const int64_t nblk = (int64_t)p.c_in * ngroups;
