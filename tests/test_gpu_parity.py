@@ -1008,3 +1008,28 @@ def test_param_plan_exact_and_bitwise(M, K, N, opts, dt):
     assert torch.equal(p1.spmm(x), p0.spmm(x))
     with pytest.raises(srt.SparseRTError):  # too large for the parameter space
         srt.Plan.from_csr(gen.pruned_weights(3072, 768, 90, seed=1), dtype=tdt, n_hint=N, plan_source=1)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f16"])
+def test_conv_interleaved_overlapped_prepass_exact(dt, monkeypatch):
+    # the opt-in overlapped form (pre-pass and conv kernel concurrently, per-image-group ready
+    # counters): exact on integer data, bitwise equal to the sequential form
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    cin, cout, B, H, W = 64, 48, 9, 14, 14
+    vw, vx = (3, 3) if dt == "f32" else (2, 4)
+    w = gen.int_weights(cout, 9 * cin, 90, seed=91, vmax=vw)
+    x = gen.int_x(cin * B * H, W, seed=92, vmax=vx).reshape(cin, B, H, W)
+    plan = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B,
+                             conv_kernel=4, rows_per_warp=4, k_chunk=8, stages=2)
+    xt = torch.from_numpy(x).to(dev).to(tdt)
+    monkeypatch.setenv("SPARSERT_CONV_OVERLAP", "1")
+    y1 = plan.conv3x3(xt)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("SPARSERT_CONV_OVERLAP", "0")
+    y0 = plan.conv3x3(xt)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    ref = oracle.conv3x3(cout, w.row_ptr, w.col_idx, w.values.astype(np.float64), x.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(y1.double().cpu().numpy(), ref)
