@@ -2149,7 +2149,7 @@ int upload_plan(Plan& p, std::string& err) {
     cudaFree(mem);
     return cuda_fail(e, "cudaMemcpy(plan)", err);
   }
-  if (p.executor == 3 &&
+  if ((p.executor == 3 || p.executor == 4) &&
       ((e = cudaMemcpy(b + o_tcpo, p.tcp_step_off.data(), p.tcp_step_off.size() * 4, cudaMemcpyHostToDevice)) !=
            cudaSuccess ||
        (e = cudaMemcpy(b + o_tcps, p.tcp_steps.data(), p.tcp_steps.size(), cudaMemcpyHostToDevice)) != cudaSuccess)) {
@@ -2174,7 +2174,7 @@ int upload_plan(Plan& p, std::string& err) {
     p.d_tc_cb = (const int32_t*)(b + o_tccb);
     p.d_ws_row = (const int32_t*)(b + o_wsr);
   }
-  if (p.executor == 3) {
+  if (p.executor == 3 || p.executor == 4) {
     p.d_tcp_step_off = (const int32_t*)(b + o_tcpo);
     p.d_tcp_steps = b + o_tcps;
   }
@@ -2515,9 +2515,268 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   return SPARSE_OK;
 }
 
+// ------------------------------------------------------------------ tcgen05 blocks (executor 4)
+// SURVEY NEXT #1 on Blackwell's 5th-generation tensor cores: W's nonzero 128 x 64 blocks (stored
+// dense, pre-swizzled by the inspector) times X on tcgen05.mma, fp32 accumulators in TMEM.
+// Tile = 128 rows of W x 256 columns of X; a persistent CTA walks tiles (row block fastest, so
+// concurrently running CTAs share the X tile in L2).  Warp roles (the canonical sm_100 GEMM
+// shape): warp 0 = producer (per nonzero block of the tile's row block: one bulk copy of the
+// 16 KB W block + four 128-byte-swizzled TMA boxes of X (64 k rows x 64 columns each) into a
+// ring stage), warp 1 = MMA issuer (one elected lane: 4 x tcgen05.mma M128 N256 K16 per stage,
+// tcgen05.commit releases the stage), warps 2-5 = epilogue (tcgen05.ld of their 32 TMEM lanes =
+// 32 rows, fp32 -> 16-bit, fused bias / beta / ReLU, stores).  Two TMEM accumulators (2 x 256
+// columns) let the epilogue of a tile overlap the MMAs of the next.  Summation order: k-block
+// ascending, the tensor core's order inside a K16 step (within tolerance; exact on integer data).
+struct TcgArgs {
+  const uint8_t* blocks;     // [nblocks][16 KB] pre-swizzled W blocks
+  const int32_t* meta;       // [nrb + 1] prefix, then k-block indices
+  uint8_t* Y;
+  int64_t ldy, N;
+  int32_t M, nrb, stages;
+  const uint8_t* bias;
+  float beta;
+  int32_t relu;
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+template <bool BF>
+__global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                          const TcgArgs a) {
+  constexpr int BN = 256, A_BYTES = 128 * 64 * 2, B_BYTES = 64 * BN * 2, ST_BYTES = A_BYTES + B_BYTES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);  // SW128: 1 KB atoms
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.stages;
+  uint64_t* bars = (uint64_t*)(smem + (size_t)S * ST_BYTES);
+  const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * S;
+  const uint32_t tfull0 = empty0 + 8 * S, tempty0 = tfull0 + 16;
+  uint32_t* tslot = (uint32_t*)(bars + 2 * S + 4);
+  const int64_t nnb = (a.N + BN - 1) / BN;
+  const int64_t ntiles = (int64_t)a.nrb * nnb;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: two 128 x 256 fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tbase = *tslot;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == 0) {
+    // ---------------- producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int rb = (int)(t % a.nrb);
+        const int64_t n0 = (t / a.nrb) * BN;
+        const int j0 = a.meta[rb], j1 = a.meta[rb + 1];
+        for (int j = j0; j < j1; ++j) {
+          const int kb = a.meta[a.nrb + 1 + j];
+          mbar_wait(empty0 + 8 * s, ph ^ 1u);
+          uint8_t* st = smem + (size_t)s * ST_BYTES;
+          const uint32_t fb = full0 + 8 * s;
+          mbar_arrive_expect_tx(fb, (uint32_t)ST_BYTES);
+          bulk_load(smem_u32(st), a.blocks + (size_t)j * A_BYTES, (uint32_t)A_BYTES, fb);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            tma_load_2d(smem_u32(st + A_BYTES + q * (B_BYTES / 4)), &tmap, (int)(n0 + 64 * q), kb * 64, fb);
+          if (++s == S) s = 0, ph ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one lane)
+    if (lane == 0) {
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph[2] = {0u, 0u};
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int rb = (int)(t % a.nrb);
+        const int j0 = a.meta[rb], j1 = a.meta[rb + 1];
+        mbar_wait(tempty0 + 8 * acc, aph[acc] ^ 1u);  // the epilogue drained this accumulator
+        tm_fence_after();
+        const uint32_t d = tbase + (uint32_t)(acc * BN);
+        for (int j = j0; j < j1; ++j) {
+          mbar_wait(full0 + 8 * s, ph);
+          tm_fence_after();
+          const uint32_t sa = smem_u32(smem + (size_t)s * ST_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            // A: K-major SW128 (rows of 128 B, 8-row atoms of 1 KB): K16 step = +32 B
+            // B: MN-major SW128 (64-column groups of 8 KB, 8-row atoms of 1 KB): K16 step = +2 KB
+            const uint64_t da = umma_desc_sw128(sa + 32u * k, 16u, 1024u);
+            const uint64_t db = umma_desc_sw128(sb + 2048u * k, (uint32_t)(B_BYTES / 4), 1024u);
+            const uint32_t en = (j > j0 || k > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                "l"(da), "l"(db), "r"(a.idesc), "r"(en)
+                : "memory");
+          }
+          tm_commit(empty0 + 8 * s);  // the stage is free once these MMAs have read it
+          if (++s == S) s = 0, ph ^= 1u;
+        }
+        tm_commit(tfull0 + 8 * acc);  // accumulator complete (also when the row block is empty)
+        aph[acc] ^= 1u;
+        acc ^= 1;
+      }
+    }
+  } else {
+    // ---------------- epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31 = rows of the tile
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t aph[2] = {0u, 0u};
+    const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int rb = (int)(t % a.nrb);
+      const int64_t n0 = (t / a.nrb) * BN;
+      const bool has = a.meta[rb + 1] > a.meta[rb];
+      mbar_wait(tfull0 + 8 * acc, aph[acc]);
+      tm_fence_after();
+      const int row = rb * 128 + q * 32 + lane;
+      const int ncol = (int)min((int64_t)BN, a.N - n0);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(ta));
+        tm_wait_ld();
+        if (row >= a.M || c0 >= ncol) continue;
+        uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + c0) * 2;
+        alignas(16) uint16_t h[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          float f = has ? __uint_as_float(v[c]) : 0.0f;
+          if (epi && c0 + c < ncol) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp + c * 2, a.relu);
+          h[c] = to16<BF>(f);
+        }
+        if (c0 + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) *(uint4*)(yp + c * 2) = *(const uint4*)(h + c);
+        } else {
+          for (int c = 0; c < 32 && c0 + c < ncol; ++c) ((uint16_t*)yp)[c] = h[c];
+        }
+      }
+      tm_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      aph[acc] ^= 1u;
+      acc ^= 1;
+    }
+  }
+  tm_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+
+static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy, void* stream,
+                      std::string& err, const Epilogue& ep) {
+  const bool bf = p.dtype == SPARSE_BF16;
+  auto encode = tensor_map_encoder();
+  if (!encode) {
+    err = "internal: no tensor-map encoder";
+    return SPARSE_EINTERNAL;
+  }
+  DeviceGuard dg(p.device);
+  if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
+  using TFn = void (*)(const CUtensorMap, const TcgArgs);
+  TFn fn = bf ? spmm_tcg_kernel<true> : spmm_tcg_kernel<false>;
+  cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
+  const void* Xa = X;
+  int64_t lda = ldx;
+  void* scratch = nullptr;
+  if (((uintptr_t)X % 16) != 0 || ((ldx * 2) % 16) != 0) {
+    const int rc = launch_repack(p.device, p.K, N, 2, X, ldx, &scratch, &lda, stream, err);
+    if (rc != SPARSE_OK) return rc;
+    Xa = scratch;
+  }
+  struct Free {
+    void* b;
+    void* st;
+    int dev;
+    ~Free() {
+      if (b) free_repack(dev, b, st);
+    }
+  } fr{scratch, stream, p.device};
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof tmap);
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)p.K};
+  cuuint64_t strides[1] = {(cuuint64_t)(lda * 2)};
+  cuuint32_t box[2] = {64u, 64u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&tmap, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                      const_cast<void*>(Xa), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "tcgen05 blocks: cuTensorMapEncodeTiled failed";
+    return SPARSE_EINTERNAL;
+  }
+  TcgArgs a;
+  a.blocks = p.d_tcp_steps;
+  a.meta = p.d_tcp_step_off;
+  a.Y = (uint8_t*)Y;
+  a.ldy = ldy;
+  a.N = N;
+  a.M = p.M;
+  a.nrb = p.tcp_npanels;
+  a.stages = p.stages;
+  a.bias = (const uint8_t*)ep.bias;
+  a.beta = ep.beta;
+  a.relu = ep.relu;
+  // instruction descriptor (kind::f16): D fp32, A / B fp16 or bf16, A K-major, B MN-major,
+  // N = 256, M = 128
+  const uint32_t fmt = bf ? 1u : 0u;
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+  const int64_t ntiles = (int64_t)p.tcp_npanels * ((N + 255) / 256);
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, sms)), 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
+  if (e != cudaSuccess) return cuda_fail(e, "tcgen05 block launch", err);
+  return SPARSE_OK;
+}
+
 int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
                 void* stream, std::string& err, const Epilogue& ep) {
   if (p.executor == 3) return launch_tcp(p, N, X, ldx, Y, ldy, stream, err, ep);
+  if (p.executor == 4) return launch_tcg(p, N, X, ldx, Y, ldy, stream, err, ep);
   const bool f16 = p.dtype != SPARSE_F32;  // 16-bit X / Y (fp16 or bf16: TMA copies the bits)
   const int S = f16 ? 2 : 4;
   SpmmFn fn = p.dtype == SPARSE_BF16 ? pick_spmm<true, true>(p.R, p.gk, p.tm)

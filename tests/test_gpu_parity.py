@@ -1033,3 +1033,62 @@ def test_conv_interleaved_overlapped_prepass_exact(dt, monkeypatch):
     ref = oracle.conv3x3(cout, w.row_ptr, w.col_idx, w.values.astype(np.float64), x.astype(np.float64))
     ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
     assert np.array_equal(y1.double().cpu().numpy(), ref)
+
+
+# --------------------------------------------------------------------------- tcgen05 blocks (executor 4)
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("M,K,N,p", [(3072, 768, 2048, 90), (768, 3072, 512, 90), (300, 200, 517, 80),
+                                      (128, 64, 256, 95), (77, 1111, 300, 98), (2048, 512, 392, 90),
+                                      (16, 64, 4099, 90), (512, 2048, 49, 95)])
+def test_tcgen05_blocks_exact_and_rel_l2(M, K, N, p, dt):
+    # W's nonzero 128 x 64 blocks on tcgen05.mma (TMEM accumulators): exact on integer data
+    # (every partial sum an exact integer < 2^24, so the tensor core's internal order does not
+    # matter; 16-bit output = RN of the exact sum), rel-L2 <= 1e-2 on real-valued data
+    dev = _dev()
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float16
+    wi = gen.int_weights(M, K, p, seed=M + K + N, vmax=2)
+    xi = gen.int_x(K, N, seed=N + 1, vmax=4)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, executor=4)
+    assert plan.info["executor"] == 4
+    Y = torch.full((M, N), float("nan"), dtype=tdt, device=dev)
+    plan.spmm(torch.from_numpy(xi).to(dev).to(tdt), Y)
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), xi.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(Y.double().cpu().numpy(), ref)
+    w = gen.pruned_weights(M, K, p, seed=M * 7 + K)
+    x = gen.uniform_x(K, N, seed=3)
+    plan = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, executor=4)
+    Y = plan.spmm(torch.from_numpy(x).to(dev).to(tdt))
+    torch.cuda.synchronize()
+    wv = torch.from_numpy(w.values).to(tdt).double().numpy()
+    xv = torch.from_numpy(x).to(tdt).double().numpy()
+    err = oracle.rel_l2(Y.double().cpu().numpy(), oracle.spmm(M, K, w.row_ptr, w.col_idx, wv, xv))
+    assert err <= F16_TOL, err
+
+
+def test_tcgen05_blocks_empty_rows_epilogue_and_ld():
+    # empty row blocks (-> +0), ldx / ldy > N, fused bias + beta + ReLU
+    dev = _dev()
+    M, K, N = 400, 192, 300
+    base = gen.int_weights(M, K, 90, seed=4, vmax=2)
+    dense = gen.to_dense(base)
+    dense[128:256] = 0.0  # a whole empty 128-row block
+    keep = np.flatnonzero(dense)
+    w = gen.csr_from_mask(M, K, keep, dense.astype(np.float32))
+    xi = gen.int_x(K, N, seed=5, vmax=4)
+    rng = np.random.default_rng(6)
+    bias = rng.integers(-8, 9, M).astype(np.float32)
+    y0 = rng.integers(-8, 9, (M, N)).astype(np.float32)
+    plan = srt.Plan.from_csr(w, dtype=torch.float16, n_hint=N, executor=4)
+    Xb = torch.zeros((K, N + 40), dtype=torch.float16, device=dev)
+    Xb[:, :N] = torch.from_numpy(xi).to(dev).half()
+    Yb = torch.zeros((M, N + 24), dtype=torch.float16, device=dev)
+    Yb[:, :N] = torch.from_numpy(y0).to(dev).half()
+    plan.spmm(Xb[:, :N], Yb[:, :N], bias=torch.from_numpy(bias).to(dev).half(), beta=0.5, relu=True)
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), xi.astype(np.float64))
+    ref = np.maximum(ref + bias[:, None] + 0.5 * y0, 0.0)
+    assert np.array_equal(Yb[:, :N].double().cpu().numpy(), _f16_round(ref))
+    assert torch.count_nonzero(Yb[:, N:]) == 0
