@@ -548,11 +548,13 @@ class Run:
             t = json.load(open(tpath)).get(d["name"])
             traffic = t and t.get("traffic_bytes_per_launch")
         pinfo = self.plans[dom].info
-        if pinfo.get("executor") == 3:
-            # condensed-panel tensor cores (DESIGN.md kernel 5b): a dense 16-bit contraction of
-            # the panels' column unions; executed flops = 2 * 16 * 16 * N per k16 step, against
-            # the measured dense bf16 peak (fp16 runs at the same tensor rate)
-            tc_flops = 2 * 16 * 16 * d["N"] * pinfo["tc_panel_steps"]
+        if pinfo.get("executor") in (3, 4):
+            # tensor cores: executor 3 = condensed panels (DESIGN.md kernel 5b), a dense 16-bit
+            # contraction of the panels' column unions, 2 * 16 * 16 * N flops per k16 step;
+            # executor 4 = W's nonzero 128 x 64 blocks on tcgen05 (kernel 5d), 2 * 128 * 64 * N
+            # flops per block; against the measured dense bf16 peak (fp16 runs at the same rate)
+            per = 2 * 16 * 16 if pinfo["executor"] == 3 else 2 * 128 * 64
+            tc_flops = per * d["N"] * pinfo["tc_panel_steps"]
             roof = {"bound": "tensor", "achieved": tc_flops / sec / 1e12, "peak": peaks["bf16_tflops"],
                     "unit": "TFLOP/s", "useful_tflops": 2 * d["nnz"] * d["N"] / sec / 1e12,
                     "executed_flops_per_launch": tc_flops}

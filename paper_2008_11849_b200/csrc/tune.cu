@@ -132,9 +132,12 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     BuildOpts j = base;
     j.executor = 1;
     cands.push_back(j);
-    if (S == 2) {  // condensed-panel tensor cores (fp16 and bf16)
+    if (S == 2) {  // tensor cores (fp16 and bf16): condensed panels on mma.sync,
+                   // and W's nonzero 128 x 64 blocks on tcgen05 (TMEM accumulators)
       BuildOpts t = base;
       t.executor = 3;
+      cands.push_back(t);
+      t.executor = 4;
       cands.push_back(t);
     }
   } else {
