@@ -287,6 +287,8 @@ class Plan:
                 o.update(jit_rows=i["jit_rows"], jit_warps=i["jit_warps"])
             if i["plan_source"]:
                 o.update(plan_source=i["plan_source"])
+            if i["executor"] == 4:  # the tcgen05 block executor has its own fixed ring
+                o.pop("stages")
         else:
             o.update(k_chunk=i["k_chunk"], conv_kernel=i["conv_kernel"])
             o.pop("split_k")
