@@ -65,11 +65,12 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   bo.jit_warps = o.jit_warps;
   bo.cm = o.x_multicast;
   bo.tm = o.x_source;
-  if (o.conv_kernel < 0 || o.conv_kernel > 4)
+  if (o.conv_kernel < 0 || o.conv_kernel > 5)
     return fail(SPARSE_EINVAL,
-                "conv_kernel must be 0 (auto), 1 (position-strided), 2 (TMA-fed), 3 (register-staged) "
-                "or 4 (packed)");
-  bo.conv_vec = o.conv_kernel == 1 ? 0 : o.conv_kernel == 3 ? 1 : o.conv_kernel == 4 ? 4 : 2;
+                "conv_kernel must be 0 (auto), 1 (position-strided), 2 (TMA-fed), 3 (register-staged), "
+                "4 (interleaved) or 5 (tcgen05 blocks)");
+  bo.conv_vec = o.conv_kernel == 1 ? 0 : o.conv_kernel == 3 ? 1 : (o.conv_kernel == 4 || o.conv_kernel == 5) ? 4 : 2;
+  if (o.kind == SPARSE_CONV3X3 && o.conv_kernel == 5) bo.executor = 4;
   if (o.row_order != 0 && o.row_order != 1)
     return fail(SPARSE_EINVAL, "row_order must be 0 (load balanced) or 1 (natural)");
   bo.row_order = o.row_order;
@@ -394,7 +395,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->tuned_us = p.tuned_us;
   out->x_multicast = p.cm;
   out->x_source = p.tm;
-  out->conv_kernel = p.kind != SPARSE_CONV3X3 ? 0 : !p.conv_vec ? 1 : p.conv_vec == 2 ? 2 : p.conv_vec == 4 ? 4 : 3;
+  out->conv_kernel = p.kind != SPARSE_CONV3X3 ? 0 : p.executor == 4 ? 5 : !p.conv_vec ? 1 : p.conv_vec == 2 ? 2 : p.conv_vec == 4 ? 4 : 3;
   out->row_order = p.row_order;
   out->tc_min_density = p.tc_ntiles > 0 || p.tc_min_pct > 0 ? p.tc_min_pct : 0;
   out->tc_row_blocks = p.tc_nrb;

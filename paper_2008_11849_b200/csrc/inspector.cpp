@@ -862,18 +862,33 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // block holds ~820 nonzeros and the tensor cores' ~30x throughput advantage outweighs the
     // ~10x zero work.  Row panel metadata: tcp_step_off = [nrb + 1] prefix of nonzero blocks,
     // then their k-block indices; tcp_steps = the blocks (16 KB each), row block major.
-    if (o.kind != SPARSE_SPMM || dtype == SPARSE_F32) {
-      err = "executor = 4 (tcgen05 blocks) needs an fp16 or bf16 SpMM plan";
+    if (dtype == SPARSE_F32) {
+      err = "executor = 4 (tcgen05 blocks) / conv_kernel = 5 needs an fp16 or bf16 plan";
       return SPARSE_EUNSUPPORTED;
     }
+    const bool conv = o.kind == SPARSE_CONV3X3;
     const int BM = 128, BK = 64;
-    const int32_t nrb = (M + BM - 1) / BM, nkb = (K + BK - 1) / BK;
+    // conv: implicit im2col over the interleaved dx-shifted copies (kernel 3b layout); the K
+    // axis is ordered tap-major, k-block = (tap, 64 input channels), so the B tile of a k-block
+    // is one 2-D slab of copy dx shifted by (dy - 1) pitches
+    int32_t ncb = 0;
+    if (conv) {
+      ncb = (o.c_in + BK - 1) / BK;
+      int gg = 1;
+      while ((gg * o.w) % 8) ++gg;  // pitch a multiple of 8 elements: 16-byte TMA box starts
+      p.tcg_g = gg;
+      p.tcg_ncb = ncb;
+    }
+    // k-block of column k: SpMM k / 64; conv (ci, tap) -> tap * ncb + ci / 64, column ci % 64
+    auto kblock = [&](int32_t k) { return conv ? (k % 9) * ncb + (k / 9) / BK : k / BK; };
+    auto kcol = [&](int32_t k) { return conv ? (k / 9) % BK : k % BK; };
+    const int32_t nrb = (M + BM - 1) / BM, nkb = conv ? 9 * ncb : (K + BK - 1) / BK;
     p.tcp_npanels = nrb;
     p.tcp_nchunks = nkb;
     std::vector<int32_t> pref(1, 0), kbs;
     std::vector<char> nzb((size_t)nrb * nkb, 0);
     for (int32_t m = 0; m < M; ++m)
-      for (const Entry& en : rows[m]) nzb[(size_t)(m / BM) * nkb + en.k / BK] = 1;
+      for (const Entry& en : rows[m]) nzb[(size_t)(m / BM) * nkb + kblock(en.k)] = 1;
     for (int32_t rb = 0; rb < nrb; ++rb) {
       for (int32_t kb = 0; kb < nkb; ++kb)
         if (nzb[(size_t)rb * nkb + kb]) kbs.push_back(kb);
@@ -889,8 +904,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     for (int32_t m = 0; m < M; ++m) {
       const int r = m % BM;
       for (const Entry& en : rows[m]) {
-        const int64_t bi = slot[(size_t)(m / BM) * nkb + en.k / BK];
-        const int c = en.k % BK;
+        const int64_t bi = slot[(size_t)(m / BM) * nkb + kblock(en.k)];
+        const int c = kcol(en.k);
         const size_t off = (size_t)bi * blk + (size_t)(r / 8) * 1024 + (size_t)(r % 8) * 128 +
                            (size_t)(((c / 8) ^ (r % 8)) * 16) + (size_t)(c % 8) * 2;
         std::memcpy(&p.tcp_steps[off], &en.wh, 2);
@@ -898,9 +913,9 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     }
     p.tcp_nsteps = (int64_t)kbs.size();
     p.executor = 4;
-    p.n_tile = 256;
+    if (!conv) p.n_tile = 256;
     p.stages = 4;
-    p.smem_bytes = p.stages * (16 * 1024 + 32 * 1024) + 1024 + 256;  // + 1 KB alignment slack
+    p.smem_bytes = p.stages * (16 * 1024 + 32 * 1024) + 1024 + 2048;  // + align slack, barriers, conv table
     p.plan_bytes += (int64_t)p.tcp_steps.size() + (int64_t)p.tcp_step_off.size() * 4;
   } else if (o.executor == 3) {
     // ---- condensed-panel tensor-core executor (fp16 SpMM) ----

@@ -2531,12 +2531,16 @@ struct TcgArgs {
   const uint8_t* blocks;     // [nblocks][16 KB] pre-swizzled W blocks
   const int32_t* meta;       // [nrb + 1] prefix, then k-block indices
   uint8_t* Y;
-  int64_t ldy, N;
+  int64_t ldy, N;            // conv: N = the span of the interleaved copies (positions incl. halo)
   int32_t M, nrb, stages;
   const uint8_t* bias;
   float beta;
   int32_t relu;
   uint32_t idesc;
+  // conv (implicit im2col over the interleaved copies): pitch P = g W, group stride Sg =
+  // (H + 2) P, 64-channel blocks per tap ncb, batch Bt, output plane B H W
+  int32_t P, g, Sg, H, W, ncb, Bt;
+  int64_t plane;
 };
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -2544,7 +2548,7 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-template <bool BF>
+template <bool BF, bool CONV = false>
 __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const TcgArgs a) {
   constexpr int BN = 256, A_BYTES = 128 * 64 * 2, B_BYTES = 64 * BN * 2, ST_BYTES = A_BYTES + B_BYTES;
@@ -2597,9 +2601,21 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
           const uint32_t fb = full0 + 8 * s;
           mbar_arrive_expect_tx(fb, (uint32_t)ST_BYTES);
           bulk_load(smem_u32(st), a.blocks + (size_t)j * A_BYTES, (uint32_t)A_BYTES, fb);
+          if (CONV) {  // k-block (tap, 64 channels): copy dx, shifted by (dy - 1) pitches
+            const int tap = kb / a.ncb, cb = kb - tap * a.ncb;
+            const int s0 = (int)n0 + (tap / 3 - 1) * a.P;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            tma_load_2d(smem_u32(st + A_BYTES + q * (B_BYTES / 4)), &tmap, (int)(n0 + 64 * q), kb * 64, fb);
+            for (int q = 0; q < 4; ++q)
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(st + A_BYTES + q * (B_BYTES / 4))),
+                  "l"((uint64_t)&tmap), "r"(s0 + 64 * q), "r"(cb * 64), "r"(tap % 3), "r"(fb)
+                  : "memory");
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              tma_load_2d(smem_u32(st + A_BYTES + q * (B_BYTES / 4)), &tmap, (int)(n0 + 64 * q), kb * 64, fb);
+          }
           if (++s == S) s = 0, ph ^= 1u;
         }
       }
@@ -2646,10 +2662,26 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
     int acc = 0;
     uint32_t aph[2] = {0u, 0u};
     const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
+    int32_t* otab = (int32_t*)((uint8_t*)tslot + 64);  // conv: span position -> output offset
+    int64_t tab_n0 = -1;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int rb = (int)(t % a.nrb);
       const int64_t n0 = (t / a.nrb) * BN;
       const bool has = a.meta[rb + 1] > a.meta[rb];
+      if (CONV && n0 != tab_n0) {
+        // the 128 epilogue threads decode the tile's 256 span positions once (named barrier
+        // among the epilogue warps only): s -> group q, row r, column (image j, x)
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's readers are done
+        for (int c = threadIdx.x - 64; c < BN; c += 128) {
+          const int64_t sp = n0 + c;
+          const int64_t gq = sp / a.Sg;
+          const int rem = (int)(sp - gq * a.Sg), r = rem / a.P, xx = rem - r * a.P, jj = xx / a.W;
+          const int64_t b = gq * a.g + jj;
+          otab[c] = (sp < a.N && r >= 1 && r <= a.H && b < a.Bt) ? (int32_t)((b * a.H + (r - 1)) * a.W + (xx - jj * a.W)) : -1;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        tab_n0 = n0;
+      }
       mbar_wait(tfull0 + 8 * acc, aph[acc]);
       tm_fence_after();
       const int row = rb * 128 + q * 32 + lane;
@@ -2667,6 +2699,19 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(ta));
         tm_wait_ld();
+        if (CONV) {
+          if (row >= a.M) continue;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int32_t o = otab[c0 + c];
+            if (o < 0) continue;
+            uint8_t* yp = a.Y + ((int64_t)row * a.plane + o) * 2;
+            float f = has ? __uint_as_float(v[c]) : 0.0f;
+            if (epi) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp, a.relu);
+            *(uint16_t*)yp = to16<BF>(f);
+          }
+          continue;
+        }
         if (row >= a.M || c0 >= ncol) continue;
         uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + c0) * 2;
         alignas(16) uint16_t h[32];
@@ -2770,6 +2815,107 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
   if (e != cudaSuccess) return cuda_fail(e, "tcgen05 block launch", err);
+  return SPARSE_OK;
+}
+
+// Conv on the tcgen05 block executor (conv_kernel 5): the interleaved copies pre-pass (pitch a
+// multiple of 8 elements), then spmm_tcg_kernel<CONV> over the span of the copies.
+static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y, void* stream, std::string& err,
+                           const Epilogue& ep) {
+  const bool bf = p.dtype == SPARSE_BF16;
+  const int S = 2;
+  auto encode = tensor_map_encoder();
+  if (!encode) {
+    err = "internal: no tensor-map encoder";
+    return SPARSE_EINTERNAL;
+  }
+  const int g = p.tcg_g, P = g * p.w, Sg = (p.h + 2) * P;
+  const int64_t ngroups = (batch + g - 1) / g, span = ngroups * Sg;
+  if (span > INT32_MAX - 4096 || batch > INT32_MAX / 2) {
+    err = "conv (tcgen05): batch too large for one launch";
+    return SPARSE_EUNSUPPORTED;
+  }
+  DeviceGuard dg(p.device);
+  if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
+  using TFn = void (*)(const CUtensorMap, const TcgArgs);
+  TFn fn = bf ? spmm_tcg_kernel<true, true> : spmm_tcg_kernel<false, true>;
+  cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
+  void* xp = nullptr;
+  e = cudaMallocAsync(&xp, (size_t)(3 * p.c_in * span * S), (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(e, "cudaMallocAsync(conv copies)", err);
+  }
+  struct Free {
+    void* b;
+    void* st;
+    ~Free() { cudaFreeAsync(b, (cudaStream_t)st); }
+  } fr{xp, stream};
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+  {
+    const int blk = g * p.h * p.w;
+    const int pp = (int)std::max<int64_t>(1, std::min<int64_t>(16, (96 * 1024) / ((int64_t)blk * S)));
+    const size_t psm = (size_t)pp * blk * S;
+    const int64_t nblk = (int64_t)p.c_in * ngroups;
+    const unsigned pg = (unsigned)std::min<int64_t>((nblk + pp - 1) / pp, (int64_t)sms * 8);
+    if ((e = ensure_smem_attr(il_pad_input<uint16_t>, (int)psm)) != cudaSuccess)
+      return cuda_fail(e, "cudaFuncSetAttribute(il pad)", err);
+    il_pad_input<uint16_t><<<pg, 256, psm, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, p.c_in,
+                                                                   (int)batch, p.h, p.w, g, (int)ngroups, Sg, pp,
+                                                                   nullptr);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "il pad launch", err);
+  }
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof tmap);
+  cuuint64_t dims[3] = {(cuuint64_t)span, (cuuint64_t)p.c_in, 3};
+  cuuint64_t strides[2] = {(cuuint64_t)(span * S), (cuuint64_t)(span * S * p.c_in)};
+  cuuint32_t box[3] = {64u, 64u, 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(&tmap, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, xp, dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "conv (tcgen05): cuTensorMapEncodeTiled failed";
+    return SPARSE_EINTERNAL;
+  }
+  TcgArgs a;
+  a.blocks = p.d_tcp_steps;
+  a.meta = p.d_tcp_step_off;
+  a.Y = (uint8_t*)y;
+  a.ldy = 0;
+  a.N = span;
+  a.M = p.M;
+  a.nrb = p.tcp_npanels;
+  a.stages = p.stages;
+  a.bias = (const uint8_t*)ep.bias;
+  a.beta = ep.beta;
+  a.relu = ep.relu;
+  const uint32_t fmt = bf ? 1u : 0u;
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+  a.P = P;
+  a.g = g;
+  a.Sg = Sg;
+  a.H = p.h;
+  a.W = p.w;
+  a.ncb = p.tcg_ncb;
+  a.Bt = (int32_t)batch;
+  a.plane = batch * (int64_t)p.h * p.w;
+  const int64_t ntiles = (int64_t)p.tcp_npanels * ((span + 255) / 256);
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, sms)), 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
+  if (e != cudaSuccess) return cuda_fail(e, "conv3x3 (tcgen05) launch", err);
   return SPARSE_OK;
 }
 
@@ -3167,6 +3313,7 @@ int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* s
   const bool f16 = p.dtype != SPARSE_F32;  // 16-bit data (bf16 plans always take the TMA-fed kernel)
   ConvFn fn = p.conv_vec ? (f16 ? pick_conv_vec<true>(p.R) : pick_conv_vec<false>(p.R))
                         : (f16 ? pick_conv<true>(p.R, p.C) : pick_conv<false>(p.R, p.C));
+  if (p.executor == 4) return launch_conv_tcg(p, batch, x, y, stream, err, ep);
   if (p.conv_vec == 4) return launch_conv_il(p, batch, x, y, stream, err, ep);
   if (!fn && p.conv_vec != 2) {
     err = "internal: no conv kernel instance for this tile configuration";

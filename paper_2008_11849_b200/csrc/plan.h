@@ -93,6 +93,9 @@ struct Plan {
   // (pitch il_g * w), per chunk three TMA boxes of il_lc elements x cc channels (copy dx at
   // dx * conv_cs elements), a zero block of il_lc, then the plan block at il_blk_at bytes
   int32_t il_g = 0, il_lc = 0, il_stage_bytes = 0, il_blk_at = 0;
+  // conv on the tcgen05 block executor (executor 4, conv_kernel 5): images per row group of the
+  // interleaved copies (pitch tcg_g * w a multiple of 8 elements: 16-byte TMA box starts)
+  int32_t tcg_g = 0, tcg_ncb = 0;
 
   // packed plan (host copy)
   std::vector<int32_t> row_id;   // npanels * Mp, -1 = empty slot

@@ -1092,3 +1092,33 @@ def test_tcgen05_blocks_empty_rows_epilogue_and_ld():
     ref = np.maximum(ref + bias[:, None] + 0.5 * y0, 0.0)
     assert np.array_equal(Yb[:, :N].double().cpu().numpy(), _f16_round(ref))
     assert torch.count_nonzero(Yb[:, N:]) == 0
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("cin,cout,B,H,W,p", [(256, 256, 6, 14, 14, 90), (64, 64, 3, 56, 56, 90),
+                                              (128, 128, 4, 28, 28, 95), (512, 512, 3, 7, 7, 90),
+                                              (40, 200, 5, 10, 6, 80), (16, 24, 2, 14, 14, 90)])
+def test_conv_tcgen05_exact(cin, cout, B, H, W, p, dt):
+    # conv_kernel 5: implicit im2col over the interleaved copies on the tcgen05 block executor
+    # (k-blocks = (tap, 64 channels)): exact on integer data, rel-L2 <= 1e-2 on real data
+    dev = _dev()
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float16
+    wi = gen.int_weights(cout, 9 * cin, p, seed=cin + H, vmax=2)
+    x = gen.int_x(cin * B * H, W, seed=cout, vmax=4).reshape(cin, B, H, W)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, conv_kernel=5)
+    assert plan.info["conv_kernel"] == 5
+    y = torch.full((cout, B, H, W), float("nan"), dtype=tdt, device=dev)
+    plan.conv3x3(torch.from_numpy(x).to(dev).to(tdt), y)
+    torch.cuda.synchronize()
+    ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), x.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(y.double().cpu().numpy(), ref)
+    w = gen.pruned_weights(cout, 9 * cin, p, seed=cin * 5 + H)
+    xr = gen.relu_normal_x((cin, B, H, W), seed=B + 5)
+    plan = srt.Plan.from_csr(w, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, conv_kernel=5)
+    y = plan.conv3x3(torch.from_numpy(xr).to(dev).to(tdt))
+    torch.cuda.synchronize()
+    wv = torch.from_numpy(w.values).to(tdt).double().numpy()
+    xv = torch.from_numpy(xr).to(tdt).double().numpy()
+    err = oracle.rel_l2(y.double().cpu().numpy(), oracle.conv3x3(cout, w.row_ptr, w.col_idx, wv, xv))
+    assert err <= F16_TOL, err
