@@ -69,7 +69,8 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
     return fail(SPARSE_EINVAL,
                 "conv_kernel must be 0 (auto), 1 (position-strided), 2 (TMA-fed), 3 (register-staged), "
                 "4 (interleaved) or 5 (tcgen05 blocks)");
-  bo.conv_vec = o.conv_kernel == 1 ? 0 : o.conv_kernel == 3 ? 1 : (o.conv_kernel == 4 || o.conv_kernel == 5) ? 4 : 2;
+  // (conv_kernel 5 runs on the tcgen05 block executor; its CUDA-core plan is the default TMA-fed one)
+  bo.conv_vec = o.conv_kernel == 1 ? 0 : o.conv_kernel == 3 ? 1 : o.conv_kernel == 4 ? 4 : 2;
   if (o.kind == SPARSE_CONV3X3 && o.conv_kernel == 5) bo.executor = 4;
   if (o.row_order != 0 && o.row_order != 1)
     return fail(SPARSE_EINVAL, "row_order must be 0 (load balanced) or 1 (natural)");
