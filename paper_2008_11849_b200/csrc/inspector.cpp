@@ -915,7 +915,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     p.executor = 4;
     if (!conv) p.n_tile = 256;
     p.stages = 4;
-    p.smem_bytes = p.stages * (16 * 1024 + 32 * 1024) + 1024 + 2048;  // + align slack, barriers, conv table
+    p.smem_bytes = p.stages * (16 * 1024 + 32 * 1024) + 1024 + 2048 + 8192;  // + align, barriers, conv table, block lists
     p.plan_bytes += (int64_t)p.tcp_steps.size() + (int64_t)p.tcp_step_off.size() * 4;
   } else if (o.executor == 3) {
     // ---- condensed-panel tensor-core executor (fp16 SpMM) ----

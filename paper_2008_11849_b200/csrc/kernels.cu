@@ -2527,9 +2527,11 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
 // 32 rows, fp32 -> 16-bit, fused bias / beta / ReLU, stores).  Two TMEM accumulators (2 x 256
 // columns) let the epilogue of a tile overlap the MMAs of the next.  Summation order: k-block
 // ascending, the tensor core's order inside a K16 step (within tolerance; exact on integer data).
+constexpr int kTcgMetaMax = 2048;  // block-list entries kept in shared memory
 struct TcgArgs {
   const uint8_t* blocks;     // [nblocks][16 KB] pre-swizzled W blocks
   const int32_t* meta;       // [nrb + 1] prefix, then k-block indices
+  int32_t nblk;              // nonzero blocks (k-block list length)
   uint8_t* Y;
   int64_t ldy, N;            // conv: N = the span of the interleaved copies (positions incl. halo)
   int32_t M, nrb, stages;
@@ -2582,6 +2584,16 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
   __syncthreads();
   tm_fence_after();
   const uint32_t tbase = *tslot;
+  // the block lists, copied once into shared memory (dependent global loads on the producer's
+  // issue path were the kernel's top stall)
+  const int nmeta = a.nrb + 1 + a.nblk;
+  const int32_t* meta = a.meta;
+  if (nmeta <= kTcgMetaMax) {
+    int32_t* sm = (int32_t*)((uint8_t*)tslot + 64 + 1024);
+    for (int i = threadIdx.x; i < nmeta; i += blockDim.x) sm[i] = __ldg(a.meta + i);
+    __syncthreads();
+    meta = sm;
+  }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
@@ -2593,9 +2605,9 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int rb = (int)(t % a.nrb);
         const int64_t n0 = (t / a.nrb) * BN;
-        const int j0 = a.meta[rb], j1 = a.meta[rb + 1];
+        const int j0 = meta[rb], j1 = meta[rb + 1];
         for (int j = j0; j < j1; ++j) {
-          const int kb = a.meta[a.nrb + 1 + j];
+          const int kb = meta[a.nrb + 1 + j];
           mbar_wait(empty0 + 8 * s, ph ^ 1u);
           uint8_t* st = smem + (size_t)s * ST_BYTES;
           const uint32_t fb = full0 + 8 * s;
@@ -2627,7 +2639,7 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
       uint32_t ph = 0, aph[2] = {0u, 0u};
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int rb = (int)(t % a.nrb);
-        const int j0 = a.meta[rb], j1 = a.meta[rb + 1];
+        const int j0 = meta[rb], j1 = meta[rb + 1];
         mbar_wait(tempty0 + 8 * acc, aph[acc] ^ 1u);  // the epilogue drained this accumulator
         tm_fence_after();
         const uint32_t d = tbase + (uint32_t)(acc * BN);
@@ -2667,7 +2679,7 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int rb = (int)(t % a.nrb);
       const int64_t n0 = (t / a.nrb) * BN;
-      const bool has = a.meta[rb + 1] > a.meta[rb];
+      const bool has = meta[rb + 1] > meta[rb];
       if (CONV && n0 != tab_n0) {
         // the 128 epilogue threads decode the tile's 256 span positions once (named barrier
         // among the epilogue warps only): s -> group q, row r, column (image j, x)
@@ -2786,6 +2798,7 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   TcgArgs a;
   a.blocks = p.d_tcp_steps;
   a.meta = p.d_tcp_step_off;
+  a.nblk = (int32_t)p.tcp_nsteps;
   a.Y = (uint8_t*)Y;
   a.ldy = ldy;
   a.N = N;
@@ -2883,6 +2896,7 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   TcgArgs a;
   a.blocks = p.d_tcp_steps;
   a.meta = p.d_tcp_step_off;
+  a.nblk = (int32_t)p.tcp_nsteps;
   a.Y = (uint8_t*)y;
   a.ldy = 0;
   a.N = span;
