@@ -12,7 +12,7 @@ configs[4], the ResNet-50 sparse 3x3 conv (256 channels, 14x14) at batch 
 sparsity in fp32 (the paper's precision) -- the largest configuration BASELINE names
 that fits one GPU and the one it shards over 1/2/4/8 GPUs.  The same JSON line carries a
 `secondary` block with the BERT-base FFN layers at N = 32 x 512 (configs[3]) in fp32 and
-fp16, timed the same way.  L2 is flushed (256 MiB write + 256 MiB read) before every timed
+fp16 and the same conv in fp16, timed the same way.  L2 is flushed (256 MiB write + 256 MiB read) before every timed
 step, outside the timed events, so every layer reads cold HBM.
 
 After timing, every timed plan is checked against the CPU oracle (`parity`): the timed
@@ -513,7 +513,7 @@ class Run:
         plan has dense tiles; conv: the conv kernel (+ the input pre-pass of conv_kernel 2)."""
         info = self.plans[i].info
         if self.layers[i]["kind"] != "spmm":
-            return 2 if info["conv_kernel"] == 2 else 1
+            return 2 if info["conv_kernel"] in (2, 4, 5) else 1  # pre-pass + conv kernel
         X = self.xs[i]
         unaligned = (X.data_ptr() % 16) != 0 or (X.stride(0) * X.element_size()) % 16 != 0
         return 1 + int(unaligned) + int(info["tc_tiles"] > 0)
@@ -554,7 +554,11 @@ class Run:
             # executor 4 = W's nonzero 128 x 64 blocks on tcgen05 (kernel 5d), 2 * 128 * 64 * N
             # flops per block; against the measured dense bf16 peak (fp16 runs at the same rate)
             per = 2 * 16 * 16 if pinfo["executor"] == 3 else 2 * 128 * 64
-            tc_flops = per * d["N"] * pinfo["tc_panel_steps"]
+            cols = d["N"]
+            if self.layers[dom]["kind"] == "conv":  # the MMA runs over the interleaved span
+                Ld, g = self.layers[dom], pinfo["conv_images_per_tile"]
+                cols = -(-Ld["B"] // g) * (Ld["H"] + 2) * g * Ld["W"]
+            tc_flops = per * cols * pinfo["tc_panel_steps"]
             roof = {"bound": "tensor", "achieved": tc_flops / sec / 1e12, "peak": peaks["bf16_tflops"],
                     "unit": "TFLOP/s", "useful_tflops": 2 * d["nnz"] * d["N"] / sec / 1e12,
                     "executed_flops_per_launch": tc_flops}
@@ -813,7 +817,7 @@ class Run:
 
 def parse_secondary(spec: str, world: int):
     if spec == "auto":
-        spec = "bert:f32:90,bert:f16:90" if world == 1 else ""
+        spec = "bert:f32:90,bert:f16:90,conv:f16:90" if world == 1 else ""
     out = []
     for item in filter(None, spec.split(",")):
         wl, dt, sp = item.split(":")
@@ -833,7 +837,8 @@ def main():
     ap.add_argument("--sparsity", type=int, default=90)
     ap.add_argument("--secondary", default="auto",
                     help="extra workloads timed the same way, 'wl:dtype:sparsity,...'; 'auto' = "
-                         "BERT FFN fp32 and fp16 at 90%% on 1 GPU, none on N > 1; '' = none")
+                         "BERT FFN fp32 and fp16 and the C5 conv in fp16 at 90%% on 1 GPU, none on "
+                         "N > 1; '' = none")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -382,7 +382,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->smem_bytes = p.smem_bytes;
   out->device = p.device;
   out->conv_rows_per_tile = p.conv_rb;
-  out->conv_images_per_tile = p.conv_ipt;
+  out->conv_images_per_tile = p.kind == SPARSE_CONV3X3 && p.executor == 4 ? p.tcg_g : p.conv_ipt;
   out->max_panel_nnz = p.max_panel_nnz;
   out->min_panel_nnz = p.min_panel_nnz;
   out->build_ms = p.build_ms;

@@ -1688,12 +1688,39 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
   const int HW = H * W, P = g * W, blk = g * HW;
   const int nblk = cin * ngroups;
   const int64_t span = (int64_t)ngroups * Sg;
-  const int nv = Sg / 4;  // 4-element vectors per (block, copy)
   // the conv kernel may start now (it waits on the per-group counters, not on this grid)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // blocks in group-major order (bb = q cin + ci): the first image groups complete first, in the
   // order the conv kernel's tiles consume them
-  const float rnv = 1.0f / nv, rcin = 1.0f / cin, rP = 1.0f / P, rW = 1.0f / W;
+  const float rcin = 1.0f / cin, rP = 1.0f / P, rW = 1.0f / W;
+  // vectors of V elements never leave their row: fp32 V = 4 (16 B); 16-bit V = 8 (16 B) when
+  // P % 8 == 0, else V = 4 (8-byte stores)
+  auto write_copies = [&](int b0, int nb, auto vtag) {
+    constexpr int V = decltype(vtag)::value;
+    const int nvv = Sg / V;
+    const float rnv = 1.0f / nvv;
+    for (int i = threadIdx.x; i < 3 * nb * nvv; i += blockDim.x) {
+      const int t = div_rcp(i, nvv, rnv), e0 = (i - t * nvv) * V;
+      const int k = div_rcp(t, 3, 1.0f / 3.0f), dx = t - 3 * k;
+      const int bb = b0 + k, q = div_rcp(bb, cin, rcin), ci = bb - q * cin;
+      const int r = div_rcp(e0, P, rP), xx = e0 - r * P;
+      int j = div_rcp(xx, W, rW), xw = xx - j * W;
+      const T* sb = sp + (size_t)k * blk + (size_t)(r - 1) * W;
+      alignas(16) T v[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) {
+        const int xs = xw + dx - 1;
+        v[c] = (r >= 1 && r <= H && xs >= 0 && xs < W) ? sb[j * HW + xs] : T(0);
+        if (++xw == W) xw = 0, ++j;
+      }
+      T* dst = xp + ((int64_t)dx * cin + ci) * span + (int64_t)q * Sg + e0;
+      if (V * sizeof(T) == 16)
+        *(uint4*)dst = *(const uint4*)v;
+      else
+        *(uint2*)dst = *(const uint2*)v;
+    }
+  };
+  const bool v8 = sizeof(T) == 2 && P % 8 == 0;
   for (int b0 = blockIdx.x * pp; b0 < nblk; b0 += gridDim.x * pp) {
     const int nb = min(pp, nblk - b0);
     for (int k = 0; k < nb; ++k) {  // block (q, ci): g contiguous planes (zero past the batch)
@@ -1702,26 +1729,10 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
       stage_contig<T>(sp + (size_t)k * blk, x + ((int64_t)ci * B + (int64_t)q * g) * HW, blk, valid);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 3 * nb * nv; i += blockDim.x) {
-      const int t = div_rcp(i, nv, rnv), e0 = (i - t * nv) * 4;
-      const int k = div_rcp(t, 3, 1.0f / 3.0f), dx = t - 3 * k;
-      const int bb = b0 + k, q = div_rcp(bb, cin, rcin), ci = bb - q * cin;
-      const int r = div_rcp(e0, P, rP), xx = e0 - r * P;
-      int j = div_rcp(xx, W, rW), xw = xx - j * W;
-      const T* sb = sp + (size_t)k * blk + (size_t)(r - 1) * W;
-      alignas(16) T v[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int xs = xw + dx - 1;
-        v[c] = (r >= 1 && r <= H && xs >= 0 && xs < W) ? sb[j * HW + xs] : T(0);
-        if (++xw == W) xw = 0, ++j;
-      }
-      T* dst = xp + ((int64_t)dx * cin + ci) * span + (int64_t)q * Sg + e0;
-      if (sizeof(T) == 4)
-        *(uint4*)dst = *(const uint4*)v;
-      else
-        *(uint2*)dst = *(const uint2*)v;
-    }
+    if (v8)
+      write_copies(b0, nb, std::integral_constant<int, 8>{});
+    else
+      write_copies(b0, nb, std::integral_constant<int, 4>{});
     if (ready) __threadfence();  // this thread's copies visible at device scope
     __syncthreads();
     if (ready && threadIdx.x < nb) {  // publish: block (q, ci) of every copy is written

@@ -156,6 +156,12 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
             o.conv_vec = vec;
             cands.push_back(o);
           }
+    if (S == 2) {  // 16-bit: implicit im2col on the tcgen05 block executor (conv_kernel 5)
+      BuildOpts o = base;
+      o.conv_vec = 2;
+      o.executor = 4;
+      cands.push_back(o);
+    }
   }
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {

@@ -293,6 +293,8 @@ class Plan:
             o.update(k_chunk=i["k_chunk"], conv_kernel=i["conv_kernel"])
             o.pop("split_k")
             o.pop("stages")
+            if i["conv_kernel"] == 5:  # tcgen05 blocks: the tile options are the executor's own
+                o = dict(conv_kernel=5)
         return o
 
     def _check_tensor(self, t, name):
