@@ -61,11 +61,15 @@ spmm_case("spmm_jit", 128, 256, 700, f32, executor=1)
 spmm_case("spmm_tc_subblocks", 256, 512, 392, f16, tc_min_density=10)
 spmm_case("spmm_tcp_panels", 512, 768, 1000, f16, executor=3)
 spmm_case("spmm_unaligned_repack", 200, 100, 49, f32)
+spmm_case("spmm_param_plan", 128, 64, 1000, f32, plan_source=1)
+spmm_case("spmm_tcgen05_blocks", 300, 200, 517, f16, executor=4)
+spmm_case("spmm_tcgen05_blocks_bf16", 256, 128, 600, bf16, executor=4)
 conv_case("conv_position_strided", 16, 24, 2, 14, 14, f32, conv_kernel=1)
 conv_case("conv_tma_fed", 32, 48, 3, 14, 14, f32, conv_kernel=2)
 conv_case("conv_register_staged", 32, 48, 3, 14, 14, f16, conv_kernel=3)
-conv_case("conv_packed", 32, 48, 3, 14, 14, f32, conv_kernel=4)
-conv_case("conv_packed_f16", 32, 48, 3, 14, 14, f16, conv_kernel=4)
+conv_case("conv_interleaved", 32, 48, 3, 14, 14, f32, conv_kernel=4)
+conv_case("conv_interleaved_f16", 32, 48, 3, 14, 14, f16, conv_kernel=4)
+conv_case("conv_tcgen05", 64, 48, 3, 14, 14, f16, conv_kernel=5)
 if not only or "linear" in only:
     w = gen.int_weights(96, 128, 90, seed=9, vmax=3)
     xt = gen.int_x(300, 128, seed=10, vmax=3)
