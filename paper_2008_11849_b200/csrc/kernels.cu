@@ -1688,8 +1688,11 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
   const int HW = H * W, P = g * W, blk = g * HW;
   const int nblk = cin * ngroups;
   const int64_t span = (int64_t)ngroups * Sg;
-  // the conv kernel may start now (it waits on the per-group counters, not on this grid)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // overlap mode: the conv kernel may start now (it waits on the per-group counters, not on
+  // this grid).  Sequential mode: no early trigger -- a conv CTA launched early would sit on
+  // an SM (in griddepcontrol.wait) and take the resources this pre-pass needs (measured 70 ->
+  // 89 us).
+  if (ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // blocks in group-major order (bb = q cin + ci): the first image groups complete first, in the
   // order the conv kernel's tiles consume them
   const float rcin = 1.0f / cin, rP = 1.0f / P, rW = 1.0f / W;
