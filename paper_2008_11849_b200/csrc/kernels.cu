@@ -1693,9 +1693,19 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
   // an SM (in griddepcontrol.wait) and take the resources this pre-pass needs (measured 70 ->
   // 89 us).
   if (ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // blocks in group-major order (bb = q cin + ci): the first image groups complete first, in the
-  // order the conv kernel's tiles consume them
-  const float rcin = 1.0f / cin, rP = 1.0f / P, rW = 1.0f / W;
+  // block order: overlap mode group-major (bb = q cin + ci: the first image groups complete
+  // first, in the order the conv kernel's tiles consume them); sequential mode channel-major
+  // (bb = ci ngroups + q: a CTA's consecutive blocks are one contiguous run of the input)
+  const float rcin = 1.0f / cin, rng = 1.0f / ngroups, rP = 1.0f / P, rW = 1.0f / W;
+  auto decode = [&](int bb, int& q, int& ci) {
+    if (ready) {
+      q = div_rcp(bb, cin, rcin);
+      ci = bb - q * cin;
+    } else {
+      ci = div_rcp(bb, ngroups, rng);
+      q = bb - ci * ngroups;
+    }
+  };
   // vectors of V elements never leave their row: fp32 V = 4 (16 B); 16-bit V = 8 (16 B) when
   // P % 8 == 0, else V = 4 (8-byte stores)
   auto write_copies = [&](int b0, int nb, auto vtag) {
@@ -1705,7 +1715,8 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
     for (int i = threadIdx.x; i < 3 * nb * nvv; i += blockDim.x) {
       const int t = div_rcp(i, nvv, rnv), e0 = (i - t * nvv) * V;
       const int k = div_rcp(t, 3, 1.0f / 3.0f), dx = t - 3 * k;
-      const int bb = b0 + k, q = div_rcp(bb, cin, rcin), ci = bb - q * cin;
+      int q, ci;
+      decode(b0 + k, q, ci);
       const int r = div_rcp(e0, P, rP), xx = e0 - r * P;
       int j = div_rcp(xx, W, rW), xw = xx - j * W;
       const T* sb = sp + (size_t)k * blk + (size_t)(r - 1) * W;
@@ -1726,10 +1737,14 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
   const bool v8 = sizeof(T) == 2 && P % 8 == 0;
   for (int b0 = blockIdx.x * pp; b0 < nblk; b0 += gridDim.x * pp) {
     const int nb = min(pp, nblk - b0);
-    for (int k = 0; k < nb; ++k) {  // block (q, ci): g contiguous planes (zero past the batch)
-      const int bb = b0 + k, q = div_rcp(bb, cin, rcin), ci = bb - q * cin;
-      const int valid = max(0, min(g, B - q * g)) * HW;
-      stage_contig<T>(sp + (size_t)k * blk, x + ((int64_t)ci * B + (int64_t)q * g) * HW, blk, valid);
+    for (int k = 0; k < nb;) {  // block (q, ci): g contiguous planes (zero past the batch)
+      int q, ci;
+      decode(b0 + k, q, ci);
+      // sequential mode: the run of this channel's blocks is contiguous in x
+      const int run = ready ? 1 : min(nb - k, ngroups - q);
+      const int valid = max(0, min(run * g, B - q * g)) * HW;
+      stage_contig<T>(sp + (size_t)k * blk, x + ((int64_t)ci * B + (int64_t)q * g) * HW, run * blk, valid);
+      k += run;
     }
     __syncthreads();
     if (v8) {
@@ -1740,7 +1755,8 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
       for (int i = threadIdx.x; i < 3 * nb * nv; i += blockDim.x) {
         const int t = div_rcp(i, nv, rnv), e0 = (i - t * nv) * 4;
         const int k = div_rcp(t, 3, 1.0f / 3.0f), dx = t - 3 * k;
-        const int bb = b0 + k, q = div_rcp(bb, cin, rcin), ci = bb - q * cin;
+          int q, ci;
+        decode(b0 + k, q, ci);
         const int r = div_rcp(e0, P, rP), xx = e0 - r * P;
         int j = div_rcp(xx, W, rW), xw = xx - j * W;
         const T* sb = sp + (size_t)k * blk + (size_t)(r - 1) * W;
@@ -1761,7 +1777,7 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
     if (ready) __threadfence();  // this thread's copies visible at device scope
     __syncthreads();
     if (ready && threadIdx.x < nb) {  // publish: block (q, ci) of every copy is written
-      const int bb = b0 + threadIdx.x, q = bb / cin;
+      const int bb = b0 + threadIdx.x, q = bb / cin;  // (overlap mode: group-major order)
       __threadfence();
       atomicAdd(ready + q, 1u);
     }
