@@ -553,13 +553,18 @@ class Run:
             # contraction of the panels' column unions, 2 * 16 * 16 * N flops per k16 step;
             # executor 4 = W's nonzero 128 x 64 blocks on tcgen05 (kernel 5d), 2 * 128 * 64 * N
             # flops per block; against the measured dense bf16 peak (fp16 runs at the same rate)
-            per = 2 * 16 * 16 if pinfo["executor"] == 3 else 2 * 128 * 64
+            # (x_multicast row blocks per union entry); fp32 plans run 3xTF32 (three K8 MMAs per
+            # 128 x 32 block) against the TF32 peak = the measured bf16 peak x the nominal 1/2
+            tf = S == 4 and pinfo["executor"] == 4
+            per = 2 * 16 * 16 if pinfo["executor"] == 3 else \
+                (3 * 2 * 128 * 32 if tf else 2 * 128 * 64) * max(1, pinfo.get("x_multicast", 1))
             cols = d["N"]
             if self.layers[dom]["kind"] == "conv":  # the MMA runs over the interleaved span
                 Ld, g = self.layers[dom], pinfo["conv_images_per_tile"]
                 cols = -(-Ld["B"] // g) * (Ld["H"] + 2) * g * Ld["W"]
             tc_flops = per * cols * pinfo["tc_panel_steps"]
-            roof = {"bound": "tensor", "achieved": tc_flops / sec / 1e12, "peak": peaks["bf16_tflops"],
+            roof = {"bound": "tensor", "achieved": tc_flops / sec / 1e12,
+                    "peak": peaks["bf16_tflops"] * (0.5 if tf else 1.0),
                     "unit": "TFLOP/s", "useful_tflops": 2 * d["nnz"] * d["N"] / sec / 1e12,
                     "executed_flops_per_launch": tc_flops}
         elif d["bound"] == "hbm":
@@ -572,7 +577,8 @@ class Run:
         roof["traffic"] = traffic
         roof["kernel"] = d["name"]
         roof["peak_source"] = peaks["source"] if roof["bound"] == "hbm" else \
-            ("MEASURED_PEAKS.json bf16_tflops (dense tcgen05 cuBLAS)" if roof["bound"] == "tensor" else
+            (("MEASURED_PEAKS.json bf16_tflops (dense tcgen05 cuBLAS)" +
+              (" x 1/2 (TF32 nominal ratio)" if S == 4 else "")) if roof["bound"] == "tensor" else
              "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)")
         roof["alg_bytes_per_launch"] = d["alg_bytes"]
         roof["flops_per_launch"] = 2 * d["nnz"] * d["N"]

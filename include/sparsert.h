@@ -97,13 +97,25 @@ typedef struct {
                             panel and 64-row K chunk the union of the panel's nonzero columns runs
                             as a dense mma.sync m16n8k16 block (fp32 accumulate) with the union's X
                             rows gathered by ldmatrix; summation order differs from the CUDA-core
-                            kernels (within tolerance; exact on integer data). */
+                            kernels (within tolerance; exact on integer data).
+                            4 = tcgen05 blocks (SURVEY NEXT #1 on Blackwell tensor cores): W's
+                            nonzero 128-row x 64-column (fp32: 32-column) blocks stored dense and
+                            pre-swizzled, tcgen05.mma M128 N256 with fp32 accumulators in TMEM;
+                            fp16 / bf16 directly, fp32 as 3xTF32 (W and X each split into two
+                            TF32 halves, W_hi X_hi + W_lo X_hi + W_hi X_lo: relative error
+                            ~2^-22 per product; X is split on the device into a stream-ordered
+                            scratch).  Summation order differs from the CUDA-core kernels
+                            (within tolerance; exact on integer data). */
   int32_t jit_rows;      /* JIT: rows per panel (accumulator registers per thread), 0 = auto */
   int32_t jit_warps;     /* JIT: warps per CTA (each owns 32 columns), 0 = auto */
   int32_t x_multicast;   /* SpMM, k_split == 1: CTAs of a thread-block cluster (consecutive row
                             panels, same N tile) that share every staged X tile through one TMA
                             multicast load, dividing the L2 -> SM traffic of X: 1, 2, 4 or 8;
-                            0 = 1.  Result-neutral. */
+                            0 = 1.  Result-neutral.  With executor 4 (and conv_kernel 5): CTAs
+                            of a cluster = consecutive 128-row blocks on the same N tile, each
+                            loading 1 / x_multicast of every X tile and multicasting it (1, 2
+                            or 4); the group walks the union of its row blocks' nonzero
+                            k-blocks. */
   int32_t x_source;      /* SpMM: where the executor's FMA loop reads X from.  0 = shared memory
                             (LDS.128, default); 1 = tensor memory: every staged X chunk is copied
                             smem -> TMEM (tcgen05.cp, replicated to the 4 lane quarters) and read
@@ -119,7 +131,10 @@ typedef struct {
                             3 = register-staged vectorised kernel; 4 = image-interleaved kernel:
                             g images side by side per row so that no output position is padding
                             (copies from a pre-pass, one TMA span box per copy and chunk; images
-                            up to ~28 wide).  All result-identical. */
+                            up to ~28 wide).  All result-identical.  5 = the tcgen05 block
+                            executor (executor 4; fp16 / bf16 plans): implicit im2col over
+                            interleaved dx-shifted copies, k-blocks = (tap, 64 channels);
+                            summation order of the tensor cores (exact on integer data). */
   int32_t row_order;     /* 0 = load-balanced panels (rows sorted by nnz, LPT-binned, P:163-165;
                             default); 1 = natural contiguous row ranges (the "no load balancing"
                             ablation of P:385).  Result-neutral for split_k = k_split = 1. */

@@ -394,7 +394,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->jit_cubin_bytes = p.jit_cubin_bytes;
   out->jit_compile_ms = p.jit_compile_ms;
   out->tuned_us = p.tuned_us;
-  out->x_multicast = p.cm;
+  out->x_multicast = p.executor == 4 ? p.tcg_cs : p.cm;
   out->x_source = p.tm;
   out->conv_kernel = p.kind != SPARSE_CONV3X3 ? 0 : p.executor == 4 ? 5 : !p.conv_vec ? 1 : p.conv_vec == 2 ? 2 : p.conv_vec == 4 ? 4 : 3;
   out->row_order = p.row_order;

@@ -97,6 +97,17 @@ static int pow2_ceil(int v) {
 
 static int64_t align16(int64_t v) { return (v + 15) & ~int64_t(15); }
 
+// fp32 -> nearest TF32 value (10 explicit mantissa bits, round to nearest even), kept in an
+// fp32 container with the low 13 bits zero (finite inputs; the 3xTF32 split W = hi + lo)
+static float tf32_rn(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0xfffu + ((u >> 13) & 1u);
+  u &= 0xffffe000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
 namespace {
 struct Entry {
   int32_t k;
@@ -568,6 +579,16 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     err = "x_multicast must be 1, 2, 4 or 8";
     return SPARSE_EUNSUPPORTED;
   }
+  if (o.executor == 4) {
+    // the tcgen05 block executor's own cluster (row blocks sharing each X tile); the CUDA-core
+    // part of the plan (conv plans keep one) does not multicast
+    if (p.cm > 4) {
+      err = "x_multicast must be 1, 2 or 4 for the tcgen05 block executor";
+      return SPARSE_EUNSUPPORTED;
+    }
+    p.tcg_cs = p.cm;
+    p.cm = 1;
+  }
   if (p.cm > 1 && (o.kind != SPARSE_SPMM || p.ks > 1)) {
     err = "x_multicast > 1 needs an SpMM plan with k_split = 1";
     return SPARSE_EUNSUPPORTED;
@@ -851,23 +872,32 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     const int rc = jit_generate(p, re, o, err);
     if (rc != SPARSE_OK) return rc;
   } else if (o.executor == 4) {
-    // ---- tcgen05 block executor (SURVEY NEXT #1 on Blackwell's 5th-generation tensor cores;
-    // 16-bit SpMM).  W is cut into 128-row x 64-column blocks; every block holding at least one
-    // nonzero is stored dense (zeros included) in the tcgen05 K-major, 128-byte-swizzled shared
-    // memory layout (8-row atoms of 1 KB, 16-byte chunk c of row r at c ^ (r % 8)), so the
-    // executor copies it verbatim into shared memory and multiplies it with tcgen05.mma
-    // (M = 128 rows, N = 256 columns, K = 16 per instruction, fp32 accumulate in TMEM).
+    // ---- tcgen05 block executor (SURVEY NEXT #1 on Blackwell's 5th-generation tensor cores).
+    // W is cut into 128-row x BK-column blocks (BK = 64 for 16-bit data, 32 for fp32); every
+    // block holding at least one nonzero is stored dense (zeros included) in the tcgen05
+    // K-major, 128-byte-swizzled shared memory layout (8-row atoms of 1 KB, 16-byte chunk c of
+    // row r at c ^ (r % 8)), so the executor copies it verbatim into shared memory and
+    // multiplies it with tcgen05.mma (M = 128 rows, N = 256 columns, fp32 accumulate in TMEM).
+    // fp32 plans run as 3xTF32: W = W_hi + W_lo with both halves exact TF32 values (RN), the
+    // block stores [W_hi | W_lo] (2 x 16 KB), and the executor sums W_hi X_hi + W_lo X_hi +
+    // W_hi X_lo (X split the same way on the device) - relative error ~2^-22 per product.
     // All-zero blocks are skipped.  "Dense enough" is decided by measurement: the tuner times
     // this executor against the CUDA-core ones; at 90 % uniform sparsity a 128 x 64
     // block holds ~820 nonzeros and the tensor cores' ~30x throughput advantage outweighs the
-    // ~10x zero work.  Row panel metadata: tcp_step_off = [nrb + 1] prefix of nonzero blocks,
-    // then their k-block indices; tcp_steps = the blocks (16 KB each), row block major.
-    if (dtype == SPARSE_F32) {
-      err = "executor = 4 (tcgen05 blocks) / conv_kernel = 5 needs an fp16 or bf16 plan";
+    // ~10x zero work.  A group of tcg_cs consecutive row blocks (one thread-block cluster,
+    // sharing each X tile by multicast) walks the union of its row blocks' nonzero k-blocks
+    // (a row block lacking one gets a zero block).  Metadata: tcp_step_off = [ngroups + 1]
+    // prefix of union entries, then their k-block indices; tcp_steps = the blocks, entry-major
+    // then rank (entry j of the group list, rank r at (j * tcg_cs + r)).
+    const bool conv = o.kind == SPARSE_CONV3X3;
+    const bool f32 = dtype == SPARSE_F32;
+    if (f32 && conv) {
+      err = "conv_kernel = 5 (tcgen05 blocks) needs an fp16 or bf16 plan";
       return SPARSE_EUNSUPPORTED;
     }
-    const bool conv = o.kind == SPARSE_CONV3X3;
-    const int BM = 128, BK = 64;
+    const int BM = 128, BK = f32 ? 32 : 64, S = f32 ? 4 : 2;
+    const int CS = p.tcg_cs;
+    p.tcg_bk = BK;
     // conv: implicit im2col over the interleaved dx-shifted copies (kernel 3b layout); the K
     // axis is ordered tap-major, k-block = (tap, 64 input channels), so the B tile of a k-block
     // is one 2-D slab of copy dx shifted by (dy - 1) pitches
@@ -879,43 +909,59 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       p.tcg_g = gg;
       p.tcg_ncb = ncb;
     }
-    // k-block of column k: SpMM k / 64; conv (ci, tap) -> tap * ncb + ci / 64, column ci % 64
+    // k-block of column k: SpMM k / BK; conv (ci, tap) -> tap * ncb + ci / BK, column ci % BK
     auto kblock = [&](int32_t k) { return conv ? (k % 9) * ncb + (k / 9) / BK : k / BK; };
     auto kcol = [&](int32_t k) { return conv ? (k / 9) % BK : k % BK; };
     const int32_t nrb = (M + BM - 1) / BM, nkb = conv ? 9 * ncb : (K + BK - 1) / BK;
+    const int32_t ngroups = (nrb + CS - 1) / CS;
     p.tcp_npanels = nrb;
     p.tcp_nchunks = nkb;
+    p.tcg_ngroups = ngroups;
     std::vector<int32_t> pref(1, 0), kbs;
-    std::vector<char> nzb((size_t)nrb * nkb, 0);
+    std::vector<char> nzb((size_t)ngroups * CS * nkb, 0);
     for (int32_t m = 0; m < M; ++m)
       for (const Entry& en : rows[m]) nzb[(size_t)(m / BM) * nkb + kblock(en.k)] = 1;
-    for (int32_t rb = 0; rb < nrb; ++rb) {
-      for (int32_t kb = 0; kb < nkb; ++kb)
-        if (nzb[(size_t)rb * nkb + kb]) kbs.push_back(kb);
+    std::vector<int64_t> slot((size_t)ngroups * CS * nkb, -1);  // (row block, k-block) -> block
+    for (int32_t g = 0; g < ngroups; ++g) {
+      for (int32_t kb = 0; kb < nkb; ++kb) {
+        bool any = false;
+        for (int r = 0; r < CS; ++r) any = any || nzb[(size_t)(g * CS + r) * nkb + kb];
+        if (!any) continue;
+        for (int r = 0; r < CS; ++r) slot[(size_t)(g * CS + r) * nkb + kb] = (int64_t)kbs.size() * CS + r;
+        kbs.push_back(kb);
+      }
       pref.push_back((int32_t)kbs.size());
     }
     p.tcp_step_off = pref;
     p.tcp_step_off.insert(p.tcp_step_off.end(), kbs.begin(), kbs.end());
-    const size_t blk = (size_t)BM * BK * 2;
-    p.tcp_steps.assign(kbs.size() * blk, 0);
-    std::vector<int64_t> slot((size_t)nrb * nkb, -1);
-    for (size_t i = 0, rb = 0; rb < (size_t)nrb; ++rb)
-      for (int32_t j = pref[rb]; j < pref[rb + 1]; ++j, ++i) slot[rb * nkb + kbs[j]] = (int64_t)i;
+    const size_t half = (size_t)BM * BK * S, blk = f32 ? 2 * half : half;
+    p.tcp_steps.assign(kbs.size() * CS * blk, 0);
+    // byte offset of (row r, column c) inside a 128 x BK block (128-byte rows, SW128)
+    auto sw = [&](int r, int c) {
+      const int b = c * S;
+      return (size_t)(r / 8) * 1024 + (size_t)(r % 8) * 128 + (size_t)(((b / 16) ^ (r % 8)) * 16) + (size_t)(b % 16);
+    };
     for (int32_t m = 0; m < M; ++m) {
       const int r = m % BM;
       for (const Entry& en : rows[m]) {
         const int64_t bi = slot[(size_t)(m / BM) * nkb + kblock(en.k)];
-        const int c = kcol(en.k);
-        const size_t off = (size_t)bi * blk + (size_t)(r / 8) * 1024 + (size_t)(r % 8) * 128 +
-                           (size_t)(((c / 8) ^ (r % 8)) * 16) + (size_t)(c % 8) * 2;
-        std::memcpy(&p.tcp_steps[off], &en.wh, 2);
+        const size_t off = (size_t)bi * blk + sw(r, kcol(en.k));
+        if (f32) {
+          const float hi = tf32_rn(en.w), lo = tf32_rn(en.w - hi);
+          std::memcpy(&p.tcp_steps[off], &hi, 4);
+          std::memcpy(&p.tcp_steps[off + half], &lo, 4);
+        } else {
+          std::memcpy(&p.tcp_steps[off], &en.wh, 2);
+        }
       }
     }
     p.tcp_nsteps = (int64_t)kbs.size();
     p.executor = 4;
     if (!conv) p.n_tile = 256;
-    p.stages = 4;
-    p.smem_bytes = p.stages * (16 * 1024 + 32 * 1024) + 1024 + 2048 + 8192;  // + align, barriers, conv table, block lists
+    // stage = the W block(s) + a 256-column X tile (fp32: X_hi and X_lo): 48 KB / 96 KB
+    const int st_bytes = f32 ? 96 * 1024 : 48 * 1024;
+    p.stages = f32 ? 2 : 4;
+    p.smem_bytes = p.stages * st_bytes + 1024 + 2048 + 8192;  // + align, barriers, conv table, block lists
     p.plan_bytes += (int64_t)p.tcp_steps.size() + (int64_t)p.tcp_step_off.size() * 4;
   } else if (o.executor == 3) {
     // ---- condensed-panel tensor-core executor (fp16 SpMM) ----
@@ -1087,7 +1133,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
                          p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
                          p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm,
                          p.conv_vec, p.row_order, p.executor, p.jit_mp, p.jit_warps, p.stages,
-                         p.tc_min_pct, p.ps};
+                         p.tc_min_pct, p.ps, p.tcg_cs, p.tcg_bk};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

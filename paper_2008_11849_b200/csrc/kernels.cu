@@ -2581,12 +2581,12 @@ static int launch_tcp(const Plan& p, int64_t N, const void* X, int64_t ldx, void
 // ascending, the tensor core's order inside a K16 step (within tolerance; exact on integer data).
 constexpr int kTcgMetaMax = 2048;  // block-list entries kept in shared memory
 struct TcgArgs {
-  const uint8_t* blocks;     // [nblocks][16 KB] pre-swizzled W blocks
-  const int32_t* meta;       // [nrb + 1] prefix, then k-block indices
-  int32_t nblk;              // nonzero blocks (k-block list length)
+  const uint8_t* blocks;     // [entries][cs][A bytes] pre-swizzled W blocks (fp32: [W_hi | W_lo])
+  const int32_t* meta;       // [ngroups + 1] prefix, then k-block indices
+  int32_t nblk;              // union entries of all groups (k-block list length)
   uint8_t* Y;
   int64_t ldy, N;            // conv: N = the span of the interleaved copies (positions incl. halo)
-  int32_t M, nrb, stages;
+  int32_t M, ngroups, cs, stages;
   const uint8_t* bias;
   float beta;
   int32_t relu;
@@ -2597,33 +2597,94 @@ struct TcgArgs {
   int64_t plane;
 };
 
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// shared-memory matrix descriptor: start, leading / stride byte offsets, version 1 (bit 46),
+// layout type (bits 61-63): 2 = 128-byte swizzle (16-byte chunks, 8-row atoms), 1 = 128-byte
+// swizzle of 32-byte chunks (4-row atoms; the only layout for MN-major TF32 operands)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                                    uint32_t layout = 2u) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
+}
+template <bool TF>
+__device__ __forceinline__ void umma(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t en) {
+  if (TF)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(da), "l"(db), "r"(idesc), "r"(en)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(da), "l"(db), "r"(idesc), "r"(en)
+        : "memory");
+}
+// arrive on the mbarrier at offset `bar` of every CTA in `mask` once this thread's MMAs are done
+__device__ __forceinline__ void tm_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          bar),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t bar, uint16_t mask, bool mc) {
+  if (mc)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
 }
 
-template <bool BF, bool CONV = false>
-__global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant__ CUtensorMap tmap,
+// TF = fp32 plan as 3xTF32.  Per stage (k-block):
+//   16-bit: A = one 128 x 64 W block (16 KB), B = 64 k x 256 columns of X as 4 boxes of 64
+//           columns (8 KB each); 4 x tcgen05.mma kind::f16 K16
+//   TF:     A = [W_hi | W_lo] (2 x 16 KB, 128 x 32 fp32 each), B = [X_hi | X_lo] (2 x 32 KB,
+//           8 boxes of 32 k x 32 columns each); per K8 step 3 x tcgen05.mma kind::tf32:
+//           W_hi X_hi + W_lo X_hi + W_hi X_lo
+// Cluster of cs CTAs = cs consecutive row blocks (one group) on the same N tile: CTA rank r
+// loads boxes [r * NBOX / cs, (r + 1) * NBOX / cs) and multicasts them to the whole cluster;
+// a stage is refilled only when every CTA of the cluster has consumed it (each CTA's MMA
+// commit arrives on the stage's empty barrier in all cs CTAs).
+template <bool BF, bool CONV = false, bool TF = false>
+__global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                          const __grid_constant__ CUtensorMap tmap2,
                                                           const TcgArgs a) {
-  constexpr int BN = 256, A_BYTES = 128 * 64 * 2, B_BYTES = 64 * BN * 2, ST_BYTES = A_BYTES + B_BYTES;
+  constexpr int BN = 256, A_HALF = 128 * 128, A_BYTES = TF ? 2 * A_HALF : A_HALF;
+  constexpr int NBOX = TF ? 8 : 4, BOX_BYTES = TF ? 32 * 128 : 64 * 128, BOX_COLS = TF ? 32 : 64;
+  constexpr int B_HALF = NBOX * BOX_BYTES, B_BYTES = TF ? 2 * B_HALF : B_HALF;
+  constexpr int ST_BYTES = A_BYTES + B_BYTES, KSTEP_B = TF ? 1024 : 2048;
+  // epilogue warps, and k-blocks per TMEM partial (TF: short truncating chains, see below)
+  constexpr int NEPI = TF ? 8 : 4, FLUSH = TF ? 8 : (1 << 30);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);  // SW128: 1 KB atoms
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = a.stages;
+  const int S = a.stages, CS = a.cs;
+  const uint32_t rank = CS > 1 ? cluster_rank() : 0u;
+  const uint16_t mask = (uint16_t)((1u << CS) - 1u);
+  const int64_t cl = blockIdx.x / CS, ncl = gridDim.x / CS;
   uint64_t* bars = (uint64_t*)(smem + (size_t)S * ST_BYTES);
   const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * S;
   const uint32_t tfull0 = empty0 + 8 * S, tempty0 = tfull0 + 16;
   uint32_t* tslot = (uint32_t*)(bars + 2 * S + 4);
   const int64_t nnb = (a.N + BN - 1) / BN;
-  const int64_t ntiles = (int64_t)a.nrb * nnb;
+  const int64_t ntiles = (int64_t)a.ngroups * nnb;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, (uint32_t)CS);  // one MMA commit per CTA of the cluster
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull0 + 8 * b, 1);
-      mbar_init(tempty0 + 8 * b, 4);  // one arrive per epilogue warp
+      mbar_init(tempty0 + 8 * b, NEPI);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -2634,11 +2695,12 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
   }
   tm_fence_before();
   __syncthreads();
+  if (CS > 1) cluster_sync_all();  // peers multicast into this CTA's stages and barriers
   tm_fence_after();
   const uint32_t tbase = *tslot;
   // the block lists, copied once into shared memory (dependent global loads on the producer's
   // issue path were the kernel's top stall)
-  const int nmeta = a.nrb + 1 + a.nblk;
+  const int nmeta = a.ngroups + 1 + a.nblk;
   const int32_t* meta = a.meta;
   if (nmeta <= kTcgMetaMax) {
     int32_t* sm = (int32_t*)((uint8_t*)tslot + 64 + 1024);
@@ -2652,33 +2714,36 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
   if (warp == 0) {
     // ---------------- producer
     if (lane == 0) {
+      const int nb = NBOX / CS;  // X boxes per operand this CTA loads (and multicasts)
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int rb = (int)(t % a.nrb);
-        const int64_t n0 = (t / a.nrb) * BN;
-        const int j0 = meta[rb], j1 = meta[rb + 1];
+      for (int64_t t = cl; t < ntiles; t += ncl) {
+        const int gi = (int)(t % a.ngroups);
+        const int64_t n0 = (t / a.ngroups) * BN;
+        const int j0 = meta[gi], j1 = meta[gi + 1];
         for (int j = j0; j < j1; ++j) {
-          const int kb = meta[a.nrb + 1 + j];
+          const int kb = meta[a.ngroups + 1 + j];
           mbar_wait(empty0 + 8 * s, ph ^ 1u);
           uint8_t* st = smem + (size_t)s * ST_BYTES;
           const uint32_t fb = full0 + 8 * s;
           mbar_arrive_expect_tx(fb, (uint32_t)ST_BYTES);
-          bulk_load(smem_u32(st), a.blocks + (size_t)j * A_BYTES, (uint32_t)A_BYTES, fb);
-          if (CONV) {  // k-block (tap, 64 channels): copy dx, shifted by (dy - 1) pitches
-            const int tap = kb / a.ncb, cb = kb - tap * a.ncb;
-            const int s0 = (int)n0 + (tap / 3 - 1) * a.P;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              asm volatile(
-                  "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                  " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(st + A_BYTES + q * (B_BYTES / 4))),
-                  "l"((uint64_t)&tmap), "r"(s0 + 64 * q), "r"(cb * 64), "r"(tap % 3), "r"(fb)
-                  : "memory");
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              tma_load_2d(smem_u32(st + A_BYTES + q * (B_BYTES / 4)), &tmap, (int)(n0 + 64 * q), kb * 64, fb);
+          bulk_load(smem_u32(st), a.blocks + ((size_t)j * CS + rank) * A_BYTES, (uint32_t)A_BYTES, fb);
+          for (int qq = 0; qq < nb; ++qq) {
+            const int q = (int)rank * nb + qq;
+            const uint32_t dst = smem_u32(st + A_BYTES + q * BOX_BYTES);
+            if (CONV) {  // k-block (tap, 64 channels): copy dx, shifted by (dy - 1) pitches
+              const int tap = kb / a.ncb, cb = kb - tap * a.ncb;
+              const int s0 = (int)n0 + (tap / 3 - 1) * a.P;
+              tma_load_3d(dst, &tmap, s0 + BOX_COLS * q, cb * 64, tap % 3, fb, mask, CS > 1);
+            } else {
+              const int c0 = (int)(n0 + BOX_COLS * q), c1 = kb * (TF ? 32 : 64);
+              if (CS > 1) tma_load_2d_mc(dst, &tmap, c0, c1, fb, mask);
+              else tma_load_2d(dst, &tmap, c0, c1, fb);
+              if (TF) {
+                if (CS > 1) tma_load_2d_mc(dst + B_HALF, &tmap2, c0, c1, fb, mask);
+                else tma_load_2d(dst + B_HALF, &tmap2, c0, c1, fb);
+              }
+            }
           }
           if (++s == S) s = 0, ph ^= 1u;
         }
@@ -2686,38 +2751,122 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one lane)
+    // A tile's k-blocks run in chunks of FLUSH k-blocks, each into a fresh TMEM partial
+    // (alternating between the two 256-column buffers); 16-bit plans: one chunk per tile
     if (lane == 0) {
       int s = 0, acc = 0;
       uint32_t ph = 0, aph[2] = {0u, 0u};
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int rb = (int)(t % a.nrb);
-        const int j0 = meta[rb], j1 = meta[rb + 1];
-        mbar_wait(tempty0 + 8 * acc, aph[acc] ^ 1u);  // the epilogue drained this accumulator
-        tm_fence_after();
-        const uint32_t d = tbase + (uint32_t)(acc * BN);
-        for (int j = j0; j < j1; ++j) {
-          mbar_wait(full0 + 8 * s, ph);
+      for (int64_t t = cl; t < ntiles; t += ncl) {
+        const int gi = (int)(t % a.ngroups);
+        const int j0 = meta[gi], j1 = meta[gi + 1];
+        int j = j0;
+        do {
+          const int jc = j, je = min(j1, j + FLUSH);
+          mbar_wait(tempty0 + 8 * acc, aph[acc] ^ 1u);  // the epilogue drained this buffer
           tm_fence_after();
-          const uint32_t sa = smem_u32(smem + (size_t)s * ST_BYTES), sb = sa + A_BYTES;
+          const uint32_t d = tbase + (uint32_t)(acc * BN);
+          for (; j < je; ++j) {
+            mbar_wait(full0 + 8 * s, ph);
+            tm_fence_after();
+            const uint32_t sa = smem_u32(smem + (size_t)s * ST_BYTES), sb = sa + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            // A: K-major SW128 (rows of 128 B, 8-row atoms of 1 KB): K16 step = +32 B
-            // B: MN-major SW128 (64-column groups of 8 KB, 8-row atoms of 1 KB): K16 step = +2 KB
-            const uint64_t da = umma_desc_sw128(sa + 32u * k, 16u, 1024u);
-            const uint64_t db = umma_desc_sw128(sb + 2048u * k, (uint32_t)(B_BYTES / 4), 1024u);
-            const uint32_t en = (j > j0 || k > 0) ? 1u : 0u;
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-                "l"(da), "l"(db), "r"(a.idesc), "r"(en)
-                : "memory");
+            for (int k = 0; k < 4; ++k) {
+              // A: K-major SW128 (rows of 128 B, 8-row atoms of 1 KB): K step (16 x 16-bit or
+              //    8 x tf32) = +32 B
+              // B: MN-major (128-byte column groups of BOX_BYTES): 16-bit: 128-byte swizzle,
+              //    8-row atoms (SBO 1 KB), K16 step = +2 KB; TF32: 32-byte-chunk swizzle, 4-row
+              //    atoms (SBO 512 B), K8 step = +1 KB
+              const uint32_t en = (j > jc || k > 0) ? 1u : 0u;
+              constexpr uint32_t B_SBO = TF ? 512u : 1024u, B_LAYOUT = TF ? 1u : 2u;
+              const uint64_t da = umma_desc_sw128(sa + 32u * k, 16u, 1024u);
+              const uint64_t db = umma_desc_sw128(sb + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
+              umma<TF>(d, da, db, a.idesc, en);
+              if (TF) {
+                const uint64_t da_lo = umma_desc_sw128(sa + A_HALF + 32u * k, 16u, 1024u);
+                const uint64_t db_lo =
+                    umma_desc_sw128(sb + B_HALF + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
+                umma<TF>(d, da_lo, db, a.idesc, 1u);
+                umma<TF>(d, da, db_lo, a.idesc, 1u);
+              }
+            }
+            // the stage is free once these MMAs have read it (in every CTA of the cluster)
+            if (CS > 1) tm_commit_mc(empty0 + 8 * s, mask);
+            else tm_commit(empty0 + 8 * s);
+            if (++s == S) s = 0, ph ^= 1u;
           }
-          tm_commit(empty0 + 8 * s);  // the stage is free once these MMAs have read it
-          if (++s == S) s = 0, ph ^= 1u;
+          tm_commit(tfull0 + 8 * acc);  // partial complete (also when the group is empty)
+          aph[acc] ^= 1u;
+          acc ^= 1;
+        } while (j < j1);
+      }
+    }
+  } else if constexpr (TF) {
+    // ---------------- epilogue (3xTF32): 8 warps; warp w reads TMEM lanes 32 (w % 4) .. + 31
+    // (rows of the tile) and columns 128 ((w - 2) / 4) .. + 127.  The tensor core's fp32
+    // accumulation truncates (measured: error linear in K, 1.1e-5 rel-L2 at K = 3072), so the
+    // chain stays short: every FLUSH k-blocks the partial is added into an fp32 master held in
+    // registers (round to nearest), in k order - a fixed summation order.
+    const int q = warp & 3, hc = ((warp - 2) >> 2) * 128;
+    int acc = 0;
+    uint32_t aph[2] = {0u, 0u};
+    const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
+    for (int64_t t = cl; t < ntiles; t += ncl) {
+      const int gi = (int)(t % a.ngroups);
+      const int rb = gi * CS + (int)rank;
+      const int64_t n0 = (t / a.ngroups) * BN;
+      const int nent = meta[gi + 1] - meta[gi];
+      const int nch = nent > 0 ? (nent + FLUSH - 1) / FLUSH : 1;
+      float m[128];
+#pragma unroll
+      for (int c = 0; c < 128; ++c) m[c] = 0.0f;
+      for (int ch = 0; ch < nch; ++ch) {
+        mbar_wait(tfull0 + 8 * acc, aph[acc]);
+        tm_fence_after();
+        if (nent > 0) {
+#pragma unroll
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t v[32];
+            const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + hc + c0);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                  "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                  "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(ta));
+            tm_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) m[c0 + c] = __fadd_rn(m[c0 + c], __uint_as_float(v[c]));
+          }
         }
-        tm_commit(tfull0 + 8 * acc);  // accumulator complete (also when the row block is empty)
+        tm_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
         aph[acc] ^= 1u;
         acc ^= 1;
+      }
+      const int row = rb * 128 + q * 32 + lane;
+      const int ncol = (int)min((int64_t)BN, a.N - n0);
+      if (row >= a.M) continue;
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        if (hc + c0 >= ncol) break;
+        uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + hc + c0) * 4;
+        if (epi) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (hc + c0 + c < ncol) m[c0 + c] = epilogue_one<false>(m[c0 + c], a.bias, row, a.beta, yp + c * 4, a.relu);
+        }
+        if (hc + c0 + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 4)
+            *(float4*)(yp + c * 4) = make_float4(m[c0 + c], m[c0 + c + 1], m[c0 + c + 2], m[c0 + c + 3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (hc + c0 + c < ncol) ((float*)yp)[c] = m[c0 + c];
+        }
       }
     }
   } else {
@@ -2728,10 +2877,11 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
     const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
     int32_t* otab = (int32_t*)((uint8_t*)tslot + 64);  // conv: span position -> output offset
     int64_t tab_n0 = -1;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int rb = (int)(t % a.nrb);
-      const int64_t n0 = (t / a.nrb) * BN;
-      const bool has = meta[rb + 1] > meta[rb];
+    for (int64_t t = cl; t < ntiles; t += ncl) {
+      const int gi = (int)(t % a.ngroups);
+      const int rb = gi * CS + (int)rank;
+      const int64_t n0 = (t / a.ngroups) * BN;
+      const bool has = meta[gi + 1] > meta[gi];
       if (CONV && n0 != tab_n0) {
         // the 128 epilogue threads decode the tile's 256 span positions once (named barrier
         // among the epilogue warps only): s -> group q, row r, column (image j, x)
@@ -2763,7 +2913,7 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(ta));
         tm_wait_ld();
-        if (CONV) {
+        if constexpr (CONV) {
           if (row >= a.M) continue;
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
@@ -2778,18 +2928,20 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
         }
         if (row >= a.M || c0 >= ncol) continue;
         uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + c0) * 2;
-        alignas(16) uint16_t h[32];
+        {
+          alignas(16) uint16_t h[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          float f = has ? __uint_as_float(v[c]) : 0.0f;
-          if (epi && c0 + c < ncol) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp + c * 2, a.relu);
-          h[c] = to16<BF>(f);
-        }
-        if (c0 + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
+          for (int c = 0; c < 32; ++c) {
+            float f = has ? __uint_as_float(v[c]) : 0.0f;
+            if (epi && c0 + c < ncol) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp + c * 2, a.relu);
+            h[c] = to16<BF>(f);
+          }
+          if (c0 + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
 #pragma unroll
-          for (int c = 0; c < 32; c += 8) *(uint4*)(yp + c * 2) = *(const uint4*)(h + c);
-        } else {
-          for (int c = 0; c < 32 && c0 + c < ncol; ++c) ((uint16_t*)yp)[c] = h[c];
+            for (int c = 0; c < 32; c += 8) *(uint4*)(yp + c * 2) = *(const uint4*)(h + c);
+          } else {
+            for (int c = 0; c < 32 && c0 + c < ncol; ++c) ((uint16_t*)yp)[c] = h[c];
+          }
         }
       }
       tm_fence_before();
@@ -2801,12 +2953,90 @@ __global__ void __launch_bounds__(192, 1) spmm_tcg_kernel(const __grid_constant_
   }
   tm_fence_before();
   __syncthreads();
+  if (CS > 1) cluster_sync_all();  // no peer may still arrive on / multicast into this CTA
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+
+// 3xTF32 operand split of X (fp32 plans on the tcgen05 block executor): X = X_hi + X_lo with
+// X_hi = TF32 RN of X and X_lo = TF32 RN of the (exact) remainder, written to two K x ldp
+// scratch matrices (ldp a multiple of 4: 16-byte TMA row strides).  Non-finite X: X_lo = 0.
+__device__ __forceinline__ float tf32_rn_dev(float f) {
+  uint32_t u = __float_as_uint(f);
+  u += 0xfffu + ((u >> 13) & 1u);
+  return __uint_as_float(u & 0xffffe000u);
+}
+__global__ void __launch_bounds__(256) split_tf32(const float* __restrict__ X, int64_t ldx, float* __restrict__ hi,
+                                                  float* __restrict__ lo, int64_t ldp, int64_t K, int64_t N) {
+  const int64_t n4 = (N + 3) / 4, total = K * n4;
+  const bool vec = ((uintptr_t)X % 16) == 0 && (ldx % 4) == 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / n4, n = (i - k * n4) * 4;
+    float x[4];
+    if (vec && n + 4 <= N) {
+      const float4 v = __ldg((const float4*)(X + k * ldx + n));
+      x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) x[c] = n + c < N ? X[k * ldx + n + c] : 0.0f;
+    }
+    float h[4], l[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      h[c] = tf32_rn_dev(x[c]);
+      l[c] = isfinite(h[c]) ? tf32_rn_dev(x[c] - h[c]) : 0.0f;
+    }
+    *(float4*)(hi + k * ldp + n) = make_float4(h[0], h[1], h[2], h[3]);
+    *(float4*)(lo + k * ldp + n) = make_float4(l[0], l[1], l[2], l[3]);
+  }
+}
+
+// grid of a persistent cluster launch: whole clusters, at most as many as can be co-resident
+template <typename Fn>
+static unsigned tcg_grid(Fn fn, cudaLaunchConfig_t cfg, int cs, int64_t ntiles, int sms) {
+  int64_t ncl = std::max<int64_t>(1, sms / cs);
+  if (cs > 1) {
+    int maxc = 0;
+    if (cudaOccupancyMaxActiveClusters(&maxc, fn, &cfg) == cudaSuccess && maxc > 0) ncl = std::min<int64_t>(ncl, maxc);
+    else cudaGetLastError();
+  }
+  ncl = std::max<int64_t>(1, std::min<int64_t>(ncl, ntiles));
+  return (unsigned)(ncl * cs);
+}
+
+static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, const CUtensorMap& tmap2,
+                      const TcgArgs& a, int64_t ntiles, void* stream, std::string& err, const char* what,
+                      int threads = 192) {
+  using TFn = void (*)(const CUtensorMap, const CUtensorMap, const TcgArgs);
+  TFn fn = (TFn)fn_;
+  cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+  const int cs = a.cs;
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.blockDim = dim3((unsigned)threads, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = (unsigned)cs;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = cs > 1 ? 2 : 1;
+  cfg.gridDim = dim3((unsigned)cs, 1, 1);
+  cfg.gridDim = dim3(tcg_grid(fn, cfg, cs, ntiles, sms), 1, 1);
+  e = cudaLaunchKernelEx(&cfg, fn, tmap, tmap2, a);
+  if (e != cudaSuccess) return cuda_fail(e, what, err);
+  return SPARSE_OK;
 }
 
 static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy, void* stream,
                       std::string& err, const Epilogue& ep) {
-  const bool bf = p.dtype == SPARSE_BF16;
+  const bool bf = p.dtype == SPARSE_BF16, tf = p.dtype == SPARSE_F32;
   auto encode = tensor_map_encoder();
   if (!encode) {
     err = "internal: no tensor-map encoder";
@@ -2814,14 +3044,34 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   }
   DeviceGuard dg(p.device);
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
-  using TFn = void (*)(const CUtensorMap, const TcgArgs);
-  TFn fn = bf ? spmm_tcg_kernel<true> : spmm_tcg_kernel<false>;
-  cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
   const void* Xa = X;
+  const void* Xb = nullptr;
   int64_t lda = ldx;
   void* scratch = nullptr;
-  if (((uintptr_t)X % 16) != 0 || ((ldx * 2) % 16) != 0) {
+  bool pooled = false;  // scratch from cudaMallocAsync (3xTF32 split) vs the repack helper
+  if (tf) {
+    // X_hi / X_lo for the 3xTF32 products, stream ordered
+    lda = (N + 3) / 4 * 4;
+    const size_t bytes = (size_t)p.K * (size_t)lda * 4;
+    cudaError_t e = cudaMallocAsync(&scratch, 2 * bytes, (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cuda_fail(e, "cudaMallocAsync(3xTF32 split)", err);
+    }
+    pooled = true;
+    Xa = scratch;
+    Xb = (const uint8_t*)scratch + bytes;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+    const int64_t work = (int64_t)p.K * ((N + 3) / 4);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)sms * 16));
+    split_tf32<<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)X, ldx, (float*)scratch, (float*)Xb, lda,
+                                                        p.K, N);
+    if ((e = cudaGetLastError()) != cudaSuccess) {
+      cudaFreeAsync(scratch, (cudaStream_t)stream);
+      return cuda_fail(e, "3xTF32 split launch", err);
+    }
+  } else if (((uintptr_t)X % 16) != 0 || ((ldx * 2) % 16) != 0) {
     const int rc = launch_repack(p.device, p.K, N, 2, X, ldx, &scratch, &lda, stream, err);
     if (rc != SPARSE_OK) return rc;
     Xa = scratch;
@@ -2830,24 +3080,35 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
     void* b;
     void* st;
     int dev;
+    bool pooled;
     ~Free() {
-      if (b) free_repack(dev, b, st);
+      if (b && pooled) cudaFreeAsync(b, (cudaStream_t)st);
+      else if (b) free_repack(dev, b, st);
     }
-  } fr{scratch, stream, p.device};
-  CUtensorMap tmap;
+  } fr{scratch, stream, p.device, pooled};
+  const int es = tf ? 4 : 2;
+  CUtensorMap tmap, tmap2;
   std::memset(&tmap, 0, sizeof tmap);
+  std::memset(&tmap2, 0, sizeof tmap2);
   cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)p.K};
-  cuuint64_t strides[1] = {(cuuint64_t)(lda * 2)};
-  cuuint32_t box[2] = {64u, 64u};
+  cuuint64_t strides[1] = {(cuuint64_t)(lda * es)};
+  cuuint32_t box[2] = {tf ? 32u : 64u, tf ? 32u : 64u};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(&tmap, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
-                      const_cast<void*>(Xa), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapDataType dt = tf ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                               : bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  // MN-major TF32 operands take the 32-byte-chunk 128-byte swizzle (UMMA layout type 1)
+  const CUtensorMapSwizzle swz = tf ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = encode(&tmap, dt, 2, const_cast<void*>(Xa), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS && tf)
+    r = encode(&tmap2, dt, 2, const_cast<void*>(Xb), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     err = "tcgen05 blocks: cuTensorMapEncodeTiled failed";
     return SPARSE_EINTERNAL;
   }
   TcgArgs a;
+  std::memset(&a, 0, sizeof a);
   a.blocks = p.d_tcp_steps;
   a.meta = p.d_tcp_step_off;
   a.nblk = (int32_t)p.tcp_nsteps;
@@ -2855,32 +3116,20 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   a.ldy = ldy;
   a.N = N;
   a.M = p.M;
-  a.nrb = p.tcp_npanels;
+  a.ngroups = p.tcg_ngroups;
+  a.cs = p.tcg_cs;
   a.stages = p.stages;
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
-  // instruction descriptor (kind::f16): D fp32, A / B fp16 or bf16, A K-major, B MN-major,
+  // instruction descriptor: D fp32, A / B fp16 (0), bf16 (1) or tf32 (2), A K-major, B MN-major,
   // N = 256, M = 128
-  const uint32_t fmt = bf ? 1u : 0u;
+  const uint32_t fmt = tf ? 2u : bf ? 1u : 0u;
   a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
-  const int64_t ntiles = (int64_t)p.tcp_npanels * ((N + 255) / 256);
-  cudaLaunchConfig_t cfg;
-  std::memset(&cfg, 0, sizeof cfg);
-  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, sms)), 1, 1);
-  cfg.blockDim = dim3(192, 1, 1);
-  cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
-  cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
-  if (e != cudaSuccess) return cuda_fail(e, "tcgen05 block launch", err);
-  return SPARSE_OK;
+  const int64_t ntiles = (int64_t)p.tcg_ngroups * ((N + 255) / 256);
+  const void* fn = tf ? (const void*)spmm_tcg_kernel<false, false, true>
+                 : bf ? (const void*)spmm_tcg_kernel<true> : (const void*)spmm_tcg_kernel<false>;
+  return tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "tcgen05 block launch", tf ? 320 : 192);
 }
 
 // Conv on the tcgen05 block executor (conv_kernel 5): the interleaved copies pre-pass (pitch a
@@ -2902,12 +3151,8 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   }
   DeviceGuard dg(p.device);
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
-  using TFn = void (*)(const CUtensorMap, const TcgArgs);
-  TFn fn = bf ? spmm_tcg_kernel<true, true> : spmm_tcg_kernel<false, true>;
-  cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
   void* xp = nullptr;
-  e = cudaMallocAsync(&xp, (size_t)(3 * p.c_in * span * S), (cudaStream_t)stream);
+  cudaError_t e = cudaMallocAsync(&xp, (size_t)(3 * p.c_in * span * S), (cudaStream_t)stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return cuda_fail(e, "cudaMallocAsync(conv copies)", err);
@@ -2946,6 +3191,7 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
     return SPARSE_EINTERNAL;
   }
   TcgArgs a;
+  std::memset(&a, 0, sizeof a);
   a.blocks = p.d_tcp_steps;
   a.meta = p.d_tcp_step_off;
   a.nblk = (int32_t)p.tcp_nsteps;
@@ -2953,7 +3199,8 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   a.ldy = 0;
   a.N = span;
   a.M = p.M;
-  a.nrb = p.tcp_npanels;
+  a.ngroups = p.tcg_ngroups;
+  a.cs = p.tcg_cs;
   a.stages = p.stages;
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
@@ -2968,21 +3215,9 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   a.ncb = p.tcg_ncb;
   a.Bt = (int32_t)batch;
   a.plane = batch * (int64_t)p.h * p.w;
-  const int64_t ntiles = (int64_t)p.tcp_npanels * ((span + 255) / 256);
-  cudaLaunchConfig_t cfg;
-  std::memset(&cfg, 0, sizeof cfg);
-  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, sms)), 1, 1);
-  cfg.blockDim = dim3(192, 1, 1);
-  cfg.dynamicSmemBytes = (size_t)p.smem_bytes;
-  cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
-  if (e != cudaSuccess) return cuda_fail(e, "conv3x3 (tcgen05) launch", err);
-  return SPARSE_OK;
+  const int64_t ntiles = (int64_t)p.tcg_ngroups * ((span + 255) / 256);
+  const void* fn = bf ? (const void*)spmm_tcg_kernel<true, true> : (const void*)spmm_tcg_kernel<false, true>;
+  return tcg_launch(p, fn, tmap, tmap, a, ntiles, stream, err, "conv3x3 (tcgen05) launch");
 }
 
 int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,

@@ -96,6 +96,10 @@ struct Plan {
   // conv on the tcgen05 block executor (executor 4, conv_kernel 5): images per row group of the
   // interleaved copies (pitch tcg_g * w a multiple of 8 elements: 16-byte TMA box starts)
   int32_t tcg_g = 0, tcg_ncb = 0;
+  // tcgen05 block executor: CTAs per cluster (tcg_cs consecutive 128-row blocks = one group
+  // that shares every X tile through TMA multicast; each CTA loads 1 / tcg_cs of it), the
+  // number of groups, and the k-block depth (64 for 16-bit data, 32 for fp32 = 3xTF32)
+  int32_t tcg_cs = 1, tcg_ngroups = 0, tcg_bk = 64;
 
   // packed plan (host copy)
   std::vector<int32_t> row_id;   // npanels * Mp, -1 = empty slot

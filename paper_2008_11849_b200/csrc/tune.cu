@@ -132,12 +132,18 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
     BuildOpts j = base;
     j.executor = 1;
     cands.push_back(j);
-    if (S == 2) {  // tensor cores (fp16 and bf16): condensed panels on mma.sync,
-                   // and W's nonzero 128 x 64 blocks on tcgen05 (TMEM accumulators)
-      BuildOpts t = base;
+    // tensor cores: condensed panels on mma.sync (16-bit), and W's nonzero
+    // 128-row blocks on tcgen05 (TMEM accumulators; fp32 as 3xTF32), alone or in clusters of
+    // 2 / 4 row blocks sharing each X tile by TMA multicast
+    BuildOpts t = base;
+    if (S == 2) {
       t.executor = 3;
       cands.push_back(t);
+    }
+    for (int cs : {1, 2, 4}) {
+      if (cs > 1 && (M + 127) / 128 < cs) continue;
       t.executor = 4;
+      t.cm = cs;
       cands.push_back(t);
     }
   } else {
@@ -157,10 +163,14 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
             cands.push_back(o);
           }
     if (S == 2) {  // 16-bit: implicit im2col on the tcgen05 block executor (conv_kernel 5)
-      BuildOpts o = base;
-      o.conv_vec = 2;
-      o.executor = 4;
-      cands.push_back(o);
+      for (int cs : {1, 2}) {
+        if (cs > 1 && (M + 127) / 128 < cs) continue;
+        BuildOpts o = base;
+        o.conv_vec = 2;
+        o.executor = 4;
+        o.cm = cs;
+        cands.push_back(o);
+      }
     }
   }
   cudaError_t e = cudaSetDevice(device);

@@ -294,7 +294,7 @@ class Plan:
             o.pop("split_k")
             o.pop("stages")
             if i["conv_kernel"] == 5:  # tcgen05 blocks: the tile options are the executor's own
-                o = dict(conv_kernel=5)
+                o = dict(conv_kernel=5, x_multicast=i["x_multicast"])
         return o
 
     def _check_tensor(self, t, name):

@@ -1122,3 +1122,97 @@ def test_conv_tcgen05_exact(cin, cout, B, H, W, p, dt):
     xv = torch.from_numpy(xr).to(tdt).double().numpy()
     err = oracle.rel_l2(y.double().cpu().numpy(), oracle.conv3x3(cout, w.row_ptr, w.col_idx, wv, xv))
     assert err <= F16_TOL, err
+
+
+# ------------------------------------------- tcgen05 blocks: multicast clusters, fp32 as 3xTF32
+
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32"])
+@pytest.mark.parametrize("cs", [1, 2, 4])
+@pytest.mark.parametrize("M,K,N,p", [(3072, 768, 2048, 90), (768, 3072, 512, 95), (300, 200, 517, 80),
+                                      (77, 1111, 300, 98), (640, 512, 392, 90), (16, 64, 4099, 90)])
+def test_tcgen05_clusters_and_tf32_exact(M, K, N, p, cs, dt):
+    # executor 4 with x_multicast = cs (row blocks of a cluster share every X tile; a group walks
+    # the union of its row blocks' k-blocks, zero blocks where a row block lacks one) and fp32
+    # plans as 3xTF32: BITWISE on integer data (|w| <= 2, |x| <= 4 are exact TF32 values, the
+    # low halves are 0 and every partial sum is an exact integer < 2^24)
+    dev = _dev()
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}[dt]
+    wi = gen.int_weights(M, K, p, seed=M + K + N + cs, vmax=2)
+    xi = gen.int_x(K, N, seed=N + cs, vmax=4)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, executor=4, x_multicast=cs)
+    assert plan.info["executor"] == 4 and plan.info["x_multicast"] == cs
+    Y = torch.full((M, N), float("nan"), dtype=tdt, device=dev)
+    plan.spmm(torch.from_numpy(xi).to(dev).to(tdt), Y)
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), xi.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(Y.double().cpu().numpy(), ref)
+    # the replica rebuilt from chosen_opts has the same digest (cluster size in the digest)
+    again = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, **plan.chosen_opts())
+    assert again.info["digest"] == plan.info["digest"]
+
+
+@pytest.mark.parametrize("cs", [1, 2, 4])
+@pytest.mark.parametrize("M,K,N,p", [(3072, 768, 2048, 90), (768, 3072, 1000, 90), (300, 200, 517, 80),
+                                      (512, 2048, 392, 95), (77, 1111, 300, 98), (128, 64, 49, 90)])
+def test_tcgen05_tf32x3_rel_l2(M, K, N, p, cs):
+    # fp32 on the tensor cores: 3xTF32 (W_hi X_hi + W_lo X_hi + W_hi X_lo) must meet the fp32
+    # bar of the north star (rel-L2 <= 1e-5) on real-valued data; one TF32 product alone would
+    # not (~1e-4)
+    dev = _dev()
+    w = gen.pruned_weights(M, K, p, seed=M * 3 + K + cs)
+    x = gen.uniform_x(K, N, seed=N + 7)
+    plan = srt.Plan.from_csr(w, dtype=torch.float32, n_hint=N, executor=4, x_multicast=cs)
+    Y = plan.spmm(torch.from_numpy(x).to(dev))
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), x.astype(np.float64))
+    err = oracle.rel_l2(Y.double().cpu().numpy(), ref)
+    assert err <= F32_TOL, err
+
+
+def test_tcgen05_tf32x3_epilogue_ld_unaligned():
+    # fp32 / 3xTF32: empty 128-row block (-> +0), X with an odd row stride (not 16-byte
+    # aligned: the on-device split handles any ldx), ldy > N, fused bias + beta + ReLU
+    dev = _dev()
+    M, K, N = 400, 192, 301
+    base = gen.int_weights(M, K, 90, seed=14, vmax=3)
+    dense = gen.to_dense(base)
+    dense[128:256] = 0.0
+    keep = np.flatnonzero(dense)
+    w = gen.csr_from_mask(M, K, keep, dense.astype(np.float32))
+    xi = gen.int_x(K, N, seed=15, vmax=3)
+    rng = np.random.default_rng(16)
+    bias = rng.integers(-8, 9, M).astype(np.float32)
+    y0 = rng.integers(-8, 9, (M, N)).astype(np.float32)
+    for cs in (1, 2, 4):
+        plan = srt.Plan.from_csr(w, dtype=torch.float32, n_hint=N, executor=4, x_multicast=cs)
+        Xb = torch.zeros((K, N + 3), dtype=torch.float32, device=dev)
+        Xb[:, :N] = torch.from_numpy(xi).to(dev)
+        Yb = torch.zeros((M, N + 24), dtype=torch.float32, device=dev)
+        Yb[:, :N] = torch.from_numpy(y0).to(dev)
+        plan.spmm(Xb[:, :N], Yb[:, :N], bias=torch.from_numpy(bias).to(dev), beta=0.5, relu=True)
+        torch.cuda.synchronize()
+        ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), xi.astype(np.float64))
+        ref = np.maximum(ref + bias[:, None] + 0.5 * y0, 0.0)
+        assert np.array_equal(Yb[:, :N].double().cpu().numpy(), ref.astype(np.float32).astype(np.float64))
+        assert torch.count_nonzero(Yb[:, N:]) == 0
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("cin,cout,B,H,W,p", [(256, 256, 6, 14, 14, 90), (128, 384, 3, 28, 28, 95),
+                                              (40, 200, 5, 10, 6, 80)])
+def test_conv_tcgen05_cluster_exact(cin, cout, B, H, W, p, dt):
+    # conv_kernel 5 with the two (or more) 128-channel row blocks in one multicast cluster
+    dev = _dev()
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float16
+    wi = gen.int_weights(cout, 9 * cin, p, seed=cin + H + 1, vmax=2)
+    x = gen.int_x(cin * B * H, W, seed=cout + 1, vmax=4).reshape(cin, B, H, W)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, conv_kernel=5,
+                             x_multicast=2)
+    assert plan.info["conv_kernel"] == 5 and plan.info["x_multicast"] == 2
+    y = torch.full((cout, B, H, W), float("nan"), dtype=tdt, device=dev)
+    plan.conv3x3(torch.from_numpy(x).to(dev).to(tdt), y)
+    torch.cuda.synchronize()
+    ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), x.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(y.double().cpu().numpy(), ref)
