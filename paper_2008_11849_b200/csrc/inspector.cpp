@@ -961,7 +961,8 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // stage = the W block(s) + a 256-column X tile (fp32: X_hi and X_lo): 48 KB / 96 KB
     const int st_bytes = f32 ? 96 * 1024 : 48 * 1024;
     p.stages = f32 ? 2 : 4;
-    p.smem_bytes = p.stages * st_bytes + 1024 + 2048 + 8192;  // + align, barriers, conv table, block lists
+    // + align, barriers, conv table, block lists, the epilogue warps' store staging (16 KB)
+    p.smem_bytes = p.stages * st_bytes + 1024 + 2048 + 8192 + 16384;
     p.plan_bytes += (int64_t)p.tcp_steps.size() + (int64_t)p.tcp_step_off.size() * 4;
   } else if (o.executor == 3) {
     // ---- condensed-panel tensor-core executor (fp16 SpMM) ----

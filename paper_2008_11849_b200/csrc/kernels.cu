@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <cstdio>
 #include <mutex>
 #include <set>
@@ -2587,6 +2589,7 @@ struct TcgArgs {
   uint8_t* Y;
   int64_t ldy, N;            // conv: N = the span of the interleaved copies (positions incl. halo)
   int32_t M, ngroups, cs, stages;
+  int32_t dbg;               // diagnostics only (SRT_TCG_DBG): 1 = skip the Y stores, 2 = skip the MMAs
   const uint8_t* bias;
   float beta;
   int32_t relu;
@@ -2627,6 +2630,25 @@ __device__ __forceinline__ void tm_commit_mc(uint32_t bar, uint16_t mask) {
           bar),
       "h"(mask)
       : "memory");
+}
+// tcgen05.ld 32x32b.x32: this warp's 32 TMEM lanes x 32 consecutive columns (no wait)
+__device__ __forceinline__ void tm_ld32(uint32_t ta, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(ta));
+}
+__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(ta));
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint32_t bar, uint16_t mask, bool mc) {
@@ -2777,6 +2799,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
               //    8-row atoms (SBO 1 KB), K16 step = +2 KB; TF32: 32-byte-chunk swizzle, 4-row
               //    atoms (SBO 512 B), K8 step = +1 KB
               const uint32_t en = (j > jc || k > 0) ? 1u : 0u;
+              if (a.dbg & 2) continue;
               constexpr uint32_t B_SBO = TF ? 512u : 1024u, B_LAYOUT = TF ? 1u : 2u;
               const uint64_t da = umma_desc_sw128(sa + 32u * k, 16u, 1024u);
               const uint64_t db = umma_desc_sw128(sb + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
@@ -2810,6 +2833,9 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     int acc = 0;
     uint32_t aph[2] = {0u, 0u};
     const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
+    // per-warp staging buffer (32 rows x 64 B) for coalesced Y stores
+    uint8_t* stg = (uint8_t*)tslot + 64 + 1024 + 4 * kTcgMetaMax + (warp - 2) * 2048;
+    const bool coal = ((a.ldy * 4) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
     for (int64_t t = cl; t < ntiles; t += ncl) {
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
@@ -2824,20 +2850,12 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         tm_fence_after();
         if (nent > 0) {
 #pragma unroll
-          for (int c0 = 0; c0 < 128; c0 += 32) {
-            uint32_t v[32];
-            const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + hc + c0);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-                "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-                  "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-                  "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                : "r"(ta));
+          for (int c0 = 0; c0 < 128; c0 += 16) {
+            uint32_t v[16];
+            tm_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + hc + c0), v);
             tm_wait_ld();
 #pragma unroll
-            for (int c = 0; c < 32; ++c) m[c0 + c] = __fadd_rn(m[c0 + c], __uint_as_float(v[c]));
+            for (int c = 0; c < 16; ++c) m[c0 + c] = __fadd_rn(m[c0 + c], __uint_as_float(v[c]));
           }
         }
         tm_fence_before();
@@ -2846,26 +2864,38 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         aph[acc] ^= 1u;
         acc ^= 1;
       }
-      const int row = rb * 128 + q * 32 + lane;
+      const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)min((int64_t)BN, a.N - n0);
-      if (row >= a.M) continue;
+      if (row0 >= a.M || (a.dbg & 1)) continue;
+      if (epi) {
 #pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+        for (int c = 0; c < 128; ++c)
+          if (row < a.M && hc + c < ncol)
+            m[c] = epilogue_one<false>(m[c], a.bias, row, a.beta, a.Y + ((int64_t)row * a.ldy + n0 + hc + c) * 4, a.relu);
+      }
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 16) {
         if (hc + c0 >= ncol) break;
-        uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + hc + c0) * 4;
-        if (epi) {
+        if (coal && hc + c0 + 16 <= ncol) {
+          // 16 fp32 of the row -> staging (16-byte chunks XOR-swizzled by row), then each store
+          // instruction writes eight whole 64-byte row segments
+          __syncwarp();
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (hc + c0 + c < ncol) m[c0 + c] = epilogue_one<false>(m[c0 + c], a.bias, row, a.beta, yp + c * 4, a.relu);
-        }
-        if (hc + c0 + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
+          for (int j = 0; j < 4; ++j)
+            *(float4*)(stg + lane * 64 + ((j ^ (lane & 3)) * 16)) =
+                make_float4(m[c0 + 4 * j], m[c0 + 4 * j + 1], m[c0 + 4 * j + 2], m[c0 + 4 * j + 3]);
+          __syncwarp();
 #pragma unroll
-          for (int c = 0; c < 32; c += 4)
-            *(float4*)(yp + c * 4) = make_float4(m[c0 + c], m[c0 + c + 1], m[c0 + c + 2], m[c0 + c + 3]);
-        } else {
+          for (int i = 0; i < 4; ++i) {
+            const int r = i * 8 + (lane >> 2), j = lane & 3;
+            const float4 d4 = *(const float4*)(stg + r * 64 + ((j ^ (r & 3)) * 16));
+            if (row0 + r < a.M) *(float4*)(a.Y + ((int64_t)(row0 + r) * a.ldy + n0 + hc + c0) * 4 + j * 16) = d4;
+          }
+        } else if (row < a.M) {
+          float* yp = (float*)(a.Y + ((int64_t)row * a.ldy + n0 + hc + c0) * 4);
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (hc + c0 + c < ncol) ((float*)yp)[c] = m[c0 + c];
+          for (int c = 0; c < 16; ++c)
+            if (hc + c0 + c < ncol) yp[c] = m[c0 + c];
         }
       }
     }
@@ -2877,6 +2907,9 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
     int32_t* otab = (int32_t*)((uint8_t*)tslot + 64);  // conv: span position -> output offset
     int64_t tab_n0 = -1;
+    // per-warp staging buffer (32 rows x 128 B) for coalesced Y stores
+    uint8_t* stg = (uint8_t*)tslot + 64 + 1024 + 4 * kTcgMetaMax + (warp - 2) * 4096;
+    const bool coal = a.beta == 0.0f && ((a.ldy * 2) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
     for (int64_t t = cl; t < ntiles; t += ncl) {
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
@@ -2898,49 +2931,106 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       }
       mbar_wait(tfull0 + 8 * acc, aph[acc]);
       tm_fence_after();
-      const int row = rb * 128 + q * 32 + lane;
+      const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)min((int64_t)BN, a.N - n0);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
+      for (int c0 = 0; c0 < BN; c0 += 64) {
+        uint32_t v[64];
         const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(ta));
+        tm_ld32(ta, v);
+        tm_ld32(ta + 32, v + 32);
         tm_wait_ld();
         if constexpr (CONV) {
-          if (row >= a.M) continue;
+          if (a.beta != 0.0f) {  // beta * Y_old: element-wise (the fp32 sum needs Y_old)
+            if (row >= a.M) continue;
+            for (int c = 0; c < 64; ++c) {
+              const int32_t o = otab[c0 + c];
+              if (o < 0) continue;
+              uint8_t* yp = a.Y + ((int64_t)row * a.plane + o) * 2;
+              const float f = epilogue_one<true, BF>(has ? __uint_as_float(v[c]) : 0.0f, a.bias, row, a.beta, yp, a.relu);
+              *(uint16_t*)yp = to16<BF>(f);
+            }
+            continue;
+          }
+          // rows' values through the staging buffer, then one output row per store instruction
+          // (the lanes write 32 consecutive span positions: contiguous runs of the CNHW plane)
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int32_t o = otab[c0 + c];
-            if (o < 0) continue;
-            uint8_t* yp = a.Y + ((int64_t)row * a.plane + o) * 2;
-            float f = has ? __uint_as_float(v[c]) : 0.0f;
-            if (epi) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp, a.relu);
-            *(uint16_t*)yp = to16<BF>(f);
+          for (int h = 0; h < 2; ++h) {
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t w4[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float f0 = has ? __uint_as_float(v[32 * h + 8 * j + 2 * e]) : 0.0f;
+                float f1 = has ? __uint_as_float(v[32 * h + 8 * j + 2 * e + 1]) : 0.0f;
+                if (epi) {
+                  f0 = epilogue_one<true, BF>(f0, a.bias, row, 0.0f, nullptr, a.relu);
+                  f1 = epilogue_one<true, BF>(f1, a.bias, row, 0.0f, nullptr, a.relu);
+                }
+                w4[e] = (uint32_t)to16<BF>(f0) | ((uint32_t)to16<BF>(f1) << 16);
+              }
+              *(uint4*)(stg + lane * 64 + ((j ^ (lane & 3)) * 16)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            }
+            __syncwarp();
+            const int32_t o = otab[c0 + 32 * h + lane];
+            if (o >= 0) {
+              const int j = lane >> 3;
+              for (int r = 0; r < 32 && row0 + r < a.M; ++r) {
+                const uint16_t hv = *(const uint16_t*)(stg + r * 64 + ((j ^ (r & 3)) * 16) + (lane & 7) * 2);
+                *(uint16_t*)(a.Y + ((int64_t)(row0 + r) * a.plane + o) * 2) = hv;
+              }
+            }
           }
           continue;
         }
-        if (row >= a.M || c0 >= ncol) continue;
-        uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + c0) * 2;
-        {
-          alignas(16) uint16_t h[32];
+        if (row0 >= a.M || c0 >= ncol) continue;
+        if (coal && c0 + 64 <= ncol) {
+          // 16-bit row of 64 values -> staging (16-byte chunks XOR-swizzled by row), then each
+          // store instruction writes four whole 128-byte row segments (coalesced)
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float f0 = has ? __uint_as_float(v[8 * j + 2 * e]) : 0.0f;
+              float f1 = has ? __uint_as_float(v[8 * j + 2 * e + 1]) : 0.0f;
+              if (epi) {
+                f0 = epilogue_one<true, BF>(f0, a.bias, row, 0.0f, nullptr, a.relu);
+                f1 = epilogue_one<true, BF>(f1, a.bias, row, 0.0f, nullptr, a.relu);
+              }
+              w4[e] = (uint32_t)to16<BF>(f0) | ((uint32_t)to16<BF>(f1) << 16);
+            }
+            *(uint4*)(stg + lane * 128 + ((j ^ (lane & 7)) * 16)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + (lane >> 3), j = lane & 7;
+            const uint4 d4 = *(const uint4*)(stg + r * 128 + ((j ^ (r & 7)) * 16));
+            if (row0 + r < a.M) *(uint4*)(a.Y + ((int64_t)(row0 + r) * a.ldy + n0 + c0) * 2 + j * 16) = d4;
+          }
+          continue;
+        }
+        if (row >= a.M) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = c0 + 32 * h;
+          if (cc >= ncol) break;
+          uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + cc) * 2;
+          alignas(16) uint16_t hv[32];
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
-            float f = has ? __uint_as_float(v[c]) : 0.0f;
-            if (epi && c0 + c < ncol) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp + c * 2, a.relu);
-            h[c] = to16<BF>(f);
+            float f = has ? __uint_as_float(v[32 * h + c]) : 0.0f;
+            if (epi && cc + c < ncol) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp + c * 2, a.relu);
+            hv[c] = to16<BF>(f);
           }
-          if (c0 + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
+          if (cc + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
 #pragma unroll
-            for (int c = 0; c < 32; c += 8) *(uint4*)(yp + c * 2) = *(const uint4*)(h + c);
+            for (int c = 0; c < 32; c += 8) *(uint4*)(yp + c * 2) = *(const uint4*)(hv + c);
           } else {
-            for (int c = 0; c < 32 && c0 + c < ncol; ++c) ((uint16_t*)yp)[c] = h[c];
+            for (int c = 0; c < 32 && cc + c < ncol; ++c) ((uint16_t*)yp)[c] = hv[c];
           }
         }
       }
@@ -3119,6 +3209,7 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   a.ngroups = p.tcg_ngroups;
   a.cs = p.tcg_cs;
   a.stages = p.stages;
+  if (const char* dbg = std::getenv("SRT_TCG_DBG")) a.dbg = std::atoi(dbg);
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
@@ -3202,6 +3293,7 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   a.ngroups = p.tcg_ngroups;
   a.cs = p.tcg_cs;
   a.stages = p.stages;
+  if (const char* dbg = std::getenv("SRT_TCG_DBG")) a.dbg = std::atoi(dbg);
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
