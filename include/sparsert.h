@@ -132,9 +132,10 @@ typedef struct {
                             g images side by side per row so that no output position is padding
                             (copies from a pre-pass, one TMA span box per copy and chunk; images
                             up to ~28 wide).  All result-identical.  5 = the tcgen05 block
-                            executor (executor 4; fp16 / bf16 plans): implicit im2col over
-                            interleaved dx-shifted copies, k-blocks = (tap, 64 channels);
-                            summation order of the tensor cores (exact on integer data). */
+                            executor (executor 4): implicit im2col over interleaved dx-shifted
+                            copies, k-blocks = (tap, 64 channels; fp32: 32 channels as 3xTF32,
+                            the pre-pass writes the copies split into TF32 halves); summation
+                            order of the tensor cores (within tolerance; exact on integer data). */
   int32_t row_order;     /* 0 = load-balanced panels (rows sorted by nnz, LPT-binned, P:163-165;
                             default); 1 = natural contiguous row ranges (the "no load balancing"
                             ablation of P:385).  Result-neutral for split_k = k_split = 1. */
@@ -268,7 +269,8 @@ typedef struct {
   uint64_t digest;      /* FNV-1a of the packed plan: equal digests <=> identical replicas */
   int32_t x_multicast;  /* CTAs per cluster sharing X tiles (TMA multicast) */
   int32_t x_source;     /* 0 shared memory, 1 tensor memory */
-  int32_t conv_kernel;  /* conv: 1 position-strided, 2 TMA-fed vectorised, 3 register-staged vectorised */
+  int32_t conv_kernel;  /* conv: 1 position-strided, 2 TMA-fed vectorised, 3 register-staged vectorised,
+                           4 image-interleaved, 5 tcgen05 blocks */
   int32_t row_order;    /* 0 LPT panels, 1 natural order */
   int32_t tc_min_density; /* effective threshold (%), 0 = no tensor-core sub-blocks */
   int32_t tc_row_blocks;  /* 16-row blocks with >= 1 dense tile */

@@ -891,16 +891,13 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     // then rank (entry j of the group list, rank r at (j * tcg_cs + r)).
     const bool conv = o.kind == SPARSE_CONV3X3;
     const bool f32 = dtype == SPARSE_F32;
-    if (f32 && conv) {
-      err = "conv_kernel = 5 (tcgen05 blocks) needs an fp16 or bf16 plan";
-      return SPARSE_EUNSUPPORTED;
-    }
     const int BM = 128, BK = f32 ? 32 : 64, S = f32 ? 4 : 2;
     const int CS = p.tcg_cs;
     p.tcg_bk = BK;
     // conv: implicit im2col over the interleaved dx-shifted copies (kernel 3b layout); the K
-    // axis is ordered tap-major, k-block = (tap, 64 input channels), so the B tile of a k-block
-    // is one 2-D slab of copy dx shifted by (dy - 1) pitches
+    // axis is ordered tap-major, k-block = (tap, BK input channels), so the B tile of a k-block
+    // is one 2-D slab of copy dx shifted by (dy - 1) pitches (fp32: slabs of the X_hi and the
+    // X_lo copies, which the pre-pass writes split)
     int32_t ncb = 0;
     if (conv) {
       ncb = (o.c_in + BK - 1) / BK;

@@ -1652,6 +1652,14 @@ __device__ __forceinline__ int div_rcp(int a, int b, float rb) {
   return q;
 }
 
+// fp32 -> nearest TF32 value (round to nearest even on the 13 dropped mantissa bits), in an fp32
+// container (finite inputs; 3xTF32 operand splits)
+__device__ __forceinline__ float tf32_rn_dev(float f) {
+  uint32_t u = __float_as_uint(f);
+  u += 0xfffu + ((u >> 13) & 1u);
+  return __uint_as_float(u & 0xffffe000u);
+}
+
 // Shared-memory staging of `count` contiguous elements (16-byte vectors when the source and the
 // count allow it, 4 in flight per thread), zero-filled past `valid`.
 template <typename T>
@@ -1684,7 +1692,7 @@ __device__ __forceinline__ void stage_contig(T* dst, const T* __restrict__ src, 
 template <typename T>
 __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* __restrict__ xp, int cin, int B,
                                                     int H, int W, int g, int ngroups, int Sg, int pp,
-                                                    uint32_t* ready) {
+                                                    uint32_t* ready, T* __restrict__ xlo = nullptr) {
   extern __shared__ __align__(16) uint8_t il_smem[];
   T* sp = (T*)il_smem;  // [pp][g][H][W]
   const int HW = H * W, P = g * W, blk = g * HW;
@@ -1769,11 +1777,23 @@ __global__ void __launch_bounds__(256) il_pad_input(const T* __restrict__ x, T* 
           v[c] = (r >= 1 && r <= H && xs >= 0 && xs < W) ? sb[j * HW + xs] : T(0);
           if (++xw == W) xw = 0, ++j;
         }
-        T* dst = xp + ((int64_t)dx * cin + ci) * span + (int64_t)q * Sg + e0;
-        if (sizeof(T) == 4)
-          *(uint4*)dst = *(const uint4*)v;
-        else
-          *(uint2*)dst = *(const uint2*)v;
+        const int64_t di = ((int64_t)dx * cin + ci) * span + (int64_t)q * Sg + e0;
+        if constexpr (sizeof(T) == 4) {
+          if (xlo) {  // 3xTF32 operand split (conv on the tcgen05 block executor): v = hi + lo
+            float h[4], l[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              h[c] = tf32_rn_dev(v[c]);
+              l[c] = isfinite(h[c]) ? tf32_rn_dev(v[c] - h[c]) : 0.0f;
+            }
+            *(float4*)(xp + di) = make_float4(h[0], h[1], h[2], h[3]);
+            *(float4*)(xlo + di) = make_float4(l[0], l[1], l[2], l[3]);
+          } else {
+            *(uint4*)(xp + di) = *(const uint4*)v;
+          }
+        } else {
+          *(uint2*)(xp + di) = *(const uint2*)v;
+        }
       }
     }
     if (ready) __threadfence();  // this thread's copies visible at device scope
@@ -2666,6 +2686,22 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
+// conv epilogue: the NT epilogue threads (tid 0 .. NT - 1) decode the tile's 256 span positions
+// once (named barrier among the epilogue warps only): s -> group q, row r, column (image j, x)
+// -> the CNHW offset of the output pixel, -1 for halo rows, padding images and past the span
+template <int NT>
+__device__ __forceinline__ void tcg_conv_table(int32_t* otab, int64_t n0, const TcgArgs& a, int tid) {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");  // the previous tile's readers are done
+  for (int c = tid; c < 256; c += NT) {
+    const int64_t sp = n0 + c;
+    const int64_t gq = sp / a.Sg;
+    const int rem = (int)(sp - gq * a.Sg), r = rem / a.P, xx = rem - r * a.P, jj = xx / a.W;
+    const int64_t b = gq * a.g + jj;
+    otab[c] = (sp < a.N && r >= 1 && r <= a.H && b < a.Bt) ? (int32_t)((b * a.H + (r - 1)) * a.W + (xx - jj * a.W)) : -1;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
 // TF = fp32 plan as 3xTF32.  Per stage (k-block):
 //   16-bit: A = one 128 x 64 W block (16 KB), B = 64 k x 256 columns of X as 4 boxes of 64
 //           columns (8 KB each); 4 x tcgen05.mma kind::f16 K16
@@ -2753,10 +2789,12 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
           for (int qq = 0; qq < nb; ++qq) {
             const int q = (int)rank * nb + qq;
             const uint32_t dst = smem_u32(st + A_BYTES + q * BOX_BYTES);
-            if (CONV) {  // k-block (tap, 64 channels): copy dx, shifted by (dy - 1) pitches
+            if (CONV) {  // k-block (tap, 64 / 32 channels): copy dx, shifted by (dy - 1) pitches
               const int tap = kb / a.ncb, cb = kb - tap * a.ncb;
               const int s0 = (int)n0 + (tap / 3 - 1) * a.P;
-              tma_load_3d(dst, &tmap, s0 + BOX_COLS * q, cb * 64, tap % 3, fb, mask, CS > 1);
+              tma_load_3d(dst, &tmap, s0 + BOX_COLS * q, cb * (TF ? 32 : 64), tap % 3, fb, mask, CS > 1);
+              if (TF)  // the X_lo copies
+                tma_load_3d(dst + B_HALF, &tmap2, s0 + BOX_COLS * q, cb * 32, tap % 3, fb, mask, CS > 1);
             } else {
               const int c0 = (int)(n0 + BOX_COLS * q), c1 = kb * (TF ? 32 : 64);
               if (CS > 1) tma_load_2d_mc(dst, &tmap, c0, c1, fb, mask);
@@ -2836,11 +2874,17 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     // per-warp staging buffer (32 rows x 64 B) for coalesced Y stores
     uint8_t* stg = (uint8_t*)tslot + 64 + 1024 + 4 * kTcgMetaMax + (warp - 2) * 2048;
     const bool coal = ((a.ldy * 4) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
+    int32_t* otab = (int32_t*)((uint8_t*)tslot + 64);  // conv: span position -> output offset
+    int64_t tab_n0 = -1;
     for (int64_t t = cl; t < ntiles; t += ncl) {
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
       const int64_t n0 = (t / a.ngroups) * BN;
       const int nent = meta[gi + 1] - meta[gi];
+      if (CONV && n0 != tab_n0) {
+        tcg_conv_table<32 * NEPI>(otab, n0, a, threadIdx.x - 64);
+        tab_n0 = n0;
+      }
       const int nch = nent > 0 ? (nent + FLUSH - 1) / FLUSH : 1;
       float m[128];
 #pragma unroll
@@ -2867,6 +2911,40 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)min((int64_t)BN, a.N - n0);
       if (row0 >= a.M || (a.dbg & 1)) continue;
+      if constexpr (CONV) {
+        // span positions -> CNHW pixels (otab; -1 = halo / padding / past the span)
+        if (epi) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            const int32_t o = otab[hc + c];
+            if (row < a.M && o >= 0)
+              m[c] = epilogue_one<false>(m[c], a.bias, row, a.beta, a.Y + ((int64_t)row * a.plane + o) * 4, a.relu);
+          }
+        }
+        // 16 positions of the warp's 32 rows through the staging buffer, then each store
+        // instruction writes 16 consecutive span positions of two output rows
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *(float4*)(stg + lane * 64 + ((j ^ (lane & 3)) * 16)) =
+                make_float4(m[c0 + 4 * j], m[c0 + 4 * j + 1], m[c0 + 4 * j + 2], m[c0 + 4 * j + 3]);
+          __syncwarp();
+          const int c = lane & 15;
+          const int32_t o = otab[hc + c0 + c];
+          if (o >= 0) {
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+              const int r = 2 * i + (lane >> 4);
+              if (row0 + r >= a.M) break;
+              const float v = *(const float*)(stg + r * 64 + (((c >> 2) ^ (r & 3)) * 16) + (c & 3) * 4);
+              *(float*)(a.Y + ((int64_t)(row0 + r) * a.plane + o) * 4) = v;
+            }
+          }
+        }
+        continue;
+      }
       if (epi) {
 #pragma unroll
         for (int c = 0; c < 128; ++c)
@@ -2916,17 +2994,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int64_t n0 = (t / a.ngroups) * BN;
       const bool has = meta[gi + 1] > meta[gi];
       if (CONV && n0 != tab_n0) {
-        // the 128 epilogue threads decode the tile's 256 span positions once (named barrier
-        // among the epilogue warps only): s -> group q, row r, column (image j, x)
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's readers are done
-        for (int c = threadIdx.x - 64; c < BN; c += 128) {
-          const int64_t sp = n0 + c;
-          const int64_t gq = sp / a.Sg;
-          const int rem = (int)(sp - gq * a.Sg), r = rem / a.P, xx = rem - r * a.P, jj = xx / a.W;
-          const int64_t b = gq * a.g + jj;
-          otab[c] = (sp < a.N && r >= 1 && r <= a.H && b < a.Bt) ? (int32_t)((b * a.H + (r - 1)) * a.W + (xx - jj * a.W)) : -1;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        tcg_conv_table<128>(otab, n0, a, threadIdx.x - 64);
         tab_n0 = n0;
       }
       mbar_wait(tfull0 + 8 * acc, aph[acc]);
@@ -3050,11 +3118,6 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
 // 3xTF32 operand split of X (fp32 plans on the tcgen05 block executor): X = X_hi + X_lo with
 // X_hi = TF32 RN of X and X_lo = TF32 RN of the (exact) remainder, written to two K x ldp
 // scratch matrices (ldp a multiple of 4: 16-byte TMA row strides).  Non-finite X: X_lo = 0.
-__device__ __forceinline__ float tf32_rn_dev(float f) {
-  uint32_t u = __float_as_uint(f);
-  u += 0xfffu + ((u >> 13) & 1u);
-  return __uint_as_float(u & 0xffffe000u);
-}
 __global__ void __launch_bounds__(256) split_tf32(const float* __restrict__ X, int64_t ldx, float* __restrict__ hi,
                                                   float* __restrict__ lo, int64_t ldp, int64_t K, int64_t N) {
   const int64_t n4 = (N + 3) / 4, total = K * n4;
@@ -3227,8 +3290,8 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
 // multiple of 8 elements), then spmm_tcg_kernel<CONV> over the span of the copies.
 static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y, void* stream, std::string& err,
                            const Epilogue& ep) {
-  const bool bf = p.dtype == SPARSE_BF16;
-  const int S = 2;
+  const bool bf = p.dtype == SPARSE_BF16, tf = p.dtype == SPARSE_F32;
+  const int S = tf ? 4 : 2;
   auto encode = tensor_map_encoder();
   if (!encode) {
     err = "internal: no tensor-map encoder";
@@ -3242,8 +3305,9 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   }
   DeviceGuard dg(p.device);
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
-  void* xp = nullptr;
-  cudaError_t e = cudaMallocAsync(&xp, (size_t)(3 * p.c_in * span * S), (cudaStream_t)stream);
+  void* xp = nullptr;  // the copies (3xTF32: the X_hi copies, then the X_lo copies)
+  const size_t cbytes = (size_t)3 * p.c_in * span * S;
+  cudaError_t e = cudaMallocAsync(&xp, tf ? 2 * cbytes : cbytes, (cudaStream_t)stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return cuda_fail(e, "cudaMallocAsync(conv copies)", err);
@@ -3261,22 +3325,38 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
     const size_t psm = (size_t)pp * blk * S;
     const int64_t nblk = (int64_t)p.c_in * ngroups;
     const unsigned pg = (unsigned)std::min<int64_t>((nblk + pp - 1) / pp, (int64_t)sms * 8);
-    if ((e = ensure_smem_attr(il_pad_input<uint16_t>, (int)psm)) != cudaSuccess)
-      return cuda_fail(e, "cudaFuncSetAttribute(il pad)", err);
-    il_pad_input<uint16_t><<<pg, 256, psm, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, p.c_in,
-                                                                   (int)batch, p.h, p.w, g, (int)ngroups, Sg, pp,
-                                                                   nullptr);
+    if (tf) {
+      if ((e = ensure_smem_attr(il_pad_input<float>, (int)psm)) != cudaSuccess)
+        return cuda_fail(e, "cudaFuncSetAttribute(il pad)", err);
+      il_pad_input<float><<<pg, 256, psm, (cudaStream_t)stream>>>((const float*)x, (float*)xp, p.c_in, (int)batch,
+                                                                  p.h, p.w, g, (int)ngroups, Sg, pp, nullptr,
+                                                                  (float*)((uint8_t*)xp + cbytes));
+    } else {
+      if ((e = ensure_smem_attr(il_pad_input<uint16_t>, (int)psm)) != cudaSuccess)
+        return cuda_fail(e, "cudaFuncSetAttribute(il pad)", err);
+      il_pad_input<uint16_t><<<pg, 256, psm, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xp, p.c_in,
+                                                                     (int)batch, p.h, p.w, g, (int)ngroups, Sg,
+                                                                     pp, nullptr);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "il pad launch", err);
   }
-  CUtensorMap tmap;
+  CUtensorMap tmap, tmap2;
   std::memset(&tmap, 0, sizeof tmap);
+  std::memset(&tmap2, 0, sizeof tmap2);
   cuuint64_t dims[3] = {(cuuint64_t)span, (cuuint64_t)p.c_in, 3};
   cuuint64_t strides[2] = {(cuuint64_t)(span * S), (cuuint64_t)(span * S * p.c_in)};
-  cuuint32_t box[3] = {64u, 64u, 1u};
+  // 16-bit: 64 positions x 64 channels, 128-byte swizzle; 3xTF32: 32 x 32 fp32, 32-byte-chunk
+  // 128-byte swizzle (the MN-major TF32 operand layout, as the SpMM form)
+  cuuint32_t box[3] = {tf ? 32u : 64u, tf ? 32u : 64u, 1u};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = encode(&tmap, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, xp, dims,
-                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  const CUtensorMapDataType dt = tf ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                               : bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUtensorMapSwizzle swz = tf ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = encode(&tmap, dt, 3, xp, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS && tf)
+    r = encode(&tmap2, dt, 3, (uint8_t*)xp + cbytes, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     err = "conv (tcgen05): cuTensorMapEncodeTiled failed";
     return SPARSE_EINTERNAL;
@@ -3297,7 +3377,7 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   a.bias = (const uint8_t*)ep.bias;
   a.beta = ep.beta;
   a.relu = ep.relu;
-  const uint32_t fmt = bf ? 1u : 0u;
+  const uint32_t fmt = tf ? 2u : bf ? 1u : 0u;
   a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
   a.P = P;
   a.g = g;
@@ -3308,8 +3388,9 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   a.Bt = (int32_t)batch;
   a.plane = batch * (int64_t)p.h * p.w;
   const int64_t ntiles = (int64_t)p.tcg_ngroups * ((span + 255) / 256);
-  const void* fn = bf ? (const void*)spmm_tcg_kernel<true, true> : (const void*)spmm_tcg_kernel<false, true>;
-  return tcg_launch(p, fn, tmap, tmap, a, ntiles, stream, err, "conv3x3 (tcgen05) launch");
+  const void* fn = tf ? (const void*)spmm_tcg_kernel<false, true, true>
+                 : bf ? (const void*)spmm_tcg_kernel<true, true> : (const void*)spmm_tcg_kernel<false, true>;
+  return tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "conv3x3 (tcgen05) launch", tf ? 320 : 192);
 }
 
 int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,

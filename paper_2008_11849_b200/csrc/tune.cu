@@ -162,7 +162,7 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
             o.conv_vec = vec;
             cands.push_back(o);
           }
-    if (S == 2) {  // 16-bit: implicit im2col on the tcgen05 block executor (conv_kernel 5)
+    {  // implicit im2col on the tcgen05 block executor (conv_kernel 5; fp32 as 3xTF32)
       for (int cs : {1, 2}) {
         if (cs > 1 && (M + 127) / 128 < cs) continue;
         BuildOpts o = base;

@@ -593,7 +593,7 @@ def test_spmm_epilogue_exact(opts, f16):
 
 
 @pytest.mark.parametrize("f16", [False, True])
-@pytest.mark.parametrize("ck", [1, 2, 3, 4])
+@pytest.mark.parametrize("ck", [1, 2, 3, 4, 5])
 def test_conv_epilogue_exact(ck, f16):
     dev = _dev()
     cin, cout, B, H, W = 24, 40, 2, 14, 14
@@ -1094,15 +1094,16 @@ def test_tcgen05_blocks_empty_rows_epilogue_and_ld():
     assert torch.count_nonzero(Yb[:, N:]) == 0
 
 
-@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32"])
 @pytest.mark.parametrize("cin,cout,B,H,W,p", [(256, 256, 6, 14, 14, 90), (64, 64, 3, 56, 56, 90),
                                               (128, 128, 4, 28, 28, 95), (512, 512, 3, 7, 7, 90),
                                               (40, 200, 5, 10, 6, 80), (16, 24, 2, 14, 14, 90)])
 def test_conv_tcgen05_exact(cin, cout, B, H, W, p, dt):
     # conv_kernel 5: implicit im2col over the interleaved copies on the tcgen05 block executor
-    # (k-blocks = (tap, 64 channels)): exact on integer data, rel-L2 <= 1e-2 on real data
+    # (k-blocks = (tap, 64 channels); fp32: (tap, 32 channels) as 3xTF32): exact on integer
+    # data, rel-L2 <= 1e-2 (16-bit) / 1e-5 (fp32) on real data
     dev = _dev()
-    tdt = torch.bfloat16 if dt == "bf16" else torch.float16
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}[dt]
     wi = gen.int_weights(cout, 9 * cin, p, seed=cin + H, vmax=2)
     x = gen.int_x(cin * B * H, W, seed=cout, vmax=4).reshape(cin, B, H, W)
     plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, conv_kernel=5)
@@ -1121,7 +1122,7 @@ def test_conv_tcgen05_exact(cin, cout, B, H, W, p, dt):
     wv = torch.from_numpy(w.values).to(tdt).double().numpy()
     xv = torch.from_numpy(xr).to(tdt).double().numpy()
     err = oracle.rel_l2(y.double().cpu().numpy(), oracle.conv3x3(cout, w.row_ptr, w.col_idx, wv, xv))
-    assert err <= F16_TOL, err
+    assert err <= (F32_TOL if dt == "f32" else F16_TOL), err
 
 
 # ------------------------------------------- tcgen05 blocks: multicast clusters, fp32 as 3xTF32
@@ -1198,13 +1199,13 @@ def test_tcgen05_tf32x3_epilogue_ld_unaligned():
         assert torch.count_nonzero(Yb[:, N:]) == 0
 
 
-@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32"])
 @pytest.mark.parametrize("cin,cout,B,H,W,p", [(256, 256, 6, 14, 14, 90), (128, 384, 3, 28, 28, 95),
                                               (40, 200, 5, 10, 6, 80)])
 def test_conv_tcgen05_cluster_exact(cin, cout, B, H, W, p, dt):
     # conv_kernel 5 with the two (or more) 128-channel row blocks in one multicast cluster
     dev = _dev()
-    tdt = torch.bfloat16 if dt == "bf16" else torch.float16
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}[dt]
     wi = gen.int_weights(cout, 9 * cin, p, seed=cin + H + 1, vmax=2)
     x = gen.int_x(cin * B * H, W, seed=cout + 1, vmax=4).reshape(cin, B, H, W)
     plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, conv_kernel=5,
