@@ -895,9 +895,11 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     const int CS = p.tcg_cs;
     p.tcg_bk = BK;
     // conv: implicit im2col over the interleaved dx-shifted copies (kernel 3b layout); the K
-    // axis is ordered tap-major, k-block = (tap, BK input channels), so the B tile of a k-block
-    // is one 2-D slab of copy dx shifted by (dy - 1) pitches (fp32: slabs of the X_hi and the
-    // X_lo copies, which the pre-pass writes split)
+    // axis is cut into k-blocks = (BK input channels, tap), so the B tile of a k-block is one
+    // 2-D slab of copy dx shifted by (dy - 1) pitches (fp32: slabs of the X_hi and the X_lo
+    // copies, which the pre-pass writes split).  Order: channel block, then dx, then dy - the
+    // three dy slabs of one copy overlap in all but 2 pitches, so consecutive k-blocks hit in
+    // L2 and each copy is read from HBM about once per tile (tap-major order re-read it 3x)
     int32_t ncb = 0;
     if (conv) {
       ncb = (o.c_in + BK - 1) / BK;
@@ -906,8 +908,11 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       p.tcg_g = gg;
       p.tcg_ncb = ncb;
     }
-    // k-block of column k: SpMM k / BK; conv (ci, tap) -> tap * ncb + ci / BK, column ci % BK
-    auto kblock = [&](int32_t k) { return conv ? (k % 9) * ncb + (k / 9) / BK : k / BK; };
+    // k-block of column k: SpMM k / BK; conv (ci, tap = 3 dy + dx) -> (ci / BK) 9 + 3 dx + dy,
+    // column ci % BK
+    auto kblock = [&](int32_t k) {
+      return conv ? ((k / 9) / BK) * 9 + ((k % 9) % 3) * 3 + (k % 9) / 3 : k / BK;
+    };
     auto kcol = [&](int32_t k) { return conv ? (k / 9) % BK : k % BK; };
     const int32_t nrb = (M + BM - 1) / BM, nkb = conv ? 9 * ncb : (K + BK - 1) / BK;
     const int32_t ngroups = (nrb + CS - 1) / CS;

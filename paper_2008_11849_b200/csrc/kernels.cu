@@ -2618,7 +2618,29 @@ struct TcgArgs {
   // (H + 2) P, 64-channel blocks per tap ncb, batch Bt, output plane B H W
   int32_t P, g, Sg, H, W, ncb, Bt;
   int64_t plane;
+  // split tail (sp > 1): the first `rounds` x clusters tiles run whole; the remaining `ntail`
+  // tiles are each cut into sp column slices of np = 256 / sp columns (whole X boxes), one per
+  // cluster, each over the full k-block list with an N = np instruction descriptor (idesc_p).
+  // No partial sums: a slice is the same per-column dot products, just fewer columns.
+  int32_t rounds, sp, ntail, np;
+  uint32_t idesc_p;
 };
+
+// work item i of cluster cl: tile t and column slice (-1 = the whole tile)
+__device__ __forceinline__ bool tcg_work(const TcgArgs& a, int64_t cl, int64_t ncl, int64_t i, int64_t ntiles,
+                                         int64_t& t, int& slice) {
+  slice = -1;
+  if (a.sp <= 1 || i < a.rounds) {
+    t = cl + i * ncl;
+    return t < ntiles;
+  }
+  if (i == a.rounds && cl < (int64_t)a.ntail * a.sp) {
+    t = (int64_t)a.rounds * ncl + cl / a.sp;
+    slice = (int)(cl % a.sp);
+    return true;
+  }
+  return false;
+}
 
 // shared-memory matrix descriptor: start, leading / stride byte offsets, version 1 (bit 46),
 // layout type (bits 61-63): 2 = 128-byte swizzle (16-byte chunks, 8-row atoms), 1 = 128-byte
@@ -2775,28 +2797,42 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int nb = NBOX / CS;  // X boxes per operand this CTA loads (and multicasts)
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = cl; t < ntiles; t += ncl) {
+      int64_t t;
+      int slice;
+      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
         const int gi = (int)(t % a.ngroups);
         const int64_t n0 = (t / a.ngroups) * BN;
         const int j0 = meta[gi], j1 = meta[gi + 1];
+        // boxes of this work item: the whole tile (this CTA loads boxes rank nb .. + nb - 1 and
+        // multicasts them), or the slice's nbs boxes (box i loaded by rank i % CS) stored from
+        // box 0 of the stage.  This thread's loads: stage positions pos0 + i pstep, i < cnt, of
+        // tile box position + boff.  (The issue path is kept short: for 16-bit plans a stage's
+        // MMAs take ~0.26 us, the single producer thread must issue its loads within that.)
+        const int nbs = slice < 0 ? NBOX : NBOX / a.sp;
+        const int pos0 = slice < 0 ? (int)rank * nb : (int)rank, pstep = slice < 0 ? 1 : CS;
+        const int cnt = slice < 0 ? nb : ((int)rank < nbs ? (nbs - 1 - (int)rank) / CS + 1 : 0);
+        const int boff = slice < 0 ? 0 : slice * nbs;
+        const uint32_t tx = (uint32_t)(A_BYTES + (TF ? 2 : 1) * nbs * BOX_BYTES);
         for (int j = j0; j < j1; ++j) {
           const int kb = meta[a.ngroups + 1 + j];
           mbar_wait(empty0 + 8 * s, ph ^ 1u);
           uint8_t* st = smem + (size_t)s * ST_BYTES;
           const uint32_t fb = full0 + 8 * s;
-          mbar_arrive_expect_tx(fb, (uint32_t)ST_BYTES);
+          mbar_arrive_expect_tx(fb, tx);
           bulk_load(smem_u32(st), a.blocks + ((size_t)j * CS + rank) * A_BYTES, (uint32_t)A_BYTES, fb);
-          for (int qq = 0; qq < nb; ++qq) {
-            const int q = (int)rank * nb + qq;
-            const uint32_t dst = smem_u32(st + A_BYTES + q * BOX_BYTES);
-            if (CONV) {  // k-block (tap, 64 / 32 channels): copy dx, shifted by (dy - 1) pitches
-              const int tap = kb / a.ncb, cb = kb - tap * a.ncb;
-              const int s0 = (int)n0 + (tap / 3 - 1) * a.P;
-              tma_load_3d(dst, &tmap, s0 + BOX_COLS * q, cb * (TF ? 32 : 64), tap % 3, fb, mask, CS > 1);
-              if (TF)  // the X_lo copies
-                tma_load_3d(dst + B_HALF, &tmap2, s0 + BOX_COLS * q, cb * 32, tap % 3, fb, mask, CS > 1);
-            } else {
-              const int c0 = (int)(n0 + BOX_COLS * q), c1 = kb * (TF ? 32 : 64);
+          uint32_t dst = smem_u32(st + A_BYTES + pos0 * BOX_BYTES);
+          if (CONV) {  // k-block (channel block, dx, dy): copy dx, shifted by (dy - 1) pitches
+            const int cb = kb / 9, r9 = kb - cb * 9, dx = r9 / 3, dy = r9 - dx * 3;
+            int c0 = (int)n0 + (dy - 1) * a.P + BOX_COLS * (pos0 + boff);
+            const int c1 = cb * (TF ? 32 : 64);
+            for (int i = 0; i < cnt; ++i, dst += pstep * BOX_BYTES, c0 += pstep * BOX_COLS) {
+              tma_load_3d(dst, &tmap, c0, c1, dx, fb, mask, CS > 1);
+              if (TF) tma_load_3d(dst + B_HALF, &tmap2, c0, c1, dx, fb, mask, CS > 1);  // X_lo copies
+            }
+          } else {
+            int c0 = (int)n0 + BOX_COLS * (pos0 + boff);
+            const int c1 = kb * (TF ? 32 : 64);
+            for (int i = 0; i < cnt; ++i, dst += pstep * BOX_BYTES, c0 += pstep * BOX_COLS) {
               if (CS > 1) tma_load_2d_mc(dst, &tmap, c0, c1, fb, mask);
               else tma_load_2d(dst, &tmap, c0, c1, fb);
               if (TF) {
@@ -2816,9 +2852,12 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     if (lane == 0) {
       int s = 0, acc = 0;
       uint32_t ph = 0, aph[2] = {0u, 0u};
-      for (int64_t t = cl; t < ntiles; t += ncl) {
+      int64_t t;
+      int slice;
+      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
         const int gi = (int)(t % a.ngroups);
         const int j0 = meta[gi], j1 = meta[gi + 1];
+        const uint32_t idesc = slice < 0 ? a.idesc : a.idesc_p;
         int j = j0;
         do {
           const int jc = j, je = min(j1, j + FLUSH);
@@ -2841,13 +2880,13 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
               constexpr uint32_t B_SBO = TF ? 512u : 1024u, B_LAYOUT = TF ? 1u : 2u;
               const uint64_t da = umma_desc_sw128(sa + 32u * k, 16u, 1024u);
               const uint64_t db = umma_desc_sw128(sb + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
-              umma<TF>(d, da, db, a.idesc, en);
+              umma<TF>(d, da, db, idesc, en);
               if (TF) {
                 const uint64_t da_lo = umma_desc_sw128(sa + A_HALF + 32u * k, 16u, 1024u);
                 const uint64_t db_lo =
                     umma_desc_sw128(sb + B_HALF + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
-                umma<TF>(d, da_lo, db, a.idesc, 1u);
-                umma<TF>(d, da, db_lo, a.idesc, 1u);
+                umma<TF>(d, da_lo, db, idesc, 1u);
+                umma<TF>(d, da, db_lo, idesc, 1u);
               }
             }
             // the stage is free once these MMAs have read it (in every CTA of the cluster)
@@ -2876,14 +2915,19 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     const bool coal = ((a.ldy * 4) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
     int32_t* otab = (int32_t*)((uint8_t*)tslot + 64);  // conv: span position -> output offset
     int64_t tab_n0 = -1;
-    for (int64_t t = cl; t < ntiles; t += ncl) {
+    int64_t t;
+    int slice;
+    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
-      const int64_t n0 = (t / a.ngroups) * BN;
+      const int64_t nt0 = (t / a.ngroups) * BN;
+      // accumulator column c = tile column cbase + c (a slice: the first nacc columns)
+      const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BN : a.np;
+      const int64_t n0 = nt0 + cbase;
       const int nent = meta[gi + 1] - meta[gi];
-      if (CONV && n0 != tab_n0) {
-        tcg_conv_table<32 * NEPI>(otab, n0, a, threadIdx.x - 64);
-        tab_n0 = n0;
+      if (CONV && nt0 != tab_n0) {
+        tcg_conv_table<32 * NEPI>(otab, nt0, a, threadIdx.x - 64);
+        tab_n0 = nt0;
       }
       const int nch = nent > 0 ? (nent + FLUSH - 1) / FLUSH : 1;
       float m[128];
@@ -2909,14 +2953,15 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         acc ^= 1;
       }
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
-      const int ncol = (int)min((int64_t)BN, a.N - n0);
+      const int ncol = (int)max((int64_t)0, min((int64_t)nacc, a.N - n0));
       if (row0 >= a.M || (a.dbg & 1)) continue;
       if constexpr (CONV) {
         // span positions -> CNHW pixels (otab; -1 = halo / padding / past the span)
+        if (hc >= nacc) continue;
         if (epi) {
 #pragma unroll
           for (int c = 0; c < 128; ++c) {
-            const int32_t o = otab[hc + c];
+            const int32_t o = hc + c < nacc ? otab[cbase + hc + c] : -1;
             if (row < a.M && o >= 0)
               m[c] = epilogue_one<false>(m[c], a.bias, row, a.beta, a.Y + ((int64_t)row * a.plane + o) * 4, a.relu);
           }
@@ -2932,7 +2977,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
                 make_float4(m[c0 + 4 * j], m[c0 + 4 * j + 1], m[c0 + 4 * j + 2], m[c0 + 4 * j + 3]);
           __syncwarp();
           const int c = lane & 15;
-          const int32_t o = otab[hc + c0 + c];
+          const int32_t o = hc + c0 + c < nacc ? otab[cbase + hc + c0 + c] : -1;
           if (o >= 0) {
 #pragma unroll 4
             for (int i = 0; i < 16; ++i) {
@@ -2988,21 +3033,27 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     // per-warp staging buffer (32 rows x 128 B) for coalesced Y stores
     uint8_t* stg = (uint8_t*)tslot + 64 + 1024 + 4 * kTcgMetaMax + (warp - 2) * 4096;
     const bool coal = a.beta == 0.0f && ((a.ldy * 2) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
-    for (int64_t t = cl; t < ntiles; t += ncl) {
+    int64_t t;
+    int slice;
+    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
-      const int64_t n0 = (t / a.ngroups) * BN;
+      const int64_t nt0 = (t / a.ngroups) * BN;
+      // accumulator column c = tile column cbase + c (a slice: the first nacc columns)
+      const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BN : a.np;
+      const int64_t n0 = nt0 + cbase;
       const bool has = meta[gi + 1] > meta[gi];
-      if (CONV && n0 != tab_n0) {
-        tcg_conv_table<128>(otab, n0, a, threadIdx.x - 64);
-        tab_n0 = n0;
+      if (CONV && nt0 != tab_n0) {
+        tcg_conv_table<128>(otab, nt0, a, threadIdx.x - 64);
+        tab_n0 = nt0;
       }
+      const int32_t* ot = otab + cbase;
       mbar_wait(tfull0 + 8 * acc, aph[acc]);
       tm_fence_after();
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
-      const int ncol = (int)min((int64_t)BN, a.N - n0);
+      const int ncol = (int)min((int64_t)nacc, a.N - n0);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 64) {
+      for (int c0 = 0; c0 < nacc; c0 += 64) {
         uint32_t v[64];
         const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0);
         tm_ld32(ta, v);
@@ -3012,7 +3063,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
           if (a.beta != 0.0f) {  // beta * Y_old: element-wise (the fp32 sum needs Y_old)
             if (row >= a.M) continue;
             for (int c = 0; c < 64; ++c) {
-              const int32_t o = otab[c0 + c];
+              const int32_t o = ot[c0 + c];
               if (o < 0) continue;
               uint8_t* yp = a.Y + ((int64_t)row * a.plane + o) * 2;
               const float f = epilogue_one<true, BF>(has ? __uint_as_float(v[c]) : 0.0f, a.bias, row, a.beta, yp, a.relu);
@@ -3041,7 +3092,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
               *(uint4*)(stg + lane * 64 + ((j ^ (lane & 3)) * 16)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             }
             __syncwarp();
-            const int32_t o = otab[c0 + 32 * h + lane];
+            const int32_t o = ot[c0 + 32 * h + lane];
             if (o >= 0) {
               const int j = lane >> 3;
               for (int r = 0; r < 32 && row0 + r < a.M; ++r) {
@@ -3157,8 +3208,9 @@ static unsigned tcg_grid(Fn fn, cudaLaunchConfig_t cfg, int cs, int64_t ntiles, 
 }
 
 static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, const CUtensorMap& tmap2,
-                      const TcgArgs& a, int64_t ntiles, void* stream, std::string& err, const char* what,
+                      TcgArgs a, int64_t ntiles, void* stream, std::string& err, const char* what,
                       int threads = 192) {
+  const bool tf = p.dtype == SPARSE_F32;
   using TFn = void (*)(const CUtensorMap, const CUtensorMap, const TcgArgs);
   TFn fn = (TFn)fn_;
   cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
@@ -3182,6 +3234,21 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   cfg.numAttrs = cs > 1 ? 2 : 1;
   cfg.gridDim = dim3((unsigned)cs, 1, 1);
   cfg.gridDim = dim3(tcg_grid(fn, cfg, cs, ntiles, sms), 1, 1);
+  // split tail: when the tiles do not fill the last round of the persistent clusters (C5 conv:
+  // 224 tiles on 74 clusters = 3 rounds + 2 tiles), each last-round tile is cut into sp column
+  // slices of whole X boxes (a power of two: 16-bit <= 4, fp32 <= 8), one per otherwise idle
+  // cluster; a slice streams the tile's whole W block list with an N = 256 / sp MMA.
+  // SRT_TCG_SPLIT_TAIL=0 disables it (A/B); n > 0 caps sp.
+  const int64_t ncl = cfg.gridDim.x / cs;
+  int cap = tf ? 8 : 4;
+  if (const char* st = std::getenv("SRT_TCG_SPLIT_TAIL")) cap = std::min(cap, std::max(1, std::atoi(st)));
+  a.rounds = (int32_t)(ntiles / ncl);
+  a.ntail = (int32_t)(ntiles % ncl);
+  a.sp = 1;
+  if (a.ntail > 0)
+    while (a.sp * 2 <= cap && (int64_t)a.sp * 2 * a.ntail <= ncl) a.sp *= 2;
+  a.np = 256 / a.sp;
+  a.idesc_p = (a.idesc & ~(0x3Fu << 17)) | ((uint32_t)(a.np >> 3) << 17);
   e = cudaLaunchKernelEx(&cfg, fn, tmap, tmap2, a);
   if (e != cudaSuccess) return cuda_fail(e, what, err);
   return SPARSE_OK;

@@ -1217,3 +1217,70 @@ def test_conv_tcgen05_cluster_exact(cin, cout, B, H, W, p, dt):
     ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), x.astype(np.float64))
     ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
     assert np.array_equal(y.double().cpu().numpy(), ref)
+
+
+# ------------------------------------------- tcgen05 blocks: split tail (column slices)
+
+@pytest.mark.parametrize("dt", ["f16", "f32"])
+@pytest.mark.parametrize("M,K,N,cs", [(128, 512, 38300, 1), (256, 320, 38400, 2), (128, 64, 37000, 1)])
+def test_tcgen05_split_tail(M, K, N, cs, dt, monkeypatch):
+    # ~150 tiles on 148 (74) persistent CTAs (clusters): the last round's tiles run as column
+    # slices on otherwise idle clusters (N = 256 / sp MMAs).  Exact on integer data with and
+    # without the split, and the split changes nothing on real-valued data beyond the tolerance
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    tol = F16_TOL if dt == "f16" else F32_TOL
+    wi = gen.int_weights(M, K, 90, seed=M + K + cs, vmax=2)
+    xi = gen.int_x(K, N, seed=N % 1000, vmax=4)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, executor=4, x_multicast=cs)
+    ref = oracle.spmm(M, K, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), xi.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    X = torch.from_numpy(xi).to(dev).to(tdt)
+    outs = {}
+    for st in ("0", "8"):
+        monkeypatch.setenv("SRT_TCG_SPLIT_TAIL", st)
+        Y = torch.full((M, N), float("nan"), dtype=tdt, device=dev)
+        plan.spmm(X, Y)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.double().cpu().numpy(), ref), st
+    w = gen.pruned_weights(M, K, 90, seed=M * 5 + K)
+    x = gen.uniform_x(K, N, seed=11)
+    plan = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, executor=4, x_multicast=cs)
+    wv = torch.from_numpy(w.values).to(tdt).double().numpy()
+    xv = torch.from_numpy(x).to(tdt).double().numpy()
+    exact = oracle.spmm(M, K, w.row_ptr, w.col_idx, wv, xv)
+    for st in ("0", "8"):
+        monkeypatch.setenv("SRT_TCG_SPLIT_TAIL", st)
+        Y = plan.spmm(torch.from_numpy(x).to(dev).to(tdt))
+        torch.cuda.synchronize()
+        outs[st] = Y.double().cpu().numpy()
+        assert oracle.rel_l2(outs[st], exact) <= tol
+    assert oracle.rel_l2(outs["8"], outs["0"]) <= tol
+
+
+@pytest.mark.parametrize("dt", ["f16", "f32"])
+def test_conv_tcgen05_split_tail(dt, monkeypatch):
+    # the C5 conv at batch 256: 224 tiles on 74 clusters -> 2 tail tiles as column slices
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    cin = cout = 256
+    B, H, W = 256, 14, 14
+    wi = gen.int_weights(cout, 9 * cin, 90, seed=71, vmax=2)
+    x = gen.int_x(cin * B * H, W, seed=72, vmax=4).reshape(cin, B, H, W)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, conv_kernel=5,
+                             x_multicast=2)
+    xd = torch.from_numpy(x).to(dev).to(tdt)
+    outs = {}
+    for st in ("0", "8"):
+        monkeypatch.setenv("SRT_TCG_SPLIT_TAIL", st)
+        y = torch.full((cout, B, H, W), float("nan"), dtype=tdt, device=dev)
+        plan.conv3x3(xd, y)
+        torch.cuda.synchronize()
+        outs[st] = y
+    assert torch.equal(outs["0"], outs["8"])
+    # the last images (the tail tiles' span) against the oracle
+    sel = list(range(B - 12, B))
+    ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64),
+                         np.ascontiguousarray(x[:, sel]).astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(outs["8"][:, sel].double().cpu().numpy(), ref)
