@@ -151,6 +151,14 @@ typedef struct {
                             constant cache; the paper keeps A's values in the constant cache,
                             P:185.  Needs split_k = k_split = x_multicast = 1, x_source = 0,
                             no tensor-core sub-blocks.  Result-neutral (bitwise). */
+  int32_t cta_pair;      /* executor 4 (tcgen05 blocks, SpMM and conv_kernel 5): 1 = CTA pairs -
+                            the two CTAs of a 2-CTA cluster (two consecutive 128-row blocks) run
+                            one tcgen05.mma.cta_group::2 M = 256 per step, each holding its own
+                            W block and HALF of the X tile (the pair's tensor cores read both
+                            halves), so every SM receives A + B/2 bytes per k-block instead of
+                            A + B; x_multicast must be 0, 1 or 2 (the pair is the cluster).
+                            0 = one CTA per 128-row block (default).  Same per-column products
+                            (within tolerance; exact on integer data). */
 } sparse_plan_opts;
 
 /* Fill *opts with defaults (kind SPMM, device -1, everything else 0). */
@@ -279,6 +287,7 @@ typedef struct {
   int64_t tc_panel_steps; /* executor 3: k16 steps over all (panel, chunk) pairs; the tensor cores
                              execute 2 * 16 * 16 * N flops per step (useful: 2 * nnz * N) */
   int32_t plan_source;  /* 0 staged with X, 1 kernel parameters */
+  int32_t cta_pair;     /* executor 4: 1 = CTA pairs (cta_group::2, M = 256) */
 } sparse_plan_info_t;
 
 int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out);

@@ -65,6 +65,8 @@ int sparse_plan_create(sparse_plan_t* out, int32_t M, int32_t K, int64_t nnz,
   bo.jit_warps = o.jit_warps;
   bo.cm = o.x_multicast;
   bo.tm = o.x_source;
+  if (o.cta_pair != 0 && o.cta_pair != 1) return fail(SPARSE_EINVAL, "cta_pair must be 0 or 1");
+  bo.pair = o.cta_pair;
   if (o.conv_kernel < 0 || o.conv_kernel > 5)
     return fail(SPARSE_EINVAL,
                 "conv_kernel must be 0 (auto), 1 (position-strided), 2 (TMA-fed), 3 (register-staged), "
@@ -395,6 +397,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->jit_compile_ms = p.jit_compile_ms;
   out->tuned_us = p.tuned_us;
   out->x_multicast = p.executor == 4 ? p.tcg_cs : p.cm;
+  out->cta_pair = p.tcg_pair;
   out->x_source = p.tm;
   out->conv_kernel = p.kind != SPARSE_CONV3X3 ? 0 : p.executor == 4 ? 5 : !p.conv_vec ? 1 : p.conv_vec == 2 ? 2 : p.conv_vec == 4 ? 4 : 3;
   out->row_order = p.row_order;

@@ -586,8 +586,16 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
       err = "x_multicast must be 1, 2 or 4 for the tcgen05 block executor";
       return SPARSE_EUNSUPPORTED;
     }
-    p.tcg_cs = p.cm;
+    if (o.pair && p.cm > 2) {
+      err = "cta_pair = 1 needs x_multicast 0, 1 or 2 (the CTA pair is the cluster)";
+      return SPARSE_EUNSUPPORTED;
+    }
+    p.tcg_pair = o.pair ? 1 : 0;
+    p.tcg_cs = o.pair ? 2 : p.cm;
     p.cm = 1;
+  } else if (o.pair) {
+    err = "cta_pair = 1 needs the tcgen05 block executor (executor 4 / conv_kernel 5)";
+    return SPARSE_EUNSUPPORTED;
   }
   if (p.cm > 1 && (o.kind != SPARSE_SPMM || p.ks > 1)) {
     err = "x_multicast > 1 needs an SpMM plan with k_split = 1";
@@ -960,9 +968,10 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     p.tcp_nsteps = (int64_t)kbs.size();
     p.executor = 4;
     if (!conv) p.n_tile = 256;
-    // stage = the W block(s) + a 256-column X tile (fp32: X_hi and X_lo): 48 KB / 96 KB
-    const int st_bytes = f32 ? 96 * 1024 : 48 * 1024;
-    p.stages = f32 ? 2 : 4;
+    // stage = the W block(s) + a 256-column X tile (fp32: X_hi and X_lo): 48 KB / 96 KB; a CTA
+    // of a pair stages half of the X tile: 32 KB / 64 KB
+    const int st_bytes = p.tcg_pair ? (f32 ? 64 * 1024 : 32 * 1024) : (f32 ? 96 * 1024 : 48 * 1024);
+    p.stages = p.tcg_pair ? (f32 ? 3 : 6) : (f32 ? 2 : 4);
     // + align, barriers, conv table, block lists, the epilogue warps' store staging (16 KB)
     p.smem_bytes = p.stages * st_bytes + 1024 + 2048 + 8192 + 16384;
     p.plan_bytes += (int64_t)p.tcp_steps.size() + (int64_t)p.tcp_step_off.size() * 4;
@@ -1136,7 +1145,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
                          p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
                          p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm,
                          p.conv_vec, p.row_order, p.executor, p.jit_mp, p.jit_warps, p.stages,
-                         p.tc_min_pct, p.ps, p.tcg_cs, p.tcg_bk};
+                         p.tc_min_pct, p.ps, p.tcg_cs, p.tcg_bk, p.tcg_pair};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

@@ -93,6 +93,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// the wait with cluster-scope acquire: the phase was completed (also) by a release.cluster
+// arrive of another CTA of the cluster (CTA pairs: rank 1 forwards its stages to rank 0)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// arrive on an mbarrier of another CTA of the cluster (shared::cluster address)
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 // the same wait with a suspend-time hint: the warp sleeps until the phase completes (or the
 // hint elapses) instead of re-polling, so waiting warps do not steal issue slots
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
@@ -2624,6 +2642,9 @@ struct TcgArgs {
   // No partial sums: a slice is the same per-column dot products, just fewer columns.
   int32_t rounds, sp, ntail, np;
   uint32_t idesc_p;
+  // CTA pair (cs == 2): rank 0 issues tcgen05.mma.cta_group::2 (M = 256) over both CTAs' W
+  // blocks and X halves; rank 1's MMA thread forwards its stages' completion to rank 0
+  int32_t pair;
 };
 
 // work item i of cluster cl: tile t and column slice (-1 = the whole tile)
@@ -2651,7 +2672,23 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
 }
 template <bool TF>
-__device__ __forceinline__ void umma(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t en) {
+__device__ __forceinline__ void umma(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t en,
+                                     bool pair = false) {
+  if (pair) {  // CTA pair: M = 256 over both CTAs' A and B halves, D in both CTAs' TMEM
+    if (TF)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+          "l"(da), "l"(db), "r"(idesc), "r"(en)
+          : "memory");
+    else
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+          "l"(da), "l"(db), "r"(idesc), "r"(en)
+          : "memory");
+    return;
+  }
   if (TF)
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -2671,6 +2708,14 @@ __device__ __forceinline__ void tm_commit_mc(uint32_t bar, uint16_t mask) {
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           bar),
       "h"(mask)
+      : "memory");
+}
+// CTA pair: arrive on the mbarrier at offset `bar` of both CTAs once the pair's MMAs are done
+__device__ __forceinline__ void tm_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          bar),
+      "h"((uint16_t)3)
       : "memory");
 }
 // tcgen05.ld 32x32b.x32: this warp's 32 TMEM lanes x 32 consecutive columns (no wait)
@@ -2708,6 +2753,24 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
+// CTA pair: TMA load into this CTA's shared memory whose completion is signalled on the
+// mbarrier `bar` of the pair's rank 0 (shared::cluster address) - the 2-SM load form
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
 // conv epilogue: the NT epilogue threads (tid 0 .. NT - 1) decode the tile's 256 span positions
 // once (named barrier among the epilogue warps only): s -> group q, row r, column (image j, x)
 // -> the CNHW offset of the output pixel, -1 for halo rows, padding images and past the span
@@ -2734,9 +2797,12 @@ __device__ __forceinline__ void tcg_conv_table(int32_t* otab, int64_t n0, const 
 // loads boxes [r * NBOX / cs, (r + 1) * NBOX / cs) and multicasts them to the whole cluster;
 // a stage is refilled only when every CTA of the cluster has consumed it (each CTA's MMA
 // commit arrives on the stage's empty barrier in all cs CTAs).
-template <bool BF, bool CONV = false, bool TF = false>
+// PAIR (a template parameter: a kernel containing cta_group::2 instructions cannot be launched
+// without a cluster) = CTA pairs, see TcgArgs::pair.
+template <bool BF, bool CONV = false, bool TF = false, bool PAIR = false>
 __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const __grid_constant__ CUtensorMap tmap2,
+                                                          const __grid_constant__ CUtensorMap tmapA,
                                                           const TcgArgs a) {
   constexpr int BN = 256, A_HALF = 128 * 128, A_BYTES = TF ? 2 * A_HALF : A_HALF;
   constexpr int NBOX = TF ? 8 : 4, BOX_BYTES = TF ? 32 * 128 : 64 * 128, BOX_COLS = TF ? 32 : 64;
@@ -2751,7 +2817,10 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
   const uint32_t rank = CS > 1 ? cluster_rank() : 0u;
   const uint16_t mask = (uint16_t)((1u << CS) - 1u);
   const int64_t cl = blockIdx.x / CS, ncl = gridDim.x / CS;
-  uint64_t* bars = (uint64_t*)(smem + (size_t)S * ST_BYTES);
+  // a CTA of a pair stages its W block and half of the X tile (one operand half = BHE bytes)
+  constexpr bool pair = PAIR;
+  const int BHE = pair ? B_HALF / 2 : B_HALF, STB = A_BYTES + (TF ? 2 : 1) * BHE;
+  uint64_t* bars = (uint64_t*)(smem + (size_t)S * STB);
   const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * S;
   const uint32_t tfull0 = empty0 + 8 * S, tempty0 = tfull0 + 16;
   uint32_t* tslot = (uint32_t*)(bars + 2 * S + 4);
@@ -2759,19 +2828,26 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
   const int64_t ntiles = (int64_t)a.ngroups * nnb;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
+      // pair: only rank 0's full barriers are used (both CTAs' loads complete on them)
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, (uint32_t)CS);  // one MMA commit per CTA of the cluster
+      // one MMA commit per CTA of the cluster (pair: rank 0's one commit reaches both)
+      mbar_init(empty0 + 8 * s, pair ? 1u : (uint32_t)CS);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull0 + 8 * b, 1);
-      mbar_init(tempty0 + 8 * b, NEPI);  // one arrive per epilogue warp
+      mbar_init(tempty0 + 8 * b, pair ? 2 * NEPI : NEPI);  // one arrive per epilogue warp (of the pair)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  if (warp == 1) {  // TMEM: two 128 x 256 fp32 accumulators
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  if (warp == 1) {  // TMEM: two 128 x 256 fp32 accumulators (pair: allocated in both CTAs at once)
+    if (pair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tm_fence_before();
   __syncthreads();
@@ -2795,6 +2871,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     // ---------------- producer
     if (lane == 0) {
       const int nb = NBOX / CS;  // X boxes per operand this CTA loads (and multicasts)
+      const bool mc = CS > 1 && !pair;
       int s = 0;
       uint32_t ph = 0;
       int64_t t;
@@ -2808,36 +2885,58 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         // box 0 of the stage.  This thread's loads: stage positions pos0 + i pstep, i < cnt, of
         // tile box position + boff.  (The issue path is kept short: for 16-bit plans a stage's
         // MMAs take ~0.26 us, the single producer thread must issue its loads within that.)
+        // A pair: each CTA loads (no multicast) and stages its half of the item's boxes.
         const int nbs = slice < 0 ? NBOX : NBOX / a.sp;
-        const int pos0 = slice < 0 ? (int)rank * nb : (int)rank, pstep = slice < 0 ? 1 : CS;
-        const int cnt = slice < 0 ? nb : ((int)rank < nbs ? (nbs - 1 - (int)rank) / CS + 1 : 0);
-        const int boff = slice < 0 ? 0 : slice * nbs;
-        const uint32_t tx = (uint32_t)(A_BYTES + (TF ? 2 : 1) * nbs * BOX_BYTES);
+        int pos0, pstep, cnt, boff, nst;
+        if (pair) {
+          pos0 = 0, pstep = 1, cnt = nbs / 2, boff = (slice < 0 ? 0 : slice * nbs) + (int)rank * (nbs / 2);
+          nst = nbs / 2;
+        } else {
+          pos0 = slice < 0 ? (int)rank * nb : (int)rank, pstep = slice < 0 ? 1 : CS;
+          cnt = slice < 0 ? nb : ((int)rank < nbs ? (nbs - 1 - (int)rank) / CS + 1 : 0);
+          boff = slice < 0 ? 0 : slice * nbs;
+          nst = nbs;
+        }
+        const uint32_t tx = (uint32_t)(A_BYTES + (TF ? 2 : 1) * nst * BOX_BYTES);
         for (int j = j0; j < j1; ++j) {
           const int kb = meta[a.ngroups + 1 + j];
           mbar_wait(empty0 + 8 * s, ph ^ 1u);
-          uint8_t* st = smem + (size_t)s * ST_BYTES;
-          const uint32_t fb = full0 + 8 * s;
-          mbar_arrive_expect_tx(fb, tx);
-          bulk_load(smem_u32(st), a.blocks + ((size_t)j * CS + rank) * A_BYTES, (uint32_t)A_BYTES, fb);
+          uint8_t* st = smem + (size_t)s * STB;
+          // pair: both CTAs' loads complete on rank 0's barrier, which expects both CTAs' bytes
+          const uint32_t fb = pair ? map_rank(full0 + 8 * s, 0) : full0 + 8 * s;
+          if (!pair || rank == 0) mbar_arrive_expect_tx(full0 + 8 * s, pair ? 2 * tx : tx);
+          if constexpr (pair)  // the W block through a plain 2-D map of 128-byte rows
+            tma_load_2d_pair(smem_u32(st), &tmapA, 0, (int)(((int64_t)j * CS + rank) * (A_BYTES / 128)), fb);
+          else
+            bulk_load(smem_u32(st), a.blocks + ((size_t)j * CS + rank) * A_BYTES, (uint32_t)A_BYTES, fb);
           uint32_t dst = smem_u32(st + A_BYTES + pos0 * BOX_BYTES);
           if (CONV) {  // k-block (channel block, dx, dy): copy dx, shifted by (dy - 1) pitches
             const int cb = kb / 9, r9 = kb - cb * 9, dx = r9 / 3, dy = r9 - dx * 3;
             int c0 = (int)n0 + (dy - 1) * a.P + BOX_COLS * (pos0 + boff);
             const int c1 = cb * (TF ? 32 : 64);
             for (int i = 0; i < cnt; ++i, dst += pstep * BOX_BYTES, c0 += pstep * BOX_COLS) {
-              tma_load_3d(dst, &tmap, c0, c1, dx, fb, mask, CS > 1);
-              if (TF) tma_load_3d(dst + B_HALF, &tmap2, c0, c1, dx, fb, mask, CS > 1);  // X_lo copies
+              if constexpr (pair) {
+                tma_load_3d_pair(dst, &tmap, c0, c1, dx, fb);
+                if (TF) tma_load_3d_pair(dst + BHE, &tmap2, c0, c1, dx, fb);
+              } else {
+                tma_load_3d(dst, &tmap, c0, c1, dx, fb, mask, mc);
+                if (TF) tma_load_3d(dst + BHE, &tmap2, c0, c1, dx, fb, mask, mc);  // X_lo copies
+              }
             }
           } else {
             int c0 = (int)n0 + BOX_COLS * (pos0 + boff);
             const int c1 = kb * (TF ? 32 : 64);
             for (int i = 0; i < cnt; ++i, dst += pstep * BOX_BYTES, c0 += pstep * BOX_COLS) {
-              if (CS > 1) tma_load_2d_mc(dst, &tmap, c0, c1, fb, mask);
+              if constexpr (pair) {
+                tma_load_2d_pair(dst, &tmap, c0, c1, fb);
+                if (TF) tma_load_2d_pair(dst + BHE, &tmap2, c0, c1, fb);
+                continue;
+              }
+              if (mc) tma_load_2d_mc(dst, &tmap, c0, c1, fb, mask);
               else tma_load_2d(dst, &tmap, c0, c1, fb);
               if (TF) {
-                if (CS > 1) tma_load_2d_mc(dst + B_HALF, &tmap2, c0, c1, fb, mask);
-                else tma_load_2d(dst + B_HALF, &tmap2, c0, c1, fb);
+                if (mc) tma_load_2d_mc(dst + BHE, &tmap2, c0, c1, fb, mask);
+                else tma_load_2d(dst + BHE, &tmap2, c0, c1, fb);
               }
             }
           }
@@ -2849,7 +2948,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     // ---------------- MMA issuer (one lane)
     // A tile's k-blocks run in chunks of FLUSH k-blocks, each into a fresh TMEM partial
     // (alternating between the two 256-column buffers); 16-bit plans: one chunk per tile
-    if (lane == 0) {
+    if (lane == 0 && (!pair || rank == 0)) {  // (pair: rank 0 issues the pair's MMAs)
       int s = 0, acc = 0;
       uint32_t ph = 0, aph[2] = {0u, 0u};
       int64_t t;
@@ -2861,13 +2960,15 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         int j = j0;
         do {
           const int jc = j, je = min(j1, j + FLUSH);
-          mbar_wait(tempty0 + 8 * acc, aph[acc] ^ 1u);  // the epilogue drained this buffer
+          // the epilogue (pair: of both CTAs) drained this buffer
+          if (pair) mbar_wait_cluster(tempty0 + 8 * acc, aph[acc] ^ 1u);
+          else mbar_wait(tempty0 + 8 * acc, aph[acc] ^ 1u);
           tm_fence_after();
           const uint32_t d = tbase + (uint32_t)(acc * BN);
           for (; j < je; ++j) {
             mbar_wait(full0 + 8 * s, ph);
             tm_fence_after();
-            const uint32_t sa = smem_u32(smem + (size_t)s * ST_BYTES), sb = sa + A_BYTES;
+            const uint32_t sa = smem_u32(smem + (size_t)s * STB), sb = sa + A_BYTES;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               // A: K-major SW128 (rows of 128 B, 8-row atoms of 1 KB): K step (16 x 16-bit or
@@ -2880,21 +2981,24 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
               constexpr uint32_t B_SBO = TF ? 512u : 1024u, B_LAYOUT = TF ? 1u : 2u;
               const uint64_t da = umma_desc_sw128(sa + 32u * k, 16u, 1024u);
               const uint64_t db = umma_desc_sw128(sb + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
-              umma<TF>(d, da, db, idesc, en);
+              umma<TF>(d, da, db, idesc, en, pair);
               if (TF) {
                 const uint64_t da_lo = umma_desc_sw128(sa + A_HALF + 32u * k, 16u, 1024u);
                 const uint64_t db_lo =
-                    umma_desc_sw128(sb + B_HALF + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
-                umma<TF>(d, da_lo, db, idesc, 1u);
-                umma<TF>(d, da, db_lo, idesc, 1u);
+                    umma_desc_sw128(sb + (uint32_t)BHE + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
+                umma<TF>(d, da_lo, db, idesc, 1u, pair);
+                umma<TF>(d, da, db_lo, idesc, 1u, pair);
               }
             }
             // the stage is free once these MMAs have read it (in every CTA of the cluster)
-            if (CS > 1) tm_commit_mc(empty0 + 8 * s, mask);
+            if (pair) tm_commit_pair(empty0 + 8 * s);
+            else if (CS > 1) tm_commit_mc(empty0 + 8 * s, mask);
             else tm_commit(empty0 + 8 * s);
             if (++s == S) s = 0, ph ^= 1u;
           }
-          tm_commit(tfull0 + 8 * acc);  // partial complete (also when the group is empty)
+          // partial complete (also when the group is empty); pair: in both CTAs' TMEM
+          if (pair) tm_commit_pair(tfull0 + 8 * acc);
+          else tm_commit(tfull0 + 8 * acc);
           aph[acc] ^= 1u;
           acc ^= 1;
         } while (j < j1);
@@ -2948,7 +3052,10 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         }
         tm_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        if (lane == 0) {
+          if (pair && rank == 1) mbar_arrive_remote(map_rank(tempty0 + 8 * acc, 0));
+          else mbar_arrive(tempty0 + 8 * acc);
+        }
         aph[acc] ^= 1u;
         acc ^= 1;
       }
@@ -3155,7 +3262,10 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       }
       tm_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      if (lane == 0) {
+          if (pair && rank == 1) mbar_arrive_remote(map_rank(tempty0 + 8 * acc, 0));
+          else mbar_arrive(tempty0 + 8 * acc);
+        }
       aph[acc] ^= 1u;
       acc ^= 1;
     }
@@ -3163,7 +3273,10 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
   tm_fence_before();
   __syncthreads();
   if (CS > 1) cluster_sync_all();  // no peer may still arrive on / multicast into this CTA
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+  if (warp == 1) {
+    if (pair) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+  }
 }
 
 // 3xTF32 operand split of X (fp32 plans on the tcgen05 block executor): X = X_hi + X_lo with
@@ -3211,7 +3324,7 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
                       TcgArgs a, int64_t ntiles, void* stream, std::string& err, const char* what,
                       int threads = 192) {
   const bool tf = p.dtype == SPARSE_F32;
-  using TFn = void (*)(const CUtensorMap, const CUtensorMap, const TcgArgs);
+  using TFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcgArgs);
   TFn fn = (TFn)fn_;
   cudaError_t e = ensure_smem_attr(fn, p.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
@@ -3240,7 +3353,7 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   // cluster; a slice streams the tile's whole W block list with an N = 256 / sp MMA.
   // SRT_TCG_SPLIT_TAIL=0 disables it (A/B); n > 0 caps sp.
   const int64_t ncl = cfg.gridDim.x / cs;
-  int cap = tf ? 8 : 4;
+  int cap = (tf ? 8 : 4) / (a.pair ? 2 : 1);  // a slice is >= 1 X box (pair: per CTA)
   if (const char* st = std::getenv("SRT_TCG_SPLIT_TAIL")) cap = std::min(cap, std::max(1, std::atoi(st)));
   a.rounds = (int32_t)(ntiles / ncl);
   a.ntail = (int32_t)(ntiles % ncl);
@@ -3249,7 +3362,25 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
     while (a.sp * 2 <= cap && (int64_t)a.sp * 2 * a.ntail <= ncl) a.sp *= 2;
   a.np = 256 / a.sp;
   a.idesc_p = (a.idesc & ~(0x3Fu << 17)) | ((uint32_t)(a.np >> 3) << 17);
-  e = cudaLaunchKernelEx(&cfg, fn, tmap, tmap2, a);
+  // CTA pairs: the W blocks through a 2-D map of 128-byte rows (the 2-SM TMA form signals the
+  // pair's rank-0 barrier; the 1-D bulk copy has no such form)
+  CUtensorMap tmapA;
+  std::memset(&tmapA, 0, sizeof tmapA);
+  if (a.pair) {
+    auto encode = tensor_map_encoder();
+    const int ab = tf ? 32768 : 16384;
+    cuuint64_t dims[2] = {32, (cuuint64_t)p.tcp_nsteps * cs * (ab / 128)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {32u, (cuuint32_t)(ab / 128)};
+    cuuint32_t estr[2] = {1, 1};
+    if (!encode || encode(&tmapA, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(p.d_tcp_steps), dims, strides,
+                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      err = "tcgen05 pair: cuTensorMapEncodeTiled (W blocks) failed";
+      return SPARSE_EINTERNAL;
+    }
+  }
+  e = cudaLaunchKernelEx(&cfg, fn, tmap, tmap2, tmapA, a);
   if (e != cudaSuccess) return cuda_fail(e, what, err);
   return SPARSE_OK;
 }
@@ -3346,10 +3477,17 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   // instruction descriptor: D fp32, A / B fp16 (0), bf16 (1) or tf32 (2), A K-major, B MN-major,
   // N = 256, M = 128
   const uint32_t fmt = tf ? 2u : bf ? 1u : 0u;
-  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | ((256u >> 3) << 17) |
+            (((p.tcg_pair ? 256u : 128u) >> 4) << 24);
+  a.pair = p.tcg_pair;
   const int64_t ntiles = (int64_t)p.tcg_ngroups * ((N + 255) / 256);
-  const void* fn = tf ? (const void*)spmm_tcg_kernel<false, false, true>
-                 : bf ? (const void*)spmm_tcg_kernel<true> : (const void*)spmm_tcg_kernel<false>;
+  const bool pr = p.tcg_pair != 0;
+  const void* fn = tf ? (pr ? (const void*)spmm_tcg_kernel<false, false, true, true>
+                            : (const void*)spmm_tcg_kernel<false, false, true, false>)
+                 : bf ? (pr ? (const void*)spmm_tcg_kernel<true, false, false, true>
+                            : (const void*)spmm_tcg_kernel<true, false, false, false>)
+                      : (pr ? (const void*)spmm_tcg_kernel<false, false, false, true>
+                            : (const void*)spmm_tcg_kernel<false, false, false, false>);
   return tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "tcgen05 block launch", tf ? 320 : 192);
 }
 
@@ -3445,7 +3583,9 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   a.beta = ep.beta;
   a.relu = ep.relu;
   const uint32_t fmt = tf ? 2u : bf ? 1u : 0u;
-  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) | ((256u >> 3) << 17) |
+            (((p.tcg_pair ? 256u : 128u) >> 4) << 24);
+  a.pair = p.tcg_pair;
   a.P = P;
   a.g = g;
   a.Sg = Sg;
@@ -3455,8 +3595,13 @@ static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y,
   a.Bt = (int32_t)batch;
   a.plane = batch * (int64_t)p.h * p.w;
   const int64_t ntiles = (int64_t)p.tcg_ngroups * ((span + 255) / 256);
-  const void* fn = tf ? (const void*)spmm_tcg_kernel<false, true, true>
-                 : bf ? (const void*)spmm_tcg_kernel<true, true> : (const void*)spmm_tcg_kernel<false, true>;
+  const bool pr = p.tcg_pair != 0;
+  const void* fn = tf ? (pr ? (const void*)spmm_tcg_kernel<false, true, true, true>
+                            : (const void*)spmm_tcg_kernel<false, true, true, false>)
+                 : bf ? (pr ? (const void*)spmm_tcg_kernel<true, true, false, true>
+                            : (const void*)spmm_tcg_kernel<true, true, false, false>)
+                      : (pr ? (const void*)spmm_tcg_kernel<false, true, false, true>
+                            : (const void*)spmm_tcg_kernel<false, true, false, false>);
   return tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "conv3x3 (tcgen05) launch", tf ? 320 : 192);
 }
 

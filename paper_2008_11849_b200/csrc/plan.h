@@ -100,6 +100,9 @@ struct Plan {
   // that shares every X tile through TMA multicast; each CTA loads 1 / tcg_cs of it), the
   // number of groups, and the k-block depth (64 for 16-bit data, 32 for fp32 = 3xTF32)
   int32_t tcg_cs = 1, tcg_ngroups = 0, tcg_bk = 64;
+  // CTA pairs (tcg_cs = 2): one cta_group::2 M = 256 MMA per step, each CTA stages its W block
+  // and half of the X tile
+  int32_t tcg_pair = 0;
 
   // packed plan (host copy)
   std::vector<int32_t> row_id;   // npanels * Mp, -1 = empty slot
@@ -207,6 +210,7 @@ struct BuildOpts {
   int32_t row_order = 0;  // 0 = LPT panels (load balancing), 1 = natural contiguous rows
   int32_t tc_min_pct = 50;  // tensor-core sub-blocks: min % of nonzeros in a 16x16 tile (0 = off)
   int32_t ps = 0;           // plan source (sparse_plan_opts.plan_source)
+  int32_t pair = 0;         // executor 4: CTA pairs (sparse_plan_opts.cta_pair)
 };
 
 // JIT executor (jit.cpp).  Row entries per row (k ascending) as validated by the

@@ -146,6 +146,12 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
       t.cm = cs;
       cands.push_back(t);
     }
+    if ((M + 127) / 128 >= 2) {  // CTA pairs (cta_group::2, M = 256)
+      t.cm = 2;
+      t.pair = 1;
+      cands.push_back(t);
+      t.pair = 0;
+    }
   } else {
     // vectorised kernels (16-byte loads of consecutive positions; TMA-fed = 2, register-
     // staged = 1) and the position-strided one (0); cc = channels per chunk (0: inspector)
@@ -163,12 +169,13 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
             cands.push_back(o);
           }
     {  // implicit im2col on the tcgen05 block executor (conv_kernel 5; fp32 as 3xTF32)
-      for (int cs : {1, 2}) {
-        if (cs > 1 && (M + 127) / 128 < cs) continue;
+      for (int cs : {1, 2, 3}) {  // 3 = a CTA pair
+        if (cs > 1 && (M + 127) / 128 < 2) continue;
         BuildOpts o = base;
         o.conv_vec = 2;
         o.executor = 4;
-        o.cm = cs;
+        o.cm = cs == 3 ? 2 : cs;
+        o.pair = cs == 3;
         cands.push_back(o);
       }
     }

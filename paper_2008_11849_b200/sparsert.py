@@ -51,7 +51,7 @@ class sparse_plan_opts(ctypes.Structure):
                 ("jit_warps", ctypes.c_int32), ("x_multicast", ctypes.c_int32),
                 ("x_source", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
                 ("row_order", ctypes.c_int32), ("tc_min_density", ctypes.c_int32),
-                ("plan_source", ctypes.c_int32)]
+                ("plan_source", ctypes.c_int32), ("cta_pair", ctypes.c_int32)]
 
 
 class sparse_epilogue(ctypes.Structure):
@@ -78,7 +78,7 @@ class sparse_plan_info_t(ctypes.Structure):
                 ("row_order", ctypes.c_int32), ("tc_min_density", ctypes.c_int32),
                 ("tc_row_blocks", ctypes.c_int32), ("tc_tiles", ctypes.c_int64),
                 ("tc_nnz", ctypes.c_int64), ("tc_panel_steps", ctypes.c_int64),
-                ("plan_source", ctypes.c_int32)]
+                ("plan_source", ctypes.c_int32), ("cta_pair", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -289,12 +289,16 @@ class Plan:
                 o.update(plan_source=i["plan_source"])
             if i["executor"] == 4:  # the tcgen05 block executor has its own fixed ring
                 o.pop("stages")
+                if i["cta_pair"]:
+                    o.update(cta_pair=1)
         else:
             o.update(k_chunk=i["k_chunk"], conv_kernel=i["conv_kernel"])
             o.pop("split_k")
             o.pop("stages")
             if i["conv_kernel"] == 5:  # tcgen05 blocks: the tile options are the executor's own
                 o = dict(conv_kernel=5, x_multicast=i["x_multicast"])
+                if i["cta_pair"]:
+                    o.update(cta_pair=1)
         return o
 
     def _check_tensor(self, t, name):

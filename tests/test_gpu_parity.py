@@ -1284,3 +1284,89 @@ def test_conv_tcgen05_split_tail(dt, monkeypatch):
                          np.ascontiguousarray(x[:, sel]).astype(np.float64))
     ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
     assert np.array_equal(outs["8"][:, sel].double().cpu().numpy(), ref)
+
+
+# ------------------------------------------- tcgen05 blocks: CTA pairs (cta_group::2, M = 256)
+
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32"])
+@pytest.mark.parametrize("M,K,N,p", [(3072, 768, 2048, 90), (768, 3072, 512, 95), (300, 200, 517, 80),
+                                      (256, 64, 256, 90), (640, 512, 392, 90), (130, 1111, 300, 98),
+                                      (512, 256, 38300, 90)])
+def test_tcgen05_pair_exact(M, K, N, p, dt):
+    # two consecutive 128-row blocks per CTA pair: one tcgen05.mma.cta_group::2 (M = 256) per
+    # step, each CTA staging its W block and half of the X tile.  Bitwise on integer data;
+    # real-valued data within the dtype's tolerance
+    dev = _dev()
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}[dt]
+    wi = gen.int_weights(M, K, p, seed=M + 3 * K + N, vmax=2)
+    xi = gen.int_x(K, N, seed=N + 5, vmax=4)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, executor=4, cta_pair=1)
+    assert plan.info["executor"] == 4 and plan.info["cta_pair"] == 1 and plan.info["x_multicast"] == 2
+    Y = torch.full((M, N), float("nan"), dtype=tdt, device=dev)
+    plan.spmm(torch.from_numpy(xi).to(dev).to(tdt), Y)
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), xi.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(Y.double().cpu().numpy(), ref)
+    again = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, **plan.chosen_opts())
+    assert again.info["digest"] == plan.info["digest"] and again.info["cta_pair"] == 1
+    w = gen.pruned_weights(M, K, p, seed=M * 11 + K)
+    x = gen.uniform_x(K, N, seed=N + 9)
+    plan = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, executor=4, cta_pair=1)
+    Y = plan.spmm(torch.from_numpy(x).to(dev).to(tdt))
+    torch.cuda.synchronize()
+    wv = torch.from_numpy(w.values).to(tdt).double().numpy()
+    xv = torch.from_numpy(x).to(tdt).double().numpy()
+    err = oracle.rel_l2(Y.double().cpu().numpy(), oracle.spmm(M, K, w.row_ptr, w.col_idx, wv, xv))
+    assert err <= (F32_TOL if dt == "f32" else F16_TOL), err
+
+
+@pytest.mark.parametrize("dt", ["f16", "f32"])
+def test_tcgen05_pair_epilogue(dt):
+    # empty 128-row block (-> +0 in one CTA of a pair), ldx / ldy > N, bias + beta + ReLU
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    M, K, N = 400, 192, 300
+    base = gen.int_weights(M, K, 90, seed=24, vmax=2)
+    dense = gen.to_dense(base)
+    dense[128:256] = 0.0
+    keep = np.flatnonzero(dense)
+    w = gen.csr_from_mask(M, K, keep, dense.astype(np.float32))
+    xi = gen.int_x(K, N, seed=25, vmax=4)
+    rng = np.random.default_rng(26)
+    bias = rng.integers(-8, 9, M).astype(np.float32)
+    y0 = rng.integers(-8, 9, (M, N)).astype(np.float32)
+    plan = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, executor=4, cta_pair=1)
+    Xb = torch.zeros((K, N + 40), dtype=tdt, device=dev)
+    Xb[:, :N] = torch.from_numpy(xi).to(dev).to(tdt)
+    Yb = torch.zeros((M, N + 24), dtype=tdt, device=dev)
+    Yb[:, :N] = torch.from_numpy(y0).to(dev).to(tdt)
+    plan.spmm(Xb[:, :N], Yb[:, :N], bias=torch.from_numpy(bias).to(dev).to(tdt), beta=0.5, relu=True)
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), xi.astype(np.float64))
+    ref = np.maximum(ref + bias[:, None] + 0.5 * y0, 0.0)
+    ref = _f16_round(ref) if dt == "f16" else ref.astype(np.float32).astype(np.float64)
+    assert np.array_equal(Yb[:, :N].double().cpu().numpy(), ref)
+    assert torch.count_nonzero(Yb[:, N:]) == 0
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32"])
+@pytest.mark.parametrize("cin,cout,B,H,W,p", [(256, 256, 6, 14, 14, 90), (128, 384, 3, 28, 28, 95),
+                                              (40, 200, 5, 10, 6, 80), (256, 256, 256, 14, 14, 90)])
+def test_conv_tcgen05_pair_exact(cin, cout, B, H, W, p, dt):
+    # conv_kernel 5 on CTA pairs; batch 256 = the C5 bench shape (split tail included)
+    dev = _dev()
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}[dt]
+    wi = gen.int_weights(cout, 9 * cin, p, seed=cin + H + 7, vmax=2)
+    x = gen.int_x(cin * B * H, W, seed=cout + 7, vmax=4).reshape(cin, B, H, W)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, conv_kernel=5,
+                             cta_pair=1)
+    assert plan.info["conv_kernel"] == 5 and plan.info["cta_pair"] == 1
+    y = torch.full((cout, B, H, W), float("nan"), dtype=tdt, device=dev)
+    plan.conv3x3(torch.from_numpy(x).to(dev).to(tdt), y)
+    torch.cuda.synchronize()
+    sel = list(range(B)) if B <= 8 else [0, 1, 2, B // 2, B - 3, B - 2, B - 1]
+    ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64),
+                         np.ascontiguousarray(x[:, sel]).astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(y[:, sel].double().cpu().numpy(), ref)
