@@ -2066,6 +2066,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+static PFN_cuTensorMapEncodeIm2col_v12000 tensor_map_encoder_im2col() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeIm2col_v12000)p;
+  });
+  return fn;
+}
+
 // Row repack of an X whose base or row stride is not 16-byte aligned (TMA needs both):
 // Xp[k][0..N) = X[k][0..N), Xp with a padded row stride.  Pure data movement.
 __global__ void repack_rows(const uint8_t* __restrict__ X, int64_t ldx_b, uint8_t* __restrict__ Xp,
@@ -2125,6 +2138,36 @@ __global__ void transpose_2d(const T* __restrict__ in, int64_t ldi, T* __restric
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t c = c0 + i, r = r0 + threadIdx.x;
     if (r < rows && c < cols) out[c * ldo + r] = tile[threadIdx.x][i];
+  }
+}
+
+// CNHW -> NHWC for the im2col conv on the tcgen05 block executor: out[p][c] = in[c][p] (P = B H W
+// pixels), 32 channels x 64 pixels per CTA through shared memory; SPLIT (fp32 plans, 3xTF32):
+// out = TF32 RN of x, out_lo = TF32 RN of the remainder (x_lo = 0 for non-finite x).  Pure data
+// movement (+ the operand split).
+template <typename T, bool SPLIT>
+__global__ void __launch_bounds__(256) nhwc_pack(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ out_lo,
+                                                 int64_t C, int64_t P) {
+  __shared__ T tile[32][65];
+  const int64_t p0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 pixels x 4 channel rows per pass
+  for (int i = ty; i < 32; i += 4) {
+    const int64_t c = c0 + i, px = p0 + tx;
+    tile[i][tx] = (c < C && px < P) ? in[c * P + px] : T(0);
+  }
+  __syncthreads();
+  const int cx = threadIdx.x & 31, py = threadIdx.x >> 5;  // 32 channels x 8 pixels per pass
+  for (int j = py; j < 64; j += 8) {
+    const int64_t px = p0 + j, c = c0 + cx;
+    if (px >= P || c >= C) continue;
+    const T v = tile[cx][j];
+    if constexpr (SPLIT) {
+      const float h = tf32_rn_dev(v);
+      out[px * C + c] = h;
+      out_lo[px * C + c] = isfinite(h) ? tf32_rn_dev(v - h) : 0.0f;
+    } else {
+      out[px * C + c] = v;
+    }
   }
 }
 
@@ -2643,8 +2686,11 @@ struct TcgArgs {
   int32_t rounds, sp, ntail, np;
   uint32_t idesc_p;
   // CTA pair (cs == 2): rank 0 issues tcgen05.mma.cta_group::2 (M = 256) over both CTAs' W
-  // blocks and X halves; rank 1's MMA thread forwards its stages' completion to rank 0
+  // blocks and X halves
   int32_t pair;
+  // conv through im2col TMA (i2c = 1): X is NHWC (plane = B H W pixels, N = plane, ldy = plane),
+  // B is K-major (pixel rows of 128-byte channel groups); each CTA loads i2c_pix pixels per tile
+  int32_t i2c, i2c_pix;
 };
 
 // work item i of cluster cl: tile t and column slice (-1 = the whole tile)
@@ -2769,6 +2815,32 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
       " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+
+// im2col TMA (NHWC input, 3x3 pad 1): `pixels` consecutive output pixels (the map's
+// pixelsPerColumn) from the one at (b, y, x), tap (dy, dx), channels c .. c + channelsPerPixel -
+// 1: smem row i = the channels of input pixel (y + dy - 1, x + dx - 1) of output pixel i (zero
+// outside the image) - the K-major B operand of the implicit GEMM, no im2col matrix in memory
+__device__ __forceinline__ void tma_im2col(uint32_t dst, const CUtensorMap* map, int c, int x, int y, int b,
+                                           uint16_t dx, uint16_t dy, uint32_t bar, uint16_t mask, int mode) {
+  if (mode == 1)  // multicast to the cluster
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8}, %9;" ::"r"(dst),
+        "l"((uint64_t)map), "r"(c), "r"(x - 1), "r"(y - 1), "r"(b), "r"(bar), "h"(dx), "h"(dy), "h"(mask)
+        : "memory");
+  else if (mode == 2)  // CTA pair: completes on rank 0's barrier
+    asm volatile(
+        "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+        "l"((uint64_t)map), "r"(c), "r"(x - 1), "r"(y - 1), "r"(b), "r"(bar), "h"(dx), "h"(dy)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+        "l"((uint64_t)map), "r"(c), "r"(x - 1), "r"(y - 1), "r"(b), "r"(bar), "h"(dx), "h"(dy)
+        : "memory");
 }
 
 // conv epilogue: the NT epilogue threads (tid 0 .. NT - 1) decode the tile's 256 span positions
@@ -2897,7 +2969,21 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
           boff = slice < 0 ? 0 : slice * nbs;
           nst = nbs;
         }
-        const uint32_t tx = (uint32_t)(A_BYTES + (TF ? 2 : 1) * nst * BOX_BYTES);
+        uint32_t tx = (uint32_t)(A_BYTES + (TF ? 2 : 1) * nst * BOX_BYTES);
+        // im2col conv: this CTA's first pixel (a pair / multicast cluster: rank r loads pixels
+        // r i2c_pix .. of the tile; a multicast CTA's stage receives the whole tile)
+        int ib = 0, iy = 0, ix = 0;
+        uint32_t i2c_dst = 0;
+        if (CONV && a.i2c) {
+          const int64_t p0 = n0 + (CS > 1 ? (int64_t)rank * a.i2c_pix : 0);
+          const int64_t hw = (int64_t)a.H * a.W;
+          ib = (int)(p0 / hw);
+          const int rem = (int)(p0 - (int64_t)ib * hw);
+          iy = rem / a.W;
+          ix = rem - iy * a.W;
+          i2c_dst = (CS > 1 && !pair) ? (uint32_t)rank * (uint32_t)a.i2c_pix * 128u : 0u;
+          tx = (uint32_t)(A_BYTES + (TF ? 2 : 1) * (pair ? a.i2c_pix : BN) * 128);
+        }
         for (int j = j0; j < j1; ++j) {
           const int kb = meta[a.ngroups + 1 + j];
           mbar_wait(empty0 + 8 * s, ph ^ 1u);
@@ -2910,7 +2996,13 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
           else
             bulk_load(smem_u32(st), a.blocks + ((size_t)j * CS + rank) * A_BYTES, (uint32_t)A_BYTES, fb);
           uint32_t dst = smem_u32(st + A_BYTES + pos0 * BOX_BYTES);
-          if (CONV) {  // k-block (channel block, dx, dy): copy dx, shifted by (dy - 1) pitches
+          if (CONV && a.i2c) {  // k-block (channel block, dx, dy): one im2col box per operand
+            const int cb = kb / 9, r9 = kb - cb * 9, dx = r9 / 3, dy = r9 - dx * 3;
+            const uint32_t d0 = smem_u32(st + A_BYTES) + i2c_dst;
+            const int mode = pair ? 2 : (CS > 1 ? 1 : 0);
+            tma_im2col(d0, &tmap, cb * (TF ? 32 : 64), ix, iy, ib, (uint16_t)dx, (uint16_t)dy, fb, mask, mode);
+            if (TF) tma_im2col(d0 + BHE, &tmap2, cb * 32, ix, iy, ib, (uint16_t)dx, (uint16_t)dy, fb, mask, mode);
+          } else if (CONV) {  // k-block (channel block, dx, dy): copy dx, shifted by (dy - 1) pitches
             const int cb = kb / 9, r9 = kb - cb * 9, dx = r9 / 3, dy = r9 - dx * 3;
             int c0 = (int)n0 + (dy - 1) * a.P + BOX_COLS * (pos0 + boff);
             const int c1 = cb * (TF ? 32 : 64);
@@ -2980,12 +3072,15 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
               if (a.dbg & 2) continue;
               constexpr uint32_t B_SBO = TF ? 512u : 1024u, B_LAYOUT = TF ? 1u : 2u;
               const uint64_t da = umma_desc_sw128(sa + 32u * k, 16u, 1024u);
-              const uint64_t db = umma_desc_sw128(sb + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
+              // im2col conv: B K-major like A (pixel rows of 128 B, K step = +32 B)
+              const uint64_t db = (CONV && a.i2c) ? umma_desc_sw128(sb + 32u * k, 16u, 1024u)
+                                                  : umma_desc_sw128(sb + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
               umma<TF>(d, da, db, idesc, en, pair);
               if (TF) {
                 const uint64_t da_lo = umma_desc_sw128(sa + A_HALF + 32u * k, 16u, 1024u);
                 const uint64_t db_lo =
-                    umma_desc_sw128(sb + (uint32_t)BHE + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
+                    (CONV && a.i2c) ? umma_desc_sw128(sb + (uint32_t)BHE + 32u * k, 16u, 1024u)
+                                    : umma_desc_sw128(sb + (uint32_t)BHE + (uint32_t)KSTEP_B * k, (uint32_t)BOX_BYTES, B_SBO, B_LAYOUT);
                 umma<TF>(d, da_lo, db, idesc, 1u, pair);
                 umma<TF>(d, da, db_lo, idesc, 1u, pair);
               }
@@ -3029,7 +3124,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BN : a.np;
       const int64_t n0 = nt0 + cbase;
       const int nent = meta[gi + 1] - meta[gi];
-      if (CONV && nt0 != tab_n0) {
+      if (CONV && !a.i2c && nt0 != tab_n0) {
         tcg_conv_table<32 * NEPI>(otab, nt0, a, threadIdx.x - 64);
         tab_n0 = nt0;
       }
@@ -3062,7 +3157,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)max((int64_t)0, min((int64_t)nacc, a.N - n0));
       if (row0 >= a.M || (a.dbg & 1)) continue;
-      if constexpr (CONV) {
+      if (CONV && !a.i2c) {
         // span positions -> CNHW pixels (otab; -1 = halo / padding / past the span)
         if (hc >= nacc) continue;
         if (epi) {
@@ -3150,7 +3245,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BN : a.np;
       const int64_t n0 = nt0 + cbase;
       const bool has = meta[gi + 1] > meta[gi];
-      if (CONV && nt0 != tab_n0) {
+      if (CONV && !a.i2c && nt0 != tab_n0) {
         tcg_conv_table<128>(otab, nt0, a, threadIdx.x - 64);
         tab_n0 = nt0;
       }
@@ -3166,7 +3261,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         tm_ld32(ta, v);
         tm_ld32(ta + 32, v + 32);
         tm_wait_ld();
-        if constexpr (CONV) {
+        if (CONV && !a.i2c) {
           if (a.beta != 0.0f) {  // beta * Y_old: element-wise (the fp32 sum needs Y_old)
             if (row >= a.M) continue;
             for (int c = 0; c < 64; ++c) {
@@ -3353,7 +3448,7 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   // cluster; a slice streams the tile's whole W block list with an N = 256 / sp MMA.
   // SRT_TCG_SPLIT_TAIL=0 disables it (A/B); n > 0 caps sp.
   const int64_t ncl = cfg.gridDim.x / cs;
-  int cap = (tf ? 8 : 4) / (a.pair ? 2 : 1);  // a slice is >= 1 X box (pair: per CTA)
+  int cap = a.i2c ? 1 : (tf ? 8 : 4) / (a.pair ? 2 : 1);  // a slice is >= 1 X box (pair: per CTA)
   if (const char* st = std::getenv("SRT_TCG_SPLIT_TAIL")) cap = std::min(cap, std::max(1, std::atoi(st)));
   a.rounds = (int32_t)(ntiles / ncl);
   a.ntail = (int32_t)(ntiles % ncl);
@@ -3493,10 +3588,114 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
 
 // Conv on the tcgen05 block executor (conv_kernel 5): the interleaved copies pre-pass (pitch a
 // multiple of 8 elements), then spmm_tcg_kernel<CONV> over the span of the copies.
+// Conv on the tcgen05 block executor through im2col TMA: the input is packed once CNHW -> NHWC
+// (fp32: split into TF32 halves), then every k-block (64 / 32 channels, tap) of every tile is ONE
+// im2col box per operand: 256 (pair: 128 per CTA) consecutive output pixels x the channel group,
+// the zero padding of P:215 done by the TMA engine (pixels outside the image read as zero).  No
+// shifted copies, no halo positions; the output tile is 256 consecutive pixels of the CNHW
+// plane, stored like an SpMM tile (ldy = plane).
+static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y, void* stream, std::string& err,
+                           const Epilogue& ep) {
+  const bool bf = p.dtype == SPARSE_BF16, tf = p.dtype == SPARSE_F32;
+  const int S = tf ? 4 : 2, BK = tf ? 32 : 64;
+  auto encode = tensor_map_encoder_im2col();
+  if (!encode) {
+    err = "internal: no im2col tensor-map encoder";
+    return SPARSE_EINTERNAL;
+  }
+  const int64_t plane = batch * (int64_t)p.h * p.w;
+  DeviceGuard dg(p.device);
+  if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
+  void* xn = nullptr;  // NHWC input (fp32: X_hi, then X_lo)
+  const size_t nb = (size_t)plane * p.c_in * S;
+  cudaError_t e = cudaMallocAsync(&xn, tf ? 2 * nb : nb, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(e, "cudaMallocAsync(conv NHWC)", err);
+  }
+  struct Free {
+    void* b;
+    void* st;
+    ~Free() { cudaFreeAsync(b, (cudaStream_t)st); }
+  } fr{xn, stream};
+  {
+    const dim3 grid((unsigned)((plane + 63) / 64), (unsigned)((p.c_in + 31) / 32));
+    if (tf)
+      nhwc_pack<float, true><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)x, (float*)xn,
+                                                                     (float*)((uint8_t*)xn + nb), p.c_in, plane);
+    else
+      nhwc_pack<uint16_t, false><<<grid, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)x, (uint16_t*)xn, nullptr,
+                                                                         p.c_in, plane);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "NHWC pack launch", err);
+  }
+  const int cs = p.tcg_cs, pix = 256 / cs;
+  CUtensorMap tmap, tmap2;
+  std::memset(&tmap, 0, sizeof tmap);
+  std::memset(&tmap2, 0, sizeof tmap2);
+  cuuint64_t dims[4] = {(cuuint64_t)p.c_in, (cuuint64_t)p.w, (cuuint64_t)p.h, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)p.c_in * S, (cuuint64_t)p.c_in * S * p.w, (cuuint64_t)p.c_in * S * p.w * p.h};
+  const int lower[2] = {-1, -1}, upper[2] = {-1, -1};  // 3 x 3, padding 1, stride 1 (W, H)
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUtensorMapDataType dt = tf ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                               : bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUresult r = encode(&tmap, dt, 4, xn, dims, strides, lower, upper, (cuuint32_t)BK, (cuuint32_t)pix, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS && tf)
+    r = encode(&tmap2, dt, 4, (uint8_t*)xn + nb, dims, strides, lower, upper, (cuuint32_t)BK, (cuuint32_t)pix, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "conv (tcgen05, im2col): cuTensorMapEncodeIm2col failed";
+    return SPARSE_EINTERNAL;
+  }
+  TcgArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.blocks = p.d_tcp_steps;
+  a.meta = p.d_tcp_step_off;
+  a.nblk = (int32_t)p.tcp_nsteps;
+  a.Y = (uint8_t*)y;
+  a.ldy = plane;
+  a.N = plane;
+  a.M = p.M;
+  a.ngroups = p.tcg_ngroups;
+  a.cs = cs;
+  a.stages = p.stages;
+  if (const char* dbg = std::getenv("SRT_TCG_DBG")) a.dbg = std::atoi(dbg);
+  a.bias = (const uint8_t*)ep.bias;
+  a.beta = ep.beta;
+  a.relu = ep.relu;
+  // D fp32, A / B fp16 (0), bf16 (1) or tf32 (2), both K-major, N = 256, M = 128 (pair: 256)
+  const uint32_t fmt = tf ? 2u : bf ? 1u : 0u;
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((256u >> 3) << 17) | (((p.tcg_pair ? 256u : 128u) >> 4) << 24);
+  a.pair = p.tcg_pair;
+  a.i2c = 1;
+  a.i2c_pix = pix;
+  a.H = p.h;
+  a.W = p.w;
+  a.Bt = (int32_t)batch;
+  a.plane = plane;
+  const int64_t ntiles = (int64_t)p.tcg_ngroups * ((plane + 255) / 256);
+  const bool pr = p.tcg_pair != 0;
+  const void* fn = tf ? (pr ? (const void*)spmm_tcg_kernel<false, true, true, true>
+                            : (const void*)spmm_tcg_kernel<false, true, true, false>)
+                 : bf ? (pr ? (const void*)spmm_tcg_kernel<true, true, false, true>
+                            : (const void*)spmm_tcg_kernel<true, true, false, false>)
+                      : (pr ? (const void*)spmm_tcg_kernel<false, true, false, true>
+                            : (const void*)spmm_tcg_kernel<false, true, false, false>);
+  return tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "conv3x3 (tcgen05, im2col) launch", tf ? 320 : 192);
+}
+
 static int launch_conv_tcg(const Plan& p, int64_t batch, const void* x, void* y, void* stream, std::string& err,
                            const Epilogue& ep) {
   const bool bf = p.dtype == SPARSE_BF16, tf = p.dtype == SPARSE_F32;
   const int S = tf ? 4 : 2;
+  {  // im2col TMA (default; SRT_CONV_IM2COL=0 selects the interleaved dx-shifted copies)
+    const char* ev = std::getenv("SRT_CONV_IM2COL");
+    const bool rows16 = ((int64_t)p.c_in * S) % 16 == 0;  // TMA: 16-byte pixel strides
+    if ((!ev || std::atoi(ev) != 0) && rows16 && batch * (int64_t)p.h * p.w < INT32_MAX)
+      return launch_conv_i2c(p, batch, x, y, stream, err, ep);
+  }
   auto encode = tensor_map_encoder();
   if (!encode) {
     err = "internal: no tensor-map encoder";
