@@ -308,3 +308,53 @@ def test_tensor_core_panel_steps(M, K, p):
     # fp32 plans and conv plans do not take it
     with pytest.raises(srt.SparseRTError):
         _plan(w, torch.float32, n_hint=256, executor=3)
+
+
+@pytest.mark.parametrize("dt", ["f16", "f32"])
+@pytest.mark.parametrize("M,K,p", [(300, 200, 90), (512, 512, 98), (768, 3072, 99), (130, 64, 95)])
+@pytest.mark.parametrize("pair", [0, 1])
+def test_tcgen05_block_list(M, K, p, dt, pair):
+    # executor 4: the inspector keeps every (128-row block, BK-column block) holding a nonzero,
+    # BK = 64 (16-bit) / 32 (fp32, 3xTF32); a CTA pair (two row blocks) walks the union of its
+    # two blocks' k-block lists.  Independent count of the union entries:
+    import torch
+    w = gen.pruned_weights(M, K, p, seed=M * 3 + K)
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    info = _plan(w, tdt, n_hint=512, executor=4, cta_pair=pair).info
+    assert info["executor"] == 4 and info["cta_pair"] == pair
+    assert info["x_multicast"] == (2 if pair else 1)
+    bk = 64 if dt == "f16" else 32
+    rows = np.repeat(np.arange(M), np.diff(w.row_ptr))
+    grp = (rows // 128) // (2 if pair else 1)
+    keys = np.unique(grp.astype(np.int64) * 100000 + w.col_idx // bk)
+    assert info["tc_panel_steps"] == keys.size
+
+
+@pytest.mark.parametrize("dt", ["f16", "f32"])
+def test_tcgen05_conv_block_list(dt):
+    # conv_kernel 5: k-blocks are (BK input channels, tap); K index k = ci * 9 + tap
+    import torch
+    cin, cout = 96, 200
+    w = gen.pruned_weights(cout, 9 * cin, 95, seed=5)
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    info = _plan(w, tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=14, w=14, n_hint=8, conv_kernel=5, cta_pair=1).info
+    assert info["conv_kernel"] == 5 and info["cta_pair"] == 1
+    bk = 64 if dt == "f16" else 32
+    rows = np.repeat(np.arange(cout), np.diff(w.row_ptr))
+    kb = (w.col_idx // 9) // bk * 9 + w.col_idx % 9
+    keys = np.unique(((rows // 128) // 2).astype(np.int64) * 100000 + kb)
+    assert info["tc_panel_steps"] == keys.size
+
+
+def test_cta_pair_validation():
+    w = gen.pruned_weights(256, 128, 90, seed=1)
+    import torch
+    with pytest.raises(srt.SparseRTError):   # CTA pairs are a tcgen05 block executor option
+        _plan(w, torch.float16, n_hint=256, executor=0, cta_pair=1)
+    with pytest.raises(srt.SparseRTError):   # the pair is the cluster
+        _plan(w, torch.float16, n_hint=256, executor=4, cta_pair=1, x_multicast=4)
+    with pytest.raises(srt.SparseRTError):
+        _plan(w, torch.float16, n_hint=256, executor=4, cta_pair=2)
+    a = _plan(w, torch.float16, n_hint=256, executor=4, cta_pair=1).info
+    b = _plan(w, torch.float16, n_hint=256, executor=4, x_multicast=2).info
+    assert a["digest"] != b["digest"]  # same blocks, different executor geometry
