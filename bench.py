@@ -559,9 +559,12 @@ class Run:
             per = 2 * 16 * 16 if pinfo["executor"] == 3 else \
                 (3 * 2 * 128 * 32 if tf else 2 * 128 * 64) * max(1, pinfo.get("x_multicast", 1))
             cols = d["N"]
-            if self.layers[dom]["kind"] == "conv":  # the MMA runs over the interleaved span
-                Ld, g = self.layers[dom], pinfo["conv_images_per_tile"]
+            Ld = self.layers[dom]
+            im2col = os.environ.get("SRT_CONV_IM2COL", "1") != "0" and (Ld.get("c_in", 0) * S) % 16 == 0
+            if Ld["kind"] == "conv" and not im2col:  # the MMA runs over the interleaved span
+                g = pinfo["conv_images_per_tile"]
                 cols = -(-Ld["B"] // g) * (Ld["H"] + 2) * g * Ld["W"]
+            # (im2col TMA, the default: the MMA runs over the B H W output pixels only)
             tc_flops = per * cols * pinfo["tc_panel_steps"]
             roof = {"bound": "tensor", "achieved": tc_flops / sec / 1e12,
                     "peak": peaks["bf16_tflops"] * (0.5 if tf else 1.0),

@@ -64,12 +64,24 @@ spmm_case("spmm_unaligned_repack", 200, 100, 49, f32)
 spmm_case("spmm_param_plan", 128, 64, 1000, f32, plan_source=1)
 spmm_case("spmm_tcgen05_blocks", 300, 200, 517, f16, executor=4)
 spmm_case("spmm_tcgen05_blocks_bf16", 256, 128, 600, bf16, executor=4)
+spmm_case("spmm_tcgen05_tf32x3", 300, 200, 517, f32, executor=4)
+spmm_case("spmm_tcgen05_multicast", 512, 256, 600, f16, executor=4, x_multicast=2)
+spmm_case("spmm_tcgen05_pair_f16", 512, 256, 600, f16, executor=4, cta_pair=1)
+spmm_case("spmm_tcgen05_pair_tf32x3", 300, 200, 517, f32, executor=4, cta_pair=1)
+spmm_case("spmm_tcgen05_split_tail", 128, 64, 38300, f16, executor=4)
 conv_case("conv_position_strided", 16, 24, 2, 14, 14, f32, conv_kernel=1)
 conv_case("conv_tma_fed", 32, 48, 3, 14, 14, f32, conv_kernel=2)
 conv_case("conv_register_staged", 32, 48, 3, 14, 14, f16, conv_kernel=3)
 conv_case("conv_interleaved", 32, 48, 3, 14, 14, f32, conv_kernel=4)
 conv_case("conv_interleaved_f16", 32, 48, 3, 14, 14, f16, conv_kernel=4)
 conv_case("conv_tcgen05", 64, 48, 3, 14, 14, f16, conv_kernel=5)
+conv_case("conv_tcgen05_im2col_pair_f16", 64, 256, 3, 14, 14, f16, conv_kernel=5, cta_pair=1)
+conv_case("conv_tcgen05_im2col_pair_tf32x3", 64, 256, 3, 14, 14, f32, conv_kernel=5, cta_pair=1)
+conv_case("conv_tcgen05_im2col_mc_tf32x3", 64, 256, 3, 14, 14, f32, conv_kernel=5, x_multicast=2)
+if not only or "conv_tcgen05_copies" in only:
+    os.environ["SRT_CONV_IM2COL"] = "0"
+    conv_case("conv_tcgen05_copies_f32", 64, 256, 3, 14, 14, f32, conv_kernel=5, x_multicast=2)
+    del os.environ["SRT_CONV_IM2COL"]
 if not only or "linear" in only:
     w = gen.int_weights(96, 128, 90, seed=9, vmax=3)
     xt = gen.int_x(300, 128, seed=10, vmax=3)
