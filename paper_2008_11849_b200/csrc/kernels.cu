@@ -2142,31 +2142,64 @@ __global__ void transpose_2d(const T* __restrict__ in, int64_t ldi, T* __restric
 }
 
 // CNHW -> NHWC for the im2col conv on the tcgen05 block executor: out[p][c] = in[c][p] (P = B H W
-// pixels), 32 channels x 64 pixels per CTA through shared memory; SPLIT (fp32 plans, 3xTF32):
-// out = TF32 RN of x, out_lo = TF32 RN of the remainder (x_lo = 0 for non-finite x).  Pure data
-// movement (+ the operand split).
+// pixels).  A CTA moves 32 channels x 128 pixels through shared memory: 16-byte loads along the
+// pixels of each channel row, 16-byte stores along the 32 channels of each pixel (128-byte
+// segments).  SPLIT (fp32 plans, 3xTF32): out = TF32 RN of x, out_lo = TF32 RN of the remainder
+// (0 for non-finite x).  Pure data movement (+ the operand split).
 template <typename T, bool SPLIT>
 __global__ void __launch_bounds__(256) nhwc_pack(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ out_lo,
                                                  int64_t C, int64_t P) {
-  __shared__ T tile[32][65];
-  const int64_t p0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 32;
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 pixels x 4 channel rows per pass
-  for (int i = ty; i < 32; i += 4) {
-    const int64_t c = c0 + i, px = p0 + tx;
-    tile[i][tx] = (c < C && px < P) ? in[c * P + px] : T(0);
+  constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
+  __shared__ T tile[32][128 + V];
+  const int64_t p0 = (int64_t)blockIdx.x * 128, c0 = (int64_t)blockIdx.y * 32;
+  const bool vec_in = (P % V) == 0 && p0 + 128 <= P && ((uintptr_t)in % 16) == 0;
+  // loads: warp w takes channel rows w, w + 8, ...; lane l the pixels l V .. l V + V - 1
+  for (int i = threadIdx.x >> 5; i < 32; i += 8) {
+    const int64_t c = c0 + i;
+    for (int e0 = (threadIdx.x & 31) * V; e0 < 128; e0 += 32 * V) {
+      if (vec_in && c < C) {
+        const uint4 v = __ldg((const uint4*)(in + c * P + p0 + e0));
+        const T* t = (const T*)&v;
+#pragma unroll
+        for (int k = 0; k < V; ++k) tile[i][e0 + k] = t[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const int64_t px = p0 + e0 + k;
+          tile[i][e0 + k] = (c < C && px < P) ? in[c * P + px] : T(0);
+        }
+      }
+    }
   }
   __syncthreads();
-  const int cx = threadIdx.x & 31, py = threadIdx.x >> 5;  // 32 channels x 8 pixels per pass
-  for (int j = py; j < 64; j += 8) {
-    const int64_t px = p0 + j, c = c0 + cx;
-    if (px >= P || c >= C) continue;
-    const T v = tile[cx][j];
-    if constexpr (SPLIT) {
-      const float h = tf32_rn_dev(v);
-      out[px * C + c] = h;
-      out_lo[px * C + c] = isfinite(h) ? tf32_rn_dev(v - h) : 0.0f;
+  // stores: 32 / V threads per pixel (one 16-byte vector of channels each)
+  constexpr int TPP = 32 / V;
+  const bool vec_out = (C % V) == 0 && c0 + 32 <= C;
+  for (int j = threadIdx.x / TPP; j < 128; j += 256 / TPP) {
+    const int64_t px = p0 + j;
+    if (px >= P) break;
+    const int cv = (threadIdx.x % TPP) * V;
+    alignas(16) T h[V], l[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const T v = tile[cv + k][j];
+      if constexpr (SPLIT) {
+        h[k] = tf32_rn_dev(v);
+        l[k] = isfinite(h[k]) ? tf32_rn_dev(v - h[k]) : 0.0f;
+      } else {
+        h[k] = v;
+      }
+    }
+    if (vec_out) {
+      *(uint4*)(out + px * C + c0 + cv) = *(const uint4*)h;
+      if constexpr (SPLIT) *(uint4*)(out_lo + px * C + c0 + cv) = *(const uint4*)l;
     } else {
-      out[px * C + c] = v;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if (c0 + cv + k >= C) break;
+        out[px * C + c0 + cv + k] = h[k];
+        if constexpr (SPLIT) out_lo[px * C + c0 + cv + k] = l[k];
+      }
     }
   }
 }
@@ -2691,6 +2724,9 @@ struct TcgArgs {
   // conv through im2col TMA (i2c = 1): X is NHWC (plane = B H W pixels, N = plane, ldy = plane),
   // B is K-major (pixel rows of 128-byte channel groups); each CTA loads i2c_pix pixels per tile
   int32_t i2c, i2c_pix;
+  // tile width (columns of Y per tile; 0 = 256): the im2col conv picks it so that the tiles fill
+  // the persistent clusters' rounds (C5: 196 tiles of 256 on 74 pairs = 2.65 rounds; 210 of 240)
+  int32_t bn;
 };
 
 // work item i of cluster cl: tile t and column slice (-1 = the whole tile)
@@ -2896,7 +2932,8 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
   const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * S;
   const uint32_t tfull0 = empty0 + 8 * S, tempty0 = tfull0 + 16;
   uint32_t* tslot = (uint32_t*)(bars + 2 * S + 4);
-  const int64_t nnb = (a.N + BN - 1) / BN;
+  const int BNT = a.bn > 0 ? a.bn : BN;  // tile width (the TMEM accumulators stay BN apart)
+  const int64_t nnb = (a.N + BNT - 1) / BNT;
   const int64_t ntiles = (int64_t)a.ngroups * nnb;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -2950,7 +2987,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       int slice;
       for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
         const int gi = (int)(t % a.ngroups);
-        const int64_t n0 = (t / a.ngroups) * BN;
+        const int64_t n0 = (t / a.ngroups) * BNT;
         const int j0 = meta[gi], j1 = meta[gi + 1];
         // boxes of this work item: the whole tile (this CTA loads boxes rank nb .. + nb - 1 and
         // multicasts them), or the slice's nbs boxes (box i loaded by rank i % CS) stored from
@@ -2982,7 +3019,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
           iy = rem / a.W;
           ix = rem - iy * a.W;
           i2c_dst = (CS > 1 && !pair) ? (uint32_t)rank * (uint32_t)a.i2c_pix * 128u : 0u;
-          tx = (uint32_t)(A_BYTES + (TF ? 2 : 1) * (pair ? a.i2c_pix : BN) * 128);
+          tx = (uint32_t)(A_BYTES + (TF ? 2 : 1) * (pair ? a.i2c_pix : BNT) * 128);
         }
         for (int j = j0; j < j1; ++j) {
           const int kb = meta[a.ngroups + 1 + j];
@@ -3119,9 +3156,9 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
-      const int64_t nt0 = (t / a.ngroups) * BN;
+      const int64_t nt0 = (t / a.ngroups) * BNT;
       // accumulator column c = tile column cbase + c (a slice: the first nacc columns)
-      const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BN : a.np;
+      const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BNT : a.np;
       const int64_t n0 = nt0 + cbase;
       const int nent = meta[gi + 1] - meta[gi];
       if (CONV && !a.i2c && nt0 != tab_n0) {
@@ -3240,9 +3277,9 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
-      const int64_t nt0 = (t / a.ngroups) * BN;
+      const int64_t nt0 = (t / a.ngroups) * BNT;
       // accumulator column c = tile column cbase + c (a slice: the first nacc columns)
-      const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BN : a.np;
+      const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BNT : a.np;
       const int64_t n0 = nt0 + cbase;
       const bool has = meta[gi + 1] > meta[gi];
       if (CONV && !a.i2c && nt0 != tab_n0) {
@@ -3619,7 +3656,7 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
     ~Free() { cudaFreeAsync(b, (cudaStream_t)st); }
   } fr{xn, stream};
   {
-    const dim3 grid((unsigned)((plane + 63) / 64), (unsigned)((p.c_in + 31) / 32));
+    const dim3 grid((unsigned)((plane + 127) / 128), (unsigned)((p.c_in + 31) / 32));
     if (tf)
       nhwc_pack<float, true><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)x, (float*)xn,
                                                                      (float*)((uint8_t*)xn + nb), p.c_in, plane);
@@ -3628,7 +3665,29 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
                                                                          p.c_in, plane);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "NHWC pack launch", err);
   }
-  const int cs = p.tcg_cs, pix = 256 / cs;
+  // tile width: fp32 (3xTF32, MMA-bound) fills the rounds of the persistent clusters (cost ~
+  // rounds x (width + a fixed per-tile cost of ~32 columns); C5: 240 -> 229 to 218 us); 16-bit
+  // plans keep 256 (their k-blocks are bounded by the W block bytes, which do not shrink with
+  // the width: 240 measured 68 -> 73 us).  SRT_CONV_BN overrides; a multiple of 16 (M = 256)
+  const int cs = p.tcg_cs;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+  int bn = 256;
+  {
+    const int64_t ncl = std::max(1, sms / cs);
+    int64_t best = INT64_MAX;
+    for (int w = 256; w >= (tf ? 128 : 256); w -= 16) {
+      if ((w / cs) % 8) continue;  // a CTA's pixel rows: whole 8-row (1 KB) swizzle atoms
+      const int64_t tiles = (int64_t)p.tcg_ngroups * ((plane + w - 1) / w);
+      const int64_t cost = (tiles + ncl - 1) / ncl * (w + 32);
+      if (cost < best) best = cost, bn = w;
+    }
+    if (const char* ev = std::getenv("SRT_CONV_BN")) {
+      const int v = std::atoi(ev);
+      if (v >= 16 * cs && v <= 256 && v % 16 == 0 && (v / cs) % 8 == 0) bn = v;
+    }
+  }
+  const int pix = bn / cs;
   CUtensorMap tmap, tmap2;
   std::memset(&tmap, 0, sizeof tmap);
   std::memset(&tmap2, 0, sizeof tmap2);
@@ -3667,15 +3726,17 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
   a.relu = ep.relu;
   // D fp32, A / B fp16 (0), bf16 (1) or tf32 (2), both K-major, N = 256, M = 128 (pair: 256)
   const uint32_t fmt = tf ? 2u : bf ? 1u : 0u;
-  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((256u >> 3) << 17) | (((p.tcg_pair ? 256u : 128u) >> 4) << 24);
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (((uint32_t)bn >> 3) << 17) |
+            (((p.tcg_pair ? 256u : 128u) >> 4) << 24);
   a.pair = p.tcg_pair;
   a.i2c = 1;
   a.i2c_pix = pix;
+  a.bn = bn;
   a.H = p.h;
   a.W = p.w;
   a.Bt = (int32_t)batch;
   a.plane = plane;
-  const int64_t ntiles = (int64_t)p.tcg_ngroups * ((plane + 255) / 256);
+  const int64_t ntiles = (int64_t)p.tcg_ngroups * ((plane + bn - 1) / bn);
   const bool pr = p.tcg_pair != 0;
   const void* fn = tf ? (pr ? (const void*)spmm_tcg_kernel<false, true, true, true>
                             : (const void*)spmm_tcg_kernel<false, true, true, false>)
