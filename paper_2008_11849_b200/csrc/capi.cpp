@@ -340,6 +340,12 @@ int sparse_conv3x3_nhwc(sparse_plan_t plan, int64_t batch, const void* x, void* 
   const srt::Plan& p = plan->p;
   const int S = p.dtype != SPARSE_F32 ? 2 : 4;
   const int64_t N = batch * (int64_t)p.h * p.w;
+  {  // tcgen05 block executor: the im2col TMA reads NHWC and the epilogue writes NHWC directly
+    std::string err;
+    const int rc = srt::launch_conv3x3_nhwc(p, batch, x, y, stream, err);
+    if (rc == SPARSE_OK) return ok();
+    if (rc != SPARSE_EUNSUPPORTED) return fail(rc, err);
+  }
   Scratch xt(p.device, (size_t)(p.c_in * N * S), stream), yt(p.device, (size_t)(p.M * N * S), stream);
   if (!xt.ok || !yt.ok) return fail(SPARSE_ENOMEM, "sparse_conv3x3_nhwc: cannot allocate the CNHW scratch");
   std::string err;

@@ -2727,6 +2727,9 @@ struct TcgArgs {
   // tile width (columns of Y per tile; 0 = 256): the im2col conv picks it so that the tiles fill
   // the persistent clusters' rounds (C5: 196 tiles of 256 on 74 pairs = 2.65 rounds; 210 of 240)
   int32_t bn;
+  // column stride of Y in elements (0 = 1): the NHWC conv writes Y[pixel][channel] (ldy = 1,
+  // ycs = M) - consecutive lanes (rows = output channels) store consecutive addresses
+  int64_t ycs;
 };
 
 // work item i of cluster cl: tile t and column slice (-1 = the whole tile)
@@ -3148,7 +3151,8 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     const bool epi = a.bias != nullptr || a.beta != 0.0f || a.relu;
     // per-warp staging buffer (32 rows x 64 B) for coalesced Y stores
     uint8_t* stg = (uint8_t*)tslot + 64 + 1024 + 4 * kTcgMetaMax + (warp - 2) * 2048;
-    const bool coal = ((a.ldy * 4) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
+    const int64_t ycs = a.ycs > 0 ? a.ycs : 1;
+    const bool coal = ycs == 1 && ((a.ldy * 4) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
     int32_t* otab = (int32_t*)((uint8_t*)tslot + 64);  // conv: span position -> output offset
     int64_t tab_n0 = -1;
     int64_t t;
@@ -3233,7 +3237,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
 #pragma unroll
         for (int c = 0; c < 128; ++c)
           if (row < a.M && hc + c < ncol)
-            m[c] = epilogue_one<false>(m[c], a.bias, row, a.beta, a.Y + ((int64_t)row * a.ldy + n0 + hc + c) * 4, a.relu);
+            m[c] = epilogue_one<false>(m[c], a.bias, row, a.beta, a.Y + ((int64_t)row * a.ldy + (n0 + hc + c) * ycs) * 4, a.relu);
       }
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 16) {
@@ -3254,10 +3258,10 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
             if (row0 + r < a.M) *(float4*)(a.Y + ((int64_t)(row0 + r) * a.ldy + n0 + hc + c0) * 4 + j * 16) = d4;
           }
         } else if (row < a.M) {
-          float* yp = (float*)(a.Y + ((int64_t)row * a.ldy + n0 + hc + c0) * 4);
+          float* yp = (float*)(a.Y + ((int64_t)row * a.ldy + (n0 + hc + c0) * ycs) * 4);
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (hc + c0 + c < ncol) yp[c] = m[c0 + c];
+            if (hc + c0 + c < ncol) yp[c * ycs] = m[c0 + c];
         }
       }
     }
@@ -3271,7 +3275,8 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     int64_t tab_n0 = -1;
     // per-warp staging buffer (32 rows x 128 B) for coalesced Y stores
     uint8_t* stg = (uint8_t*)tslot + 64 + 1024 + 4 * kTcgMetaMax + (warp - 2) * 4096;
-    const bool coal = a.beta == 0.0f && ((a.ldy * 2) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
+    const int64_t ycs = a.ycs > 0 ? a.ycs : 1;
+    const bool coal = ycs == 1 && a.beta == 0.0f && ((a.ldy * 2) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
     int64_t t;
     int slice;
     for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
@@ -3376,15 +3381,17 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         for (int h = 0; h < 2; ++h) {
           const int cc = c0 + 32 * h;
           if (cc >= ncol) break;
-          uint8_t* yp = a.Y + ((int64_t)row * a.ldy + n0 + cc) * 2;
+          uint8_t* yp = a.Y + ((int64_t)row * a.ldy + (n0 + cc) * ycs) * 2;
           alignas(16) uint16_t hv[32];
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
             float f = has ? __uint_as_float(v[32 * h + c]) : 0.0f;
-            if (epi && cc + c < ncol) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp + c * 2, a.relu);
+            if (epi && cc + c < ncol) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp + c * ycs * 2, a.relu);
             hv[c] = to16<BF>(f);
           }
-          if (cc + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
+          if (ycs != 1) {
+            for (int c = 0; c < 32 && cc + c < ncol; ++c) ((uint16_t*)yp)[c * ycs] = hv[c];
+          } else if (cc + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
 #pragma unroll
             for (int c = 0; c < 32; c += 8) *(uint4*)(yp + c * 2) = *(const uint4*)(hv + c);
           } else {
@@ -3632,7 +3639,7 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
 // shifted copies, no halo positions; the output tile is 256 consecutive pixels of the CNHW
 // plane, stored like an SpMM tile (ldy = plane).
 static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y, void* stream, std::string& err,
-                           const Epilogue& ep) {
+                           const Epilogue& ep, bool nhwc = false) {
   const bool bf = p.dtype == SPARSE_BF16, tf = p.dtype == SPARSE_F32;
   const int S = tf ? 4 : 2, BK = tf ? 32 : 64;
   auto encode = tensor_map_encoder_im2col();
@@ -3644,8 +3651,9 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
   DeviceGuard dg(p.device);
   if (dg.st != cudaSuccess) return cuda_fail(dg.st, "cudaSetDevice", err);
   void* xn = nullptr;  // NHWC input (fp32: X_hi, then X_lo)
+  const void* xn_user = nullptr;  // 16-bit NHWC input: read in place
   const size_t nb = (size_t)plane * p.c_in * S;
-  cudaError_t e = cudaMallocAsync(&xn, tf ? 2 * nb : nb, (cudaStream_t)stream);
+  cudaError_t e = cudaMallocAsync(&xn, (nhwc && !tf) ? 16 : (tf ? 2 * nb : nb), (cudaStream_t)stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return cuda_fail(e, "cudaMallocAsync(conv NHWC)", err);
@@ -3655,7 +3663,17 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
     void* st;
     ~Free() { cudaFreeAsync(b, (cudaStream_t)st); }
   } fr{xn, stream};
-  {
+  if (nhwc) {  // the input is NHWC already: 16-bit needs nothing, fp32 only the TF32 split
+    if (tf) {
+      const int64_t work = plane * ((p.c_in + 3) / 4);
+      const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)148 * 16));
+      split_tf32<<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)x, p.c_in, (float*)xn,
+                                                          (float*)((uint8_t*)xn + nb), p.c_in, plane, p.c_in);
+      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "3xTF32 split launch", err);
+    } else {
+      xn_user = x;
+    }
+  } else {
     const dim3 grid((unsigned)((plane + 127) / 128), (unsigned)((p.c_in + 31) / 32));
     if (tf)
       nhwc_pack<float, true><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)x, (float*)xn,
@@ -3697,7 +3715,8 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
   cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUtensorMapDataType dt = tf ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                : bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  CUresult r = encode(&tmap, dt, 4, xn, dims, strides, lower, upper, (cuuint32_t)BK, (cuuint32_t)pix, estr,
+  CUresult r = encode(&tmap, dt, 4, xn_user ? const_cast<void*>(xn_user) : xn, dims, strides, lower, upper,
+                      (cuuint32_t)BK, (cuuint32_t)pix, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r == CUDA_SUCCESS && tf)
@@ -3714,7 +3733,8 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
   a.meta = p.d_tcp_step_off;
   a.nblk = (int32_t)p.tcp_nsteps;
   a.Y = (uint8_t*)y;
-  a.ldy = plane;
+  a.ldy = nhwc ? 1 : plane;  // CNHW: Y[channel][pixel]; NHWC: Y[pixel][channel]
+  a.ycs = nhwc ? p.M : 1;
   a.N = plane;
   a.M = p.M;
   a.ngroups = p.tcg_ngroups;
@@ -4252,6 +4272,20 @@ static int launch_conv_il(const Plan& p, int64_t batch, const void* x, void* y, 
   e = cudaLaunchKernelEx(&cfg, fn, tmap, a);
   if (e != cudaSuccess) return cuda_fail(e, "conv3x3 (interleaved) launch", err);
   return SPARSE_OK;
+}
+
+// Channels-last conv directly on the tcgen05 block executor's im2col path: x NHWC is what the
+// im2col TMA reads (16-bit: in place; fp32: split into TF32 halves), y NHWC is written by the
+// epilogue with column stride M.  SPARSE_EUNSUPPORTED when the plan is not eligible (the caller
+// then transposes around launch_conv3x3).
+int launch_conv3x3_nhwc(const Plan& p, int64_t batch, const void* x, void* y, void* stream, std::string& err) {
+  const int S = p.dtype == SPARSE_F32 ? 4 : 2;
+  const char* ev = std::getenv("SRT_CONV_IM2COL");
+  if (p.executor != 4 || (ev && std::atoi(ev) == 0) || ((int64_t)p.c_in * S) % 16 != 0 || ((uintptr_t)x % 16) != 0 ||
+      batch * (int64_t)p.h * p.w >= INT32_MAX)
+    return SPARSE_EUNSUPPORTED;
+  Epilogue ep;
+  return launch_conv_i2c(p, batch, x, y, stream, err, ep, true);
 }
 
 int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* stream,

@@ -258,6 +258,7 @@ struct Epilogue {  // Y = act(acc + bias + beta * Y); see sparse_epilogue
 };
 int launch_spmm(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy,
                 void* stream, std::string& err, const Epilogue& ep = Epilogue());
+int launch_conv3x3_nhwc(const Plan& p, int64_t batch, const void* x, void* y, void* stream, std::string& err);
 int launch_conv3x3(const Plan& p, int64_t batch, const void* x, void* y, void* stream,
                    std::string& err, const Epilogue& ep = Epilogue());
 // Unaligned X (base or row stride not a 16-byte multiple): stream-ordered copy into a

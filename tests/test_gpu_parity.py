@@ -959,16 +959,18 @@ def test_conv1x1_strided_exact(cin, cout, B, h, w, s, dt):
     assert np.array_equal(y.double().cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("opts", [{}, {"conv_kernel": 5}, {"conv_kernel": 5, "cta_pair": 1}])
 @pytest.mark.parametrize("dt", ["f32", "f16"])
 @pytest.mark.parametrize("cin,cout,B,H,W", [(64, 64, 2, 56, 56), (256, 256, 3, 14, 14), (12, 20, 2, 7, 9)])
-def test_conv3x3_nhwc_exact(cin, cout, B, H, W, dt):
-    # channels-last activations: exact on integer data, and bitwise the CNHW call
+def test_conv3x3_nhwc_exact(cin, cout, B, H, W, dt, opts):
+    # channels-last activations: exact on integer data, and bitwise the CNHW call (conv_kernel 5:
+    # the im2col TMA reads NHWC in place and the epilogue writes NHWC, no transposes)
     dev = _dev()
     tdt = torch.float16 if dt == "f16" else torch.float32
     vw, vx = (3, 3) if dt == "f32" else (2, 4)
     wi = gen.int_weights(cout, 9 * cin, 90, seed=cin + W, vmax=vw)
     x = gen.int_x(cin * B * H, W, seed=cout, vmax=vx).reshape(cin, B, H, W)
-    plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, **opts)
     xt = torch.from_numpy(x).to(dev).to(tdt)
     y_nhwc = plan.conv3x3_nhwc(xt.permute(1, 2, 3, 0).contiguous())
     y_cnhw = plan.conv3x3(xt)
