@@ -385,7 +385,7 @@ int sparse_plan_info(sparse_plan_t plan, sparse_plan_info_t* out) {
   out->k_chunk = p.kind == SPARSE_CONV3X3 ? p.cc : p.kc;
   out->chunks = p.nchunks;
   out->split_k = p.gk;
-  out->k_split = p.ks;
+  out->k_split = p.executor == 4 ? p.tcg_ks : p.ks;
   out->stages = p.stages;
   out->smem_bytes = p.smem_bytes;
   out->device = p.device;

@@ -565,6 +565,20 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
     err = "rows_per_warp too large for this dtype (accumulator registers)";
     return SPARSE_EUNSUPPORTED;
   }
+  if (o.executor == 4) {
+    // tcgen05 block executor: k_split = K slices per tile, partial sums reduced in slice order by
+    // a second kernel (small-N layers: few tiles for 148 SMs); the CUDA-core part keeps 1
+    p.tcg_ks = o.k_split ? o.k_split : 1;
+    p.ks = 1;
+    if (p.tcg_ks != 1 && p.tcg_ks != 2 && p.tcg_ks != 4 && p.tcg_ks != 8 && p.tcg_ks != 16) {
+      err = "k_split must be 1, 2, 4, 8 or 16 for the tcgen05 block executor";
+      return SPARSE_EUNSUPPORTED;
+    }
+    if (p.tcg_ks > 1 && o.kind != SPARSE_SPMM) {
+      err = "k_split is only supported for SpMM plans";
+      return SPARSE_EUNSUPPORTED;
+    }
+  }
   if (p.ks != 1 && p.ks != 2 && p.ks != 4 && p.ks != 8) {
     err = "k_split must be 1, 2, 4 or 8";
     return SPARSE_EUNSUPPORTED;
@@ -1145,7 +1159,7 @@ int build_plan(Plan& p, int32_t M, int32_t K, int64_t nnz, const int32_t* row_pt
                          p.w,  p.warps,  p.R,       p.gk,      p.C,      p.n_tile,
                          p.kc, p.nchunks, p.npanels, p.conv_rb, p.conv_ipt, p.ks, p.cm, p.tm,
                          p.conv_vec, p.row_order, p.executor, p.jit_mp, p.jit_warps, p.stages,
-                         p.tc_min_pct, p.ps, p.tcg_cs, p.tcg_bk, p.tcg_pair};
+                         p.tc_min_pct, p.ps, p.tcg_cs, p.tcg_bk, p.tcg_pair, p.tcg_ks};
   h = fnv1a(h, cfg, sizeof cfg);
   h = fnv1a(h, p.row_id.data(), p.row_id.size() * 4);
   h = fnv1a(h, p.blk_off.data(), p.blk_off.size() * 8);

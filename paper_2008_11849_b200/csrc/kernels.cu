@@ -2730,12 +2730,21 @@ struct TcgArgs {
   // column stride of Y in elements (0 = 1): the NHWC conv writes Y[pixel][channel] (ldy = 1,
   // ycs = M) - consecutive lanes (rows = output channels) store consecutive addresses
   int64_t ycs;
+  // K slices per tile (ks > 1): work item = (tile, slice), a slice's k-block range is
+  // [j0 + L s / ks, j0 + L (s + 1) / ks); its fp32 partial goes to ws[s][column][row] (rows
+  // contiguous: lanes store consecutive addresses) and tcg_ksum adds the slices in order
+  int32_t ks;
+  float* ws;
 };
 
 // work item i of cluster cl: tile t and column slice (-1 = the whole tile)
 __device__ __forceinline__ bool tcg_work(const TcgArgs& a, int64_t cl, int64_t ncl, int64_t i, int64_t ntiles,
                                          int64_t& t, int& slice) {
   slice = -1;
+  if (a.ks > 1) {  // (tile, K slice) items; t carries the slice in its low bits: see tcg_kslice
+    t = cl + i * ncl;
+    return t < ntiles * a.ks;
+  }
   if (a.sp <= 1 || i < a.rounds) {
     t = cl + i * ncl;
     return t < ntiles;
@@ -2746,6 +2755,24 @@ __device__ __forceinline__ bool tcg_work(const TcgArgs& a, int64_t cl, int64_t n
     return true;
   }
   return false;
+}
+
+// K-sliced items (ks > 1): item -> tile (returned) and slice ksl
+__device__ __forceinline__ int64_t tcg_item(const TcgArgs& a, int64_t item, int& ksl) {
+  if (a.ks <= 1) {
+    ksl = 0;
+    return item;
+  }
+  const int64_t t = item / a.ks;
+  ksl = (int)(item - t * a.ks);
+  return t;
+}
+// the slice's part [j0, j1) of the group's k-block entries
+__device__ __forceinline__ void tcg_krange(const TcgArgs& a, int ksl, int& j0, int& j1) {
+  if (a.ks <= 1) return;
+  const int L = j1 - j0, jb = j0;
+  j0 = jb + (int)((int64_t)L * ksl / a.ks);
+  j1 = jb + (int)((int64_t)L * (ksl + 1) / a.ks);
 }
 
 // shared-memory matrix descriptor: start, leading / stride byte offsets, version 1 (bit 46),
@@ -2989,9 +3016,12 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       int64_t t;
       int slice;
       for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
+        int ksl;
+        t = tcg_item(a, t, ksl);
         const int gi = (int)(t % a.ngroups);
         const int64_t n0 = (t / a.ngroups) * BNT;
-        const int j0 = meta[gi], j1 = meta[gi + 1];
+        int j0 = meta[gi], j1 = meta[gi + 1];
+        tcg_krange(a, ksl, j0, j1);
         // boxes of this work item: the whole tile (this CTA loads boxes rank nb .. + nb - 1 and
         // multicasts them), or the slice's nbs boxes (box i loaded by rank i % CS) stored from
         // box 0 of the stage.  This thread's loads: stage positions pos0 + i pstep, i < cnt, of
@@ -3086,8 +3116,11 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       int64_t t;
       int slice;
       for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
+        int ksl;
+        t = tcg_item(a, t, ksl);
         const int gi = (int)(t % a.ngroups);
-        const int j0 = meta[gi], j1 = meta[gi + 1];
+        int j0 = meta[gi], j1 = meta[gi + 1];
+        tcg_krange(a, ksl, j0, j1);
         const uint32_t idesc = slice < 0 ? a.idesc : a.idesc_p;
         int j = j0;
         do {
@@ -3158,13 +3191,17 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     int64_t t;
     int slice;
     for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
+      int ksl;
+      t = tcg_item(a, t, ksl);
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
       const int64_t nt0 = (t / a.ngroups) * BNT;
       // accumulator column c = tile column cbase + c (a slice: the first nacc columns)
       const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BNT : a.np;
       const int64_t n0 = nt0 + cbase;
-      const int nent = meta[gi + 1] - meta[gi];
+      int kj0 = meta[gi], kj1 = meta[gi + 1];
+      tcg_krange(a, ksl, kj0, kj1);
+      const int nent = kj1 - kj0;
       if (CONV && !a.i2c && nt0 != tab_n0) {
         tcg_conv_table<32 * NEPI>(otab, nt0, a, threadIdx.x - 64);
         tab_n0 = nt0;
@@ -3198,6 +3235,15 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)max((int64_t)0, min((int64_t)nacc, a.N - n0));
       if (row0 >= a.M || (a.dbg & 1)) continue;
+      if (a.ks > 1) {  // K slice: the fp32 partial, column-major (lanes = consecutive rows)
+        if (row < a.M) {
+          float* wp = a.ws + ((size_t)ksl * a.N + n0 + hc) * a.M + row;
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (hc + c < ncol) wp[(size_t)c * a.M] = m[c];
+        }
+        continue;
+      }
       if (CONV && !a.i2c) {
         // span positions -> CNHW pixels (otab; -1 = halo / padding / past the span)
         if (hc >= nacc) continue;
@@ -3280,13 +3326,17 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     int64_t t;
     int slice;
     for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
+      int ksl;
+      t = tcg_item(a, t, ksl);
       const int gi = (int)(t % a.ngroups);
       const int rb = gi * CS + (int)rank;
       const int64_t nt0 = (t / a.ngroups) * BNT;
       // accumulator column c = tile column cbase + c (a slice: the first nacc columns)
       const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BNT : a.np;
       const int64_t n0 = nt0 + cbase;
-      const bool has = meta[gi + 1] > meta[gi];
+      int kj0 = meta[gi], kj1 = meta[gi + 1];
+      tcg_krange(a, ksl, kj0, kj1);
+      const bool has = kj1 > kj0;
       if (CONV && !a.i2c && nt0 != tab_n0) {
         tcg_conv_table<128>(otab, nt0, a, threadIdx.x - 64);
         tab_n0 = nt0;
@@ -3303,6 +3353,15 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         tm_ld32(ta, v);
         tm_ld32(ta + 32, v + 32);
         tm_wait_ld();
+        if (a.ks > 1) {  // K slice: the fp32 partial, column-major (lanes = consecutive rows)
+          if (row < a.M && c0 < ncol) {
+            float* wp = a.ws + ((size_t)ksl * a.N + n0 + c0) * a.M + row;
+#pragma unroll
+            for (int c = 0; c < 64; ++c)
+              if (c0 + c < ncol) wp[(size_t)c * a.M] = has ? __uint_as_float(v[c]) : 0.0f;
+          }
+          continue;
+        }
         if (CONV && !a.i2c) {
           if (a.beta != 0.0f) {  // beta * Y_old: element-wise (the fp32 sum needs Y_old)
             if (row >= a.M) continue;
@@ -3485,14 +3544,15 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   cfg.attrs = attr;
   cfg.numAttrs = cs > 1 ? 2 : 1;
   cfg.gridDim = dim3((unsigned)cs, 1, 1);
-  cfg.gridDim = dim3(tcg_grid(fn, cfg, cs, ntiles, sms), 1, 1);
+  const int64_t items = a.ks > 1 ? ntiles * a.ks : ntiles;  // (tile, K slice) work items
+  cfg.gridDim = dim3(tcg_grid(fn, cfg, cs, items, sms), 1, 1);
   // split tail: when the tiles do not fill the last round of the persistent clusters (C5 conv:
   // 224 tiles on 74 clusters = 3 rounds + 2 tiles), each last-round tile is cut into sp column
   // slices of whole X boxes (a power of two: 16-bit <= 4, fp32 <= 8), one per otherwise idle
   // cluster; a slice streams the tile's whole W block list with an N = 256 / sp MMA.
   // SRT_TCG_SPLIT_TAIL=0 disables it (A/B); n > 0 caps sp.
   const int64_t ncl = cfg.gridDim.x / cs;
-  int cap = a.i2c ? 1 : (tf ? 8 : 4) / (a.pair ? 2 : 1);  // a slice is >= 1 X box (pair: per CTA)
+  int cap = (a.i2c || a.ks > 1) ? 1 : (tf ? 8 : 4) / (a.pair ? 2 : 1);  // a slice is >= 1 X box (pair: per CTA)
   if (const char* st = std::getenv("SRT_TCG_SPLIT_TAIL")) cap = std::min(cap, std::max(1, std::atoi(st)));
   a.rounds = (int32_t)(ntiles / ncl);
   a.ntail = (int32_t)(ntiles % ncl);
@@ -3522,6 +3582,36 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   e = cudaLaunchKernelEx(&cfg, fn, tmap, tmap2, tmapA, a);
   if (e != cudaSuccess) return cuda_fail(e, what, err);
   return SPARSE_OK;
+}
+
+// K-sliced tcgen05 tiles: Y = epilogue(sum over slices s = 0 .. ks - 1, in order, of ws[s]); ws is
+// column-major per slice ([s][column][row]).  32 x 32 tiles through shared memory: reads along
+// the rows, writes along the columns.  fp32 sums, one rounding to the output type.
+template <int S, bool BF>
+__global__ void __launch_bounds__(256) tcg_ksum(const float* __restrict__ ws, int ks, int64_t M, int64_t N,
+                                                uint8_t* __restrict__ Y, int64_t ldy, const uint8_t* __restrict__ bias,
+                                                float beta, int relu) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int j = ty; j < 32; j += 8) {
+    const int64_t c = c0 + j, r = r0 + tx;
+    float v = 0.0f;
+    if (c < N && r < M) {
+      v = __ldg(ws + c * M + r);
+      for (int sx = 1; sx < ks; ++sx) v = __fadd_rn(v, __ldg(ws + ((int64_t)sx * N + c) * M + r));
+    }
+    tile[j][tx] = v;
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    const int64_t r = r0 + j, c = c0 + tx;
+    if (r >= M || c >= N) continue;
+    uint8_t* yp = Y + (r * ldy + c) * S;
+    const float f = epilogue_one<S == 2, BF>(tile[tx][j], bias, (int)r, beta, yp, relu);
+    if constexpr (S == 2) *(uint16_t*)yp = to16<BF>(f);
+    else *(float*)yp = f;
+  }
 }
 
 static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void* Y, int64_t ldy, void* stream,
@@ -3627,7 +3717,37 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
                             : (const void*)spmm_tcg_kernel<true, false, false, false>)
                       : (pr ? (const void*)spmm_tcg_kernel<false, false, false, true>
                             : (const void*)spmm_tcg_kernel<false, false, false, false>);
-  return tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "tcgen05 block launch", tf ? 320 : 192);
+  if (p.tcg_ks <= 1)
+    return tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "tcgen05 block launch", tf ? 320 : 192);
+  // K slices: fp32 partials in a stream-ordered workspace, then tcg_ksum (ordered sum + epilogue)
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, (size_t)p.tcg_ks * (size_t)N * (size_t)p.M * 4, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_fail(e, "cudaMallocAsync(K-slice partials)", err);
+  }
+  struct FreeWs {
+    void* b;
+    void* st;
+    ~FreeWs() { cudaFreeAsync(b, (cudaStream_t)st); }
+  } fw{ws, stream};
+  a.ks = p.tcg_ks;
+  a.ws = (float*)ws;
+  a.bias = nullptr, a.beta = 0.0f, a.relu = 0;
+  int rc = tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "tcgen05 block launch (K slices)", tf ? 320 : 192);
+  if (rc != SPARSE_OK) return rc;
+  const dim3 grid((unsigned)((p.M + 31) / 32), (unsigned)((N + 31) / 32));
+  if (tf)
+    tcg_ksum<4, false><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)ws, p.tcg_ks, p.M, N, (uint8_t*)Y, ldy,
+                                                               (const uint8_t*)ep.bias, ep.beta, ep.relu);
+  else if (bf)
+    tcg_ksum<2, true><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)ws, p.tcg_ks, p.M, N, (uint8_t*)Y, ldy,
+                                                              (const uint8_t*)ep.bias, ep.beta, ep.relu);
+  else
+    tcg_ksum<2, false><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)ws, p.tcg_ks, p.M, N, (uint8_t*)Y, ldy,
+                                                               (const uint8_t*)ep.bias, ep.beta, ep.relu);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "K-slice sum launch", err);
+  return SPARSE_OK;
 }
 
 // Conv on the tcgen05 block executor (conv_kernel 5): the interleaved copies pre-pass (pitch a

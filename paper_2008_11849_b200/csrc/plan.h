@@ -103,6 +103,8 @@ struct Plan {
   // CTA pairs (tcg_cs = 2): one cta_group::2 M = 256 MMA per step, each CTA stages its W block
   // and half of the X tile
   int32_t tcg_pair = 0;
+  // K slices per tile (k_split for executor 4): fp32 partials to a workspace, then tcg_ksum
+  int32_t tcg_ks = 1;
 
   // packed plan (host copy)
   std::vector<int32_t> row_id;   // npanels * Mp, -1 = empty slot

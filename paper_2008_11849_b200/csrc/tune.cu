@@ -152,6 +152,20 @@ int tune_plan(Plan& best, int32_t M, int32_t K, int64_t nnz, const int32_t* row_
       cands.push_back(t);
       t.pair = 0;
     }
+    // few tiles for 148 SMs (small N): K slices per tile, reduced in order by a second kernel
+    {
+      const int64_t tiles = (int64_t)((M + 127) / 128) * ((base.n_hint + 255) / 256);
+      const int bk = S == 2 ? 64 : 32, nkb = (K + bk - 1) / bk;
+      for (int ks : {2, 4, 8, 16}) {
+        if (tiles * ks > 2 * 148 || nkb < 2 * ks) continue;
+        t.cm = (M + 127) / 128 >= 2 ? 2 : 1;
+        t.pair = t.cm == 2;
+        t.k_split = ks;
+        cands.push_back(t);
+      }
+      t.k_split = base.k_split;
+      t.pair = 0;
+    }
   } else {
     // vectorised kernels (16-byte loads of consecutive positions; TMA-fed = 2, register-
     // staged = 1) and the position-strided one (0); cc = channels per chunk (0: inspector)

@@ -358,3 +358,18 @@ def test_cta_pair_validation():
     a = _plan(w, torch.float16, n_hint=256, executor=4, cta_pair=1).info
     b = _plan(w, torch.float16, n_hint=256, executor=4, x_multicast=2).info
     assert a["digest"] != b["digest"]  # same blocks, different executor geometry
+
+
+def test_tcgen05_kslices_option():
+    # k_split on the tcgen05 block executor: 1, 2, 4, 8 or 16 K slices per tile (SpMM only)
+    import torch
+    w = gen.pruned_weights(256, 1024, 90, seed=2)
+    info = _plan(w, torch.float16, n_hint=392, executor=4, k_split=16).info
+    assert info["executor"] == 4 and info["k_split"] == 16
+    with pytest.raises(srt.SparseRTError):
+        _plan(w, torch.float16, n_hint=392, executor=4, k_split=3)
+    with pytest.raises(srt.SparseRTError):   # the CUDA-core executor's cluster K split stops at 8
+        _plan(w, torch.float16, n_hint=392, executor=0, k_split=16)
+    a = _plan(w, torch.float16, n_hint=392, executor=4, k_split=4).info
+    b = _plan(w, torch.float16, n_hint=392, executor=4, k_split=8).info
+    assert a["digest"] != b["digest"]

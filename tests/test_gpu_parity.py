@@ -1372,3 +1372,64 @@ def test_conv_tcgen05_pair_exact(cin, cout, B, H, W, p, dt):
                          np.ascontiguousarray(x[:, sel]).astype(np.float64))
     ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
     assert np.array_equal(y[:, sel].double().cpu().numpy(), ref)
+
+
+# ------------------------------------------- tcgen05 blocks: K slices per tile (small N)
+
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32"])
+@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("M,K,N,ks", [(512, 2048, 392, 16), (2048, 512, 392, 4), (256, 1024, 1568, 8),
+                                       (300, 200, 517, 2), (128, 3072, 49, 16)])
+def test_tcgen05_kslices_exact(M, K, N, ks, pair, dt):
+    # k_split = ks on the tcgen05 block executor: every tile's k-blocks cut into ks slices on
+    # different CTAs, fp32 partials summed in slice order by tcg_ksum.  Bitwise on integer data;
+    # real-valued data within the dtype's tolerance
+    dev = _dev()
+    if pair and M <= 128:
+        pytest.skip("a CTA pair needs two row blocks")
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}[dt]
+    wi = gen.int_weights(M, K, 90, seed=M + K + ks, vmax=2)
+    xi = gen.int_x(K, N, seed=N + ks, vmax=4)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, executor=4, k_split=ks, cta_pair=pair)
+    assert plan.info["executor"] == 4 and plan.info["k_split"] == ks
+    Y = torch.full((M, N), float("nan"), dtype=tdt, device=dev)
+    plan.spmm(torch.from_numpy(xi).to(dev).to(tdt), Y)
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), xi.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(Y.double().cpu().numpy(), ref)
+    again = srt.Plan.from_csr(wi, dtype=tdt, n_hint=N, **plan.chosen_opts())
+    assert again.info["digest"] == plan.info["digest"]
+    w = gen.pruned_weights(M, K, 90, seed=M * 13 + K)
+    x = gen.uniform_x(K, N, seed=N + 19)
+    plan = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, executor=4, k_split=ks, cta_pair=pair)
+    Y = plan.spmm(torch.from_numpy(x).to(dev).to(tdt))
+    torch.cuda.synchronize()
+    wv = torch.from_numpy(w.values).to(tdt).double().numpy()
+    xv = torch.from_numpy(x).to(tdt).double().numpy()
+    err = oracle.rel_l2(Y.double().cpu().numpy(), oracle.spmm(M, K, w.row_ptr, w.col_idx, wv, xv))
+    assert err <= (F32_TOL if dt == "f32" else F16_TOL), err
+
+
+@pytest.mark.parametrize("dt", ["f16", "f32"])
+def test_tcgen05_kslices_epilogue(dt):
+    # K slices + fused bias / beta / ReLU (applied once, by the ordered sum), ldy > N
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    M, K, N = 400, 1024, 300
+    w = gen.int_weights(M, K, 90, seed=34, vmax=2)
+    xi = gen.int_x(K, N, seed=35, vmax=4)
+    rng = np.random.default_rng(36)
+    bias = rng.integers(-8, 9, M).astype(np.float32)
+    y0 = rng.integers(-8, 9, (M, N)).astype(np.float32)
+    plan = srt.Plan.from_csr(w, dtype=tdt, n_hint=N, executor=4, k_split=8, cta_pair=1)
+    Yb = torch.zeros((M, N + 24), dtype=tdt, device=dev)
+    Yb[:, :N] = torch.from_numpy(y0).to(dev).to(tdt)
+    plan.spmm(torch.from_numpy(xi).to(dev).to(tdt), Yb[:, :N], bias=torch.from_numpy(bias).to(dev).to(tdt),
+              beta=0.5, relu=True)
+    torch.cuda.synchronize()
+    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), xi.astype(np.float64))
+    ref = np.maximum(ref + bias[:, None] + 0.5 * y0, 0.0)
+    ref = _f16_round(ref) if dt == "f16" else ref.astype(np.float32).astype(np.float64)
+    assert np.array_equal(Yb[:, :N].double().cpu().numpy(), ref)
+    assert torch.count_nonzero(Yb[:, N:]) == 0
