@@ -3720,6 +3720,10 @@ static int launch_tcg(const Plan& p, int64_t N, const void* X, int64_t ldx, void
   if (p.tcg_ks <= 1)
     return tcg_launch(p, fn, tmap, tmap2, a, ntiles, stream, err, "tcgen05 block launch", tf ? 320 : 192);
   // K slices: fp32 partials in a stream-ordered workspace, then tcg_ksum (ordered sum + epilogue)
+  if ((N + 31) / 32 > 65535 || (p.M + 31) / 32 > INT32_MAX) {
+    err = "tcgen05 K slices: N too large for the slice sum (use k_split = 1)";
+    return SPARSE_EUNSUPPORTED;
+  }
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, (size_t)p.tcg_ks * (size_t)N * (size_t)p.M * 4, (cudaStream_t)stream);
   if (e != cudaSuccess) {
