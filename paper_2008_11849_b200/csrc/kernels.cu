@@ -2735,12 +2735,24 @@ struct TcgArgs {
   // contiguous: lanes store consecutive addresses) and tcg_ksum adds the slices in order
   int32_t ks;
   float* ws;
+  // tail K slices (tks > 1, chosen at launch): the `ntail` tiles left after `rounds` full rounds
+  // are each cut into tks K slices, one per otherwise idle cluster; slice partials go to
+  // tws[(slice ntail + tail tile) BNT + column][group row] and tcg_tailsum adds them in order
+  int32_t tks;
+  float* tws;
 };
 
 // work item i of cluster cl: tile t and column slice (-1 = the whole tile)
 __device__ __forceinline__ bool tcg_work(const TcgArgs& a, int64_t cl, int64_t ncl, int64_t i, int64_t ntiles,
-                                         int64_t& t, int& slice) {
+                                         int64_t& t, int& slice, int& tk) {
   slice = -1;
+  tk = -1;
+  if (a.tks > 1 && i >= a.rounds) {  // tail K slices
+    if (i > a.rounds || cl >= (int64_t)a.ntail * a.tks) return false;
+    t = (int64_t)a.rounds * ncl + cl / a.tks;
+    tk = (int)(cl % a.tks);
+    return true;
+  }
   if (a.ks > 1) {  // (tile, K slice) items; t carries the slice in its low bits: see tcg_kslice
     t = cl + i * ncl;
     return t < ntiles * a.ks;
@@ -2767,12 +2779,13 @@ __device__ __forceinline__ int64_t tcg_item(const TcgArgs& a, int64_t item, int&
   ksl = (int)(item - t * a.ks);
   return t;
 }
-// the slice's part [j0, j1) of the group's k-block entries
-__device__ __forceinline__ void tcg_krange(const TcgArgs& a, int ksl, int& j0, int& j1) {
-  if (a.ks <= 1) return;
+// the slice's part [j0, j1) of the group's k-block entries (plan K slices, or a tail K slice)
+__device__ __forceinline__ void tcg_krange(const TcgArgs& a, int ksl, int tk, int& j0, int& j1) {
+  const int n = tk >= 0 ? a.tks : a.ks, k = tk >= 0 ? tk : ksl;
+  if (n <= 1) return;
   const int L = j1 - j0, jb = j0;
-  j0 = jb + (int)((int64_t)L * ksl / a.ks);
-  j1 = jb + (int)((int64_t)L * (ksl + 1) / a.ks);
+  j0 = jb + (int)((int64_t)L * k / n);
+  j1 = jb + (int)((int64_t)L * (k + 1) / n);
 }
 
 // shared-memory matrix descriptor: start, leading / stride byte offsets, version 1 (bit 46),
@@ -3014,14 +3027,14 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       int s = 0;
       uint32_t ph = 0;
       int64_t t;
-      int slice;
-      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
+      int slice, tk;
+      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk); ++it) {
         int ksl;
         t = tcg_item(a, t, ksl);
         const int gi = (int)(t % a.ngroups);
         const int64_t n0 = (t / a.ngroups) * BNT;
         int j0 = meta[gi], j1 = meta[gi + 1];
-        tcg_krange(a, ksl, j0, j1);
+        tcg_krange(a, ksl, tk, j0, j1);
         // boxes of this work item: the whole tile (this CTA loads boxes rank nb .. + nb - 1 and
         // multicasts them), or the slice's nbs boxes (box i loaded by rank i % CS) stored from
         // box 0 of the stage.  This thread's loads: stage positions pos0 + i pstep, i < cnt, of
@@ -3114,13 +3127,13 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       int s = 0, acc = 0;
       uint32_t ph = 0, aph[2] = {0u, 0u};
       int64_t t;
-      int slice;
-      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
+      int slice, tk;
+      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk); ++it) {
         int ksl;
         t = tcg_item(a, t, ksl);
         const int gi = (int)(t % a.ngroups);
         int j0 = meta[gi], j1 = meta[gi + 1];
-        tcg_krange(a, ksl, j0, j1);
+        tcg_krange(a, ksl, tk, j0, j1);
         const uint32_t idesc = slice < 0 ? a.idesc : a.idesc_p;
         int j = j0;
         do {
@@ -3189,8 +3202,8 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     int32_t* otab = (int32_t*)((uint8_t*)tslot + 64);  // conv: span position -> output offset
     int64_t tab_n0 = -1;
     int64_t t;
-    int slice;
-    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
+    int slice, tk;
+    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk); ++it) {
       int ksl;
       t = tcg_item(a, t, ksl);
       const int gi = (int)(t % a.ngroups);
@@ -3200,7 +3213,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BNT : a.np;
       const int64_t n0 = nt0 + cbase;
       int kj0 = meta[gi], kj1 = meta[gi + 1];
-      tcg_krange(a, ksl, kj0, kj1);
+      tcg_krange(a, ksl, tk, kj0, kj1);
       const int nent = kj1 - kj0;
       if (CONV && !a.i2c && nt0 != tab_n0) {
         tcg_conv_table<32 * NEPI>(otab, nt0, a, threadIdx.x - 64);
@@ -3235,6 +3248,15 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)max((int64_t)0, min((int64_t)nacc, a.N - n0));
       if (row0 >= a.M || (a.dbg & 1)) continue;
+      if (tk >= 0) {  // tail K slice: the fp32 partial of this CTA's rows, lanes = consecutive rows
+        const int R = CS * 128;
+        float* wp = a.tws + ((size_t)(tk * a.ntail + (t - (int64_t)a.rounds * ncl)) * BNT + hc) * R +
+                    (int)rank * 128 + q * 32 + lane;
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (hc + c < ncol) wp[(size_t)c * R] = m[c];
+        continue;
+      }
       if (a.ks > 1) {  // K slice: the fp32 partial, column-major (lanes = consecutive rows)
         if (row < a.M) {
           float* wp = a.ws + ((size_t)ksl * a.N + n0 + hc) * a.M + row;
@@ -3324,8 +3346,8 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     const int64_t ycs = a.ycs > 0 ? a.ycs : 1;
     const bool coal = ycs == 1 && a.beta == 0.0f && ((a.ldy * 2) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
     int64_t t;
-    int slice;
-    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice); ++it) {
+    int slice, tk;
+    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk); ++it) {
       int ksl;
       t = tcg_item(a, t, ksl);
       const int gi = (int)(t % a.ngroups);
@@ -3335,7 +3357,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BNT : a.np;
       const int64_t n0 = nt0 + cbase;
       int kj0 = meta[gi], kj1 = meta[gi + 1];
-      tcg_krange(a, ksl, kj0, kj1);
+      tcg_krange(a, ksl, tk, kj0, kj1);
       const bool has = kj1 > kj0;
       if (CONV && !a.i2c && nt0 != tab_n0) {
         tcg_conv_table<128>(otab, nt0, a, threadIdx.x - 64);
@@ -3353,6 +3375,17 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         tm_ld32(ta, v);
         tm_ld32(ta + 32, v + 32);
         tm_wait_ld();
+        if (tk >= 0) {  // tail K slice: the fp32 partial of this CTA's rows
+          if (row0 < a.M && c0 < ncol) {
+            const int R = CS * 128;
+            float* wp = a.tws + ((size_t)(tk * a.ntail + (t - (int64_t)a.rounds * ncl)) * BNT + c0) * R +
+                        (int)rank * 128 + q * 32 + lane;
+#pragma unroll
+            for (int c = 0; c < 64; ++c)
+              if (c0 + c < ncol) wp[(size_t)c * R] = has ? __uint_as_float(v[c]) : 0.0f;
+          }
+          continue;
+        }
         if (a.ks > 1) {  // K slice: the fp32 partial, column-major (lanes = consecutive rows)
           if (row < a.M && c0 < ncol) {
             float* wp = a.ws + ((size_t)ksl * a.N + n0 + c0) * a.M + row;
@@ -3505,6 +3538,50 @@ __global__ void __launch_bounds__(256) split_tf32(const float* __restrict__ X, i
   }
 }
 
+// Tail K slices: Y tile = epilogue(sum over slices s = 0 .. tks - 1, in order, of the slices'
+// partials) for the ntail tail tiles (tile rounds * ncl + tt: group t % ngroups, N tile t /
+// ngroups); 32 x 32 blocks through shared memory.  Y element (row, col) at row ldy + col ycs.
+template <int S, bool BF>
+__global__ void __launch_bounds__(256) tcg_tailsum(const float* __restrict__ tws, int tks, int ntail, int bnt, int R,
+                                                   int64_t tile0, int ngroups, int64_t M, int64_t N,
+                                                   uint8_t* __restrict__ Y, int64_t ldy, int64_t ycs,
+                                                   const uint8_t* __restrict__ bias, float beta, int relu) {
+  __shared__ float tile[32][33];
+  const int tt = blockIdx.z;
+  const int64_t t = tile0 + tt;
+  const int64_t row0 = (t % ngroups) * R + (int64_t)blockIdx.x * 32, col0 = (t / ngroups) * bnt + (int64_t)blockIdx.y * 32;
+  const int cl0 = blockIdx.y * 32, rl0 = blockIdx.x * 32;  // within the tile
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int j = ty; j < 32; j += 8) {
+    const int cl = cl0 + j;
+    float v = 0.0f;
+    if (cl < bnt && row0 + tx < M && col0 + j < N) {
+      const size_t off = (size_t)cl * R + rl0 + tx;
+      v = __ldg(tws + (size_t)tt * bnt * R + off);
+      for (int sx = 1; sx < tks; ++sx) v = __fadd_rn(v, __ldg(tws + ((size_t)sx * ntail + tt) * bnt * R + off));
+    }
+    tile[j][tx] = v;
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    const int64_t r = row0 + j, c = col0 + tx;
+    if (r >= M || c >= N || cl0 + tx >= bnt) continue;
+    uint8_t* yp = Y + (r * ldy + c * ycs) * S;
+    const float f = epilogue_one<S == 2, BF>(tile[tx][j], bias, (int)r, beta, yp, relu);
+    if constexpr (S == 2) *(uint16_t*)yp = to16<BF>(f);
+    else *(float*)yp = f;
+  }
+}
+
+// tail K slices per tail tile: the idle clusters of the last round share the tail tiles' k-blocks
+// (at least 2 k-blocks per slice on average, at most 16 slices)
+static int tcg_tail_slices(int64_t ncl, int64_t ntail, int64_t nblk, int64_t ngroups) {
+  if (ntail <= 0) return 1;
+  const int64_t per = nblk / std::max<int64_t>(1, ngroups);
+  const int64_t t = std::min(std::min(ncl / ntail, (int64_t)16), per / 2);
+  return t >= 2 ? (int)t : 1;
+}
+
 // grid of a persistent cluster launch: whole clusters, at most as many as can be co-resident
 template <typename Fn>
 static unsigned tcg_grid(Fn fn, cudaLaunchConfig_t cfg, int cs, int64_t ntiles, int sms) {
@@ -3546,6 +3623,24 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   cfg.gridDim = dim3((unsigned)cs, 1, 1);
   const int64_t items = a.ks > 1 ? ntiles * a.ks : ntiles;  // (tile, K slice) work items
   cfg.gridDim = dim3(tcg_grid(fn, cfg, cs, items, sms), 1, 1);
+  // tail K slices for fp32 (3xTF32: long tiles; measured counter-productive for 16-bit tiles,
+  // whose partial-sum pass costs more than the idle clusters save): with fewer tiles than
+  // co-resident clusters the grid is sized for the slices, not the tiles
+  const bool copies_conv = a.plane > 0 && !a.i2c;  // (its epilogue maps span positions)
+  int tks = 1;
+  if (tf && a.ks <= 1 && !copies_conv) {
+    const int64_t ncl_max = tcg_grid(fn, cfg, cs, INT64_MAX / 4, sms) / cs;
+    const int64_t tail = ntiles % ncl_max;
+    tks = tcg_tail_slices(ncl_max, tail, a.nblk, a.ngroups);
+    // worth it only when the idle time it saves, (1 - 1/tks) of a tile (~1 us per fp32 k-block,
+    // measured), exceeds the partial-sum pass (~15 us): C5 at batch 32 - 128 yes (72 k-blocks),
+    // BERT 3072 x 768 no (24 k-blocks: 264 -> 272 us with it)
+    const int64_t per = a.nblk / std::max<int64_t>(1, a.ngroups);
+    if (tks > 1 && per * (tks - 1) / tks < 15) tks = 1;
+    if (const char* ev = std::getenv("SRT_TCG_TAIL_KS"))
+      if (std::atoi(ev) == 0) tks = 1;
+    if (tks > 1 && ntiles < ncl_max) cfg.gridDim = dim3((unsigned)(std::min(ncl_max, ntiles * tks) * cs), 1, 1);
+  }
   // split tail: when the tiles do not fill the last round of the persistent clusters (C5 conv:
   // 224 tiles on 74 clusters = 3 rounds + 2 tiles), each last-round tile is cut into sp column
   // slices of whole X boxes (a power of two: 16-bit <= 4, fp32 <= 8), one per otherwise idle
@@ -3557,10 +3652,31 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   a.rounds = (int32_t)(ntiles / ncl);
   a.ntail = (int32_t)(ntiles % ncl);
   a.sp = 1;
-  if (a.ntail > 0)
+  // tail K slices (preferred): the tail tiles' k-blocks spread over the idle clusters, partial
+  // sums added in order by tcg_tailsum (SRT_TCG_TAIL_KS=0 disables)
+  a.tks = tks > 1 && a.ntail > 0 ? tks : 1;
+  if (a.tks > 1 && a.rounds == 0) a.tks = std::max<int>(1, (int)std::min<int64_t>(a.tks, ncl / a.ntail));
+  if (a.ntail > 0 && a.tks <= 1)
     while (a.sp * 2 <= cap && (int64_t)a.sp * 2 * a.ntail <= ncl) a.sp *= 2;
   a.np = 256 / a.sp;
   a.idesc_p = (a.idesc & ~(0x3Fu << 17)) | ((uint32_t)(a.np >> 3) << 17);
+  const int bnt = a.bn > 0 ? a.bn : 256, R = cs * 128;
+  void* tws = nullptr;
+  if (a.tks > 1) {
+    e = cudaMallocAsync(&tws, (size_t)a.tks * a.ntail * bnt * R * 4, (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cuda_fail(e, "cudaMallocAsync(tail K-slice partials)", err);
+    }
+    a.tws = (float*)tws;
+  }
+  struct FreeT {
+    void* b;
+    void* st;
+    ~FreeT() {
+      if (b) cudaFreeAsync(b, (cudaStream_t)st);
+    }
+  } ft{tws, stream};
   // CTA pairs: the W blocks through a 2-D map of 128-byte rows (the 2-SM TMA form signals the
   // pair's rank-0 barrier; the 1-D bulk copy has no such form)
   CUtensorMap tmapA;
@@ -3581,6 +3697,21 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   }
   e = cudaLaunchKernelEx(&cfg, fn, tmap, tmap2, tmapA, a);
   if (e != cudaSuccess) return cuda_fail(e, what, err);
+  if (a.tks > 1) {
+    const int S = tf ? 4 : 2;
+    const dim3 grid((unsigned)(R / 32), (unsigned)((bnt + 31) / 32), (unsigned)a.ntail);
+    const int64_t tile0 = (int64_t)a.rounds * ncl, ycs = a.ycs > 0 ? a.ycs : 1;
+    if (S == 4)
+      tcg_tailsum<4, false><<<grid, 256, 0, (cudaStream_t)stream>>>(a.tws, a.tks, a.ntail, bnt, R, tile0, a.ngroups, a.M,
+                                                                    a.N, a.Y, a.ldy, ycs, a.bias, a.beta, a.relu);
+    else if (p.dtype == SPARSE_BF16)
+      tcg_tailsum<2, true><<<grid, 256, 0, (cudaStream_t)stream>>>(a.tws, a.tks, a.ntail, bnt, R, tile0, a.ngroups, a.M,
+                                                                   a.N, a.Y, a.ldy, ycs, a.bias, a.beta, a.relu);
+    else
+      tcg_tailsum<2, false><<<grid, 256, 0, (cudaStream_t)stream>>>(a.tws, a.tks, a.ntail, bnt, R, tile0, a.ngroups, a.M,
+                                                                    a.N, a.Y, a.ldy, ycs, a.bias, a.beta, a.relu);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "tail K-slice sum launch", err);
+  }
   return SPARSE_OK;
 }
 
@@ -3807,10 +3938,10 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
                                                                          p.c_in, plane);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "NHWC pack launch", err);
   }
-  // tile width: fp32 (3xTF32, MMA-bound) fills the rounds of the persistent clusters (cost ~
-  // rounds x (width + a fixed per-tile cost of ~32 columns); C5: 240 -> 229 to 218 us); 16-bit
-  // plans keep 256 (their k-blocks are bounded by the W block bytes, which do not shrink with
-  // the width: 240 measured 68 -> 73 us).  SRT_CONV_BN overrides; a multiple of 16 (M = 256)
+  // tile width: fp32 (3xTF32) fills the rounds of the persistent clusters (cost ~ rounds, the
+  // tail counted as K slices where it leaves >= 2 clusters per tile, x the operand bytes of a
+  // k-block; C5: 240 -> 229 to 218 us); 16-bit plans keep 256 (240 measured 68 -> 73 us).
+  // SRT_CONV_BN overrides; a multiple of 16 (M = 256)
   const int cs = p.tcg_cs;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
@@ -3821,7 +3952,14 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
     for (int w = 256; w >= (tf ? 128 : 256); w -= 16) {
       if ((w / cs) % 8) continue;  // a CTA's pixel rows: whole 8-row (1 KB) swizzle atoms
       const int64_t tiles = (int64_t)p.tcg_ngroups * ((plane + w - 1) / w);
-      const int64_t cost = (tiles + ncl - 1) / ncl * (w + 32);
+      // rounds of whole tiles, the tail as K slices when it leaves >= 2 clusters per tile
+      const int64_t full = tiles / ncl, tail = tiles % ncl;
+      const int tks = tcg_tail_slices(ncl, tail, p.tcp_nsteps, p.tcg_ngroups);
+      const int64_t r100 = full * 100 + (tail ? (tks > 1 ? 100 / tks + 15 : 100) : 0);
+      // a k-block's time ~ the operand bytes into the SM (measured bound, DESIGN 5d): the W
+      // block(s) + this CTA's pixel rows of 128 bytes per operand
+      const int64_t ops = tf ? 2 : 1, abytes = 16384 * ops, bbytes = (int64_t)(p.tcg_pair ? w / 2 : w) * 128 * ops;
+      const int64_t cost = r100 * (abytes + bbytes);
       if (cost < best) best = cost, bn = w;
     }
     if (const char* ev = std::getenv("SRT_CONV_BN")) {
