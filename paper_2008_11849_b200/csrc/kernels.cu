@@ -3368,6 +3368,41 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       tm_fence_after();
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)min((int64_t)nacc, a.N - n0);
+      if (tk >= 0 || a.ks > 1) {
+        // K slice (plan K slices or a tail K slice): the tile's fp32 partial, column-major (lanes
+        // = consecutive rows).  A separate loop: the plain store loop below stays as lean as it
+        // was (these branches inside it cost short-K 16-bit tiles ~15 %, measured)
+#pragma unroll 1
+        for (int c0 = 0; c0 < nacc; c0 += 32) {
+          uint32_t v[32];
+          tm_ld32(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+          tm_wait_ld();
+          if (c0 >= ncol || row0 >= a.M) continue;
+          float* wp;
+          size_t cst;
+          if (tk >= 0) {
+            cst = (size_t)CS * 128;
+            wp = a.tws + ((size_t)(tk * a.ntail + (t - (int64_t)a.rounds * ncl)) * BNT + c0) * cst +
+                 (int)rank * 128 + q * 32 + lane;
+          } else {
+            if (row >= a.M) continue;
+            cst = (size_t)a.M;
+            wp = a.ws + ((size_t)ksl * a.N + n0 + c0) * a.M + row;
+          }
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c0 + c < ncol) wp[c * cst] = has ? __uint_as_float(v[c]) : 0.0f;
+        }
+        tm_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (pair && rank == 1) mbar_arrive_remote(map_rank(tempty0 + 8 * acc, 0));
+          else mbar_arrive(tempty0 + 8 * acc);
+        }
+        aph[acc] ^= 1u;
+        acc ^= 1;
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < nacc; c0 += 64) {
         uint32_t v[64];
@@ -3375,26 +3410,6 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         tm_ld32(ta, v);
         tm_ld32(ta + 32, v + 32);
         tm_wait_ld();
-        if (tk >= 0) {  // tail K slice: the fp32 partial of this CTA's rows
-          if (row0 < a.M && c0 < ncol) {
-            const int R = CS * 128;
-            float* wp = a.tws + ((size_t)(tk * a.ntail + (t - (int64_t)a.rounds * ncl)) * BNT + c0) * R +
-                        (int)rank * 128 + q * 32 + lane;
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (c0 + c < ncol) wp[(size_t)c * R] = has ? __uint_as_float(v[c]) : 0.0f;
-          }
-          continue;
-        }
-        if (a.ks > 1) {  // K slice: the fp32 partial, column-major (lanes = consecutive rows)
-          if (row < a.M && c0 < ncol) {
-            float* wp = a.ws + ((size_t)ksl * a.N + n0 + c0) * a.M + row;
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (c0 + c < ncol) wp[(size_t)c * a.M] = has ? __uint_as_float(v[c]) : 0.0f;
-          }
-          continue;
-        }
         if (CONV && !a.i2c) {
           if (a.beta != 0.0f) {  // beta * Y_old: element-wise (the fp32 sum needs Y_old)
             if (row >= a.M) continue;
