@@ -826,7 +826,7 @@ class Run:
 
 def parse_secondary(spec: str, world: int):
     if spec == "auto":
-        spec = "bert:f32:90,bert:f16:90,conv:f16:90" if world == 1 else ""
+        spec = "bert:f32:90,bert:f16:90,conv:f16:90,conv:f32:95" if world == 1 else ""
     out = []
     for item in filter(None, spec.split(",")):
         wl, dt, sp = item.split(":")
@@ -846,7 +846,7 @@ def main():
     ap.add_argument("--sparsity", type=int, default=90)
     ap.add_argument("--secondary", default="auto",
                     help="extra workloads timed the same way, 'wl:dtype:sparsity,...'; 'auto' = "
-                         "BERT FFN fp32 and fp16 and the C5 conv in fp16 at 90%% on 1 GPU, none on "
+                         "BERT FFN fp32 and fp16 and the C5 conv in fp16 at 90%%, the C5 conv fp32 at 95%% on 1 GPU, none on "
                          "N > 1; '' = none")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
