@@ -1433,3 +1433,24 @@ def test_tcgen05_kslices_epilogue(dt):
     ref = _f16_round(ref) if dt == "f16" else ref.astype(np.float32).astype(np.float64)
     assert np.array_equal(Yb[:, :N].double().cpu().numpy(), ref)
     assert torch.count_nonzero(Yb[:, N:]) == 0
+
+
+@pytest.mark.parametrize("dt", ["f16", "f32"])
+@pytest.mark.parametrize("opts", [{"conv_kernel": 5}, {"conv_kernel": 5, "cta_pair": 1},
+                                  {"conv_kernel": 5, "x_multicast": 2}])
+@pytest.mark.parametrize("cin,cout,B,H,W", [(256, 256, 1, 14, 14), (64, 130, 1, 56, 56), (128, 512, 1, 7, 7),
+                                            (96, 256, 7, 13, 11)])
+def test_conv_tcgen05_small_batch(cin, cout, B, H, W, opts, dt):
+    # batch 1 (the Table-3 convs) and odd sizes on the im2col path: few tiles for 148 SMs (tile
+    # widths / tail slices chosen at launch), pixels crossing image boundaries inside a tile
+    dev = _dev()
+    tdt = torch.float16 if dt == "f16" else torch.float32
+    wi = gen.int_weights(cout, 9 * cin, 90, seed=cin + cout + H, vmax=2)
+    x = gen.int_x(cin * B * H, W, seed=W + B, vmax=4).reshape(cin, B, H, W)
+    plan = srt.Plan.from_csr(wi, dtype=tdt, kind=srt.SPARSE_CONV3X3, c_in=cin, h=H, w=W, n_hint=B, **opts)
+    y = torch.full((cout, B, H, W), float("nan"), dtype=tdt, device=dev)
+    plan.conv3x3(torch.from_numpy(x).to(dev).to(tdt), y)
+    torch.cuda.synchronize()
+    ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), x.astype(np.float64))
+    ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
+    assert np.array_equal(y.double().cpu().numpy(), ref)
