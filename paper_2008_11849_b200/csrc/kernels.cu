@@ -2740,31 +2740,13 @@ struct TcgArgs {
   // tws[(slice ntail + tail tile) BNT + column][group row] and tcg_tailsum adds them in order
   int32_t tks;
   float* tws;
-  // stream-K (skl > 0, fp32, every group has skl k-block entries): cluster c takes the range
-  // [c W / ncl, (c + 1) W / ncl) of the W = ntiles skl (tile, k-block) units in tile order;
-  // a tile split between clusters leaves one partial per cluster ("piece", k order) in
-  // sws[(tile skp + piece) BNT + column][group row], and tcg_sksum adds them in order
-  int32_t skl, skp;
-  float* sws;
 };
 
 // work item i of cluster cl: tile t and column slice (-1 = the whole tile)
 __device__ __forceinline__ bool tcg_work(const TcgArgs& a, int64_t cl, int64_t ncl, int64_t i, int64_t ntiles,
-                                         int64_t& t, int& slice, int& tk, int& sk0, int& sk1, int& piece) {
+                                         int64_t& t, int& slice, int& tk) {
   slice = -1;
   tk = -1;
-  sk0 = -1, sk1 = -1, piece = -1;
-  if (a.skl > 0) {  // stream-K segment i of cluster cl
-    const int64_t W = ntiles * a.skl, s = cl * W / ncl, e = (cl + 1) * W / ncl;
-    if (s >= e) return false;
-    const int64_t t0 = s / a.skl, t1 = (e - 1) / a.skl;
-    t = t0 + i;
-    if (t > t1) return false;
-    sk0 = t == t0 ? (int)(s - t0 * a.skl) : 0;
-    sk1 = t == t1 ? (int)(e - 1 - t1 * a.skl) + 1 : a.skl;
-    if (sk0 > 0 || sk1 < a.skl) piece = (int)(cl - ((t * a.skl + 1) * ncl - 1) / W);
-    return true;
-  }
   if (a.tks > 1 && i >= a.rounds) {  // tail K slices
     if (i > a.rounds || cl >= (int64_t)a.ntail * a.tks) return false;
     t = (int64_t)a.rounds * ncl + cl / a.tks;
@@ -2797,14 +2779,8 @@ __device__ __forceinline__ int64_t tcg_item(const TcgArgs& a, int64_t item, int&
   ksl = (int)(item - t * a.ks);
   return t;
 }
-// the slice's part [j0, j1) of the group's k-block entries (plan K slices, a tail K slice, or a
-// stream-K segment [sk0, sk1))
-__device__ __forceinline__ void tcg_krange(const TcgArgs& a, int ksl, int tk, int sk0, int sk1, int& j0, int& j1) {
-  if (sk0 >= 0) {
-    j1 = j0 + sk1;
-    j0 = j0 + sk0;
-    return;
-  }
+// the slice's part [j0, j1) of the group's k-block entries (plan K slices, or a tail K slice)
+__device__ __forceinline__ void tcg_krange(const TcgArgs& a, int ksl, int tk, int& j0, int& j1) {
   const int n = tk >= 0 ? a.tks : a.ks, k = tk >= 0 ? tk : ksl;
   if (n <= 1) return;
   const int L = j1 - j0, jb = j0;
@@ -3051,14 +3027,14 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       int s = 0;
       uint32_t ph = 0;
       int64_t t;
-      int slice, tk, sk0, sk1, piece;
-      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk, sk0, sk1, piece); ++it) {
+      int slice, tk;
+      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk); ++it) {
         int ksl;
         t = tcg_item(a, t, ksl);
         const int gi = (int)(t % a.ngroups);
         const int64_t n0 = (t / a.ngroups) * BNT;
         int j0 = meta[gi], j1 = meta[gi + 1];
-        tcg_krange(a, ksl, tk, sk0, sk1, j0, j1);
+        tcg_krange(a, ksl, tk, j0, j1);
         // boxes of this work item: the whole tile (this CTA loads boxes rank nb .. + nb - 1 and
         // multicasts them), or the slice's nbs boxes (box i loaded by rank i % CS) stored from
         // box 0 of the stage.  This thread's loads: stage positions pos0 + i pstep, i < cnt, of
@@ -3151,13 +3127,13 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       int s = 0, acc = 0;
       uint32_t ph = 0, aph[2] = {0u, 0u};
       int64_t t;
-      int slice, tk, sk0, sk1, piece;
-      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk, sk0, sk1, piece); ++it) {
+      int slice, tk;
+      for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk); ++it) {
         int ksl;
         t = tcg_item(a, t, ksl);
         const int gi = (int)(t % a.ngroups);
         int j0 = meta[gi], j1 = meta[gi + 1];
-        tcg_krange(a, ksl, tk, sk0, sk1, j0, j1);
+        tcg_krange(a, ksl, tk, j0, j1);
         const uint32_t idesc = slice < 0 ? a.idesc : a.idesc_p;
         int j = j0;
         do {
@@ -3226,8 +3202,8 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     int32_t* otab = (int32_t*)((uint8_t*)tslot + 64);  // conv: span position -> output offset
     int64_t tab_n0 = -1;
     int64_t t;
-    int slice, tk, sk0, sk1, piece;
-    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk, sk0, sk1, piece); ++it) {
+    int slice, tk;
+    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk); ++it) {
       int ksl;
       t = tcg_item(a, t, ksl);
       const int gi = (int)(t % a.ngroups);
@@ -3237,7 +3213,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BNT : a.np;
       const int64_t n0 = nt0 + cbase;
       int kj0 = meta[gi], kj1 = meta[gi + 1];
-      tcg_krange(a, ksl, tk, sk0, sk1, kj0, kj1);
+      tcg_krange(a, ksl, tk, kj0, kj1);
       const int nent = kj1 - kj0;
       if (CONV && !a.i2c && nt0 != tab_n0) {
         tcg_conv_table<32 * NEPI>(otab, nt0, a, threadIdx.x - 64);
@@ -3272,10 +3248,9 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)max((int64_t)0, min((int64_t)nacc, a.N - n0));
       if (row0 >= a.M || (a.dbg & 1)) continue;
-      if (tk >= 0 || piece >= 0) {  // tail K slice / stream-K piece: the fp32 partial of this CTA's rows
+      if (tk >= 0) {  // tail K slice: the fp32 partial of this CTA's rows, lanes = consecutive rows
         const int R = CS * 128;
-        float* wp = (piece >= 0 ? a.sws + ((size_t)(t * a.skp + piece) * BNT + hc) * R
-                                : a.tws + ((size_t)(tk * a.ntail + (t - (int64_t)a.rounds * ncl)) * BNT + hc) * R) +
+        float* wp = a.tws + ((size_t)(tk * a.ntail + (t - (int64_t)a.rounds * ncl)) * BNT + hc) * R +
                     (int)rank * 128 + q * 32 + lane;
 #pragma unroll
         for (int c = 0; c < 128; ++c)
@@ -3371,8 +3346,8 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
     const int64_t ycs = a.ycs > 0 ? a.ycs : 1;
     const bool coal = ycs == 1 && a.beta == 0.0f && ((a.ldy * 2) % 16) == 0 && ((uintptr_t)a.Y % 16) == 0;
     int64_t t;
-    int slice, tk, sk0, sk1, piece;
-    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk, sk0, sk1, piece); ++it) {
+    int slice, tk;
+    for (int64_t it = 0; tcg_work(a, cl, ncl, it, ntiles, t, slice, tk); ++it) {
       int ksl;
       t = tcg_item(a, t, ksl);
       const int gi = (int)(t % a.ngroups);
@@ -3382,7 +3357,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       const int cbase = slice < 0 ? 0 : slice * a.np, nacc = slice < 0 ? BNT : a.np;
       const int64_t n0 = nt0 + cbase;
       int kj0 = meta[gi], kj1 = meta[gi + 1];
-      tcg_krange(a, ksl, tk, sk0, sk1, kj0, kj1);
+      tcg_krange(a, ksl, tk, kj0, kj1);
       const bool has = kj1 > kj0;
       if (CONV && !a.i2c && nt0 != tab_n0) {
         tcg_conv_table<128>(otab, nt0, a, threadIdx.x - 64);
@@ -3393,7 +3368,7 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
       tm_fence_after();
       const int row0 = rb * 128 + q * 32, row = row0 + lane;
       const int ncol = (int)min((int64_t)nacc, a.N - n0);
-      if (tk >= 0 || piece >= 0 || a.ks > 1) {
+      if (tk >= 0 || a.ks > 1) {
         // K slice (plan K slices or a tail K slice): the tile's fp32 partial, column-major (lanes
         // = consecutive rows).  A separate loop: the plain store loop below stays as lean as it
         // was (these branches inside it cost short-K 16-bit tiles ~15 %, measured)
@@ -3405,10 +3380,9 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
           if (c0 >= ncol || row0 >= a.M) continue;
           float* wp;
           size_t cst;
-          if (tk >= 0 || piece >= 0) {
+          if (tk >= 0) {
             cst = (size_t)CS * 128;
-            wp = (piece >= 0 ? a.sws + ((size_t)(t * a.skp + piece) * BNT + c0) * cst
-                             : a.tws + ((size_t)(tk * a.ntail + (t - (int64_t)a.rounds * ncl)) * BNT + c0) * cst) +
+            wp = a.tws + ((size_t)(tk * a.ntail + (t - (int64_t)a.rounds * ncl)) * BNT + c0) * cst +
                  (int)rank * 128 + q * 32 + lane;
           } else {
             if (row >= a.M) continue;
@@ -3614,52 +3588,6 @@ __global__ void __launch_bounds__(256) tcg_tailsum(const float* __restrict__ tws
   }
 }
 
-// Stream-K fixup: for every tile split between clusters (pieces = the clusters whose ranges meet
-// it), Y tile = epilogue(sum of the pieces in k order); whole tiles were stored by the kernel
-template <int S, bool BF>
-__global__ void __launch_bounds__(256) tcg_sksum(const float* __restrict__ sws, int skp, int skl, int bnt, int R,
-                                                 int64_t ncl, int64_t ntiles, int ngroups, int64_t M, int64_t N,
-                                                 uint8_t* __restrict__ Y, int64_t ldy, int64_t ycs,
-                                                 const uint8_t* __restrict__ bias, float beta, int relu) {
-  __shared__ float tile[32][33];
-  const int64_t t = blockIdx.z, W = ntiles * skl;
-  const int64_t cf = ((t * skl + 1) * ncl - 1) / W, cl_ = ((t * skl + skl) * ncl - 1) / W;
-  const int np = (int)(cl_ - cf + 1);
-  if (np <= 1) return;
-  const int64_t row0 = (t % ngroups) * R + (int64_t)blockIdx.x * 32, col0 = (t / ngroups) * bnt + (int64_t)blockIdx.y * 32;
-  const int cl0 = blockIdx.y * 32, rl0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int j = ty; j < 32; j += 8) {
-    const int cl = cl0 + j;
-    float v = 0.0f;
-    if (cl < bnt && row0 + tx < M && col0 + j < N) {
-      const size_t off = (size_t)cl * R + rl0 + tx;
-      v = __ldg(sws + (size_t)t * skp * bnt * R + off);
-      for (int pc = 1; pc < np; ++pc) v = __fadd_rn(v, __ldg(sws + ((size_t)t * skp + pc) * bnt * R + off));
-    }
-    tile[j][tx] = v;
-  }
-  __syncthreads();
-  for (int j = ty; j < 32; j += 8) {
-    const int64_t r = row0 + j, c = col0 + tx;
-    if (r >= M || c >= N || cl0 + tx >= bnt) continue;
-    uint8_t* yp = Y + (r * ldy + c * ycs) * S;
-    const float f = epilogue_one<S == 2, BF>(tile[tx][j], bias, (int)r, beta, yp, relu);
-    if constexpr (S == 2) *(uint16_t*)yp = to16<BF>(f);
-    else *(float*)yp = f;
-  }
-}
-
-// k-block entries per group when every group has the same count (stream-K units), else 0
-static int64_t tcg_uniform_len(const Plan& p) {
-  const int64_t ng = p.tcg_ngroups;
-  if (ng <= 0 || (int64_t)p.tcp_step_off.size() < ng + 1) return 0;
-  const int64_t L = p.tcp_step_off[1] - p.tcp_step_off[0];
-  for (int64_t g = 1; g < ng; ++g)
-    if (p.tcp_step_off[g + 1] - p.tcp_step_off[g] != L) return 0;
-  return L;
-}
-
 // tail K slices per tail tile: the idle clusters of the last round share the tail tiles' k-blocks
 // (at least 2 k-blocks per slice on average, at most 16 slices)
 static int tcg_tail_slices(int64_t ncl, int64_t ntail, int64_t nblk, int64_t ngroups) {
@@ -3715,30 +3643,7 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   // co-resident clusters the grid is sized for the slices, not the tiles
   const bool copies_conv = a.plane > 0 && !a.i2c;  // (its epilogue maps span positions)
   int tks = 1;
-  // stream-K (fp32, every group with the same k-block count L; opt-in SRT_TCG_STREAMK=1): the
-  // clusters share the ntiles L units evenly instead of in whole-tile rounds, when the rounds
-  // would leave >= ~16 k-blocks of a round idle.  Measured slower than the rounds + tail K
-  // slices on every shape tried (C5 batch 256 216 -> 260 us, batch 32 57 -> 69 us, BERT
-  // 768 x 3072 368 -> 419 us; profiles/r02_v18_streamk_time.txt), so off by default
-  a.skl = 0;
   if (tf && a.ks <= 1 && !copies_conv) {
-    const int64_t L = tcg_uniform_len(p);
-    const int64_t ncl_max = tcg_grid(fn, cfg, cs, INT64_MAX / 4, sms) / cs;
-    const char* ev = std::getenv("SRT_TCG_STREAMK");
-    if (L > 0 && ntiles * L >= 2 * ncl_max && ntiles <= 65535 && ev && std::atoi(ev) != 0) {
-      const int64_t rounds_up = (ntiles + ncl_max - 1) / ncl_max;
-      const int64_t idle_kb = (rounds_up * ncl_max - ntiles) * L / ncl_max;  // per cluster
-      const int64_t per0 = ntiles * L / ncl_max;
-      const int64_t skp0 = std::min<int64_t>(ncl_max, (L + per0 - 1) / per0 + 1);
-      if (idle_kb >= 16 && (size_t)ntiles * skp0 * (a.bn > 0 ? a.bn : 256) * cs * 128 * 4 <= ((size_t)1 << 29)) {
-        a.skl = (int32_t)L;
-        const int64_t per = ntiles * L / ncl_max;  // units per cluster (>= 2)
-        a.skp = (int32_t)std::min<int64_t>(ncl_max, (L + per - 1) / per + 1);
-        cfg.gridDim = dim3((unsigned)(ncl_max * cs), 1, 1);
-      }
-    }
-  }
-  if (tf && a.ks <= 1 && !copies_conv && a.skl == 0) {
     const int64_t ncl_max = tcg_grid(fn, cfg, cs, INT64_MAX / 4, sms) / cs;
     const int64_t tail = ntiles % ncl_max;
     tks = tcg_tail_slices(ncl_max, tail, a.nblk, a.ngroups);
@@ -3764,9 +3669,9 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   a.sp = 1;
   // tail K slices (preferred): the tail tiles' k-blocks spread over the idle clusters, partial
   // sums added in order by tcg_tailsum (SRT_TCG_TAIL_KS=0 disables)
-  a.tks = tks > 1 && a.ntail > 0 && a.skl == 0 ? tks : 1;
+  a.tks = tks > 1 && a.ntail > 0 ? tks : 1;
   if (a.tks > 1 && a.rounds == 0) a.tks = std::max<int>(1, (int)std::min<int64_t>(a.tks, ncl / a.ntail));
-  if (a.ntail > 0 && a.tks <= 1 && a.skl == 0)
+  if (a.ntail > 0 && a.tks <= 1)
     while (a.sp * 2 <= cap && (int64_t)a.sp * 2 * a.ntail <= ncl) a.sp *= 2;
   a.np = 256 / a.sp;
   a.idesc_p = (a.idesc & ~(0x3Fu << 17)) | ((uint32_t)(a.np >> 3) << 17);
@@ -3787,16 +3692,6 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
       if (b) cudaFreeAsync(b, (cudaStream_t)st);
     }
   } ft{tws, stream};
-  void* sws = nullptr;
-  if (a.skl > 0) {
-    e = cudaMallocAsync(&sws, (size_t)ntiles * a.skp * bnt * R * 4, (cudaStream_t)stream);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return cuda_fail(e, "cudaMallocAsync(stream-K partials)", err);
-    }
-    a.sws = (float*)sws;
-  }
-  FreeT fs{sws, stream};
   // CTA pairs: the W blocks through a 2-D map of 128-byte rows (the 2-SM TMA form signals the
   // pair's rank-0 barrier; the 1-D bulk copy has no such form)
   CUtensorMap tmapA;
@@ -3817,13 +3712,6 @@ static int tcg_launch(const Plan& p, const void* fn_, const CUtensorMap& tmap, c
   }
   e = cudaLaunchKernelEx(&cfg, fn, tmap, tmap2, tmapA, a);
   if (e != cudaSuccess) return cuda_fail(e, what, err);
-  if (a.skl > 0) {
-    const dim3 grid((unsigned)(R / 32), (unsigned)((bnt + 31) / 32), (unsigned)ntiles);
-    const int64_t ycs = a.ycs > 0 ? a.ycs : 1;
-    tcg_sksum<4, false><<<grid, 256, 0, (cudaStream_t)stream>>>(a.sws, a.skp, a.skl, bnt, R, ncl, ntiles, a.ngroups,
-                                                                a.M, a.N, a.Y, a.ldy, ycs, a.bias, a.beta, a.relu);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "stream-K fixup launch", err);
-  }
   if (a.tks > 1) {
     const int S = tf ? 4 : 2;
     const dim3 grid((unsigned)(R / 32), (unsigned)((bnt + 31) / 32), (unsigned)a.ntail);
@@ -4079,16 +3967,10 @@ static int launch_conv_i2c(const Plan& p, int64_t batch, const void* x, void* y,
     for (int w = 256; w >= (tf ? 128 : 256); w -= 16) {
       if ((w / cs) % 8) continue;  // a CTA's pixel rows: whole 8-row (1 KB) swizzle atoms
       const int64_t tiles = (int64_t)p.tcg_ngroups * ((plane + w - 1) / w);
-      // rounds of whole tiles, the tail as K slices when it leaves >= 2 clusters per tile; or
-      // stream-K (fp32, tcg_launch's criterion): the units spread evenly, plus the fixup pass
+      // rounds of whole tiles, the tail as K slices when it leaves >= 2 clusters per tile
       const int64_t full = tiles / ncl, tail = tiles % ncl;
       const int tks = tcg_tail_slices(ncl, tail, p.tcp_nsteps, p.tcg_ngroups);
-      int64_t r100 = full * 100 + (tail ? (tks > 1 ? 100 / tks + 15 : 100) : 0);
-      const int64_t L = tcg_uniform_len(p);
-      const char* sk = std::getenv("SRT_TCG_STREAMK");
-      if (tf && L > 0 && sk && std::atoi(sk) != 0 && tiles * L >= 2 * ncl &&
-          ((tiles + ncl - 1) / ncl * ncl - tiles) * L / ncl >= 16)
-        r100 = std::min<int64_t>(r100, tiles * 100 / ncl + 8);
+      const int64_t r100 = full * 100 + (tail ? (tks > 1 ? 100 / tks + 15 : 100) : 0);
       // a k-block's time ~ the operand bytes into the SM (measured bound, DESIGN 5d): the W
       // block(s) + this CTA's pixel rows of 128 bytes per operand
       const int64_t ops = tf ? 2 : 1, abytes = 16384 * ops, bbytes = (int64_t)(p.tcg_pair ? w / 2 : w) * 128 * ops;

@@ -1454,57 +1454,3 @@ def test_conv_tcgen05_small_batch(cin, cout, B, H, W, opts, dt):
     ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), x.astype(np.float64))
     ref = torch.from_numpy(ref.astype(np.float32)).to(tdt).double().numpy()
     assert np.array_equal(y.double().cpu().numpy(), ref)
-
-
-# ------------------------------------------- tcgen05 blocks: stream-K (fp32)
-
-@pytest.mark.parametrize("pair", [1, 0])
-@pytest.mark.parametrize("M,K,N", [(768, 1024, 8192), (512, 2048, 6000), (256, 3072, 2600)])
-def test_tcgen05_streamk_spmm(M, K, N, pair, monkeypatch):
-    # fp32 tiles whose count leaves a round partly idle: the clusters share the (tile, k-block)
-    # units evenly, split tiles are summed in k order by tcg_sksum.  Bitwise on integer data
-    # with and without stream-K; real data within 1e-5 of the oracle on sampled columns
-    dev = _dev()
-    wi = gen.int_weights(M, K, 90, seed=M + K + pair, vmax=2)
-    xi = gen.int_x(K, N, seed=N + 3, vmax=4)
-    plan = srt.Plan.from_csr(wi, dtype=torch.float32, n_hint=N, executor=4, cta_pair=pair)
-    cols = np.sort(np.random.default_rng(N).choice(N, 257, replace=False))
-    ref = oracle.spmm(M, K, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64), xi[:, cols].astype(np.float64))
-    X = torch.from_numpy(xi).to(dev)
-    for sk in ("0", "1"):
-        monkeypatch.setenv("SRT_TCG_STREAMK", sk)
-        Y = torch.full((M, N), float("nan"), dtype=torch.float32, device=dev)
-        plan.spmm(X, Y)
-        torch.cuda.synchronize()
-        assert not torch.isnan(Y).any()
-        assert np.array_equal(Y[:, cols].double().cpu().numpy(), ref), sk
-    w = gen.pruned_weights(M, K, 90, seed=M + 2 * K)
-    x = gen.uniform_x(K, N, seed=N + 4)
-    plan = srt.Plan.from_csr(w, dtype=torch.float32, n_hint=N, executor=4, cta_pair=pair)
-    monkeypatch.setenv("SRT_TCG_STREAMK", "1")
-    Y = plan.spmm(torch.from_numpy(x).to(dev))
-    torch.cuda.synchronize()
-    ref = oracle.spmm(M, K, w.row_ptr, w.col_idx, w.values.astype(np.float64), x[:, cols].astype(np.float64))
-    assert oracle.rel_l2(Y[:, cols].double().cpu().numpy(), ref) <= F32_TOL
-
-
-@pytest.mark.parametrize("B", [32, 64, 128, 256])
-def test_conv_tcgen05_streamk(B, monkeypatch):
-    # the C5 conv fp32 at the per-rank batches of 1/2/4/8 GPUs, stream-K on and off: bitwise on
-    # integer data against the oracle on sampled images
-    dev = _dev()
-    cin = cout = 256
-    wi = gen.int_weights(cout, 9 * cin, 90, seed=B + 5, vmax=2)
-    x = gen.int_x(cin * B * 14, 14, seed=B + 6, vmax=4).reshape(cin, B, 14, 14)
-    plan = srt.Plan.from_csr(wi, kind=srt.SPARSE_CONV3X3, c_in=cin, h=14, w=14, n_hint=B, conv_kernel=5, cta_pair=1)
-    sel = [0, 1, B // 2, B - 2, B - 1]
-    ref = oracle.conv3x3(cout, wi.row_ptr, wi.col_idx, wi.values.astype(np.float64),
-                         np.ascontiguousarray(x[:, sel]).astype(np.float64))
-    xd = torch.from_numpy(x).to(dev)
-    for sk in ("0", "1"):
-        monkeypatch.setenv("SRT_TCG_STREAMK", sk)
-        y = torch.full((cout, B, 14, 14), float("nan"), dtype=torch.float32, device=dev)
-        plan.conv3x3(xd, y)
-        torch.cuda.synchronize()
-        assert not torch.isnan(y).any()
-        assert np.array_equal(y[:, sel].double().cpu().numpy(), ref), sk
