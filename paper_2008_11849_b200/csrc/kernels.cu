@@ -3413,7 +3413,8 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
         if (CONV && !a.i2c) {
           if (a.beta != 0.0f) {  // beta * Y_old: element-wise (the fp32 sum needs Y_old)
             if (row >= a.M) continue;
-            for (int c = 0; c < 64; ++c) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {  // (unrolled: v stays in registers)
               const int32_t o = ot[c0 + c];
               if (o < 0) continue;
               uint8_t* yp = a.Y + ((int64_t)row * a.plane + o) * 2;
@@ -3496,13 +3497,19 @@ __global__ void __launch_bounds__(TF ? 320 : 192, 1) spmm_tcg_kernel(const __gri
             if (epi && cc + c < ncol) f = epilogue_one<true, BF>(f, a.bias, row, a.beta, yp + c * ycs * 2, a.relu);
             hv[c] = to16<BF>(f);
           }
+          // (compile-time indices into hv: a runtime-bounded loop put hv in local memory, which
+          // made the channels-last fp16 conv 68 -> 156 us)
           if (ycs != 1) {
-            for (int c = 0; c < 32 && cc + c < ncol; ++c) ((uint16_t*)yp)[c * ycs] = hv[c];
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (cc + c < ncol) ((uint16_t*)yp)[c * ycs] = hv[c];
           } else if (cc + 32 <= ncol && ((uintptr_t)yp % 16) == 0) {
 #pragma unroll
             for (int c = 0; c < 32; c += 8) *(uint4*)(yp + c * 2) = *(const uint4*)(hv + c);
           } else {
-            for (int c = 0; c < 32 && cc + c < ncol; ++c) ((uint16_t*)yp)[c] = hv[c];
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (cc + c < ncol) ((uint16_t*)yp)[c] = hv[c];
           }
         }
       }
